@@ -1,0 +1,154 @@
+/*
+ * deserve.h — C ABI of the B200-native DeServe stage-step path (libdeserve_b200.so).
+ *
+ * The reference (/root/reference/proj, "pipesim") has no GPU path: its stage forward is the
+ * calibration lookup `scaled_stage_time()` (src/perf_model.cpp:109-114) called from
+ * `Engine::on_compute_start` (src/sim.cpp:409-428); its swap is byte/time arithmetic in
+ * `Engine::issue_swap_in` (src/sim.cpp:328-353); its hop is `Engine::send_onward`
+ * (src/sim.cpp:430-439). Each entry point below is the call a maintainer binds at one of those
+ * slots. Conventions: every call returns ds_status (0 = ok) and never throws or aborts;
+ * ds_last_error() returns a thread-local message for the last failure. No torch types cross
+ * this boundary: plain pointers, sizes and integers only.
+ */
+#ifndef DESERVE_B200_H
+#define DESERVE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t ds_status;
+#define DS_OK 0
+#define DS_ERR_ARG 1        /* bad argument (maps to pipesim::ConfigError)               */
+#define DS_ERR_PLAN 2       /* infeasible plan / device OOM (maps to pipesim::PlanError)  */
+#define DS_ERR_RUNTIME 3    /* CUDA / NCCL / executor failure (maps to pipesim::SimError) */
+#define DS_ERR_NO_DEVICE 4  /* no CUDA device visible: the product has no CPU fallback    */
+
+const char* ds_last_error(void);
+const char* ds_version(void);
+
+/* ------------------------------------------------------------------------------------------
+ * Integer hot path (bit-exact with the reference).
+ * ------------------------------------------------------------------------------------------ */
+
+/* Reference: stage_compute_time / scaled_stage_time (src/perf_model.cpp:85-114).
+ * batch_sizes/times_us: the calibration table (batch strictly increasing). */
+ds_status ds_stage_time_us(const int64_t* batch_sizes, const int64_t* times_us, int64_t n,
+                           int64_t batch, int64_t layers, int64_t ref_layers, int64_t* out_us);
+
+/* Reference: page_bytes / kv_bytes / global_pool_size (src/perf_model.cpp:116-136). */
+ds_status ds_page_bytes(int64_t kv_bytes_per_token, int64_t layers, int64_t total_layers,
+                        int64_t* out);
+ds_status ds_global_pool_size(int64_t pcie_bw, int64_t stage_time_us, int64_t page,
+                              int64_t* out);
+
+/* Reference: plan() (src/planner.cpp:140-276) on a config document in the reference JSON format
+ * (src/config.cpp:103-252). policy: NULL/"" = config as written, else "baseline" | "offload" |
+ * "opt" (src/sweep.cpp:26-43). latency_us >= 0 overrides every link latency (sweep.cpp:45-49);
+ * nb_override >= 0 overrides scheduler.nb_override. Writes the plan JSON (byte-identical to
+ * PipelinePlan::to_json, src/planner.cpp:294-335) into out (NUL-terminated, truncated to cap);
+ * *needed receives the full length. */
+ds_status ds_plan_config(const char* config_json, const char* config_dir, const char* policy,
+                         int64_t latency_us, int64_t nb_override, char* out, size_t cap,
+                         size_t* needed);
+
+/* Reference: run() (src/sim.cpp:591-595) in virtual-clock mode. The executor's own scheduler
+ * (not the reference engine) produces the trace; write_trace format (src/trace.cpp:40-46).
+ * trace_path may be NULL. report_json receives the SimReport fields (src/sim.cpp:501-532). */
+ds_status ds_sim_config(const char* config_json, const char* config_dir, const char* policy,
+                        int64_t latency_us, int64_t nb_override, const char* trace_path,
+                        char* report_json, size_t cap);
+
+/* Same, on an explicit plan document (PipelinePlan::from_json, src/planner.cpp:337-378) instead
+ * of running the planner; the config supplies model, topology and workload. */
+ds_status ds_sim_plan(const char* config_json, const char* config_dir, const char* plan_json,
+                      const char* trace_path, char* report_json, size_t cap);
+
+/* ------------------------------------------------------------------------------------------
+ * Stage forward (the compute slot of Engine::on_compute_start, src/sim.cpp:424-425).
+ * ------------------------------------------------------------------------------------------ */
+
+typedef struct ds_model_desc {
+    int32_t n_layers;      /* whole model */
+    int32_t d_model;
+    int32_t n_heads;
+    int32_t n_kv_heads;
+    int32_t d_head;
+    int32_t ffn;
+    int32_t vocab;
+    int32_t max_seq_len;
+    float rope_theta;      /* 500000 for Llama 3 */
+    float norm_eps;        /* 1e-5 */
+} ds_model_desc;
+
+/* One row group of a circuit: n_tok consecutive positions [pos, pos+n_tok) of the request in
+ * microbatch slot `slot`. Decode rows have n_tok == 1; prefill rows carry up to prefill_chunk
+ * prompt positions (reference begin_circuit, src/sim.cpp:386-407). need_logits = 1 samples a
+ * token from the group's last position (decode rows, and the prefill group completing a prompt). */
+typedef struct ds_row {
+    int32_t slot;
+    int32_t pos;
+    int32_t n_tok;
+    int32_t need_logits;
+    int32_t is_decode;     /* 1: decode row (input = token sampled last circuit); 0: prompt rows */
+    int32_t reserved;
+    int64_t req_id;
+} ds_row;
+
+/* Synthetic prompt token of request req_id at position pos (BOS = 128000 at position 0;
+ * otherwise SplitMix64(0x5EED ^ req_id * phi ^ pos) mod 128000). The reference has no token ids
+ * (SURVEY.md Appendix C); this is the build's pinned convention, shared with the CPU oracle. */
+int32_t ds_prompt_token_id(int64_t req_id, int32_t pos);
+
+typedef struct ds_stage ds_stage;
+
+ds_status ds_stage_create(int32_t device, const ds_model_desc* model, int64_t layer_begin,
+                          int64_t layer_end, int32_t is_first, int32_t is_last,
+                          uint64_t weight_seed, int32_t max_rows, int32_t max_slots,
+                          ds_stage** out);
+ds_status ds_stage_destroy(ds_stage* stage);
+
+/* KV pool of the stage (reference MemoryBudget, include/pipesim/perf_model.hpp:57-72 and the swap
+ * plan of src/sim.cpp:296-353). page_bytes must equal reference page_bytes(). Device pages:
+ * n_mb * floor(local_bytes_per_mb / page) local + 2 * global_slot_bytes / page slot pages;
+ * pinned host backing of host_bytes_per_mb per microbatch. */
+ds_status ds_kv_create(ds_stage* stage, int64_t page_bytes, int64_t n_mb, int64_t local_bytes_per_mb,
+                       int64_t global_slot_bytes, int64_t host_bytes_per_mb);
+/* The request in (mb, slot) completed: free its pages (reference on_compute_end, sim.cpp:462-468). */
+ds_status ds_kv_release(ds_stage* stage, int32_t mb, int32_t slot);
+/* Bytes of KV pages the microbatch holds / holds outside its local pool. */
+ds_status ds_kv_usage(ds_stage* stage, int32_t mb, int64_t* total_bytes, int64_t* global_bytes);
+
+/* H2D prefetch of mb's global pages into global slot `slot` after evicting the occupant (D2H),
+ * on the stage's copy streams (reference issue_swap_in, sim.cpp:328-353). plan_bytes is the
+ * reference's integer contract (logged); the copy moves whole pages. moved_in/out may be NULL. */
+ds_status ds_swap_in(ds_stage* stage, int32_t mb, int32_t slot, int64_t plan_bytes,
+                     int64_t* moved_in, int64_t* moved_out);
+
+/* One stage step of microbatch mb over `rows`. act_in: first stage = device int32 ids sampled by
+ * the previous circuit of this mb (NULL on its first circuit); other stages = device bf16
+ * [T, d_model]. act_out: last stage = device int32 ids [R] (R = rows with need_logits); other
+ * stages = device bf16 [T, d_model]. NULL act_out keeps the result in the stage buffer
+ * (ds_stage_output). The step is stream-ordered; ds_stage_sync waits for it. */
+ds_status ds_stage_step(ds_stage* stage, int32_t mb, const ds_row* rows, int64_t n_rows,
+                        const void* act_in, void* act_out);
+ds_status ds_stage_output(ds_stage* stage, void** ptr, int64_t* bytes, int64_t* n_out);
+ds_status ds_stage_sync(ds_stage* stage);
+ds_status ds_stage_stream(ds_stage* stage, void** cuda_stream);
+/* Teacher forcing / debugging: read the fp32 logits of the last step (R x vocab) to host. */
+ds_status ds_stage_logits(ds_stage* stage, float* host_out, int64_t max_floats, int64_t* n_floats);
+
+/* ------------------------------------------------------------------------------------------
+ * Kernel-level entry points (parity tests call these through the same library).
+ * ------------------------------------------------------------------------------------------ */
+ds_status ds_dbg_gemm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t N, int32_t K,
+                      int32_t epi, const uint16_t* resid, int32_t k_splits, void* out);
+ds_status ds_dbg_has_device(int32_t* n_devices);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DESERVE_B200_H */

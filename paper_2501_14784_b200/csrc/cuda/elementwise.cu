@@ -1,0 +1,271 @@
+// HBM-bound stage-forward kernels: weight init, embedding gather, RMSNorm, RoPE + paged KV
+// append, SiLU*mul, greedy argmax and the token plumbing between circuits. All vectorised
+// 16-byte accesses; grids sized in multiples of the SM count where the row count allows.
+// Numerics follow oracle/llama_ref.c exactly (bf16 storage, fp32 math, same rounding points).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ds {
+
+// ------------------------------------------------------------ weights ----
+DS_DEVICE uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+__global__ void init_weights_kernel(__nv_bfloat16* dst, uint64_t seed, uint64_t tensor_id,
+                                    int64_t rows, int64_t cols, float scale, int part) {
+    const int64_t n = rows * cols;
+    const uint64_t base = seed + tensor_id * 0x9E3779B97F4A7C15ULL;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t h = mix64(base + uint64_t(i) * 0xD1B54A32D192ED03ULL);
+        const float u = float(h >> 40) * (1.0f / 16777216.0f);
+        const float v = __fmul_rn(__fsub_rn(__fmul_rn(2.0f, u), 1.0f), scale);
+        int64_t o = i;
+        if (part >= 0) {
+            const int64_t r = i / cols, c = i % cols;
+            o = ((r / 64) * 128 + part * 64 + (r % 64)) * cols + c;
+        }
+        dst[o] = f2bf(v);
+    }
+}
+
+void init_weights(__nv_bfloat16* dst, uint64_t seed, uint64_t tensor_id, int64_t rows, int64_t cols,
+                  float scale, int interleave_part, cudaStream_t stream) {
+    init_weights_kernel<<<kNumSMs * 16, 256, 0, stream>>>(dst, seed, tensor_id, rows, cols, scale,
+                                                          interleave_part);
+}
+
+__global__ void fill_bf16_kernel(__nv_bfloat16* dst, int64_t n, float v) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        dst[i] = f2bf(v);
+}
+void fill_bf16(__nv_bfloat16* dst, int64_t n, float v, cudaStream_t stream) {
+    fill_bf16_kernel<<<kNumSMs, 256, 0, stream>>>(dst, n, v);
+}
+
+// ---------------------------------------------------------- embedding ----
+__global__ void embed_kernel(const __nv_bfloat16* __restrict__ emb, const int32_t* __restrict__ tok,
+                             int d, __nv_bfloat16* __restrict__ x) {
+    const int t = blockIdx.x;
+    const uint4* src = reinterpret_cast<const uint4*>(emb + size_t(tok[t]) * d);
+    uint4* dst = reinterpret_cast<uint4*>(x + size_t(t) * d);
+    for (int i = threadIdx.x; i < d / 8; i += blockDim.x) dst[i] = src[i];
+}
+void embed_rows(const __nv_bfloat16* emb, const int32_t* tokens, int T, int d, __nv_bfloat16* x,
+                cudaStream_t stream) {
+    if (T > 0) embed_kernel<<<T, 128, 0, stream>>>(emb, tokens, d, x);
+}
+
+// ------------------------------------------------------------ RMSNorm ----
+// One CTA per row; d/8 16-byte vectors, at most 8 per thread kept in registers.
+template <int VPT>
+__global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ rows,
+                               int d, const __nv_bfloat16* __restrict__ g, float eps,
+                               __nv_bfloat16* __restrict__ y) {
+    const int i = blockIdx.x;
+    const int src_row = rows ? rows[i] : i;
+    const uint4* xr = reinterpret_cast<const uint4*>(x + size_t(src_row) * d);
+    const int nv = d / 8;
+    float v[VPT][8];
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        const int idx = threadIdx.x + k * blockDim.x;
+        if (idx < nv) {
+            unpack8(xr[idx], v[k]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ss += v[k][j] * v[k][j];
+        }
+    }
+    __shared__ float red[32];
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+        t = warp_sum(t);
+        if (threadIdx.x == 0) red[0] = t;
+    }
+    __syncthreads();
+    const float r = 1.0f / sqrtf(red[0] / float(d) + eps);
+    const uint4* gr = reinterpret_cast<const uint4*>(g);
+    uint4* yr = reinterpret_cast<uint4*>(y + size_t(i) * d);
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        const int idx = threadIdx.x + k * blockDim.x;
+        if (idx < nv) {
+            float gv[8], o[8];
+            unpack8(gr[idx], gv);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o[j] = gv[j] * round_bf(v[k][j] * r);
+            yr[idx] = pack8(o);
+        }
+    }
+}
+
+void rmsnorm_rows(const __nv_bfloat16* x, const int32_t* rows, int n_rows, int d,
+                  const __nv_bfloat16* g, float eps, __nv_bfloat16* y, cudaStream_t stream) {
+    if (n_rows <= 0) return;
+    const int nv = d / 8;
+    if (nv <= 128)
+        rmsnorm_kernel<1><<<n_rows, 128, 0, stream>>>(x, rows, d, g, eps, y);
+    else if (nv <= 512)
+        rmsnorm_kernel<4><<<n_rows, 128, 0, stream>>>(x, rows, d, g, eps, y);
+    else
+        rmsnorm_kernel<8><<<n_rows, 128, 0, stream>>>(x, rows, d, g, eps, y);
+}
+
+// ------------------------------------------------- RoPE + KV append ----
+__global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int n_h, int n_kv, int dh,
+                               const int32_t* __restrict__ row_pos,
+                               const int32_t* __restrict__ row_page, const float* __restrict__ rc,
+                               const float* __restrict__ rs, KvLayout kv, int layer,
+                               __nv_bfloat16* __restrict__ q_out) {
+    const int t = blockIdx.x;
+    const int pos = row_pos[t];
+    const int half = dh / 2;
+    const int width = (n_h + 2 * n_kv) * dh;
+    const __nv_bfloat16* src = qkv + size_t(t) * width;
+    const float* c = rc + size_t(pos) * half;
+    const float* s = rs + size_t(pos) * half;
+    const size_t page_base = size_t(row_page[t]) * kv.page_elems;
+    const int slot = pos & 255;
+    // rotated q and k: (head, i) pairs
+    const int n_rot = (n_h + n_kv) * half;
+    for (int w = threadIdx.x; w < n_rot; w += blockDim.x) {
+        const int head = w / half, i = w % half;
+        const float x1 = bf2f(src[head * dh + i]);
+        const float x2 = bf2f(src[head * dh + i + half]);
+        // explicit _rn ops: no FMA contraction, bit-identical to the CPU oracle
+        const float o1 = __fsub_rn(__fmul_rn(x1, c[i]), __fmul_rn(x2, s[i]));
+        const float o2 = __fadd_rn(__fmul_rn(x2, c[i]), __fmul_rn(x1, s[i]));
+        if (head < n_h) {
+            __nv_bfloat16* dq = q_out + size_t(t) * n_h * dh + head * dh;
+            dq[i] = f2bf(o1);
+            dq[i + half] = f2bf(o2);
+        } else {
+            const int kh = head - n_h;
+            __nv_bfloat16* dk = kv.pool + page_base +
+                                ((size_t(layer) * 2 + 0) * n_kv + kh) * 256 * dh + size_t(slot) * dh;
+            dk[i] = f2bf(o1);
+            dk[i + half] = f2bf(o2);
+        }
+    }
+    // v: plain copy, 16 B per thread-iteration
+    const int nv = n_kv * dh / 8;
+    for (int w = threadIdx.x; w < nv; w += blockDim.x) {
+        const int kh = (w * 8) / dh, i = (w * 8) % dh;
+        const uint4 val = *reinterpret_cast<const uint4*>(src + (n_h + n_kv) * dh + kh * dh + i);
+        __nv_bfloat16* dv = kv.pool + page_base + ((size_t(layer) * 2 + 1) * n_kv + kh) * 256 * dh +
+                            size_t(slot) * dh + i;
+        *reinterpret_cast<uint4*>(dv) = val;
+    }
+}
+
+void rope_kv_append(const __nv_bfloat16* qkv, int T, int n_h, int n_kv, int d_head,
+                    const int32_t* row_pos, const int32_t* row_page, const float* rope_cos,
+                    const float* rope_sin, const KvLayout& kv, int layer, __nv_bfloat16* q_out,
+                    cudaStream_t stream) {
+    if (T > 0)
+        rope_kv_kernel<<<T, 256, 0, stream>>>(qkv, n_h, n_kv, d_head, row_pos, row_page, rope_cos,
+                                              rope_sin, kv, layer, q_out);
+}
+
+// ----------------------------------------------------------- SiLU*mul ----
+__global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, int T, int ffn,
+                                __nv_bfloat16* __restrict__ h) {
+    const size_t total = size_t(T) * ffn / 8;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const size_t e = i * 8;
+        const size_t t = e / ffn;
+        const int f = int(e % ffn);
+        const __nv_bfloat16* row = gu + t * size_t(2 * ffn);
+        const int gcol = (f / 64) * 128 + (f % 64);
+        float g[8], u[8], o[8];
+        unpack8(*reinterpret_cast<const uint4*>(row + gcol), g);
+        unpack8(*reinterpret_cast<const uint4*>(row + gcol + 64), u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float sg = round_bf(g[j] / (1.0f + expf(-g[j])));
+            o[j] = sg * u[j];
+        }
+        *reinterpret_cast<uint4*>(h + e) = pack8(o);
+    }
+}
+void silu_mul(const __nv_bfloat16* gu, int T, int ffn, __nv_bfloat16* h, cudaStream_t stream) {
+    if (T <= 0) return;
+    const size_t total = size_t(T) * ffn / 8;
+    int blocks = int((total + 255) / 256);
+    if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+    silu_mul_kernel<<<blocks, 256, 0, stream>>>(gu, T, ffn, h);
+}
+
+// ------------------------------------------------------------- argmax ----
+__global__ void argmax_kernel(const float* __restrict__ logits, int V, int32_t* __restrict__ ids) {
+    const float* row = logits + size_t(blockIdx.x) * V;
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    const int nv = V / 4;
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+        const float4 v = reinterpret_cast<const float4*>(row)[i];
+        if (v.x > best) { best = v.x; bi = 4 * i; }
+        if (v.y > best) { best = v.y; bi = 4 * i + 1; }
+        if (v.z > best) { best = v.z; bi = 4 * i + 2; }
+        if (v.w > best) { best = v.w; bi = 4 * i + 3; }
+    }
+    for (int i = nv * 4 + threadIdx.x; i < V; i += blockDim.x)
+        if (row[i] > best) { best = row[i]; bi = i; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    __shared__ float sb[32];
+    __shared__ int si[32];
+    if ((threadIdx.x & 31) == 0) { sb[threadIdx.x >> 5] = best; si[threadIdx.x >> 5] = bi; }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int nw = blockDim.x >> 5;
+        best = threadIdx.x < nw ? sb[threadIdx.x] : -INFINITY;
+        bi = threadIdx.x < nw ? si[threadIdx.x] : 0x7fffffff;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (threadIdx.x == 0) ids[blockIdx.x] = bi;
+    }
+}
+void argmax_rows(const float* logits, int R, int V, int32_t* ids, cudaStream_t stream) {
+    if (R > 0) argmax_kernel<<<R, 512, 0, stream>>>(logits, V, ids);
+}
+
+__global__ void scatter_tokens_kernel(const int32_t* ids, const int32_t* req, int R, int32_t* last) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < R) last[req[i]] = ids[i];
+}
+void scatter_tokens(const int32_t* ids, const int32_t* req, int R, int32_t* last_token,
+                    cudaStream_t stream) {
+    if (R > 0) scatter_tokens_kernel<<<(R + 255) / 256, 256, 0, stream>>>(ids, req, R, last_token);
+}
+
+__global__ void resolve_tokens_kernel(const int32_t* prompt_tok, const int32_t* row_req,
+                                      const int32_t* last, int T, int32_t* tokens) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < T) tokens[i] = prompt_tok[i] >= 0 ? prompt_tok[i] : last[row_req[i]];
+}
+void resolve_tokens(const int32_t* prompt_tok, const int32_t* row_req, const int32_t* last_token,
+                    int T, int32_t* tokens, cudaStream_t stream) {
+    if (T > 0)
+        resolve_tokens_kernel<<<(T + 255) / 256, 256, 0, stream>>>(prompt_tok, row_req, last_token,
+                                                                    T, tokens);
+}
+
+}  // namespace ds

@@ -1,0 +1,80 @@
+// Launchers for the sm_100a stage-forward kernels (host-callable, stream-ordered).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace ds {
+
+enum GemmEpilogue : int {
+    EPI_BF16 = 0,     // out = bf16(acc)
+    EPI_RESID = 1,    // out = bf16(resid + bf16(acc))   (residual add fused; out may alias resid)
+    EPI_F32 = 2,      // out = acc (fp32, logits)
+    EPI_PARTIAL = 3,  // internal: split-K fp32 partial
+};
+
+// A weight matrix [N, K] (row-major, K contiguous) with its TMA descriptor.
+struct GemmWeight {
+    const __nv_bfloat16* data = nullptr;
+    int N = 0, K = 0;
+    alignas(64) unsigned char tmap[128];
+};
+
+int gemm_weight_init(GemmWeight* w, const __nv_bfloat16* data, int N, int K);
+int gemm_pick_splits(int T, int N, int K);
+size_t gemm_workspace_floats(int T, int N, int k_splits);
+// out[T, N] = epi(X[T, K] . W[N, K]^T). k_splits <= 0 picks automatically.
+int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_bfloat16* out_bf16,
+              const __nv_bfloat16* resid, float* out_f32, float* workspace, size_t workspace_floats,
+              int k_splits, cudaStream_t stream);
+
+// Counter-based weight init (bf16(uniform(-1,1) * scale)); see oracle/llama_ref.c ds_ref_weight.
+// If interleave64 != 0 the [rows, cols] tensor is written into the gate/up interleaved
+// layout: canonical row r of tensor `part` (0 gate, 1 up) lands at row 128*(r/64) + 64*part + r%64.
+void init_weights(__nv_bfloat16* dst, uint64_t seed, uint64_t tensor_id, int64_t rows, int64_t cols,
+                  float scale, int interleave_part, cudaStream_t stream);
+void fill_bf16(__nv_bfloat16* dst, int64_t n, float v, cudaStream_t stream);
+
+// x[t] = E[token[t]]; tokens come from prompt ids or from last_token[req] for decode rows.
+void embed_rows(const __nv_bfloat16* emb, const int32_t* tokens, int T, int d, __nv_bfloat16* x,
+                cudaStream_t stream);
+// y[i] = bf16(g * bf16(x[row_i] * rsqrt(mean(x^2) + eps))); rows = index list or identity.
+void rmsnorm_rows(const __nv_bfloat16* x, const int32_t* rows, int n_rows, int d,
+                  const __nv_bfloat16* g, float eps, __nv_bfloat16* y, cudaStream_t stream);
+
+struct KvLayout {
+    __nv_bfloat16* pool = nullptr;  // [n_pages][L_stage][2][n_kv][256][d_head]
+    int64_t page_elems = 0;
+    int n_layers = 0, n_kv = 0, d_head = 0;
+};
+
+// Rotary embedding on q and k (rotate-half, table [max_pos][d_head/2] cos / sin) and
+// the paged KV append of k, v for every row at row_pos[t] into page row_page[t].
+void rope_kv_append(const __nv_bfloat16* qkv, int T, int n_h, int n_kv, int d_head,
+                    const int32_t* row_pos, const int32_t* row_page, const float* rope_cos,
+                    const float* rope_sin, const KvLayout& kv, int layer, __nv_bfloat16* q_out,
+                    cudaStream_t stream);
+
+// Paged causal attention: row t attends positions [0, row_pos[t]] of its request, whose pages
+// are flat_pages[row_page_off[t] ...]. Output o[T, n_h * d_head] bf16.
+size_t attention_workspace_floats(int T, int n_h, int d_head, int splits);
+int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,
+                    const int32_t* row_page_off, const int32_t* flat_pages, const KvLayout& kv,
+                    int layer, int max_ctx, __nv_bfloat16* o, float* ws, size_t ws_floats,
+                    cudaStream_t stream);
+
+// h[t, f] = bf16(bf16(silu(g)) * u) from the gate/up interleaved GEMM output [T, 2*ffn].
+void silu_mul(const __nv_bfloat16* gu, int T, int ffn, __nv_bfloat16* h, cudaStream_t stream);
+
+// ids[r] = argmax_v logits[r, v] (lowest index wins ties).
+void argmax_rows(const float* logits, int R, int V, int32_t* ids, cudaStream_t stream);
+// last_token[req[r]] = ids[r]
+void scatter_tokens(const int32_t* ids, const int32_t* req, int R, int32_t* last_token,
+                    cudaStream_t stream);
+// tokens[t] = prompt_tok[t] >= 0 ? prompt_tok[t] : last_token[row_req[t]]
+void resolve_tokens(const int32_t* prompt_tok, const int32_t* row_req, const int32_t* last_token,
+                    int T, int32_t* tokens, cudaStream_t stream);
+
+}  // namespace ds

@@ -1,0 +1,721 @@
+// ds_stage: one pipeline stage on one B200 — weights, paged KV pools with pinned host backing,
+// copy streams and the per-step forward (the compute slot of reference Engine::on_compute_start,
+// src/sim.cpp:409-428). C ABI in include/deserve.h.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../host/capi_util.hpp"
+#include "common.cuh"
+#include "kernels.h"
+#include "deserve.h"
+
+using ds::GemmWeight;
+using ds::KvLayout;
+using bf16 = __nv_bfloat16;
+
+#define CK(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess) {                                                            \
+            return ds_fail(DS_ERR_RUNTIME, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+        }                                                                                   \
+    } while (0)
+
+namespace {
+
+struct LayerW {
+    bf16* attn_norm = nullptr;
+    bf16* mlp_norm = nullptr;
+    GemmWeight wqkv, wo, wgu, wd;
+};
+
+struct MbKv {
+    std::vector<int32_t> local_free;
+    std::vector<std::vector<int32_t>> pages;  // per slot: >=0 device page, <0 host page -(h+1)
+    std::vector<int64_t> slot_req;
+    std::vector<int32_t> host_free;
+    std::vector<int32_t> host_dev;  // host page -> device page while resident, -1 otherwise
+    int resident_slot = -1;
+    cudaEvent_t last_compute = nullptr;
+    bool computed = false;
+    // previous circuit's sampled rows (first+last stage loopback)
+    std::vector<int32_t> prev_logit_slots;
+};
+
+struct GlobalSlot {
+    int owner = -1;
+    std::vector<int32_t> dev_pages;
+    std::vector<int32_t> free;
+};
+
+}  // namespace
+
+struct ds_stage {
+    int device = 0;
+    ds_model_desc m{};
+    int lb = 0, le = 0, L = 0;
+    bool first = false, last = false;
+    uint64_t seed = 0;
+    int max_rows = 0, max_slots = 0;
+    cudaStream_t stream = nullptr, h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_h2d = nullptr, ev_d2h = nullptr;
+
+    bf16* wbuf = nullptr;
+    std::vector<LayerW> layers;
+    bf16* emb = nullptr;
+    bf16* final_norm = nullptr;
+    GemmWeight lm_head;
+    float* rope_cos = nullptr;
+    float* rope_sin = nullptr;
+
+    bf16 *x = nullptr, *xn = nullptr, *qkv = nullptr, *q = nullptr, *attn = nullptr, *gu = nullptr,
+         *h = nullptr;
+    float* logits = nullptr;
+    int32_t* ids = nullptr;
+    float* ws = nullptr;
+    size_t ws_floats = 0;
+    float* attn_ws = nullptr;
+    size_t attn_ws_floats = 0;
+
+    // step metadata: pinned host staging (double-buffered) + device copy
+    int32_t* h_meta[2] = {nullptr, nullptr};
+    cudaEvent_t meta_ev[2] = {nullptr, nullptr};
+    int meta_buf = 0;
+    int32_t* d_meta = nullptr;
+    size_t meta_cap = 0;  // int32 elements
+
+    // KV
+    KvLayout kv;
+    int64_t page_bytes = 0;
+    int n_mb = 0;
+    int local_pages = 0, slot_pages = 0, host_pages = 0;
+    std::vector<MbKv> mbs;
+    GlobalSlot gslot[2];
+    uint8_t* host_backing = nullptr;  // pinned [n_mb][host_pages][page_bytes]
+    int32_t* last_token = nullptr;    // [n_mb * max_slots]
+    int32_t* pending_ids = nullptr;   // [n_mb * max_rows] (single-stage loopback)
+
+    // last step
+    int last_T = 0, last_R = 0;
+    int64_t moved_in_total = 0, moved_out_total = 0;
+};
+
+namespace {
+
+int64_t page_count_for(int32_t pos_end) { return (int64_t(pos_end) + 255) / 256; }
+
+ds_status alloc_dev(void** p, size_t bytes) {
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess)
+        return ds_fail(DS_ERR_PLAN, "device allocation of " + std::to_string(bytes) +
+                                        " bytes failed: " + cudaGetErrorString(e));
+    return DS_OK;
+}
+
+uint8_t* host_page_ptr(ds_stage* s, int mb, int h) {
+    return s->host_backing + (size_t(mb) * s->host_pages + h) * size_t(s->page_bytes);
+}
+bf16* dev_page_ptr(ds_stage* s, int p) { return s->kv.pool + size_t(p) * s->kv.page_elems; }
+
+}  // namespace
+
+extern "C" {
+
+ds_status ds_dbg_has_device(int32_t* n) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) c = 0;
+    if (n) *n = c;
+    return DS_OK;
+}
+
+ds_status ds_stage_create(int32_t device, const ds_model_desc* md, int64_t layer_begin,
+                          int64_t layer_end, int32_t is_first, int32_t is_last, uint64_t weight_seed,
+                          int32_t max_rows, int32_t max_slots, ds_stage** out) {
+    if (!md || !out) return ds_fail(DS_ERR_ARG, "null argument");
+    if (layer_begin < 0 || layer_end <= layer_begin || layer_end > md->n_layers)
+        return ds_fail(DS_ERR_ARG, "bad layer range");
+    if (md->d_model % 128 || md->ffn % 64 || (md->n_heads * md->d_head) % 64 ||
+        md->vocab % 128 || (md->d_head != 64 && md->d_head != 128) ||
+        md->n_heads % md->n_kv_heads || md->n_heads / md->n_kv_heads > 8)
+        return ds_fail(DS_ERR_ARG, "unsupported model dimensions");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return ds_fail(DS_ERR_NO_DEVICE, "no CUDA device: the B200 stage path has no CPU fallback");
+    if (device < 0 || device >= ndev) return ds_fail(DS_ERR_ARG, "bad device index");
+    CK(cudaSetDevice(device));
+
+    ds_stage* s = new ds_stage();
+    *out = nullptr;
+    s->device = device;
+    s->m = *md;
+    s->lb = int(layer_begin);
+    s->le = int(layer_end);
+    s->L = s->le - s->lb;
+    s->first = is_first != 0;
+    s->last = is_last != 0;
+    s->seed = weight_seed;
+    s->max_rows = max_rows;
+    s->max_slots = max_slots;
+    const ds_model_desc& m = s->m;
+    const int d = m.d_model, qdim = m.n_heads * m.d_head, kvdim = m.n_kv_heads * m.d_head;
+    const int qkv_rows = qdim + 2 * kvdim;
+
+    CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s->h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s->d2h, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&s->ev_h2d, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&s->ev_d2h, cudaEventDisableTiming));
+
+    // ---- weights: one allocation, layer-major
+    const size_t per_layer = size_t(qkv_rows) * d + size_t(d) * qdim + size_t(2) * m.ffn * d +
+                             size_t(d) * m.ffn + 2 * size_t(d);
+    size_t total = per_layer * s->L;
+    if (s->first) total += size_t(m.vocab) * d;
+    if (s->last) total += size_t(m.vocab) * d + d;
+    ds_status st = alloc_dev(reinterpret_cast<void**>(&s->wbuf), total * sizeof(bf16));
+    if (st) { delete s; return st; }
+    bf16* cur = s->wbuf;
+    auto take = [&](size_t n) { bf16* p = cur; cur += n; return p; };
+    const float s_d = float(std::sqrt(3.0 / d));
+    const float s_q = float(std::sqrt(3.0 / qdim));
+    const float s_f = float(std::sqrt(3.0 / m.ffn));
+    s->layers.resize(s->L);
+    for (int i = 0; i < s->L; ++i) {
+        const uint64_t base = uint64_t(s->lb + i) * 16;
+        LayerW& lw = s->layers[i];
+        lw.attn_norm = take(d);
+        lw.mlp_norm = take(d);
+        ds::fill_bf16(lw.attn_norm, d, 1.0f, s->stream);
+        ds::fill_bf16(lw.mlp_norm, d, 1.0f, s->stream);
+        bf16* wqkv = take(size_t(qkv_rows) * d);
+        ds::init_weights(wqkv, weight_seed, base + 1, qdim, d, s_d, -1, s->stream);
+        ds::init_weights(wqkv + size_t(qdim) * d, weight_seed, base + 2, kvdim, d, s_d, -1, s->stream);
+        ds::init_weights(wqkv + size_t(qdim + kvdim) * d, weight_seed, base + 3, kvdim, d, s_d, -1,
+                         s->stream);
+        bf16* wo = take(size_t(d) * qdim);
+        ds::init_weights(wo, weight_seed, base + 4, d, qdim, s_q, -1, s->stream);
+        bf16* wgu = take(size_t(2) * m.ffn * d);
+        ds::init_weights(wgu, weight_seed, base + 6, m.ffn, d, s_d, 0, s->stream);
+        ds::init_weights(wgu, weight_seed, base + 7, m.ffn, d, s_d, 1, s->stream);
+        bf16* wd = take(size_t(d) * m.ffn);
+        ds::init_weights(wd, weight_seed, base + 8, d, m.ffn, s_f, -1, s->stream);
+        if (ds::gemm_weight_init(&lw.wqkv, wqkv, qkv_rows, d) ||
+            ds::gemm_weight_init(&lw.wo, wo, d, qdim) ||
+            ds::gemm_weight_init(&lw.wgu, wgu, 2 * m.ffn, d) ||
+            ds::gemm_weight_init(&lw.wd, wd, d, m.ffn)) {
+            delete s;
+            return ds_fail(DS_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for a weight");
+        }
+    }
+    if (s->first) {
+        s->emb = take(size_t(m.vocab) * d);
+        ds::init_weights(s->emb, weight_seed, uint64_t(1) << 20, m.vocab, d, 1.0f, -1, s->stream);
+    }
+    if (s->last) {
+        s->final_norm = take(d);
+        ds::fill_bf16(s->final_norm, d, 1.0f, s->stream);
+        bf16* lm = take(size_t(m.vocab) * d);
+        ds::init_weights(lm, weight_seed, (uint64_t(1) << 20) + 1, m.vocab, d, s_d, -1, s->stream);
+        if (ds::gemm_weight_init(&s->lm_head, lm, m.vocab, d)) {
+            delete s;
+            return ds_fail(DS_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for lm_head");
+        }
+    }
+
+    // ---- RoPE table (host double precision, identical to the oracle's)
+    {
+        const int half = m.d_head / 2;
+        std::vector<float> c(size_t(m.max_seq_len) * half), sn(size_t(m.max_seq_len) * half);
+        for (int p = 0; p < m.max_seq_len; ++p)
+            for (int i = 0; i < half; ++i) {
+                const double inv = std::pow(double(m.rope_theta), -2.0 * i / m.d_head);
+                const double a = double(p) * inv;
+                c[size_t(p) * half + i] = float(std::cos(a));
+                sn[size_t(p) * half + i] = float(std::sin(a));
+            }
+        if ((st = alloc_dev(reinterpret_cast<void**>(&s->rope_cos), c.size() * 4))) { delete s; return st; }
+        if ((st = alloc_dev(reinterpret_cast<void**>(&s->rope_sin), c.size() * 4))) { delete s; return st; }
+        CK(cudaMemcpy(s->rope_cos, c.data(), c.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(s->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
+    }
+
+    // ---- scratch
+    const size_t R = size_t(max_rows);
+    auto A = [&](void** p, size_t bytes) { return alloc_dev(p, bytes); };
+    if ((st = A((void**)&s->x, R * d * 2)) || (st = A((void**)&s->xn, R * d * 2)) ||
+        (st = A((void**)&s->qkv, R * qkv_rows * 2)) || (st = A((void**)&s->q, R * qdim * 2)) ||
+        (st = A((void**)&s->attn, R * qdim * 2)) || (st = A((void**)&s->gu, R * 2 * m.ffn * 2)) ||
+        (st = A((void**)&s->h, R * m.ffn * 2)) || (st = A((void**)&s->ids, R * 4))) {
+        delete s;
+        return st;
+    }
+    if (s->last && (st = A((void**)&s->logits, R * size_t(m.vocab) * 4))) { delete s; return st; }
+    {
+        size_t wsf = 0;
+        const int shapes[4][2] = {{qkv_rows, d}, {d, qdim}, {2 * m.ffn, d}, {d, m.ffn}};
+        for (int T = 1; T <= max_rows; T = (T < 64 ? T + 1 : T + 16))
+            for (auto& sh : shapes) {
+                const int ks = ds::gemm_pick_splits(T, sh[0], sh[1]);
+                if (ks > 1) wsf = std::max(wsf, ds::gemm_workspace_floats(T, sh[0], ks));
+            }
+        s->ws_floats = wsf;
+        if (wsf && (st = A((void**)&s->ws, wsf * 4))) { delete s; return st; }
+        s->attn_ws_floats = (R + 320) * m.n_heads * size_t(m.d_head + 2);
+        if ((st = A((void**)&s->attn_ws, s->attn_ws_floats * 4))) { delete s; return st; }
+    }
+    s->meta_cap = 16 * R + size_t(max_slots) * 64 + R * size_t((m.max_seq_len + 255) / 256) + 64;
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaMallocHost(&s->h_meta[i], s->meta_cap * 4));
+        CK(cudaEventCreateWithFlags(&s->meta_ev[i], cudaEventDisableTiming));
+    }
+    if ((st = A((void**)&s->d_meta, s->meta_cap * 4))) { delete s; return st; }
+    CK(cudaStreamSynchronize(s->stream));
+    *out = s;
+    return DS_OK;
+}
+
+ds_status ds_stage_destroy(ds_stage* s) {
+    if (!s) return DS_OK;
+    cudaSetDevice(s->device);
+    cudaDeviceSynchronize();
+    for (void* p : {(void*)s->wbuf, (void*)s->rope_cos, (void*)s->rope_sin, (void*)s->x, (void*)s->xn,
+                    (void*)s->qkv, (void*)s->q, (void*)s->attn, (void*)s->gu, (void*)s->h,
+                    (void*)s->logits, (void*)s->ids, (void*)s->ws, (void*)s->attn_ws,
+                    (void*)s->d_meta, (void*)s->kv.pool, (void*)s->last_token,
+                    (void*)s->pending_ids})
+        if (p) cudaFree(p);
+    for (int i = 0; i < 2; ++i) {
+        if (s->h_meta[i]) cudaFreeHost(s->h_meta[i]);
+        if (s->meta_ev[i]) cudaEventDestroy(s->meta_ev[i]);
+    }
+    if (s->host_backing) cudaFreeHost(s->host_backing);
+    for (auto& mb : s->mbs)
+        if (mb.last_compute) cudaEventDestroy(mb.last_compute);
+    if (s->ev_h2d) cudaEventDestroy(s->ev_h2d);
+    if (s->ev_d2h) cudaEventDestroy(s->ev_d2h);
+    if (s->stream) cudaStreamDestroy(s->stream);
+    if (s->h2d) cudaStreamDestroy(s->h2d);
+    if (s->d2h) cudaStreamDestroy(s->d2h);
+    delete s;
+    return DS_OK;
+}
+
+ds_status ds_kv_create(ds_stage* s, int64_t page_bytes, int64_t n_mb, int64_t local_bytes_per_mb,
+                       int64_t global_slot_bytes, int64_t host_bytes_per_mb) {
+    if (!s) return ds_fail(DS_ERR_ARG, "null stage");
+    const ds_model_desc& m = s->m;
+    const int64_t want = int64_t(256) * s->L * 2 * m.n_kv_heads * m.d_head * 2;
+    if (page_bytes != want)
+        return ds_fail(DS_ERR_ARG, "page_bytes " + std::to_string(page_bytes) +
+                                       " != 256 * L_stage * 2 * n_kv * d_head * 2 = " +
+                                       std::to_string(want));
+    if (n_mb < 1 || local_bytes_per_mb < 0 || global_slot_bytes < 0 || host_bytes_per_mb < 0)
+        return ds_fail(DS_ERR_ARG, "bad KV sizes");
+    CK(cudaSetDevice(s->device));
+    s->page_bytes = page_bytes;
+    s->n_mb = int(n_mb);
+    s->local_pages = int(local_bytes_per_mb / page_bytes);
+    s->slot_pages = int(global_slot_bytes / page_bytes);
+    s->host_pages = int(host_bytes_per_mb / page_bytes);
+    const int64_t dev_pages = int64_t(s->n_mb) * s->local_pages + 2 * int64_t(s->slot_pages);
+    s->kv.page_elems = page_bytes / 2;
+    s->kv.n_layers = s->L;
+    s->kv.n_kv = m.n_kv_heads;
+    s->kv.d_head = m.d_head;
+    ds_status st = alloc_dev(reinterpret_cast<void**>(&s->kv.pool), size_t(dev_pages) * page_bytes);
+    if (st) return st;
+    if (s->host_pages > 0) {
+        cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&s->host_backing),
+                                       size_t(s->n_mb) * s->host_pages * page_bytes);
+        if (e != cudaSuccess) return ds_fail(DS_ERR_PLAN, "pinned host KV backing allocation failed");
+    }
+    if ((st = alloc_dev(reinterpret_cast<void**>(&s->last_token), size_t(n_mb) * s->max_slots * 4)))
+        return st;
+    CK(cudaMemset(s->last_token, 0, size_t(n_mb) * s->max_slots * 4));
+    if ((st = alloc_dev(reinterpret_cast<void**>(&s->pending_ids), size_t(n_mb) * s->max_rows * 4)))
+        return st;
+    s->mbs.assign(s->n_mb, MbKv());
+    for (int b = 0; b < s->n_mb; ++b) {
+        MbKv& k = s->mbs[b];
+        for (int p = s->local_pages - 1; p >= 0; --p) k.local_free.push_back(b * s->local_pages + p);
+        k.pages.assign(s->max_slots, {});
+        k.slot_req.assign(s->max_slots, -1);
+        for (int h = s->host_pages - 1; h >= 0; --h) k.host_free.push_back(h);
+        k.host_dev.assign(s->host_pages, -1);
+        CK(cudaEventCreateWithFlags(&k.last_compute, cudaEventDisableTiming));
+    }
+    const int base = s->n_mb * s->local_pages;
+    for (int g = 0; g < 2; ++g) {
+        s->gslot[g].dev_pages.clear();
+        s->gslot[g].free.clear();
+        for (int p = 0; p < s->slot_pages; ++p) s->gslot[g].dev_pages.push_back(base + g * s->slot_pages + p);
+        for (int p = s->slot_pages - 1; p >= 0; --p) s->gslot[g].free.push_back(base + g * s->slot_pages + p);
+    }
+    return DS_OK;
+}
+
+static void release_slot(ds_stage* s, MbKv& k, int slot) {
+    for (int32_t hnd : k.pages[slot]) {
+        if (hnd >= 0) {
+            k.local_free.push_back(hnd);
+        } else {
+            const int h = -hnd - 1;
+            if (k.host_dev[h] >= 0 && k.resident_slot >= 0)
+                s->gslot[k.resident_slot].free.push_back(k.host_dev[h]);
+            k.host_dev[h] = -1;
+            k.host_free.push_back(h);
+        }
+    }
+    k.pages[slot].clear();
+    k.slot_req[slot] = -1;
+}
+
+ds_status ds_kv_release(ds_stage* s, int32_t mb, int32_t slot) {
+    if (!s || mb < 0 || mb >= s->n_mb || slot < 0 || slot >= s->max_slots)
+        return ds_fail(DS_ERR_ARG, "bad release");
+    release_slot(s, s->mbs[mb], slot);
+    return DS_OK;
+}
+
+ds_status ds_kv_usage(ds_stage* s, int32_t mb, int64_t* total, int64_t* global) {
+    if (!s || mb < 0 || mb >= s->n_mb) return ds_fail(DS_ERR_ARG, "bad mb");
+    int64_t t = 0, g = 0;
+    for (auto& v : s->mbs[mb].pages)
+        for (int32_t h : v) {
+            ++t;
+            if (h < 0) ++g;
+        }
+    if (total) *total = t * s->page_bytes;
+    if (global) *global = g * s->page_bytes;
+    return DS_OK;
+}
+
+ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, int64_t* moved_in,
+                     int64_t* moved_out) {
+    (void)plan_bytes;
+    if (!s || mb < 0 || mb >= s->n_mb || slot < 0 || slot > 1) return ds_fail(DS_ERR_ARG, "bad swap");
+    CK(cudaSetDevice(s->device));
+    int64_t in = 0, outb = 0;
+    MbKv& k = s->mbs[mb];
+    GlobalSlot& gs = s->gslot[slot];
+    // 1. evict the slot occupant (and mb itself if it sits in the other slot)
+    auto evict = [&](int owner, int g) -> ds_status {
+        MbKv& o = s->mbs[owner];
+        if (o.computed) CK(cudaStreamWaitEvent(s->d2h, o.last_compute, 0));
+        for (int h = 0; h < s->host_pages; ++h) {
+            if (o.host_dev[h] < 0) continue;
+            CK(cudaMemcpyAsync(host_page_ptr(s, owner, h), dev_page_ptr(s, o.host_dev[h]),
+                               s->page_bytes, cudaMemcpyDeviceToHost, s->d2h));
+            o.host_dev[h] = -1;
+            outb += s->page_bytes;
+        }
+        o.resident_slot = -1;
+        s->gslot[g].owner = -1;
+        s->gslot[g].free.clear();
+        for (int p = int(s->gslot[g].dev_pages.size()) - 1; p >= 0; --p)
+            s->gslot[g].free.push_back(s->gslot[g].dev_pages[p]);
+        return DS_OK;
+    };
+    ds_status st;
+    if (gs.owner >= 0 && gs.owner != mb && (st = evict(gs.owner, slot))) return st;
+    if (k.resident_slot >= 0 && k.resident_slot != slot && (st = evict(mb, k.resident_slot))) return st;
+    if (gs.owner != mb) {
+        gs.owner = -1;
+        gs.free.clear();
+        for (int p = int(gs.dev_pages.size()) - 1; p >= 0; --p) gs.free.push_back(gs.dev_pages[p]);
+    }
+    CK(cudaEventRecord(s->ev_d2h, s->d2h));
+    CK(cudaStreamWaitEvent(s->h2d, s->ev_d2h, 0));
+    if (k.computed) CK(cudaStreamWaitEvent(s->h2d, k.last_compute, 0));
+    // 2. bring mb's host pages in: migrate into free local pages first, then the slot
+    for (int sl = 0; sl < s->max_slots; ++sl)
+        for (int32_t& hnd : k.pages[sl]) {
+            if (hnd >= 0) continue;
+            const int h = -hnd - 1;
+            if (k.host_dev[h] >= 0) continue;  // already resident here
+            if (!k.local_free.empty()) {
+                const int p = k.local_free.back();
+                k.local_free.pop_back();
+                CK(cudaMemcpyAsync(dev_page_ptr(s, p), host_page_ptr(s, mb, h), s->page_bytes,
+                                   cudaMemcpyHostToDevice, s->h2d));
+                k.host_free.push_back(h);
+                hnd = p;
+            } else {
+                if (gs.free.empty()) return ds_fail(DS_ERR_RUNTIME, "global slot overflow");
+                const int p = gs.free.back();
+                gs.free.pop_back();
+                CK(cudaMemcpyAsync(dev_page_ptr(s, p), host_page_ptr(s, mb, h), s->page_bytes,
+                                   cudaMemcpyHostToDevice, s->h2d));
+                k.host_dev[h] = p;
+            }
+            in += s->page_bytes;
+        }
+    gs.owner = mb;
+    k.resident_slot = slot;
+    CK(cudaEventRecord(s->ev_h2d, s->h2d));
+    s->moved_in_total += in;
+    s->moved_out_total += outb;
+    if (moved_in) *moved_in = in;
+    if (moved_out) *moved_out = outb;
+    return DS_OK;
+}
+
+ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_rows,
+                        const void* act_in, void* act_out) {
+    if (!s || !rows || n_rows < 0) return ds_fail(DS_ERR_ARG, "null argument");
+    if (s->mbs.empty()) return ds_fail(DS_ERR_ARG, "ds_kv_create not called");
+    if (mb < 0 || mb >= s->n_mb) return ds_fail(DS_ERR_ARG, "bad microbatch index");
+    CK(cudaSetDevice(s->device));
+    const ds_model_desc& m = s->m;
+    MbKv& k = s->mbs[mb];
+
+    // ---- rows -> pages + metadata (host)
+    int T = 0, R = 0, P = 0, max_ctx = 1;
+    for (int64_t i = 0; i < n_rows; ++i) {
+        const ds_row& r = rows[i];
+        if (r.slot < 0 || r.slot >= s->max_slots || r.n_tok < 1 || r.pos < 0 ||
+            r.pos + r.n_tok > m.max_seq_len)
+            return ds_fail(DS_ERR_ARG, "bad row descriptor");
+        if (k.slot_req[r.slot] != r.req_id) {
+            if (k.slot_req[r.slot] != -1) release_slot(s, k, r.slot);
+            k.slot_req[r.slot] = r.req_id;
+        }
+        auto& pg = k.pages[r.slot];
+        const int64_t need = page_count_for(r.pos + r.n_tok);
+        while (int64_t(pg.size()) < need) {
+            if (!k.local_free.empty()) {
+                pg.push_back(k.local_free.back());
+                k.local_free.pop_back();
+            } else if (k.resident_slot >= 0 && !k.host_free.empty() &&
+                       !s->gslot[k.resident_slot].free.empty()) {
+                const int h = k.host_free.back();
+                k.host_free.pop_back();
+                const int p = s->gslot[k.resident_slot].free.back();
+                s->gslot[k.resident_slot].free.pop_back();
+                k.host_dev[h] = p;
+                pg.push_back(-(h + 1));
+            } else {
+                return ds_fail(DS_ERR_PLAN, "KV pool exhausted for microbatch " + std::to_string(mb));
+            }
+        }
+        T += r.n_tok;
+        if (r.need_logits) ++R;
+        P += int(need);
+        max_ctx = std::max(max_ctx, r.pos + r.n_tok);
+    }
+    if (T > s->max_rows) return ds_fail(DS_ERR_ARG, "circuit has more rows than max_rows");
+    // residency check (compute-requires-resident, reference replay_check sim.cpp:629-639)
+    for (int64_t i = 0; i < n_rows; ++i)
+        for (int32_t hnd : k.pages[rows[i].slot])
+            if (hnd < 0 && k.host_dev[-hnd - 1] < 0)
+                return ds_fail(DS_ERR_RUNTIME, "compute-before-swap-in: microbatch " +
+                                                   std::to_string(mb) + " has non-resident pages");
+
+    const int prevR = int(k.prev_logit_slots.size());
+    const size_t need_meta = size_t(7) * T + 2 * size_t(R) + P + prevR + 8;
+    if (need_meta > s->meta_cap) return ds_fail(DS_ERR_ARG, "step metadata exceeds capacity");
+    const int buf = s->meta_buf;
+    s->meta_buf ^= 1;
+    CK(cudaEventSynchronize(s->meta_ev[buf]));  // staging buffer no longer read by an older copy
+    int32_t* hm = s->h_meta[buf];
+    int32_t* prompt_tok = hm;
+    int32_t* row_slot = prompt_tok + T;
+    int32_t* row_pos = row_slot + T;
+    int32_t* row_page = row_pos + T;
+    int32_t* row_poff = row_page + T;
+    int32_t* logit_rows = row_poff + T;
+    int32_t* logit_slot = logit_rows + R;
+    int32_t* prev_slot = logit_slot + R;
+    int32_t* flat = prev_slot + prevR;
+    {
+        int t = 0, r = 0, poff = 0;
+        for (int64_t i = 0; i < n_rows; ++i) {
+            const ds_row& rw = rows[i];
+            const auto& pg = k.pages[rw.slot];
+            const int np = int(page_count_for(rw.pos + rw.n_tok));
+            for (int j = 0; j < np; ++j) {
+                const int32_t hnd = pg[j];
+                flat[poff + j] = hnd >= 0 ? hnd : k.host_dev[-hnd - 1];
+            }
+            for (int j = 0; j < rw.n_tok; ++j, ++t) {
+                const int pos = rw.pos + j;
+                // prefill rows read the prompt; decode rows the token sampled by the previous
+                // circuit, except the very first decode of an empty prompt (BOS at position 0)
+                prompt_tok[t] = rw.is_decode ? (pos == 0 ? kBosToken : -1)
+                                             : int32_t(ds_prompt_token(rw.req_id, pos));
+                row_slot[t] = mb * s->max_slots + rw.slot;
+                row_pos[t] = pos;
+                row_page[t] = flat[poff + pos / 256];
+                row_poff[t] = poff;
+            }
+            if (rw.need_logits) {
+                logit_rows[r] = t - 1;
+                logit_slot[r] = mb * s->max_slots + rw.slot;
+                ++r;
+            }
+            poff += np;
+        }
+        for (int j = 0; j < prevR; ++j) prev_slot[j] = k.prev_logit_slots[j];
+    }
+    const size_t meta_n = size_t(flat - hm) + P;
+    CK(cudaMemcpyAsync(s->d_meta, hm, meta_n * 4, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaEventRecord(s->meta_ev[buf], s->stream));
+    const int32_t* d_prompt = s->d_meta;
+    const int32_t* d_slot = d_prompt + T;
+    const int32_t* d_pos = d_slot + T;
+    const int32_t* d_page = d_pos + T;
+    const int32_t* d_poff = d_page + T;
+    const int32_t* d_lrows = d_poff + T;
+    const int32_t* d_lslot = d_lrows + R;
+    const int32_t* d_prev = d_lslot + R;
+    const int32_t* d_flat = d_prev + prevR;
+
+    // ---- wait for the swap-in this compute depends on
+    if (k.resident_slot >= 0) CK(cudaStreamWaitEvent(s->stream, s->ev_h2d, 0));
+
+    cudaStream_t st = s->stream;
+    const int d = m.d_model;
+    if (s->first) {
+        const int32_t* ids_in = static_cast<const int32_t*>(act_in);
+        if (!ids_in && s->last && prevR > 0) ids_in = s->pending_ids + size_t(mb) * s->max_rows;
+        if (ids_in && prevR > 0) ds::scatter_tokens(ids_in, d_prev, prevR, s->last_token, st);
+        int32_t* tokens = s->ids;  // scratch: resolved token ids for this step
+        ds::resolve_tokens(d_prompt, d_slot, s->last_token, T, tokens, st);
+        ds::embed_rows(s->emb, tokens, T, d, s->x, st);
+    } else {
+        if (!act_in) return ds_fail(DS_ERR_ARG, "non-first stage needs activations");
+        CK(cudaMemcpyAsync(s->x, act_in, size_t(T) * d * 2, cudaMemcpyDeviceToDevice, st));
+    }
+    for (int li = 0; li < s->L; ++li) {
+        LayerW& lw = s->layers[li];
+        ds::rmsnorm_rows(s->x, nullptr, T, d, lw.attn_norm, m.norm_eps, s->xn, st);
+        int rc = ds::gemm_bf16(lw.wqkv, s->xn, T, ds::EPI_BF16, s->qkv, nullptr, nullptr, s->ws,
+                               s->ws_floats, 0, st);
+        ds::rope_kv_append(s->qkv, T, m.n_heads, m.n_kv_heads, m.d_head, d_pos, d_page, s->rope_cos,
+                           s->rope_sin, s->kv, li, s->q, st);
+        rc |= ds::attention_paged(s->q, T, m.n_heads, d_pos, d_poff, d_flat, s->kv, li, max_ctx,
+                                  s->attn, s->attn_ws, s->attn_ws_floats, st);
+        rc |= ds::gemm_bf16(lw.wo, s->attn, T, ds::EPI_RESID, s->x, s->x, nullptr, s->ws,
+                            s->ws_floats, 0, st);
+        ds::rmsnorm_rows(s->x, nullptr, T, d, lw.mlp_norm, m.norm_eps, s->xn, st);
+        rc |= ds::gemm_bf16(lw.wgu, s->xn, T, ds::EPI_BF16, s->gu, nullptr, nullptr, s->ws,
+                            s->ws_floats, 0, st);
+        ds::silu_mul(s->gu, T, m.ffn, s->h, st);
+        rc |= ds::gemm_bf16(lw.wd, s->h, T, ds::EPI_RESID, s->x, s->x, nullptr, s->ws, s->ws_floats,
+                            0, st);
+        if (rc) return ds_fail(DS_ERR_RUNTIME, "kernel launch failed in layer " + std::to_string(li));
+    }
+    if (s->last) {
+        int32_t* ids_out = act_out ? static_cast<int32_t*>(act_out)
+                                   : (s->first ? s->pending_ids + size_t(mb) * s->max_rows : s->ids);
+        if (R > 0) {
+            ds::rmsnorm_rows(s->x, d_lrows, R, d, s->final_norm, m.norm_eps, s->xn, st);
+            if (ds::gemm_bf16(s->lm_head, s->xn, R, ds::EPI_F32, nullptr, nullptr, s->logits, s->ws,
+                              s->ws_floats, 0, st))
+                return ds_fail(DS_ERR_RUNTIME, "lm_head launch failed");
+            ds::argmax_rows(s->logits, R, m.vocab, ids_out, st);
+            if (act_out == nullptr && s->first == false)
+                ;  // ids stay in s->ids
+            if (s->first && act_out)
+                CK(cudaMemcpyAsync(s->pending_ids + size_t(mb) * s->max_rows, ids_out, size_t(R) * 4,
+                                   cudaMemcpyDeviceToDevice, st));
+        }
+    } else if (act_out) {
+        CK(cudaMemcpyAsync(act_out, s->x, size_t(T) * d * 2, cudaMemcpyDeviceToDevice, st));
+    }
+    // remember which slots the sampled ids belong to (consumed by this mb's next circuit)
+    if (s->first) {
+        k.prev_logit_slots.assign(logit_slot, logit_slot + R);
+    }
+    CK(cudaEventRecord(k.last_compute, st));
+    k.computed = true;
+    s->last_T = T;
+    s->last_R = R;
+    CK(cudaPeekAtLastError());
+    return DS_OK;
+}
+
+ds_status ds_stage_output(ds_stage* s, void** ptr, int64_t* bytes, int64_t* n_out) {
+    if (!s) return ds_fail(DS_ERR_ARG, "null stage");
+    if (s->last) {
+        if (ptr) *ptr = s->first ? nullptr : s->ids;
+        if (bytes) *bytes = int64_t(s->last_R) * 4;
+        if (n_out) *n_out = s->last_R;
+    } else {
+        if (ptr) *ptr = s->x;
+        if (bytes) *bytes = int64_t(s->last_T) * s->m.d_model * 2;
+        if (n_out) *n_out = s->last_T;
+    }
+    return DS_OK;
+}
+
+ds_status ds_stage_sync(ds_stage* s) {
+    if (!s) return ds_fail(DS_ERR_ARG, "null stage");
+    CK(cudaSetDevice(s->device));
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaStreamSynchronize(s->h2d));
+    CK(cudaStreamSynchronize(s->d2h));
+    return DS_OK;
+}
+
+ds_status ds_stage_stream(ds_stage* s, void** st) {
+    if (!s || !st) return ds_fail(DS_ERR_ARG, "null argument");
+    *st = s->stream;
+    return DS_OK;
+}
+
+ds_status ds_stage_logits(ds_stage* s, float* host_out, int64_t max_floats, int64_t* n_floats) {
+    if (!s || !s->last) return ds_fail(DS_ERR_ARG, "not a last stage");
+    CK(cudaSetDevice(s->device));
+    const int64_t n = int64_t(s->last_R) * s->m.vocab;
+    if (n_floats) *n_floats = n;
+    if (host_out) {
+        CK(cudaStreamSynchronize(s->stream));
+        CK(cudaMemcpy(host_out, s->logits, size_t(std::min(n, max_floats)) * 4,
+                      cudaMemcpyDeviceToHost));
+    }
+    return DS_OK;
+}
+
+ds_status ds_dbg_gemm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t N, int32_t K,
+                      int32_t epi, const uint16_t* resid, int32_t k_splits, void* out) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return ds_fail(DS_ERR_NO_DEVICE, "no CUDA device");
+    bf16 *dx = nullptr, *dw = nullptr, *dout = nullptr;
+    float *dws = nullptr, *df = nullptr;
+    const size_t out_elems = size_t(T) * N;
+    CK(cudaMalloc(&dx, size_t(T) * K * 2));
+    CK(cudaMalloc(&dw, size_t(N) * K * 2));
+    CK(cudaMalloc(&dout, out_elems * 2));
+    CK(cudaMalloc(&df, out_elems * 4));
+    const size_t wsf = size_t(8) * T * N;
+    CK(cudaMalloc(&dws, wsf * 4));
+    CK(cudaMemcpy(dx, x, size_t(T) * K * 2, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dw, w, size_t(N) * K * 2, cudaMemcpyHostToDevice));
+    if (resid) CK(cudaMemcpy(dout, resid, out_elems * 2, cudaMemcpyHostToDevice));
+    GemmWeight gw;
+    if (ds::gemm_weight_init(&gw, dw, N, K)) return ds_fail(DS_ERR_RUNTIME, "tensor map");
+    const int rc = ds::gemm_bf16(gw, dx, T, epi, dout, dout, df, dws, wsf, k_splits, 0);
+    if (rc) return ds_fail(DS_ERR_RUNTIME, "gemm launch rc=" + std::to_string(rc));
+    CK(cudaDeviceSynchronize());
+    if (epi == ds::EPI_F32)
+        CK(cudaMemcpy(out, df, out_elems * 4, cudaMemcpyDeviceToHost));
+    else
+        CK(cudaMemcpy(out, dout, out_elems * 2, cudaMemcpyDeviceToHost));
+    cudaFree(dx);
+    cudaFree(dw);
+    cudaFree(dout);
+    cudaFree(df);
+    cudaFree(dws);
+    return DS_OK;
+}
+
+}  // extern "C"

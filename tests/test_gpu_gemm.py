@@ -1,0 +1,45 @@
+"""tcgen05 GEMM parity against an fp32 numpy reference of the same bf16 operands."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(T, N, K, epi=0, splits=0, seed=0):
+    from paper_2501_14784_b200 import _native as nat
+    from paper_2501_14784_b200.bf16 import from_bf16, to_bf16
+    rng = np.random.default_rng(seed)
+    x = to_bf16(rng.standard_normal((T, K)).astype(np.float32))
+    w = to_bf16((rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32))
+    resid = to_bf16(rng.standard_normal((T, N)).astype(np.float32))
+    ref = from_bf16(x).astype(np.float64) @ from_bf16(w).astype(np.float64).T
+    out = np.zeros((T, N), dtype=np.float32 if epi == 2 else np.uint16)
+    nat.check(nat.lib.ds_dbg_gemm(x.ctypes.data, w.ctypes.data, T, N, K, epi,
+                                  resid.ctypes.data if epi == 1 else None, splits,
+                                  out.ctypes.data))
+    if epi == 1:
+        ref = from_bf16(resid) + from_bf16(to_bf16(ref.astype(np.float32)))
+    got = out if epi == 2 else from_bf16(out)
+    return got.astype(np.float64), ref
+
+
+@pytest.mark.parametrize("T", [1, 7, 16, 33, 128, 256, 300, 512, 777])
+def test_gemm_shapes(T):
+    got, ref = _run(T, 384, 256)
+    tol = 2e-2 * np.abs(ref).max() + 1e-3
+    assert np.abs(got - ref).max() <= tol
+
+
+@pytest.mark.parametrize("epi", [0, 1, 2])
+@pytest.mark.parametrize("splits", [1, 3])
+def test_gemm_epilogues_and_splits(epi, splits):
+    got, ref = _run(64, 256, 1024, epi=epi, splits=splits, seed=3)
+    tol = (1e-4 if epi == 2 else 2e-2) * np.abs(ref).max() + 1e-3
+    assert np.abs(got - ref).max() <= tol
+
+
+def test_gemm_llama8b_qkv_shape():
+    got, ref = _run(200, 6144, 4096, seed=5)
+    assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max()
