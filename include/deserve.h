@@ -45,6 +45,15 @@ ds_status ds_page_bytes(int64_t kv_bytes_per_token, int64_t layers, int64_t tota
 ds_status ds_global_pool_size(int64_t pcie_bw, int64_t stage_time_us, int64_t page,
                               int64_t* out);
 
+/* Reference: memory_budget (src/perf_model.cpp:138-167). out5 = {M_KV, M_G, M_B, M_B', local}. */
+ds_status ds_memory_budget(int64_t mem, int64_t weights, int64_t n_mb, int64_t m_global,
+                           int32_t offload, int64_t* out5);
+/* Reference: RequestGenerator::make (src/workload.cpp:36-53). out2 = {prompt_len, output_len}. */
+ds_status ds_request_lengths(uint64_t seed, int64_t prompt_min, int64_t prompt_max, int64_t output_min,
+                             int64_t output_max, int64_t index, int64_t* out2);
+/* Reference: steady_state_throughput (src/sim.cpp:597-604) on a plan document. */
+ds_status ds_steady_state_throughput(const char* plan_json, double* out);
+
 /* Reference: plan() (src/planner.cpp:140-276) on a config document in the reference JSON format
  * (src/config.cpp:103-252). policy: NULL/"" = config as written, else "baseline" | "offload" |
  * "opt" (src/sweep.cpp:26-43). latency_us >= 0 overrides every link latency (sweep.cpp:45-49);

@@ -1,0 +1,143 @@
+"""TEST INFRASTRUCTURE ONLY — parity checkers. Imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs, never by the product package.
+
+* ``Ref``  — the UNMODIFIED reference pipesim library (oracle/_ref/libpipesim_ref.so, compiled
+  from /root/reference/proj/src by oracle/Makefile) behind a small C shim (ref_shim.cpp).
+* ``LlamaRef`` — the CPU restatement of the stage forward (oracle/llama_ref.c); the reference has
+  no arithmetic for this part, so it is pinned only by its own conventions.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SO = os.path.join(HERE, "_ref", "libpipesim_ref.so")
+LLAMA_SO = os.path.join(HERE, "_build", "libllama_ref.so")
+
+
+def _b(s):
+    return None if s is None else (s.encode() if isinstance(s, str) else s)
+
+
+class RefError(RuntimeError):
+    pass
+
+
+class Ref:
+    """Compiled reference (pipesim) through ref_shim.cpp."""
+
+    def __init__(self):
+        if not os.path.exists(REF_SO):
+            raise FileNotFoundError(f"{REF_SO} missing: run `make -C {HERE}`")
+        lib = C.CDLL(REF_SO)
+        L, S, P = C.c_longlong, C.c_char_p, C.c_void_p
+        lib.ref_last_error.restype = S
+        for name, args in {
+            "ref_plan_config": [S, S, S, L, L, P, C.c_size_t],
+            "ref_sim_config": [S, S, S, L, L, S, P, C.c_size_t],
+            "ref_sim_plan": [S, S, S, S, P, C.c_size_t],
+            "ref_stage_time": [P, P, L, L, L, L, P],
+            "ref_page_bytes": [L, L, L, P],
+            "ref_global_pool_size": [L, L, L, P],
+            "ref_memory_budget": [L, L, L, L, C.c_int, P],
+            "ref_replay_check": [S, S, P, C.c_size_t],
+            "ref_windowed_stats": [S, L, L, C.c_int, P],
+            "ref_request": [C.c_ulonglong, L, L, L, L, L, P],
+        }.items():
+            getattr(lib, name).argtypes = args
+            getattr(lib, name).restype = C.c_int
+        lib.ref_steady_state.argtypes = [S]
+        lib.ref_steady_state.restype = C.c_double
+        self.lib = lib
+
+    def _ok(self, rc):
+        if rc != 0:
+            raise RefError(self.lib.ref_last_error().decode())
+
+    def plan_config(self, text, cdir="", policy=None, latency_us=-1, nb=-1) -> str:
+        buf = C.create_string_buffer(1 << 20)
+        self._ok(self.lib.ref_plan_config(_b(text), _b(cdir), _b(policy or ""), latency_us, nb,
+                                          buf, len(buf)))
+        return buf.value.decode()
+
+    def sim_config(self, text, cdir="", policy=None, latency_us=-1, nb=-1, trace_path=None) -> dict:
+        buf = C.create_string_buffer(1 << 16)
+        self._ok(self.lib.ref_sim_config(_b(text), _b(cdir), _b(policy or ""), latency_us, nb,
+                                         _b(trace_path or ""), buf, len(buf)))
+        return json.loads(buf.value.decode())
+
+    def sim_plan(self, text, plan_json, cdir="", trace_path=None) -> dict:
+        buf = C.create_string_buffer(1 << 16)
+        self._ok(self.lib.ref_sim_plan(_b(text), _b(cdir), _b(plan_json), _b(trace_path or ""),
+                                       buf, len(buf)))
+        return json.loads(buf.value.decode())
+
+    def stage_time(self, table, batch, layers, ref_layers) -> int:
+        b = (C.c_longlong * len(table))(*[x[0] for x in table])
+        t = (C.c_longlong * len(table))(*[x[1] for x in table])
+        out = C.c_longlong(0)
+        self._ok(self.lib.ref_stage_time(b, t, len(table), batch, layers, ref_layers, C.byref(out)))
+        return out.value
+
+    def page_bytes(self, kvpt, layers, total) -> int:
+        out = C.c_longlong(0)
+        self._ok(self.lib.ref_page_bytes(kvpt, layers, total, C.byref(out)))
+        return out.value
+
+    def global_pool_size(self, w, t, page) -> int:
+        out = C.c_longlong(0)
+        self._ok(self.lib.ref_global_pool_size(w, t, page, C.byref(out)))
+        return out.value
+
+    def memory_budget(self, mem, weights, nb, mg, offload) -> list[int]:
+        out = (C.c_longlong * 5)()
+        self._ok(self.lib.ref_memory_budget(mem, weights, nb, mg, int(offload), out))
+        return list(out)
+
+    def replay_check(self, trace_path, plan_json) -> list[str]:
+        buf = C.create_string_buffer(1 << 20)
+        self._ok(self.lib.ref_replay_check(_b(trace_path), _b(plan_json), buf, len(buf)))
+        return [x for x in buf.value.decode().splitlines() if x]
+
+    def windowed_stats(self, trace_path, start, end, completed=False):
+        out = (C.c_longlong * 3)()
+        self._ok(self.lib.ref_windowed_stats(_b(trace_path), start, end, int(completed), out))
+        return tuple(out)
+
+    def steady_state(self, plan_json) -> float:
+        return self.lib.ref_steady_state(_b(plan_json))
+
+    def request(self, seed, pmin, pmax, omin, omax, index):
+        out = (C.c_longlong * 2)()
+        self._ok(self.lib.ref_request(seed, pmin, pmax, omin, omax, index, out))
+        return out[0], out[1]
+
+
+class LrModel(C.Structure):
+    _fields_ = [("n_layers", C.c_int32), ("d_model", C.c_int32), ("n_heads", C.c_int32),
+                ("n_kv_heads", C.c_int32), ("d_head", C.c_int32), ("ffn", C.c_int32),
+                ("vocab", C.c_int32), ("max_seq_len", C.c_int32), ("rope_theta", C.c_float),
+                ("norm_eps", C.c_float)]
+
+
+class LlamaRef:
+    """CPU oracle of one stage (oracle/llama_ref.c), multithreaded with OpenMP."""
+
+    def __init__(self):
+        if not os.path.exists(LLAMA_SO):
+            raise FileNotFoundError(f"{LLAMA_SO} missing: run `make -C {HERE} llama`")
+        lib = C.CDLL(LLAMA_SO)
+        P = C.c_void_p
+        lib.lr_weight.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_float]
+        lib.lr_weight.restype = C.c_float
+        lib.lr_prompt_token.argtypes = [C.c_int64, C.c_int32]
+        lib.lr_prompt_token.restype = C.c_int32
+        lib.lr_stage_create.argtypes = [P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_uint64,
+                                        C.c_int32]
+        lib.lr_stage_create.restype = P
+        lib.lr_stage_destroy.argtypes = [P]
+        lib.lr_stage_step.argtypes = [P, C.c_int32, C.c_int32, P, C.c_int32, P, P, P, P, P]
+        lib.lr_stage_step.restype = C.c_int
+        self.lib = lib

@@ -69,6 +69,9 @@ def _load() -> C.CDLL:
         "ds_stage_time_us": (I32, [P, P, I64, I64, I64, I64, P]),
         "ds_page_bytes": (I32, [I64, I64, I64, P]),
         "ds_global_pool_size": (I32, [I64, I64, I64, P]),
+        "ds_memory_budget": (I32, [I64, I64, I64, I64, I32, P]),
+        "ds_request_lengths": (I32, [C.c_uint64, I64, I64, I64, I64, I64, P]),
+        "ds_steady_state_throughput": (I32, [S, P]),
         "ds_plan_config": (I32, [S, S, S, I64, I64, P, C.c_size_t, P]),
         "ds_sim_config": (I32, [S, S, S, I64, I64, S, P, C.c_size_t]),
         "ds_sim_plan": (I32, [S, S, S, S, P, C.c_size_t]),

@@ -90,6 +90,45 @@ ds_status ds_global_pool_size(int64_t pcie_bw, int64_t stage_time_us, int64_t pa
     });
 }
 
+ds_status ds_memory_budget(int64_t mem, int64_t weights, int64_t n_mb, int64_t m_global,
+                           int32_t offload, int64_t* out5) {
+    return guarded([&] {
+        dsb::Node n;
+        n.id = "node";
+        n.mem = mem;
+        const dsb::Budget b = dsb::make_budget(n, weights, n_mb, m_global, offload != 0);
+        out5[0] = b.m_kv;
+        out5[1] = b.m_global;
+        out5[2] = b.per_mb_plain;
+        out5[3] = b.per_mb_offload;
+        out5[4] = b.local_bytes();
+        return DS_OK;
+    });
+}
+
+ds_status ds_request_lengths(uint64_t seed, int64_t prompt_min, int64_t prompt_max, int64_t output_min,
+                             int64_t output_max, int64_t index, int64_t* out2) {
+    return guarded([&] {
+        dsb::Workload w;
+        w.seed = seed;
+        w.prompt_min = prompt_min;
+        w.prompt_max = prompt_max;
+        w.output_min = output_min;
+        w.output_max = output_max;
+        const auto pr = dsb::request_lengths(w, index);
+        out2[0] = pr.first;
+        out2[1] = pr.second;
+        return DS_OK;
+    });
+}
+
+ds_status ds_steady_state_throughput(const char* plan_json, double* out) {
+    return guarded([&] {
+        *out = dsb::analytic_throughput(dsb::Plan::from_json(plan_json ? plan_json : ""));
+        return DS_OK;
+    });
+}
+
 ds_status ds_plan_config(const char* config_json, const char* config_dir, const char* policy,
                          int64_t latency_us, int64_t nb_override, char* out, size_t cap,
                          size_t* needed) {

@@ -231,6 +231,8 @@ struct SimOutput {
 // the reference's. Throws SimError on plan/topology mismatch or deadlock.
 SimOutput simulate(const Plan& plan, const Topo& topo, const Workload& wl, const Model& model,
                    bool keep_trace = true, bool keep_schedule = false);
-double analytic_throughput(const Plan& plan);  // reference steady_state_throughput (sim.cpp:597-604)
+double analytic_throughput(const Plan& plan);
+// lengths of request `index` under the workload's SplitMix64 stream (reference workload.cpp:36-53)
+std::pair<Tokens, Tokens> request_lengths(const Workload& w, int64_t index);  // reference steady_state_throughput (sim.cpp:597-604)
 
 }  // namespace dsb

@@ -68,6 +68,20 @@ double analytic_throughput(const Plan& p) {
     return double(p.n_mb * p.B()) * 1e6 / double(period);
 }
 
+std::pair<Tokens, Tokens> request_lengths(const Workload& w, int64_t k) {
+    uint64_t st = w.seed + 0x9E3779B97F4A7C15ULL * uint64_t(k + 1);
+    auto draw = [&st](Tokens lo, Tokens hi) {
+        uint64_t z = (st += 0x9E3779B97F4A7C15ULL);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        z ^= z >> 31;
+        return lo + Tokens(z % (uint64_t(hi - lo) + 1));
+    };
+    const Tokens p = draw(w.prompt_min, w.prompt_max);
+    const Tokens o = draw(w.output_min, w.output_max);
+    return {p, o};
+}
+
 namespace {
 
 // Request lengths: SplitMix64 keyed by (seed, index) (reference workload.cpp:11-53), or a
@@ -92,17 +106,7 @@ public:
     std::pair<Tokens, Tokens> lengths(int64_t k) const {
         if (!fixed_.empty())
             return k < int64_t(fixed_.size()) ? fixed_[k] : std::pair<Tokens, Tokens>{-1, -1};
-        uint64_t st = w_.seed + 0x9E3779B97F4A7C15ULL * uint64_t(k + 1);
-        auto draw = [&st](Tokens lo, Tokens hi) {
-            uint64_t z = (st += 0x9E3779B97F4A7C15ULL);
-            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-            z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-            z ^= z >> 31;
-            return lo + Tokens(z % (uint64_t(hi - lo) + 1));
-        };
-        const Tokens p = draw(w_.prompt_min, w_.prompt_max);
-        const Tokens o = draw(w_.output_min, w_.output_max);
-        return {p, o};
+        return request_lengths(w_, k);
     }
     bool done() const { return !fixed_.empty() && next_ >= int64_t(fixed_.size()); }
     int64_t take() { return next_++; }

@@ -1,0 +1,88 @@
+"""Python mirror of the reference's plan/run interface over the C ABI.
+
+Reference names and meaning:
+  plan_config  -> pipesim::plan (src/planner.cpp:140-276) on a config document
+  sim_config   -> pipesim::run  (src/sim.cpp:591-595), virtual clock, executor = ours
+  sim_plan     -> run() on an explicit PipelinePlan JSON
+Errors raise ConfigError / PlanError / SimError like the reference's exception classes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+
+from ._native import check, lib
+
+
+def _b(s):
+    return None if s is None else (s.encode() if isinstance(s, str) else s)
+
+
+def read_config(path: str) -> tuple[str, str]:
+    return open(path).read(), os.path.dirname(os.path.abspath(path))
+
+
+def plan_config(config_text: str, config_dir: str = "", policy: str | None = None,
+                latency_us: int = -1, nb_override: int = -1) -> str:
+    need = C.c_size_t(0)
+    check(lib.ds_plan_config(_b(config_text), _b(config_dir), _b(policy or ""), latency_us,
+                             nb_override, None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    check(lib.ds_plan_config(_b(config_text), _b(config_dir), _b(policy or ""), latency_us,
+                             nb_override, buf, need.value, None))
+    return buf.value.decode()
+
+
+def sim_config(config_text: str, config_dir: str = "", policy: str | None = None,
+               latency_us: int = -1, nb_override: int = -1, trace_path: str | None = None) -> dict:
+    buf = C.create_string_buffer(1 << 16)
+    check(lib.ds_sim_config(_b(config_text), _b(config_dir), _b(policy or ""), latency_us,
+                            nb_override, _b(trace_path or ""), buf, len(buf)))
+    return json.loads(buf.value.decode())
+
+
+def sim_plan(config_text: str, plan_json: str, config_dir: str = "",
+             trace_path: str | None = None) -> dict:
+    buf = C.create_string_buffer(1 << 16)
+    check(lib.ds_sim_plan(_b(config_text), _b(config_dir), _b(plan_json), _b(trace_path or ""),
+                          buf, len(buf)))
+    return json.loads(buf.value.decode())
+
+
+def stage_time_us(table: list[tuple[int, int]], batch: int, layers: int, ref_layers: int) -> int:
+    b = (C.c_int64 * len(table))(*[x[0] for x in table])
+    t = (C.c_int64 * len(table))(*[x[1] for x in table])
+    out = C.c_int64(0)
+    check(lib.ds_stage_time_us(b, t, len(table), batch, layers, ref_layers, C.byref(out)))
+    return out.value
+
+
+def page_bytes(kv_bytes_per_token: int, layers: int, total_layers: int) -> int:
+    out = C.c_int64(0)
+    check(lib.ds_page_bytes(kv_bytes_per_token, layers, total_layers, C.byref(out)))
+    return out.value
+
+
+def global_pool_size(pcie: int, stage_time: int, page: int) -> int:
+    out = C.c_int64(0)
+    check(lib.ds_global_pool_size(pcie, stage_time, page, C.byref(out)))
+    return out.value
+
+
+def memory_budget(mem: int, weights: int, n_mb: int, m_global: int, offload: bool) -> list[int]:
+    out = (C.c_int64 * 5)()
+    check(lib.ds_memory_budget(mem, weights, n_mb, m_global, int(offload), out))
+    return list(out)
+
+
+def request_lengths(seed: int, pmin: int, pmax: int, omin: int, omax: int, index: int):
+    out = (C.c_int64 * 2)()
+    check(lib.ds_request_lengths(seed, pmin, pmax, omin, omax, index, out))
+    return out[0], out[1]
+
+
+def steady_state_throughput(plan_json: str) -> float:
+    out = C.c_double(0)
+    check(lib.ds_steady_state_throughput(_b(plan_json), C.byref(out)))
+    return out.value

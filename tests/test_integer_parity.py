@@ -1,0 +1,298 @@
+"""Integer hot path: the product's planner / perf model / scheduler against
+(1) the reference's own unit-test goldens and (2) the compiled reference (oracle/_ref), bit-exact.
+CPU only."""
+import hashlib
+import json
+import os
+
+import pytest
+
+from paper_2501_14784_b200 import pipeline as pl
+from paper_2501_14784_b200._native import PlanError, SimError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = json.load(open(os.path.join(ROOT, "tests", "golden", "reference_unit_goldens.json")))
+CONFIGS = os.path.join(ROOT, "configs")
+REF_CONFIGS = os.path.join(ROOT, "tests", "golden", "ref_configs")
+GIB = 1 << 30
+
+
+@pytest.fixture(scope="module")
+def ref():
+    import oracle
+    return oracle.Ref()
+
+
+def sha(path):
+    return hashlib.sha256(open(path, "rb").read()).hexdigest()
+
+
+# ------------------------------------------------------------------- unit-test goldens ----
+def test_stage_time_goldens(ref):
+    tab = GOLD["stage_time_points"]["table1"]
+    for b, us in tab:
+        assert pl.stage_time_us(tab, b, 1, 0) == us == ref.stage_time(tab, b, 1, 0)
+    for b, us in GOLD["stage_time_interp"]["cases"]:
+        assert pl.stage_time_us(tab, b, 1, 0) == us == ref.stage_time(tab, b, 1, 0)
+    small = GOLD["stage_time_clamp"]["table"]
+    for b, us in GOLD["stage_time_clamp"]["cases"]:
+        assert pl.stage_time_us(small, b, 1, 0) == us
+    for b, layers, refl, us in GOLD["scaled_stage_time"]["cases"]:
+        assert pl.stage_time_us(tab, b, layers, refl) == us == ref.stage_time(tab, b, layers, refl)
+
+
+def test_stage_time_exhaustive_vs_reference(ref):
+    tabs = [GOLD["stage_time_points"]["table1"], [[1, 2000], [64, 5000], [512, 20000]],
+            [[3, 17], [5, 17], [9, 1000], [100, 100001]]]
+    for tab in tabs:
+        for b in range(1, 700):
+            for layers, refl in [(1, 0), (10, 10), (7, 3), (40, 80), (3, 7)]:
+                assert pl.stage_time_us(tab, b, layers, refl) == ref.stage_time(tab, b, layers, refl)
+
+
+def test_page_and_pool_goldens(ref):
+    g = GOLD["page_bytes_70b"]
+    for layers, total, want in g["cases"]:
+        assert pl.page_bytes(g["kv_bytes_per_token"], layers, total) == want
+        assert ref.page_bytes(g["kv_bytes_per_token"], layers, total) == want
+    for w, t, page, want in GOLD["global_pool_size"]["cases"]:
+        assert pl.global_pool_size(w, t, page) == want == ref.global_pool_size(w, t, page)
+    for kv in [2048, 131072, 327680, 8192 * 3, 1]:
+        for total in [1, 4, 32, 80]:
+            for layers in range(1, total + 1, max(1, total // 7)):
+                assert pl.page_bytes(kv, layers, total) == ref.page_bytes(kv, layers, total)
+
+
+def test_memory_budget_grid(ref):
+    for m, w, nb, g, mb, mbo in GOLD["memory_budget_grid"]["rows"]:
+        out = pl.memory_budget(m, w, nb, g, True)
+        assert out[0] == m - w and out[2] == mb and out[3] == mbo
+        assert out == ref.memory_budget(m, w, nb, g, True)
+        plain = pl.memory_budget(m, w, nb, g, False)
+        assert plain[1] == 0 and plain[3] == mb
+        assert plain == ref.memory_budget(m, w, nb, g, False)
+
+
+def test_memory_budget_errors():
+    with pytest.raises(PlanError):
+        pl.memory_budget(8 * GIB, 9 * GIB, 4, 0, False)
+    with pytest.raises(PlanError):
+        pl.memory_budget(8 * GIB, 4 * GIB, 4, 3 * GIB, True)
+
+
+def test_request_generator_matches_reference(ref):
+    for seed in [0, 7, 42, 2 ** 63 + 5]:
+        for rng in [(0, 512, 0, 512), (7, 7, 3, 3), (3840, 3840, 256, 256), (0, 1, 0, 1)]:
+            for k in list(range(50)) + [10 ** 6, 2 ** 40]:
+                assert pl.request_lengths(seed, *rng, k) == ref.request(seed, *rng, k)
+    vals = [pl.request_lengths(42, 0, 512, 0, 512, k) for k in range(100000)]
+    mp = sum(v[0] for v in vals) / len(vals)
+    mo = sum(v[1] for v in vals) / len(vals)
+    assert 251 < mp < 261 and 251 < mo < 261  # test_workload.cpp:25-42
+
+
+def ring_config(n, mem, pcie, latency, bw, policy=None, workload=None):
+    nodes = [{"node_id": f"n{i}", "gpu_mem_bytes": mem, "pcie_bandwidth_bytes_per_s": pcie,
+              "compute_calibration": "table1"} for i in range(n)]
+    links = [{"src": f"n{i}", "dst": f"n{(i + 1) % n}", "latency_us": latency,
+              "bandwidth_bytes_per_s": bw} for i in range(n)] if n > 1 else []
+    wl = workload or {"prompt_len_min": 0, "prompt_len_max": 512, "output_len_min": 0,
+                      "output_len_max": 512, "concurrency_target": 2048, "bench_duration_s": 1200,
+                      "warmup_s": 240, "rng_seed": 42}
+    cfg = {"model": "llama3-70b", "nodes": nodes, "links": links, "workload": wl}
+    if policy:
+        cfg["scheduler"] = policy
+    return json.dumps(cfg)
+
+
+def test_planner_golden(ref):
+    g = GOLD["planner_golden"]
+    txt = ring_config(8, 24 * GIB, g["pcie"], g["latency_us"], g["bw"],
+                      {"offload": True, "calibration_ref_layers": 10})
+    mine = pl.plan_config(txt)
+    assert mine == ref.plan_config(txt)
+    p = json.loads(mine)
+    assert p["converged"] and p["iterations"] == g["iterations"]
+    assert p["stages"][0]["batch_size_per_microbatch"] == g["batch"]
+    assert p["n_microbatches"] == g["n_microbatches"] and p["stage_time_us"] == g["stage_time_us"]
+    assert all(s["budget"]["m_global_pool"] == g["m_global_pool"] for s in p["stages"])
+    assert p["stages"][0]["budget"]["m_kv"] == g["m_kv_stage0"]
+    assert p["stages"][1]["budget"]["m_kv"] == g["m_kv_stage1"]
+    assert [[s["layer_begin"], s["layer_end"]] for s in p["stages"]] == [[10 * i, 10 * i + 10] for i in range(8)]
+
+
+def test_planner_partitions_and_errors(ref):
+    txt = ring_config(2, 96 * GIB, 16 * 10 ** 9, 1000, 10 ** 9, {"offload": False})
+    p = json.loads(pl.plan_config(txt))
+    assert [[s["layer_begin"], s["layer_end"]] for s in p["stages"]] == GOLD["planner_partition"]["sym2_96gib"]
+    cfg = json.loads(ring_config(2, 120 * GIB, 16 * 10 ** 9, 1000, 10 ** 9, {"offload": False}))
+    cfg["nodes"][1]["gpu_mem_bytes"] = 40 * GIB
+    p = json.loads(pl.plan_config(json.dumps(cfg)))
+    assert [[s["layer_begin"], s["layer_end"]] for s in p["stages"]] == GOLD["planner_partition"]["big_small"]
+    assert pl.plan_config(json.dumps(cfg)) == ref.plan_config(json.dumps(cfg))
+    with pytest.raises(PlanError, match="insufficient-total-memory"):
+        pl.plan_config(ring_config(2, 24 * GIB, 16 * 10 ** 9, 1000, 10 ** 9))
+    broken = json.loads(ring_config(8, 24 * GIB, 32 * 10 ** 9, 64000, 10 ** 9, {"nb_override": 5}))
+    broken["links"].pop()
+    with pytest.raises(PlanError, match="missing-link"):
+        pl.plan_config(json.dumps(broken))
+    big = json.loads(ring_config(8, 24 * GIB, 32 * 10 ** 9, 64000, 10 ** 9))
+    big["workload"]["prompt_len_max"] = big["workload"]["output_len_max"] = 4000
+    with pytest.raises(PlanError, match="max_seq_len"):
+        pl.plan_config(json.dumps(big))
+
+
+@pytest.mark.parametrize("S,lat,t_s,want", [(4, 35000, 70000, 6), (4, 61728, 123456, 6), (8, 64000, 70000, 16)])
+def test_min_bubble_free(S, lat, t_s, want):
+    # N_B = S + ceil(S*L/T_S) (planner.cpp:80-91), through the planner with a flat calibration
+    cfg = json.loads(ring_config(S, 96 * GIB, 16 * 10 ** 9, lat, 10 ** 12, {"offload": False}))
+    open("/tmp/flat_cal.csv", "w").write(f"1,{t_s / 1000:.3f}\n100000,{t_s / 1000:.3f}\n")
+    for n in cfg["nodes"]:
+        n["compute_calibration"] = "/tmp/flat_cal.csv"
+    assert json.loads(pl.plan_config(json.dumps(cfg)))["n_microbatches"] == want
+
+
+# ---------------------------------------------------------- schedule / swap-plan parity ----
+def _short(cfg_path, duration=None, warmup=None):
+    cfg = json.load(open(cfg_path))
+    if duration:
+        cfg["workload"]["bench_duration_s"] = duration
+        cfg["workload"]["warmup_s"] = warmup
+    return json.dumps(cfg)
+
+
+REF8 = "/root/reference/proj/configs/reference_8stage.json"
+RING4 = "/root/reference/proj/configs/fig_ring4.json"
+
+
+def _ref_config(name):
+    """The reference's shipped configs; committed copies keep the test runnable off-container."""
+    p = os.path.join("/root/reference/proj/configs", name)
+    return p if os.path.exists(p) else os.path.join(REF_CONFIGS, name)
+
+
+@pytest.mark.parametrize("policy", ["baseline", "offload", "opt"])
+@pytest.mark.parametrize("latency", [0, 16000, 64000, 256000])
+def test_reference_8stage_trace_identical(ref, tmp_path, policy, latency):
+    txt = _short(_ref_config("reference_8stage.json"), 300, 60)
+    assert pl.plan_config(txt, "", policy, latency) == ref.plan_config(txt, "", policy, latency)
+    a, b = str(tmp_path / "a.tr"), str(tmp_path / "b.tr")
+    ra = pl.sim_config(txt, "", policy, latency, trace_path=a)
+    rb = ref.sim_config(txt, "", policy, latency, trace_path=b)
+    assert ra == rb
+    assert sha(a) == sha(b)
+    plan = pl.plan_config(txt, "", policy, latency)
+    assert ref.replay_check(a, plan) == []
+    assert ref.windowed_stats(a, ra["window_start_us"], ra["window_end_us"])[1] == ra["output_tokens"]
+
+
+@pytest.mark.parametrize("policy,latency", [("baseline", 0), ("baseline", 35150), ("opt", 35150), ("offload", 35150)])
+def test_fig_ring4_trace_identical(ref, tmp_path, policy, latency):
+    txt = _short(_ref_config("fig_ring4.json"), 200, 40)
+    a, b = str(tmp_path / "a.tr"), str(tmp_path / "b.tr")
+    assert pl.sim_config(txt, "", policy, latency, trace_path=a) == ref.sim_config(txt, "", policy, latency, trace_path=b)
+    assert sha(a) == sha(b)
+
+
+@pytest.mark.parametrize("name", ["tiny_2stage.json", "tiny_2stage_swap.json", "llama8b_1stage.json",
+                                  "llama8b_4stage.json", "llama8b_4stage_swap.json",
+                                  "llama70b_8stage.json", "llama70b_8stage_swap.json"])
+def test_baseline_configs_trace_identical(ref, tmp_path, name):
+    path = os.path.join(CONFIGS, name)
+    cfg = json.load(open(path))
+    if cfg["workload"]["bench_duration_s"] > 120:
+        cfg["workload"]["bench_duration_s"] = 120
+    txt = json.dumps(cfg)
+    assert pl.plan_config(txt, CONFIGS) == ref.plan_config(txt, CONFIGS)
+    a, b = str(tmp_path / "a.tr"), str(tmp_path / "b.tr")
+    ra = pl.sim_config(txt, CONFIGS, trace_path=a)
+    assert ra == ref.sim_config(txt, CONFIGS, trace_path=b)
+    assert sha(a) == sha(b)
+    assert ref.replay_check(a, pl.plan_config(txt, CONFIGS)) == []
+
+
+def decode_ring(s, nb, b, hop, concurrency=-1):
+    """tests/fixtures.hpp:20-72 as (config, plan) documents."""
+    table1 = GOLD["stage_time_points"]["table1"]
+    t_s = pl.stage_time_us(table1, b, 1, 0)
+    mem = 1 << 40
+    nodes = [{"node_id": f"n{i}", "gpu_mem_bytes": mem, "pcie_bandwidth_bytes_per_s": 32_000_000_000,
+              "compute_calibration": "table1"} for i in range(s)]
+    links = [{"src": f"n{i}", "dst": f"n{(i + 1) % s}", "latency_us": hop,
+              "bandwidth_bytes_per_s": 1_000_000_000_000} for i in range(s)] if s > 1 else []
+    period = max(nb * t_s, s * t_s + s * hop)
+    warm = 10 * period // 1_000_000 + 1
+    cfg = {"model": {"name": "synthetic", "num_layers": s, "weight_bytes_total": 2 + s,
+                     "embedding_bytes": 1, "output_layer_bytes": 1, "kv_bytes_per_token": 8192 * s,
+                     "max_seq_len": 1_000_000_000},
+           "nodes": nodes, "links": links,
+           "workload": {"prompt_len_min": 0, "prompt_len_max": 0, "output_len_min": 900_000_000,
+                        "output_len_max": 900_000_000,
+                        "concurrency_target": nb * b if concurrency < 0 else concurrency,
+                        "bench_duration_s": warm + 100 * period // 1_000_000 + 1, "warmup_s": warm,
+                        "rng_seed": 7}}
+    bud = pl.memory_budget(mem, 1, nb, 0, False)
+    plan = {"n_microbatches": nb, "stage_time_us": t_s, "offload_enabled": False, "converged": True,
+            "iterations": 0, "seq_budget_tokens": 1_000_000_000,
+            "policy": {"offload": False, "nb_override": 0, "prefill_chunk": 256,
+                       "hidden_bytes_per_token": 0, "kv_reserve_permille": 300,
+                       "calibration_ref_layers": 0, "ring_order": "config", "pool_scale_milli": 1000,
+                       "pool_time_basis": "compute"},
+            "stages": [{"node_id": f"n{i}", "layer_begin": i, "layer_end": i + 1, "stage_weight_bytes": 1,
+                        "pcie_bandwidth_bytes_per_s": 32_000_000_000, "batch_size_per_microbatch": b,
+                        "stage_time_us": t_s,
+                        "budget": {"m_total": mem, "m_weights": 1, "m_kv": bud[0], "m_global_pool": 0,
+                                   "n_microbatches": nb, "m_per_microbatch_no_offload": bud[2],
+                                   "m_per_microbatch_offload": bud[3], "offload": False}}
+                       for i in range(s)],
+            "ring_links": json.loads(json.dumps(links))}
+    return cfg, plan
+
+
+@pytest.mark.parametrize("s,nb,b,hop", [(1, 1, 32, 0), (4, 4, 16, 35150), (4, 6, 16, 35150), (2, 2, 8, 0),
+                                        (2, 5, 24, 100000), (3, 7, 12, 50000), (5, 9, 40, 20000),
+                                        (8, 16, 20, 64000), (8, 8, 64, 5000), (6, 24, 16, 250000)])
+def test_decode_ring_fixtures(ref, tmp_path, s, nb, b, hop):
+    cfg, plan = decode_ring(s, nb, b, hop)
+    txt, pj = json.dumps(cfg), json.dumps(plan)
+    a, bpath = str(tmp_path / "a.tr"), str(tmp_path / "b.tr")
+    ra = pl.sim_plan(txt, pj, trace_path=a)
+    assert ra == ref.sim_plan(txt, pj, trace_path=bpath)
+    assert sha(a) == sha(bpath)
+    # analytic oracle within 2% (test_sim.cpp:66-86)
+    assert abs(ra["output_throughput"] - pl.steady_state_throughput(pj)) <= 0.02 * pl.steady_state_throughput(pj)
+    assert pl.steady_state_throughput(pj) == pytest.approx(ref.steady_state(pj), rel=1e-15)
+
+
+def test_decode_ring_closed_forms():
+    cfg, plan = decode_ring(1, 1, 32, 0)
+    r = pl.sim_plan(json.dumps(cfg), json.dumps(plan))
+    assert r["output_throughput"] == pytest.approx(32e6 / 76500, rel=0.01)  # test_sim.cpp:23-31
+    cfg, plan = decode_ring(4, 4, 16, 35150)
+    r = pl.sim_plan(json.dumps(cfg), json.dumps(plan))
+    for st in r["stages"]:  # test_sim.cpp:33-44
+        assert st["bubble_fraction"] == pytest.approx(1 / 3, rel=0.01)
+        assert st["transfer_wait_fraction"] == 0
+
+
+def test_conservation_and_zero_work(ref, tmp_path):
+    cfg, plan = decode_ring(3, 4, 8, 10000)
+    cfg["workload"].update(output_len_min=40, output_len_max=40, prompt_len_min=10, prompt_len_max=10,
+                           concurrency_target=64, bench_duration_s=120, warmup_s=10)
+    a, b = str(tmp_path / "a.tr"), str(tmp_path / "b.tr")
+    r = pl.sim_plan(json.dumps(cfg), json.dumps(plan), trace_path=a)
+    assert r == ref.sim_plan(json.dumps(cfg), json.dumps(plan), trace_path=b) and sha(a) == sha(b)
+    assert r["live_requests"] <= 64 and r["completed_requests"] > 0
+    cfg, plan = decode_ring(2, 2, 4, 1000)
+    cfg["workload"].update(prompt_len_min=0, prompt_len_max=1, output_len_min=0, output_len_max=1,
+                           concurrency_target=32, bench_duration_s=30, warmup_s=2)
+    r = pl.sim_plan(json.dumps(cfg), json.dumps(plan), trace_path=a)
+    assert r == ref.sim_plan(json.dumps(cfg), json.dumps(plan), trace_path=b) and sha(a) == sha(b)
+    assert r["completed_requests"] > 0
+
+
+def test_plan_topology_mismatch():
+    cfg, plan = decode_ring(3, 3, 8, 1000)
+    cfg["links"][0]["latency_us"] += 5
+    with pytest.raises(SimError, match="mismatch"):
+        pl.sim_plan(json.dumps(cfg), json.dumps(plan))
