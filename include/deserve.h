@@ -76,6 +76,13 @@ ds_status ds_sim_config(const char* config_json, const char* config_dir, const c
 ds_status ds_sim_plan(const char* config_json, const char* config_dir, const char* plan_json,
                       const char* trace_path, char* report_json, size_t cap);
 
+/* The recorded schedule the GPU executor replays: {"circuits": [{mb, eff_batch, n_decode, t_end,
+ * rows: [[slot,pos,n_tok,need_logits,is_decode,req_id]...], completed: [slot...]}...],
+ * "ops": per stage [[kind(0 compute,1 swap-in,2 release), mb, slot, circuit, plan_bytes, t_us]...]}. */
+ds_status ds_schedule_config(const char* config_json, const char* config_dir, const char* policy,
+                             int64_t latency_us, int64_t nb_override, int64_t max_circuits, char* out,
+                             size_t cap, size_t* needed);
+
 /* ------------------------------------------------------------------------------------------
  * Stage forward (the compute slot of Engine::on_compute_start, src/sim.cpp:424-425).
  * ------------------------------------------------------------------------------------------ */
@@ -131,6 +138,9 @@ ds_status ds_kv_release(ds_stage* stage, int32_t mb, int32_t slot);
 /* Bytes of KV pages the microbatch holds / holds outside its local pool. */
 ds_status ds_kv_usage(ds_stage* stage, int32_t mb, int64_t* total_bytes, int64_t* global_bytes);
 
+/* 1 if every KV page of mb is device-resident (compute-requires-resident, sim.cpp:629-639). */
+ds_status ds_kv_resident(ds_stage* stage, int32_t mb, int32_t* resident);
+
 /* H2D prefetch of mb's global pages into global slot `slot` after evicting the occupant (D2H),
  * on the stage's copy streams (reference issue_swap_in, sim.cpp:328-353). plan_bytes is the
  * reference's integer contract (logged); the copy moves whole pages. moved_in/out may be NULL. */
@@ -151,11 +161,35 @@ ds_status ds_stage_stream(ds_stage* stage, void** cuda_stream);
 ds_status ds_stage_logits(ds_stage* stage, float* host_out, int64_t max_floats, int64_t* n_floats);
 
 /* ------------------------------------------------------------------------------------------
+ * Whole-pipeline GPU run (the reference's run() with real stage forwards; replay mode).
+ * ------------------------------------------------------------------------------------------ */
+typedef struct ds_gpu_opts {
+    int32_t device0;        /* first CUDA device */
+    int32_t n_devices;      /* 0 = all visible; stage s runs on device0 + s % n_devices */
+    int32_t real_delay;     /* 1: a hop may not arrive before completion + latency + bytes/bw */
+    int32_t collect_tokens; /* 1: report the sampled ids of every circuit */
+    int64_t max_circuits;   /* execute the first circuits of the schedule (0 = all) */
+    uint64_t weight_seed;
+} ds_gpu_opts;
+
+/* Plans the config (as ds_plan_config), schedules it in virtual time, then executes the schedule on
+ * GPUs: per stage, computes / swap-ins / releases in schedule order, hops with injected delay.
+ * report_json: circuits, decode tokens, wall time, per-stage busy time and (rows, ms) per step,
+ * swap plan vs moved bytes, residency top-ups, optionally the sampled ids. */
+ds_status ds_gpu_run_config(const char* config_json, const char* config_dir, const char* policy,
+                            int64_t latency_us, int64_t nb_override, const ds_model_desc* model,
+                            const ds_gpu_opts* opts, char* report_json, size_t cap, size_t* needed);
+
+/* ------------------------------------------------------------------------------------------
  * Kernel-level entry points (parity tests call these through the same library).
  * ------------------------------------------------------------------------------------------ */
 ds_status ds_dbg_gemm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t N, int32_t K,
                       int32_t epi, const uint16_t* resid, int32_t k_splits, void* out);
 ds_status ds_dbg_has_device(int32_t* n_devices);
+ds_status ds_dbg_alloc(int32_t device, int64_t bytes, void** out);
+ds_status ds_dbg_free(void* ptr);
+/* synchronous copy in any direction (cudaMemcpyDefault, unified addressing) */
+ds_status ds_dbg_copy(void* dst, const void* src, int64_t bytes);
 
 #ifdef __cplusplus
 }

@@ -56,6 +56,12 @@ class Row(C.Structure):
                 ("req_id", C.c_int64)]
 
 
+class GpuOpts(C.Structure):
+    _fields_ = [("device0", C.c_int32), ("n_devices", C.c_int32), ("real_delay", C.c_int32),
+                ("collect_tokens", C.c_int32), ("max_circuits", C.c_int64),
+                ("weight_seed", C.c_uint64)]
+
+
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is not built; run `make -C {_HERE}/csrc` "
@@ -86,8 +92,14 @@ def _load() -> C.CDLL:
         "ds_stage_sync": (I32, [P]),
         "ds_stage_stream": (I32, [P, P]),
         "ds_stage_logits": (I32, [P, P, I64, P]),
+        "ds_kv_resident": (I32, [P, I32, P]),
+        "ds_schedule_config": (I32, [S, S, S, I64, I64, I64, P, C.c_size_t, P]),
+        "ds_gpu_run_config": (I32, [S, S, S, I64, I64, P, P, P, C.c_size_t, P]),
         "ds_dbg_gemm": (I32, [P, P, I32, I32, I32, I32, P, I32, P]),
         "ds_dbg_has_device": (I32, [P]),
+        "ds_dbg_alloc": (I32, [I32, I64, P]),
+        "ds_dbg_free": (I32, [P]),
+        "ds_dbg_copy": (I32, [P, P, I64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -397,6 +397,17 @@ ds_status ds_kv_usage(ds_stage* s, int32_t mb, int64_t* total, int64_t* global) 
     return DS_OK;
 }
 
+ds_status ds_kv_resident(ds_stage* s, int32_t mb, int32_t* resident) {
+    if (!s || mb < 0 || mb >= s->n_mb || !resident) return ds_fail(DS_ERR_ARG, "bad mb");
+    const MbKv& k = s->mbs[mb];
+    int32_t ok = 1;
+    for (const auto& v : k.pages)
+        for (int32_t h : v)
+            if (h < 0 && k.host_dev[-h - 1] < 0) ok = 0;
+    *resident = ok;
+    return DS_OK;
+}
+
 ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, int64_t* moved_in,
                      int64_t* moved_out) {
     (void)plan_bytes;
@@ -681,6 +692,21 @@ ds_status ds_stage_logits(ds_stage* s, float* host_out, int64_t max_floats, int6
         CK(cudaMemcpy(host_out, s->logits, size_t(std::min(n, max_floats)) * 4,
                       cudaMemcpyDeviceToHost));
     }
+    return DS_OK;
+}
+
+ds_status ds_dbg_alloc(int32_t device, int64_t bytes, void** out) {
+    CK(cudaSetDevice(device));
+    CK(cudaMalloc(out, size_t(bytes)));
+    return DS_OK;
+}
+ds_status ds_dbg_free(void* p) {
+    CK(cudaFree(p));
+    return DS_OK;
+}
+ds_status ds_dbg_copy(void* dst, const void* src, int64_t bytes) {
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(dst, src, size_t(bytes), cudaMemcpyDefault));
     return DS_OK;
 }
 

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "capi_util.hpp"
+#include "executor.hpp"
 #include "pipeline.hpp"
 
 namespace {
@@ -172,6 +173,74 @@ ds_status ds_sim_plan(const char* config_json, const char* config_dir, const cha
             f.write(t.data(), std::streamsize(t.size()));
         }
         copy_out(o.report.to_json(), report_json, cap, nullptr);
+        return DS_OK;
+    });
+}
+
+ds_status ds_schedule_config(const char* config_json, const char* config_dir, const char* policy,
+                             int64_t latency_us, int64_t nb_override, int64_t max_circuits, char* out,
+                             size_t cap, size_t* needed) {
+    return guarded([&] {
+        auto cp = dsb::plan_from_config(config_json, config_dir, policy, latency_us, nb_override);
+        dsb::SimOutput o = dsb::simulate(cp.second, cp.first.topo, cp.first.workload, cp.first.model,
+                                         false, true);
+        const dsb::Schedule& sc = o.schedule;
+        const int64_t n = max_circuits > 0 ? std::min<int64_t>(max_circuits, sc.circuits.size())
+                                           : int64_t(sc.circuits.size());
+        std::string js = "{\"circuits\":[";
+        for (int64_t c = 0; c < n; ++c) {
+            const auto& ci = sc.circuits[c];
+            js += (c ? ",{" : "{") + std::string("\"mb\":") + std::to_string(ci.mb) +
+                  ",\"eff_batch\":" + std::to_string(ci.eff_batch) + ",\"n_decode\":" +
+                  std::to_string(ci.n_decode) + ",\"t_end\":" + std::to_string(ci.t_end) + ",\"rows\":[";
+            for (size_t k = 0; k < ci.rows.size(); ++k) {
+                const auto& r = ci.rows[k];
+                js += (k ? ",[" : "[") + std::to_string(r.slot) + "," + std::to_string(r.pos) + "," +
+                      std::to_string(r.n_tok) + "," + std::to_string(r.need_logits) + "," +
+                      std::to_string(r.is_decode) + "," + std::to_string(r.req) + "]";
+            }
+            js += "],\"completed\":[";
+            for (size_t k = 0; k < ci.completed_slots.size(); ++k)
+                js += (k ? "," : "") + std::to_string(ci.completed_slots[k]);
+            js += "]}";
+        }
+        js += "],\"ops\":[";
+        for (size_t s = 0; s < sc.ops.size(); ++s) {
+            js += s ? ",[" : "[";
+            bool first = true;
+            for (const auto& op : sc.ops[s]) {
+                if (op.kind == dsb::OpKind::Compute && op.circuit >= n) break;
+                js += (first ? "[" : ",[") + std::to_string(int(op.kind)) + "," + std::to_string(op.mb) +
+                      "," + std::to_string(op.slot) + "," + std::to_string(op.circuit) + "," +
+                      std::to_string(op.plan_bytes) + "," + std::to_string(op.t) + "]";
+                first = false;
+            }
+            js += "]";
+        }
+        js += "]}";
+        copy_out(js, out, cap, needed);
+        return DS_OK;
+    });
+}
+
+ds_status ds_gpu_run_config(const char* config_json, const char* config_dir, const char* policy,
+                            int64_t latency_us, int64_t nb_override, const ds_model_desc* model,
+                            const ds_gpu_opts* opts, char* report_json, size_t cap, size_t* needed) {
+    return guarded([&] {
+        if (!model || !opts) return ds_fail(DS_ERR_ARG, "null model/opts");
+        auto cp = dsb::plan_from_config(config_json, config_dir, policy, latency_us, nb_override);
+        dsb::SimOutput o = dsb::simulate(cp.second, cp.first.topo, cp.first.workload, cp.first.model,
+                                         false, true);
+        dsb::GpuOptions g;
+        g.device0 = opts->device0;
+        g.n_devices = opts->n_devices;
+        g.real_delay = opts->real_delay != 0;
+        g.collect_tokens = opts->collect_tokens != 0;
+        g.max_circuits = opts->max_circuits;
+        g.weight_seed = opts->weight_seed;
+        dsb::GpuRunResult r = dsb::run_on_gpus(cp.first, cp.second, o.schedule, *model, g);
+        copy_out(r.to_json(), report_json, cap, needed);
+        if (!r.error.empty()) return ds_fail(DS_ERR_RUNTIME, r.error);
         return DS_OK;
     });
 }

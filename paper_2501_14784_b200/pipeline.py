@@ -86,3 +86,55 @@ def steady_state_throughput(plan_json: str) -> float:
     out = C.c_double(0)
     check(lib.ds_steady_state_throughput(_b(plan_json), C.byref(out)))
     return out.value
+
+
+# --------------------------------------------------------------------------- GPU path ----
+# Architecture dims per config model name (the reference ModelSpec carries only byte totals;
+# kv_bytes_per_token must equal 4 * n_kv * d_head * n_layers, checked by the executor).
+MODEL_DIMS = {
+    "tiny-llama": dict(n_layers=4, d_model=256, n_heads=4, n_kv_heads=2, d_head=64, ffn=768,
+                       vocab=128256, max_seq_len=8192, rope_theta=500000.0, norm_eps=1e-5),
+    "llama3-8b": dict(n_layers=32, d_model=4096, n_heads=32, n_kv_heads=8, d_head=128, ffn=14336,
+                      vocab=128256, max_seq_len=8192, rope_theta=500000.0, norm_eps=1e-5),
+    "llama3-70b-bf16": dict(n_layers=80, d_model=8192, n_heads=64, n_kv_heads=8, d_head=128,
+                            ffn=28672, vocab=128256, max_seq_len=8192, rope_theta=500000.0,
+                            norm_eps=1e-5),
+}
+WEIGHT_SEED = 0x5EED0001
+
+
+def model_desc(name_or_dims):
+    from ._native import ModelDesc
+    d = MODEL_DIMS[name_or_dims] if isinstance(name_or_dims, str) else name_or_dims
+    return ModelDesc(**d)
+
+
+def schedule_config(config_text: str, config_dir: str = "", policy=None, latency_us=-1,
+                    nb_override=-1, max_circuits=0) -> dict:
+    need = C.c_size_t(0)
+    check(lib.ds_schedule_config(_b(config_text), _b(config_dir), _b(policy or ""), latency_us,
+                                 nb_override, max_circuits, None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    check(lib.ds_schedule_config(_b(config_text), _b(config_dir), _b(policy or ""), latency_us,
+                                 nb_override, max_circuits, buf, need.value, None))
+    return json.loads(buf.value.decode())
+
+
+def gpu_run_config(config_text: str, config_dir: str = "", policy=None, latency_us=-1,
+                   nb_override=-1, model=None, device0=0, n_devices=0, real_delay=True,
+                   collect_tokens=False, max_circuits=0, weight_seed=WEIGHT_SEED) -> dict:
+    """Plan + schedule + execute on GPUs (replay mode). Raises on any CUDA/KV/runtime error."""
+    from ._native import GpuOpts
+    if model is None:
+        model = json.loads(config_text)["model"]["name"]
+    md = model_desc(model)
+    opts = GpuOpts(device0=device0, n_devices=n_devices, real_delay=int(real_delay),
+                   collect_tokens=int(collect_tokens), max_circuits=max_circuits,
+                   weight_seed=weight_seed)
+    need = C.c_size_t(0)
+    cap = 1 << 26
+    buf = C.create_string_buffer(cap)
+    st = lib.ds_gpu_run_config(_b(config_text), _b(config_dir), _b(policy or ""), latency_us,
+                               nb_override, C.byref(md), C.byref(opts), buf, cap, C.byref(need))
+    check(st)
+    return json.loads(buf.value.decode())
