@@ -78,9 +78,11 @@ def test_llama8b_dims_first_stage_activations():
     try:
         for rows in ([(0, 0, 33, 1, 0, 1), (1, 0, 1, 1, 1, 2), (2, 0, 260, 1, 0, 3)],
                      [(1, 1, 1, 1, 1, 2), (0, 33, 4, 1, 0, 1)]):
-            if rows[0][4]:
+            ids = None
+            if rows[0][4]:  # previous circuit sampled rows: slots 0, 1, 2
                 p.last_tok[(0, 1)] = 1234
-            o = p.step(0, rows)
+                ids = np.array([111, 1234, 222], dtype=np.int32)
+            o = p.step(0, rows, ids_in=ids)
             err = np.abs(o["gpu_act"] - o["cpu_act"]).max(axis=1)
             scale = np.abs(o["cpu_act"]).max(axis=1)
             assert np.all(err <= 0.03 * scale), (err / scale).max()
