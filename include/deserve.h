@@ -138,6 +138,14 @@ ds_status ds_kv_release(ds_stage* stage, int32_t mb, int32_t slot);
 /* Bytes of KV pages the microbatch holds / holds outside its local pool. */
 ds_status ds_kv_usage(ds_stage* stage, int32_t mb, int64_t* total_bytes, int64_t* global_bytes);
 
+/* Frees every page of every microbatch (pools and pinned backing stay allocated). */
+ds_status ds_kv_reset(ds_stage* stage);
+/* Enables CUDA-event timing around every launch group of ds_stage_step (clears the records). */
+ds_status ds_stage_profile(ds_stage* stage, int32_t enable);
+/* JSON {kind: {n, ms, flops, bytes, rows}} for kinds gemm_qkv, attention, gemm_o, gemm_gate_up,
+ * gemm_down, gemm_lm_head, elementwise (algorithmic FLOPs / bytes); *launches = kernel
+ * launches issued by this stage since creation. Clears the timing records. */
+ds_status ds_stage_kernel_stats(ds_stage* stage, char* out, size_t cap, int64_t* launches);
 /* 1 if every KV page of mb is device-resident (compute-requires-resident, sim.cpp:629-639). */
 ds_status ds_kv_resident(ds_stage* stage, int32_t mb, int32_t* resident);
 
@@ -179,6 +187,17 @@ typedef struct ds_gpu_opts {
 ds_status ds_gpu_run_config(const char* config_json, const char* config_dir, const char* policy,
                             int64_t latency_us, int64_t nb_override, const ds_model_desc* model,
                             const ds_gpu_opts* opts, char* report_json, size_t cap, size_t* needed);
+
+/* The same run as a reusable session: stages and weights are created once; every ds_session_run
+ * replays the schedule from empty KV pools (bench warm-up / timed runs). profile = 1 adds CUDA
+ * events around every launch group (report "kernels": algorithmic FLOPs/bytes and ms per kind). */
+typedef struct ds_session ds_session;
+ds_status ds_session_create(const char* config_json, const char* config_dir, const char* policy,
+                            int64_t latency_us, int64_t nb_override, const ds_model_desc* model,
+                            const ds_gpu_opts* opts, ds_session** out);
+ds_status ds_session_run(ds_session* session, int32_t profile, int32_t collect_tokens,
+                         char* report_json, size_t cap, size_t* needed);
+ds_status ds_session_destroy(ds_session* session);
 
 /* ------------------------------------------------------------------------------------------
  * Kernel-level entry points (parity tests call these through the same library).

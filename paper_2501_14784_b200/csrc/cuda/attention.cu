@@ -172,6 +172,10 @@ static int pick_attn_splits(int T, int n_kv, int max_ctx) {
     return s < 1 ? 1 : s;
 }
 
+int attention_launches(int T, int n_kv, int max_ctx) {
+    return T > 0 ? (pick_attn_splits(T, n_kv, max_ctx) > 1 ? 2 : 1) : 0;
+}
+
 size_t attention_workspace_floats(int T, int n_h, int d_head, int splits) {
     return size_t(T) * n_h * splits * (d_head + 2);
 }

@@ -59,6 +59,7 @@ void rope_kv_append(const __nv_bfloat16* qkv, int T, int n_h, int n_kv, int d_he
 
 // Paged causal attention: row t attends positions [0, row_pos[t]] of its request, whose pages
 // are flat_pages[row_page_off[t] ...]. Output o[T, n_h * d_head] bf16.
+int attention_launches(int T, int n_kv, int max_ctx);
 size_t attention_workspace_floats(int T, int n_h, int d_head, int splits);
 int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,
                     const int32_t* row_page_off, const int32_t* flat_pages, const KvLayout& kv,

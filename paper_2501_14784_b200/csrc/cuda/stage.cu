@@ -101,6 +101,20 @@ struct ds_stage {
     int32_t* last_token = nullptr;    // [n_mb * max_slots]
     int32_t* pending_ids = nullptr;   // [n_mb * max_rows] (single-stage loopback)
 
+    // kernel profiling (CUDA events around every launch group; ds_stage_profile)
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    struct ProfRec {
+        int kind;
+        int64_t rows;
+        double flops, bytes;
+        size_t e0, e1;
+    };
+    std::vector<ProfRec> recs;
+    int64_t launches = 0;
+    int64_t h2d_bytes = 0;
+
     // last step
     int last_T = 0, last_R = 0;
     int64_t moved_in_total = 0, moved_out_total = 0;
@@ -122,6 +136,20 @@ uint8_t* host_page_ptr(ds_stage* s, int mb, int h) {
     return s->host_backing + (size_t(mb) * s->host_pages + h) * size_t(s->page_bytes);
 }
 bf16* dev_page_ptr(ds_stage* s, int p) { return s->kv.pool + size_t(p) * s->kv.page_elems; }
+
+enum ProfKind { PK_QKV, PK_ATTN, PK_O, PK_GU, PK_DOWN, PK_LMHEAD, PK_ELEM, PK_COUNT };
+const char* kPkName[PK_COUNT] = {"gemm_qkv", "attention", "gemm_o", "gemm_gate_up", "gemm_down",
+                                 "gemm_lm_head", "elementwise"};
+
+size_t prof_mark(ds_stage* s) {
+    if (s->ev_used == s->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        s->ev_pool.push_back(e);
+    }
+    cudaEventRecord(s->ev_pool[s->ev_used], s->stream);
+    return s->ev_used++;
+}
 
 }  // namespace
 
@@ -342,22 +370,39 @@ ds_status ds_kv_create(ds_stage* s, int64_t page_bytes, int64_t n_mb, int64_t lo
     if ((st = alloc_dev(reinterpret_cast<void**>(&s->pending_ids), size_t(n_mb) * s->max_rows * 4)))
         return st;
     s->mbs.assign(s->n_mb, MbKv());
+    for (int b = 0; b < s->n_mb; ++b)
+        CK(cudaEventCreateWithFlags(&s->mbs[b].last_compute, cudaEventDisableTiming));
+    return ds_kv_reset(s);
+}
+
+// Frees every page and forgets all requests (pool memory and host backing are kept).
+ds_status ds_kv_reset(ds_stage* s) {
+    if (!s || s->mbs.empty()) return ds_fail(DS_ERR_ARG, "ds_kv_create not called");
+    CK(cudaSetDevice(s->device));
+    CK(cudaDeviceSynchronize());
     for (int b = 0; b < s->n_mb; ++b) {
         MbKv& k = s->mbs[b];
+        k.local_free.clear();
         for (int p = s->local_pages - 1; p >= 0; --p) k.local_free.push_back(b * s->local_pages + p);
         k.pages.assign(s->max_slots, {});
         k.slot_req.assign(s->max_slots, -1);
+        k.host_free.clear();
         for (int h = s->host_pages - 1; h >= 0; --h) k.host_free.push_back(h);
         k.host_dev.assign(s->host_pages, -1);
-        CK(cudaEventCreateWithFlags(&k.last_compute, cudaEventDisableTiming));
+        k.resident_slot = -1;
+        k.computed = false;
+        k.prev_logit_slots.clear();
     }
     const int base = s->n_mb * s->local_pages;
     for (int g = 0; g < 2; ++g) {
+        s->gslot[g].owner = -1;
         s->gslot[g].dev_pages.clear();
         s->gslot[g].free.clear();
         for (int p = 0; p < s->slot_pages; ++p) s->gslot[g].dev_pages.push_back(base + g * s->slot_pages + p);
         for (int p = s->slot_pages - 1; p >= 0; --p) s->gslot[g].free.push_back(base + g * s->slot_pages + p);
     }
+    CK(cudaMemset(s->last_token, 0, size_t(s->n_mb) * s->max_slots * 4));
+    s->moved_in_total = s->moved_out_total = 0;
     return DS_OK;
 }
 
@@ -577,6 +622,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     }
     const size_t meta_n = size_t(flat - hm) + P;
     CK(cudaMemcpyAsync(s->d_meta, hm, meta_n * 4, cudaMemcpyHostToDevice, s->stream));
+    s->h2d_bytes += int64_t(meta_n) * 4;
     CK(cudaEventRecord(s->meta_ev[buf], s->stream));
     const int32_t* d_prompt = s->d_meta;
     const int32_t* d_slot = d_prompt + T;
@@ -596,44 +642,96 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     if (s->first) {
         const int32_t* ids_in = static_cast<const int32_t*>(act_in);
         if (!ids_in && s->last && prevR > 0) ids_in = s->pending_ids + size_t(mb) * s->max_rows;
-        if (ids_in && prevR > 0) ds::scatter_tokens(ids_in, d_prev, prevR, s->last_token, st);
+        if (ids_in && prevR > 0) {
+            ds::scatter_tokens(ids_in, d_prev, prevR, s->last_token, st);
+            s->launches++;
+        }
         int32_t* tokens = s->ids;  // scratch: resolved token ids for this step
         ds::resolve_tokens(d_prompt, d_slot, s->last_token, T, tokens, st);
         ds::embed_rows(s->emb, tokens, T, d, s->x, st);
+        s->launches += 2;
     } else {
         if (!act_in) return ds_fail(DS_ERR_ARG, "non-first stage needs activations");
         CK(cudaMemcpyAsync(s->x, act_in, size_t(T) * d * 2, cudaMemcpyDeviceToDevice, st));
     }
+    // algorithmic work per launch group (roofline accounting)
+    const int qkv_rows = m.n_heads * m.d_head + 2 * m.n_kv_heads * m.d_head;
+    const int qdim = m.n_heads * m.d_head;
+    double attn_bytes = 0, attn_flops = 0;
+    for (int64_t i = 0; i < n_rows; ++i) {
+        const double end = double(rows[i].pos + rows[i].n_tok);
+        attn_bytes += end * m.n_kv_heads * m.d_head * 4.0;
+        for (int j = 0; j < rows[i].n_tok; ++j)
+            attn_flops += 4.0 * m.n_heads * m.d_head * double(rows[i].pos + j + 1);
+    }
+    attn_bytes += double(T) * qdim * 4.0;
+    size_t mark = 0;
+    auto begin = [&]() { if (s->prof) mark = prof_mark(s); };
+    auto end_gemm = [&](int kind, int rows_, int N, int K, int out_bytes) {
+        s->launches += ds::gemm_pick_splits(rows_, N, K) > 1 ? 2 : 1;
+        if (!s->prof) return;
+        const size_t e1 = prof_mark(s);
+        s->recs.push_back({kind, rows_, 2.0 * rows_ * N * K,
+                           2.0 * N * K + 2.0 * rows_ * K + double(out_bytes) * rows_ * N, mark, e1});
+    };
+    auto end_other = [&](int kind, double flops, double bytes, int n_launch) {
+        s->launches += n_launch;
+        if (!s->prof) return;
+        const size_t e1 = prof_mark(s);
+        s->recs.push_back({kind, T, flops, bytes, mark, e1});
+    };
     for (int li = 0; li < s->L; ++li) {
         LayerW& lw = s->layers[li];
+        begin();
         ds::rmsnorm_rows(s->x, nullptr, T, d, lw.attn_norm, m.norm_eps, s->xn, st);
+        end_other(PK_ELEM, 0, 4.0 * T * d, 1);
+        begin();
         int rc = ds::gemm_bf16(lw.wqkv, s->xn, T, ds::EPI_BF16, s->qkv, nullptr, nullptr, s->ws,
                                s->ws_floats, 0, st);
+        end_gemm(PK_QKV, T, qkv_rows, d, 2);
+        begin();
         ds::rope_kv_append(s->qkv, T, m.n_heads, m.n_kv_heads, m.d_head, d_pos, d_page, s->rope_cos,
                            s->rope_sin, s->kv, li, s->q, st);
+        end_other(PK_ELEM, 0, 2.0 * T * qkv_rows + 2.0 * T * (qdim + 2 * m.n_kv_heads * m.d_head), 1);
+        begin();
         rc |= ds::attention_paged(s->q, T, m.n_heads, d_pos, d_poff, d_flat, s->kv, li, max_ctx,
                                   s->attn, s->attn_ws, s->attn_ws_floats, st);
+        end_other(PK_ATTN, attn_flops, attn_bytes, ds::attention_launches(T, m.n_kv_heads, max_ctx));
+        begin();
         rc |= ds::gemm_bf16(lw.wo, s->attn, T, ds::EPI_RESID, s->x, s->x, nullptr, s->ws,
                             s->ws_floats, 0, st);
+        end_gemm(PK_O, T, d, qdim, 4);
+        begin();
         ds::rmsnorm_rows(s->x, nullptr, T, d, lw.mlp_norm, m.norm_eps, s->xn, st);
+        end_other(PK_ELEM, 0, 4.0 * T * d, 1);
+        begin();
         rc |= ds::gemm_bf16(lw.wgu, s->xn, T, ds::EPI_BF16, s->gu, nullptr, nullptr, s->ws,
                             s->ws_floats, 0, st);
+        end_gemm(PK_GU, T, 2 * m.ffn, d, 2);
+        begin();
         ds::silu_mul(s->gu, T, m.ffn, s->h, st);
+        end_other(PK_ELEM, 0, 6.0 * T * m.ffn, 1);
+        begin();
         rc |= ds::gemm_bf16(lw.wd, s->h, T, ds::EPI_RESID, s->x, s->x, nullptr, s->ws, s->ws_floats,
                             0, st);
+        end_gemm(PK_DOWN, T, d, m.ffn, 4);
         if (rc) return ds_fail(DS_ERR_RUNTIME, "kernel launch failed in layer " + std::to_string(li));
     }
     if (s->last) {
         int32_t* ids_out = act_out ? static_cast<int32_t*>(act_out)
                                    : (s->first ? s->pending_ids + size_t(mb) * s->max_rows : s->ids);
         if (R > 0) {
+            begin();
             ds::rmsnorm_rows(s->x, d_lrows, R, d, s->final_norm, m.norm_eps, s->xn, st);
+            end_other(PK_ELEM, 0, 4.0 * R * d, 1);
+            begin();
             if (ds::gemm_bf16(s->lm_head, s->xn, R, ds::EPI_F32, nullptr, nullptr, s->logits, s->ws,
                               s->ws_floats, 0, st))
                 return ds_fail(DS_ERR_RUNTIME, "lm_head launch failed");
+            end_gemm(PK_LMHEAD, R, m.vocab, d, 4);
+            begin();
             ds::argmax_rows(s->logits, R, m.vocab, ids_out, st);
-            if (act_out == nullptr && s->first == false)
-                ;  // ids stay in s->ids
+            end_other(PK_ELEM, 0, 4.0 * R * m.vocab, 1);
             if (s->first && act_out)
                 CK(cudaMemcpyAsync(s->pending_ids + size_t(mb) * s->max_rows, ids_out, size_t(R) * 4,
                                    cudaMemcpyDeviceToDevice, st));
@@ -650,6 +748,49 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     s->last_T = T;
     s->last_R = R;
     CK(cudaPeekAtLastError());
+    return DS_OK;
+}
+
+ds_status ds_stage_profile(ds_stage* s, int32_t enable) {
+    if (!s) return ds_fail(DS_ERR_ARG, "null stage");
+    s->prof = enable != 0;
+    s->recs.clear();
+    s->ev_used = 0;
+    return DS_OK;
+}
+
+// Per launch-group kind: launches, total ms, algorithmic FLOPs and bytes, since the last reset.
+ds_status ds_stage_kernel_stats(ds_stage* s, char* out, size_t cap, int64_t* launches) {
+    if (!s) return ds_fail(DS_ERR_ARG, "null stage");
+    CK(cudaSetDevice(s->device));
+    CK(cudaStreamSynchronize(s->stream));
+    double ms[PK_COUNT] = {0}, fl[PK_COUNT] = {0}, by[PK_COUNT] = {0};
+    int64_t n[PK_COUNT] = {0}, rows[PK_COUNT] = {0};
+    for (const auto& r : s->recs) {
+        float t = 0;
+        CK(cudaEventElapsedTime(&t, s->ev_pool[r.e0], s->ev_pool[r.e1]));
+        ms[r.kind] += t;
+        fl[r.kind] += r.flops;
+        by[r.kind] += r.bytes;
+        n[r.kind]++;
+        rows[r.kind] += r.rows;
+    }
+    std::string js = "{";
+    char buf[256];
+    for (int k = 0; k < PK_COUNT; ++k) {
+        snprintf(buf, sizeof buf, "%s\"%s\":{\"n\":%lld,\"ms\":%.6f,\"flops\":%.6e,\"bytes\":%.6e,\"rows\":%lld}",
+                 k ? "," : "", kPkName[k], (long long)n[k], ms[k], fl[k], by[k], (long long)rows[k]);
+        js += buf;
+    }
+    js += ",\"h2d_bytes\":" + std::to_string(s->h2d_bytes) + "}";
+    if (out && cap) {
+        const size_t c = std::min(cap - 1, js.size());
+        memcpy(out, js.data(), c);
+        out[c] = 0;
+    }
+    if (launches) *launches = s->launches;
+    s->recs.clear();
+    s->ev_used = 0;
     return DS_OK;
 }
 

@@ -223,6 +223,56 @@ ds_status ds_schedule_config(const char* config_json, const char* config_dir, co
     });
 }
 
+struct ds_session {
+    dsb::Session* s = nullptr;
+};
+
+ds_status ds_session_create(const char* config_json, const char* config_dir, const char* policy,
+                            int64_t latency_us, int64_t nb_override, const ds_model_desc* model,
+                            const ds_gpu_opts* opts, ds_session** out) {
+    return guarded([&] {
+        if (!model || !opts || !out) return ds_fail(DS_ERR_ARG, "null argument");
+        auto cp = dsb::plan_from_config(config_json, config_dir, policy, latency_us, nb_override);
+        dsb::SimOutput o = dsb::simulate(cp.second, cp.first.topo, cp.first.workload, cp.first.model,
+                                         false, true);
+        dsb::GpuOptions g;
+        g.device0 = opts->device0;
+        g.n_devices = opts->n_devices;
+        g.real_delay = opts->real_delay != 0;
+        g.collect_tokens = opts->collect_tokens != 0;
+        g.max_circuits = opts->max_circuits;
+        g.weight_seed = opts->weight_seed;
+        ds_session* h = new ds_session();
+        try {
+            h->s = dsb::session_create(cp.first, cp.second, std::move(o.schedule), *model, g);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+        return DS_OK;
+    });
+}
+
+ds_status ds_session_run(ds_session* h, int32_t profile, int32_t collect_tokens, char* report_json,
+                         size_t cap, size_t* needed) {
+    return guarded([&] {
+        if (!h || !h->s) return ds_fail(DS_ERR_ARG, "null session");
+        dsb::GpuRunResult r = dsb::session_run(h->s, profile != 0, collect_tokens != 0);
+        copy_out(r.to_json(), report_json, cap, needed);
+        if (!r.error.empty()) return ds_fail(DS_ERR_RUNTIME, r.error);
+        return DS_OK;
+    });
+}
+
+ds_status ds_session_destroy(ds_session* h) {
+    return guarded([&] {
+        if (h) dsb::session_destroy(h->s);
+        delete h;
+        return DS_OK;
+    });
+}
+
 ds_status ds_gpu_run_config(const char* config_json, const char* config_dir, const char* policy,
                             int64_t latency_us, int64_t nb_override, const ds_model_desc* model,
                             const ds_gpu_opts* opts, char* report_json, size_t cap, size_t* needed) {

@@ -9,6 +9,9 @@
 // latency_us + ceil(payload * 1e6 / bw) (reference send_onward, src/sim.cpp:430-439), measured on
 // the host clock from a stream callback at the producer's completion. Only timestamps differ from
 // the virtual-clock trace; the integer contract (rows, swap bytes, slots) is executed verbatim.
+//
+// A Session owns the stages (weights initialised once) so the schedule can be replayed many
+// times (bench warm-up + timed runs); each run starts from empty KV pools.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -26,9 +29,6 @@
 #include "pipeline.hpp"
 
 namespace dsb {
-
-std::pair<Config, Plan> plan_from_config(const char* json_text, const char* dir, const char* policy,
-                                         int64_t latency_us, int64_t nb_override);
 
 namespace {
 
@@ -66,7 +66,7 @@ void CUDART_CB post_cb(void* p) {
     PostCtx* c = static_cast<PostCtx*>(p);
     {
         std::lock_guard<std::mutex> lk(c->box->mu);
-        c->box->posted = c->circuit;
+        c->box->posted = std::max(c->box->posted, c->circuit);
         c->box->t_done = now_us();
     }
     c->box->cv.notify_all();
@@ -74,8 +74,8 @@ void CUDART_CB post_cb(void* p) {
 }
 
 struct StepTiming {
-    cudaEvent_t a, b;
-    int64_t rows;
+    cudaEvent_t a = nullptr, b = nullptr;
+    int64_t rows = 0;
 };
 
 struct Worker {
@@ -85,7 +85,9 @@ struct Worker {
     cudaStream_t stream = nullptr;
     std::vector<std::unique_ptr<Mailbox>> in;  // per mb: input from the previous stage
     std::vector<void*> recv;                   // per mb: device buffer for that input
-    std::vector<StepTiming> timing;
+    std::vector<StepTiming> timing;            // event pool, reused across runs
+    size_t timing_used = 0;
+    cudaEvent_t t_begin = nullptr, t_end = nullptr;
     int64_t served = 0, topups = 0;
     int64_t moved_in = 0, moved_out = 0, plan_in = 0;
     int64_t computes = 0;
@@ -94,9 +96,28 @@ struct Worker {
 
 }  // namespace
 
-GpuRunResult run_on_gpus(const Config& cfg, const Plan& plan, const Schedule& sched,
-                         const ds_model_desc& md, const GpuOptions& opt) {
-    const int64_t S = plan.S();
+struct Session {
+    Config cfg;
+    Plan plan;
+    Schedule sched;
+    ds_model_desc md{};
+    GpuOptions opt;
+    int64_t n_circ = 0, max_rows = 16, B = 1;
+    std::vector<int64_t> prev;
+    std::vector<Worker> W;
+    int32_t* tok_pool = nullptr;
+    std::vector<int64_t> tok_off;
+};
+
+Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, const ds_model_desc& md,
+                        const GpuOptions& opt) {
+    std::unique_ptr<Session> S(new Session());
+    S->cfg = cfg;
+    S->plan = plan;
+    S->sched = std::move(sched);
+    S->md = md;
+    S->opt = opt;
+    const int64_t NS = plan.S();
     const int64_t NB = plan.n_mb;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -106,39 +127,39 @@ GpuRunResult run_on_gpus(const Config& cfg, const Plan& plan, const Schedule& sc
     if (cfg.model.kv_bytes_per_token != want_kv)
         throw ConfigError("model kv_bytes_per_token " + std::to_string(cfg.model.kv_bytes_per_token) +
                           " != 4*n_kv*d_head*L = " + std::to_string(want_kv));
+    if (md.n_layers != cfg.model.num_layers) throw ConfigError("model layer count mismatch");
 
-    // circuit limit and per-circuit bookkeeping
-    const int64_t n_circ = opt.max_circuits > 0 ? std::min<int64_t>(opt.max_circuits, sched.circuits.size())
-                                                : int64_t(sched.circuits.size());
-    int64_t max_rows = 16, max_slot = 1;
-    for (int64_t c = 0; c < n_circ; ++c) {
-        max_rows = std::max(max_rows, sched.circuits[c].eff_batch);
-        for (const auto& r : sched.circuits[c].rows) max_slot = std::max<int64_t>(max_slot, r.slot + 1);
+    const auto& circs = S->sched.circuits;
+    S->n_circ = opt.max_circuits > 0 ? std::min<int64_t>(opt.max_circuits, circs.size())
+                                     : int64_t(circs.size());
+    int64_t max_slot = 1;
+    for (int64_t c = 0; c < S->n_circ; ++c) {
+        S->max_rows = std::max(S->max_rows, circs[c].eff_batch);
+        for (const auto& r : circs[c].rows) max_slot = std::max<int64_t>(max_slot, r.slot + 1);
     }
-    max_rows = (max_rows + 15) / 16 * 16;
-    const int64_t B = std::min<int64_t>(plan.B(), std::max<int64_t>(max_slot, 1));
-    // previous circuit of the same microbatch (stage 0 input dependency)
-    std::vector<int64_t> prev(n_circ, -1);
+    S->max_rows = (S->max_rows + 15) / 16 * 16;
+    S->B = std::min<int64_t>(plan.B(), max_slot);
+    S->prev.assign(S->n_circ, -1);
     {
         std::vector<int64_t> last(NB, -1);
-        for (int64_t c = 0; c < n_circ; ++c) {
-            prev[c] = last[sched.circuits[c].mb];
-            last[sched.circuits[c].mb] = c;
+        for (int64_t c = 0; c < S->n_circ; ++c) {
+            S->prev[c] = last[circs[c].mb];
+            last[circs[c].mb] = c;
         }
     }
 
-    std::vector<Worker> W(S);
+    S->W.resize(NS);
     const bool swapping = plan.offload && NB > 2;
     const Tokens ppr = div_up(plan.seq_budget, kPage);
-    for (int64_t s = 0; s < S; ++s) {
-        Worker& w = W[s];
+    for (int64_t s = 0; s < NS; ++s) {
+        Worker& w = S->W[s];
         w.idx = int(s);
         w.device = opt.device0 + int(s % use_dev);
         const StagePlanD& sp = plan.stages[s];
-        DK(ds_stage_create(w.device, &md, sp.layer_begin, sp.layer_end, s == 0, s == S - 1,
-                           opt.weight_seed, int32_t(max_rows), int32_t(B), &w.st));
+        DK(ds_stage_create(w.device, &md, sp.layer_begin, sp.layer_end, s == 0, s == NS - 1,
+                           opt.weight_seed, int32_t(S->max_rows), int32_t(S->B), &w.st));
         const Bytes page = page_size(cfg.model, sp.layer_end - sp.layer_begin, cfg.model.num_layers);
-        const Bytes need = B * ppr * page;  // a microbatch never holds more than this
+        const Bytes need = S->B * ppr * page;  // a microbatch never holds more than this
         Bytes local = swapping ? sp.budget.local_bytes() : sp.budget.per_mb();
         local = std::min(local, need);
         const Bytes slot = swapping ? sp.budget.m_global : 0;
@@ -147,12 +168,14 @@ GpuRunResult run_on_gpus(const Config& cfg, const Plan& plan, const Schedule& sc
         DK(ds_stage_stream(w.st, &sv));
         w.stream = static_cast<cudaStream_t>(sv);
         XK(cudaSetDevice(w.device));
+        XK(cudaEventCreate(&w.t_begin));
+        XK(cudaEventCreate(&w.t_end));
         w.in.resize(NB);
         w.recv.assign(NB, nullptr);
         for (int64_t m = 0; m < NB; ++m) {
             w.in[m].reset(new Mailbox());
             XK(cudaEventCreateWithFlags(&w.in[m]->ev, cudaEventDisableTiming));
-            const size_t bytes = s == 0 ? size_t(max_rows) * 4 : size_t(max_rows) * md.d_model * 2;
+            const size_t bytes = s == 0 ? size_t(S->max_rows) * 4 : size_t(S->max_rows) * md.d_model * 2;
             XK(cudaMalloc(&w.recv[m], bytes));
             XK(cudaMemset(w.recv[m], 0, bytes));
         }
@@ -169,30 +192,65 @@ GpuRunResult run_on_gpus(const Config& cfg, const Plan& plan, const Schedule& sc
                         cudaGetLastError();
                     }
                 }
-
-    // sampled tokens (host, pinned) per circuit for the output streams
-    std::vector<int32_t*> tok_host(n_circ, nullptr);
-    int32_t* tok_pool = nullptr;
-    std::vector<int64_t> tok_off(n_circ + 1, 0);
-    for (int64_t c = 0; c < n_circ; ++c) {
+    S->tok_off.assign(S->n_circ + 1, 0);
+    for (int64_t c = 0; c < S->n_circ; ++c) {
         int64_t r = 0;
-        for (const auto& row : sched.circuits[c].rows) r += row.need_logits;
-        tok_off[c + 1] = tok_off[c] + r;
+        for (const auto& row : circs[c].rows) r += row.need_logits;
+        S->tok_off[c + 1] = S->tok_off[c] + r;
     }
-    if (opt.collect_tokens && tok_off[n_circ] > 0) {
-        XK(cudaMallocHost(&tok_pool, size_t(tok_off[n_circ]) * 4));
-        for (int64_t c = 0; c < n_circ; ++c) tok_host[c] = tok_pool + tok_off[c];
-    }
+    if (S->tok_off[S->n_circ] > 0) XK(cudaMallocHost(&S->tok_pool, size_t(S->tok_off[S->n_circ]) * 4));
+    return S.release();
+}
 
+void session_destroy(Session* S) {
+    if (!S) return;
+    for (auto& w : S->W) {
+        cudaSetDevice(w.device);
+        cudaDeviceSynchronize();
+        for (auto& m : w.in) cudaEventDestroy(m->ev);
+        for (void* p : w.recv) cudaFree(p);
+        for (auto& t : w.timing) {
+            cudaEventDestroy(t.a);
+            cudaEventDestroy(t.b);
+        }
+        if (w.t_begin) cudaEventDestroy(w.t_begin);
+        if (w.t_end) cudaEventDestroy(w.t_end);
+        ds_stage_destroy(w.st);
+    }
+    if (S->tok_pool) cudaFreeHost(S->tok_pool);
+    delete S;
+}
+
+GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
+    const int64_t NS = S->plan.S();
+    const auto& circs = S->sched.circuits;
+    const Plan& plan = S->plan;
+    const GpuOptions& opt = S->opt;
+    for (auto& w : S->W) {
+        XK(cudaSetDevice(w.device));
+        DK(ds_kv_reset(w.st));
+        DK(ds_stage_profile(w.st, profile ? 1 : 0));
+        for (auto& m : w.in) m->posted = -1;
+        w.served = w.topups = w.moved_in = w.moved_out = w.plan_in = w.computes = 0;
+        w.timing_used = 0;
+        w.error.clear();
+    }
+    int64_t launches0 = 0;
+    std::vector<int64_t> h2d0(NS, 0);
+    for (int64_t s = 0; s < NS; ++s) {
+        int64_t l = 0;
+        DK(ds_stage_kernel_stats(S->W[s].st, nullptr, 0, &l));
+        launches0 += l;
+    }
     auto hop_delay = [&](int64_t from, int64_t eff) -> int64_t {
-        if (!opt.real_delay || S < 2) return 0;
+        if (!opt.real_delay || NS < 2) return 0;
         const Link& l = plan.ring[from];
         return l.latency + div_up(eff * plan.policy.hidden_bytes_per_token * 1'000'000, l.bw);
     };
-
-    for (auto& w : W) {
+    for (auto& w : S->W) {
         XK(cudaSetDevice(w.device));
         XK(cudaDeviceSynchronize());
+        XK(cudaEventRecord(w.t_begin, w.stream));
     }
     std::atomic<bool> failed{false};
     const int64_t t0 = now_us();
@@ -201,9 +259,10 @@ GpuRunResult run_on_gpus(const Config& cfg, const Plan& plan, const Schedule& sc
         try {
             XK(cudaSetDevice(w.device));
             const int64_t s = w.idx;
-            Worker& next = W[(s + 1) % S];
+            Worker& next = S->W[(s + 1) % NS];
+            const bool last = s == NS - 1;
             std::vector<ds_row> rows;
-            for (const StageOp& op : sched.ops[s]) {
+            for (const StageOp& op : S->sched.ops[s]) {
                 if (failed) return;
                 if (op.kind == OpKind::Release) {
                     DK(ds_kv_release(w.st, op.mb, op.slot));
@@ -218,12 +277,12 @@ GpuRunResult run_on_gpus(const Config& cfg, const Plan& plan, const Schedule& sc
                     continue;
                 }
                 const int64_t c = op.circuit;
-                if (c < 0 || c >= n_circ) break;  // past the executed prefix
-                const Circuit& circ = sched.circuits[c];
+                if (c < 0 || c >= S->n_circ) break;  // past the executed prefix
+                const Circuit& circ = circs[c];
                 const int32_t mb = circ.mb;
                 w.served++;
-                // ---- input dependency
-                const int64_t need = s == 0 ? prev[c] : c;
+                // ---- input dependency: previous stage, or (stage 0) this mb's previous circuit
+                const int64_t need = s == 0 ? S->prev[c] : c;
                 bool has_input = need >= 0;
                 if (s == 0 && has_input) {
                     bool any_decode = false;
@@ -239,8 +298,8 @@ GpuRunResult run_on_gpus(const Config& cfg, const Plan& plan, const Schedule& sc
                         t_done = mbx.t_done;
                     }
                     if (failed) return;
-                    const int64_t from = (s + S - 1) % S;
-                    const int64_t arrive = t_done + hop_delay(from, sched.circuits[need].eff_batch);
+                    const int64_t from = (s + NS - 1) % NS;
+                    const int64_t arrive = t_done + hop_delay(from, circs[need].eff_batch);
                     const int64_t wait = arrive - now_us();
                     if (wait > 0) std::this_thread::sleep_for(std::chrono::microseconds(wait));
                     XK(cudaStreamWaitEvent(w.stream, mbx.ev, 0));
@@ -259,31 +318,32 @@ GpuRunResult run_on_gpus(const Config& cfg, const Plan& plan, const Schedule& sc
                 rows.clear();
                 for (const auto& r : circ.rows)
                     rows.push_back({r.slot, r.pos, r.n_tok, r.need_logits, r.is_decode, 0, r.req});
-                StepTiming tm{};
+                StepTiming* tm = nullptr;
                 if (opt.step_timing) {
-                    XK(cudaEventCreate(&tm.a));
-                    XK(cudaEventCreate(&tm.b));
-                    XK(cudaEventRecord(tm.a, w.stream));
+                    if (w.timing_used == w.timing.size()) {
+                        StepTiming n;
+                        XK(cudaEventCreate(&n.a));
+                        XK(cudaEventCreate(&n.b));
+                        w.timing.push_back(n);
+                    }
+                    tm = &w.timing[w.timing_used++];
+                    tm->rows = circ.eff_batch;
+                    XK(cudaEventRecord(tm->a, w.stream));
                 }
                 const void* act_in = s == 0 ? (has_input ? w.recv[mb] : nullptr) : w.recv[mb];
-                void* act_out = nullptr;
-                const bool last = s == S - 1;
-                if (last && S == 1) act_out = w.recv[mb];  // ids loop back to this stage
+                void* act_out = (last && NS == 1) ? w.recv[mb] : nullptr;  // ids loop back
                 DK(ds_stage_step(w.st, mb, rows.data(), int64_t(rows.size()), act_in, act_out));
-                if (opt.step_timing) {
-                    XK(cudaEventRecord(tm.b, w.stream));
-                    tm.rows = circ.eff_batch;
-                    w.timing.push_back(tm);
-                }
+                if (tm) XK(cudaEventRecord(tm->b, w.stream));
                 w.computes++;
                 // ---- hop to the next stage (or ids back to stage 0)
                 void* src = nullptr;
                 int64_t bytes = 0, n_out = 0;
                 DK(ds_stage_output(w.st, &src, &bytes, &n_out));
-                if (last && S == 1) src = w.recv[mb];
-                if (last && tok_host[c] && n_out > 0)
-                    XK(cudaMemcpyAsync(tok_host[c], src, size_t(n_out) * 4, cudaMemcpyDeviceToHost, w.stream));
-                if (S > 1 && bytes > 0) {
+                if (last && NS == 1) src = w.recv[mb];
+                if (last && collect_tokens && S->tok_pool && n_out > 0)
+                    XK(cudaMemcpyAsync(S->tok_pool + S->tok_off[c], src, size_t(n_out) * 4,
+                                       cudaMemcpyDeviceToHost, w.stream));
+                if (NS > 1 && bytes > 0) {
                     if (next.device == w.device)
                         XK(cudaMemcpyAsync(next.recv[mb], src, size_t(bytes), cudaMemcpyDeviceToDevice, w.stream));
                     else
@@ -293,33 +353,36 @@ GpuRunResult run_on_gpus(const Config& cfg, const Plan& plan, const Schedule& sc
                 XK(cudaEventRecord(out.ev, w.stream));
                 XK(cudaLaunchHostFunc(w.stream, post_cb, new PostCtx{&out, c}));
             }
+            XK(cudaEventRecord(w.t_end, w.stream));
             XK(cudaStreamSynchronize(w.stream));
         } catch (const std::exception& e) {
             w.error = e.what();
             failed = true;
-            for (auto& ww : W)
+            for (auto& ww : S->W)
                 for (auto& m : ww.in) m->cv.notify_all();
         }
     };
     std::vector<std::thread> th;
-    for (auto& w : W) th.emplace_back(body, std::ref(w));
+    for (auto& w : S->W) th.emplace_back(body, std::ref(w));
     for (auto& t : th) t.join();
-    for (auto& w : W) {
+    for (auto& w : S->W) {
         cudaSetDevice(w.device);
         ds_stage_sync(w.st);
     }
     const int64_t t1 = now_us();
 
     GpuRunResult res;
-    for (auto& w : W)
+    for (auto& w : S->W)
         if (!w.error.empty() && res.error.empty()) res.error = "stage " + std::to_string(w.idx) + ": " + w.error;
-    res.circuits = n_circ;
+    res.circuits = S->n_circ;
     res.wall_us = t1 - t0;
-    for (int64_t c = 0; c < n_circ; ++c) {
-        res.decode_tokens += sched.circuits[c].n_decode;
-        res.rows += sched.circuits[c].eff_batch;
+    for (int64_t c = 0; c < S->n_circ; ++c) {
+        res.decode_tokens += circs[c].n_decode;
+        res.rows += circs[c].eff_batch;
     }
-    for (auto& w : W) {
+    int64_t launches1 = 0;
+    for (auto& w : S->W) {
+        cudaSetDevice(w.device);
         StageRunStats st;
         st.device = w.device;
         st.computes = w.computes;
@@ -327,45 +390,64 @@ GpuRunResult run_on_gpus(const Config& cfg, const Plan& plan, const Schedule& sc
         st.swap_plan_bytes = w.plan_in;
         st.swap_in_bytes = w.moved_in;
         st.swap_out_bytes = w.moved_out;
-        for (auto& tm : w.timing) {
+        float dev_ms = 0;
+        if (res.error.empty() && cudaEventElapsedTime(&dev_ms, w.t_begin, w.t_end) == cudaSuccess)
+            st.device_ms = dev_ms;
+        res.device_us = std::max<int64_t>(res.device_us, int64_t(double(st.device_ms) * 1000.0));
+        for (size_t i = 0; i < w.timing_used; ++i) {
             float ms = 0;
-            if (cudaEventElapsedTime(&ms, tm.a, tm.b) == cudaSuccess) {
+            if (cudaEventElapsedTime(&ms, w.timing[i].a, w.timing[i].b) == cudaSuccess) {
                 st.busy_ms += ms;
-                st.steps.push_back({tm.rows, double(ms)});
+                st.steps.push_back({w.timing[i].rows, double(ms)});
             }
-            cudaEventDestroy(tm.a);
-            cudaEventDestroy(tm.b);
         }
+        std::vector<char> buf(1 << 14);
+        int64_t l = 0;
+        DK(ds_stage_kernel_stats(w.st, buf.data(), buf.size(), &l));
+        st.kernel_stats = buf.data();
+        launches1 += l;
         res.stages.push_back(std::move(st));
     }
-    if (tok_pool) {
-        res.tokens.resize(n_circ);
-        for (int64_t c = 0; c < n_circ; ++c) res.tokens[c].assign(tok_host[c], tok_host[c] + (tok_off[c + 1] - tok_off[c]));
-        cudaFreeHost(tok_pool);
+    res.launches = launches1 - launches0;
+    if (collect_tokens && S->tok_pool) {
+        res.tokens.resize(S->n_circ);
+        for (int64_t c = 0; c < S->n_circ; ++c)
+            res.tokens[c].assign(S->tok_pool + S->tok_off[c], S->tok_pool + S->tok_off[c + 1]);
     }
-    for (auto& w : W) {
-        cudaSetDevice(w.device);
-        for (auto& m : w.in) cudaEventDestroy(m->ev);
-        for (void* p : w.recv) cudaFree(p);
-        ds_stage_destroy(w.st);
-    }
+    res.d2h_bytes = collect_tokens ? S->tok_off[S->n_circ] * 4 : 0;
     return res;
+}
+
+GpuRunResult run_on_gpus(const Config& cfg, const Plan& plan, const Schedule& sched,
+                         const ds_model_desc& md, const GpuOptions& opt) {
+    Session* S = session_create(cfg, plan, sched, md, opt);
+    GpuRunResult r;
+    try {
+        r = session_run(S, false, opt.collect_tokens);
+    } catch (...) {
+        session_destroy(S);
+        throw;
+    }
+    session_destroy(S);
+    return r;
 }
 
 std::string GpuRunResult::to_json() const {
     std::ostringstream os;
     os.precision(10);
     os << "{\"circuits\":" << circuits << ",\"decode_tokens\":" << decode_tokens << ",\"rows\":" << rows
-       << ",\"wall_us\":" << wall_us << ",\"tokens_per_s\":"
+       << ",\"wall_us\":" << wall_us << ",\"device_us\":" << device_us << ",\"launches\":" << launches
+       << ",\"d2h_bytes\":" << d2h_bytes << ",\"tokens_per_s\":"
        << (wall_us > 0 ? double(decode_tokens) * 1e6 / double(wall_us) : 0.0) << ",\"error\":\"";
     for (char ch : error) os << (ch == '"' || ch == '\\' ? ' ' : ch);
     os << "\",\"stages\":[";
     for (size_t i = 0; i < stages.size(); ++i) {
         const auto& s = stages[i];
         os << (i ? "," : "") << "{\"device\":" << s.device << ",\"computes\":" << s.computes
-           << ",\"busy_ms\":" << s.busy_ms << ",\"topups\":" << s.topups
+           << ",\"busy_ms\":" << s.busy_ms << ",\"device_ms\":" << s.device_ms << ",\"topups\":" << s.topups
            << ",\"swap_plan_bytes\":" << s.swap_plan_bytes << ",\"swap_in_bytes\":" << s.swap_in_bytes
-           << ",\"swap_out_bytes\":" << s.swap_out_bytes << ",\"steps\":[";
+           << ",\"swap_out_bytes\":" << s.swap_out_bytes << ",\"kernels\":"
+           << (s.kernel_stats.empty() ? "{}" : s.kernel_stats) << ",\"steps\":[";
         for (size_t k = 0; k < s.steps.size(); ++k)
             os << (k ? "," : "") << "[" << s.steps[k].first << "," << s.steps[k].second << "]";
         os << "]}";

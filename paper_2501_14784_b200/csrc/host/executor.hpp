@@ -12,8 +12,8 @@ namespace dsb {
 
 struct GpuOptions {
     int device0 = 0;
-    int n_devices = 0;       // 0 = all visible; stage s runs on device0 + s % n_devices
-    bool real_delay = true;  // enforce the injected hop delay in wall time
+    int n_devices = 0;         // 0 = all visible; stage s runs on device0 + s % n_devices
+    bool real_delay = true;    // enforce the injected hop delay in wall time
     int64_t max_circuits = 0;  // execute only the first circuits of the schedule (0 = all)
     uint64_t weight_seed = 0x5EED0001ULL;
     bool collect_tokens = false;  // D2H the sampled ids of every circuit
@@ -24,17 +24,25 @@ struct StageRunStats {
     int device = 0;
     int64_t computes = 0, topups = 0;
     int64_t swap_plan_bytes = 0, swap_in_bytes = 0, swap_out_bytes = 0;
-    double busy_ms = 0;
+    double busy_ms = 0, device_ms = 0;
     std::vector<std::pair<int64_t, double>> steps;  // (rows, ms) per stage step
+    std::string kernel_stats;                       // ds_stage_kernel_stats JSON
 };
 
 struct GpuRunResult {
-    int64_t circuits = 0, decode_tokens = 0, rows = 0, wall_us = 0;
+    int64_t circuits = 0, decode_tokens = 0, rows = 0, wall_us = 0, device_us = 0;
+    int64_t launches = 0, d2h_bytes = 0;
     std::vector<StageRunStats> stages;
     std::vector<std::vector<int32_t>> tokens;  // per circuit: sampled ids of its need_logits rows
     std::string error;
     std::string to_json() const;
 };
+
+struct Session;
+Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, const ds_model_desc& md,
+                        const GpuOptions& opt);
+GpuRunResult session_run(Session* s, bool profile, bool collect_tokens);
+void session_destroy(Session* s);
 
 GpuRunResult run_on_gpus(const Config& cfg, const Plan& plan, const Schedule& sched,
                          const ds_model_desc& md, const GpuOptions& opt);

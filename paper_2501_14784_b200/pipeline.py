@@ -138,3 +138,40 @@ def gpu_run_config(config_text: str, config_dir: str = "", policy=None, latency_
                                nb_override, C.byref(md), C.byref(opts), buf, cap, C.byref(need))
     check(st)
     return json.loads(buf.value.decode())
+
+
+class Session:
+    """A planned + scheduled pipeline with its GPU stages built once (ds_session_*)."""
+
+    def __init__(self, config_text: str, config_dir: str = "", policy=None, latency_us=-1,
+                 nb_override=-1, model=None, device0=0, n_devices=0, real_delay=True,
+                 max_circuits=0, weight_seed=WEIGHT_SEED):
+        from ._native import GpuOpts
+        if model is None:
+            model = json.loads(config_text)["model"]["name"]
+        self._md = model_desc(model)
+        self._opts = GpuOpts(device0=device0, n_devices=n_devices, real_delay=int(real_delay),
+                             collect_tokens=0, max_circuits=max_circuits, weight_seed=weight_seed)
+        self._h = C.c_void_p()
+        check(lib.ds_session_create(_b(config_text), _b(config_dir), _b(policy or ""), latency_us,
+                                    nb_override, C.byref(self._md), C.byref(self._opts),
+                                    C.byref(self._h)))
+
+    def run(self, profile=False, collect_tokens=False) -> dict:
+        cap = 1 << 26
+        buf = C.create_string_buffer(cap)
+        need = C.c_size_t(0)
+        check(lib.ds_session_run(self._h, int(profile), int(collect_tokens), buf, cap,
+                                 C.byref(need)))
+        return json.loads(buf.value.decode())
+
+    def close(self):
+        if self._h:
+            lib.ds_session_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
