@@ -141,3 +141,71 @@ class LlamaRef:
         lib.lr_stage_step.argtypes = [P, C.c_int32, C.c_int32, P, C.c_int32, P, P, P, P, P]
         lib.lr_stage_step.restype = C.c_int
         self.lib = lib
+
+
+def replay_circuits(schedule: dict, plan: dict, dims: dict, seed: int, gpu_tokens):
+    """Runs the schedule's circuits through the CPU oracle stages (all stages of the plan, in
+    circuit order), teacher-forcing decode inputs with the GPU's sampled ids. Returns, per
+    circuit, the oracle logits of the rows that sample a token."""
+    import numpy as np
+    lr = LlamaRef()
+    m = LrModel(**dims)
+    S = len(plan["stages"])
+    B = plan["stages"][0]["batch_size_per_microbatch"]
+    NB = plan["n_microbatches"]
+    stages = [lr.lib.lr_stage_create(C.byref(m), s["layer_begin"], s["layer_end"], int(i == 0),
+                                     int(i == S - 1), seed, NB * B)
+              for i, s in enumerate(plan["stages"])]
+
+    class Row(C.Structure):
+        _fields_ = [("slot", C.c_int32), ("pos", C.c_int32), ("n_tok", C.c_int32),
+                    ("need_logits", C.c_int32), ("is_decode", C.c_int32), ("reserved", C.c_int32),
+                    ("req_id", C.c_int64)]
+    last, out = {}, []
+    try:
+        for ci, c in enumerate(schedule["circuits"]):
+            rows = c["rows"]
+            arr = (Row * len(rows))(*[Row(r[0], r[1], r[2], r[3], r[4], 0, r[5]) for r in rows])
+            toks = []
+            for r in rows:
+                for j in range(r[2]):
+                    pos = r[1] + j
+                    toks.append((128000 if pos == 0 else last[(c["mb"], r[0])]) if r[4]
+                                else lr.lib.lr_prompt_token(r[5], pos))
+            T = sum(r[2] for r in rows)
+            R = sum(r[3] for r in rows)
+            tok = np.array(toks, dtype=np.int32)
+            a = np.zeros((T, dims["d_model"]), dtype=np.float32)
+            b = np.zeros_like(a)
+            lg = np.zeros((max(R, 1), dims["vocab"]), dtype=np.float32)
+            ids = np.zeros(max(R, 1), dtype=np.int32)
+            for i in range(S):
+                src, dst = (a, b) if i % 2 == 0 else (b, a)
+                rc = lr.lib.lr_stage_step(stages[i], c["mb"], B, arr, len(rows), tok.ctypes.data,
+                                          src.ctypes.data if i else None, dst.ctypes.data,
+                                          lg.ctypes.data if i == S - 1 else None, ids.ctypes.data)
+                if rc != 0:
+                    raise RefError("oracle stage step failed")
+            k = 0
+            for r in rows:
+                if r[3]:
+                    last[(c["mb"], r[0])] = gpu_tokens[ci][k]
+                    k += 1
+            out.append(lg[:R].copy())
+    finally:
+        for s in stages:
+            lr.lib.lr_stage_destroy(s)
+    return out
+
+
+def greedy_mismatches(oracle_logits, gpu_tokens, margin):
+    """(checked, mismatched): rows whose oracle top-2 margin exceeds `margin` must agree."""
+    import numpy as np
+    checked = bad = 0
+    for ci, lg in enumerate(oracle_logits):
+        for k, row in enumerate(lg):
+            top = np.sort(row)[-2:]
+            if top[1] - top[0] > margin:
+                checked += 1
+                bad += int(int(np.argmax(row)) != int(gpu_tokens[ci][k]))
+    return checked, bad

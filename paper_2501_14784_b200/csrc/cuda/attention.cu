@@ -1,150 +1,335 @@
-// Paged causal GQA attention over the stage's KV pages (decode rows and chunked-prefill rows in
-// one launch). CTA = (row, kv-head, context split); the K/V tiles of 64 tokens (never straddling
-// a 256-token page) are staged in shared memory with 16-byte coalesced loads, the G = n_h/n_kv
-// query heads of the group share every staged tile (GQA reuse), and each warp keeps an online
-// softmax (log2 domain, fp32) per head. Context splits (flash-decoding) keep >= 2 CTAs per SM
-// when the row count is small; a combine kernel merges the (o, m, l) partials.
+// Paged causal GQA attention over the stage's KV pages on tensor cores (mma.sync m16n8k16 bf16,
+// fp32 accumulate), FlashAttention-2 style with an online softmax in the log2 domain.
 //
-// HBM roofline: each CTA reads ctx * d_head * 2 (K,V) * 2 B once; bytes/row/layer = ctx * 4 *
-// n_kv * d_head.
+// Work item = (query block, kv head, context split). A query block is either one decode row or
+// up to QP consecutive prompt positions of one request (chunked prefill, reference
+// begin_circuit sim.cpp:386-407); its G = n_h / n_kv query heads share every staged K/V tile
+// (GQA reuse), so the Q tile has QP*G rows. K/V tiles of 64 tokens (never straddling a 256-token
+// page) are double-buffered in shared memory with cp.async. Prefill blocks give each of the 4
+// warps 16 query rows over the whole tile; decode blocks (G <= 16 rows) give each warp a 16-token
+// slice of the tile and merge the 4 partial softmax states at the end. Context splits
+// (flash-decoding) keep >= 2 CTAs per SM when the block count is small; a combine kernel merges
+// the (o, m, l) partials.
+//
+// HBM roofline: each (block, kv head) reads its request's KV once: ctx * d_head * 2 (K,V) * 2 B
+// per kv head.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace ds {
 
-constexpr int kAttnTile = 64;
-constexpr int kAttnThreads = 128;
+constexpr int kTile = 64;
+constexpr int kAttnWarps = 4;
+
+DS_DEVICE void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+DS_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+DS_DEVICE void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+DS_DEVICE void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+DS_DEVICE void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+DS_DEVICE void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
 
 template <int DH>
 struct AttnSmem {
-    __nv_bfloat16 k[kAttnTile][DH + 8];
-    __nv_bfloat16 v[kAttnTile][DH + 8];
-    float q[8][DH];
+    __nv_bfloat16 k[2][kTile][DH + 8];
+    __nv_bfloat16 v[2][kTile][DH + 8];
 };
 
+// blocks: [n_blocks][3] = (first row t0, n positions, decode flag)
 template <int DH>
-__global__ void __launch_bounds__(kAttnThreads)
-attn_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __restrict__ row_pos,
-            const int32_t* __restrict__ row_page_off, const int32_t* __restrict__ flat_pages,
-            KvLayout kv, int layer, int splits, __nv_bfloat16* __restrict__ o, float* __restrict__ ws) {
-    __shared__ __align__(16) AttnSmem<DH> sm;
+__global__ void __launch_bounds__(kAttnWarps * 32)
+attn_tc_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __restrict__ row_pos,
+               const int32_t* __restrict__ row_page_off, const int32_t* __restrict__ flat_pages,
+               const int32_t* __restrict__ blocks, KvLayout kv, int layer, int splits,
+               __nv_bfloat16* __restrict__ o, float* __restrict__ ws) {
+    extern __shared__ __align__(16) uint8_t attn_smem[];
+    AttnSmem<DH>& sm = *reinterpret_cast<AttnSmem<DH>*>(attn_smem);
+    constexpr int NT = DH / 8;   // output n-tiles
+    constexpr int KS = DH / 16;  // k-steps over d_head
     const int n_kv = kv.n_kv;
     const int G = n_h / n_kv;
     const int split = blockIdx.x % splits;
     const int kvh = (blockIdx.x / splits) % n_kv;
-    const int t = blockIdx.x / (splits * n_kv);
+    const int bi = blockIdx.x / (splits * n_kv);
+    const int t0 = blocks[3 * bi], npos = blocks[3 * bi + 1];
+    const bool decode = blocks[3 * bi + 2] != 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, tq = lane & 3;
+    const int rows = npos * G;  // q rows of this block: r = p * G + h
+    const int pos0 = row_pos[t0];
+    const int last_pos = pos0 + npos - 1;
+    const int n_tiles = (last_pos + kTile) / kTile;
+    const int tile0 = split * n_tiles / splits, tile1 = (split + 1) * n_tiles / splits;
+    const int32_t* pages = flat_pages + row_page_off[t0];
 
-    const int ctx = row_pos[t] + 1;
-    const int n_tiles = (ctx + kAttnTile - 1) / kAttnTile;
-    const int tile0 = split * n_tiles / splits;
-    const int tile1 = (split + 1) * n_tiles / splits;
-    const int32_t* pages = flat_pages + row_page_off[t];
-
-    // q heads of this group, pre-scaled into the log2 domain
-    const float qscale = rsqrtf(float(DH)) * 1.4426950408889634f;
-    for (int i = threadIdx.x; i < G * DH; i += blockDim.x) {
-        const int h = i / DH, dd = i % DH;
-        sm.q[h][dd] = bf2f(q[(size_t(t) * n_h + kvh * G + h) * DH + dd]) * qscale;
+    // this warp's 16 q rows (prefill) or all rows (decode, <= 16)
+    const int r_base = decode ? 0 : warp * 16;
+    const bool warp_active = r_base < rows;
+    // Q fragments, pre-scaled by log2(e)/sqrt(d_head)
+    uint32_t qa[KS][4];
+    const float qs = rsqrtf(float(DH)) * 1.4426950408889634f;
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = r_base + g + ((i & 1) ? 8 : 0);
+            const int col = kk * 16 + 2 * tq + ((i & 2) ? 8 : 0);
+            float x0 = 0.f, x1 = 0.f;
+            if (r < rows) {
+                const int p = r / G, h = r % G;
+                const __nv_bfloat16* src = q + (size_t(t0 + p) * n_h + kvh * G + h) * DH + col;
+                const __nv_bfloat162 v2 = *reinterpret_cast<const __nv_bfloat162*>(src);
+                x0 = __bfloat162float(v2.x) * qs;
+                x1 = __bfloat162float(v2.y) * qs;
+            }
+            qa[kk][i] = pack2(x0, x1);
+        }
+    // per-thread row positions (rows g and g+8 of this warp's slice)
+    int rpos[2];
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+        const int r = r_base + g + 8 * hr;
+        rpos[hr] = r < rows ? pos0 + r / G : -1;
     }
 
-    constexpr int DPL = DH / 32;  // output dims per lane
-    float m[2], l[2], acc[2][DPL];
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+    float acc[NT][4];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        m[i] = -INFINITY;
-        l[i] = 0.f;
-#pragma unroll
-        for (int j = 0; j < DPL; ++j) acc[i][j] = 0.f;
-    }
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
 
-    const size_t kv_head_off_k = ((size_t(layer) * 2 + 0) * n_kv + kvh) * 256 * DH;
-    const size_t kv_head_off_v = ((size_t(layer) * 2 + 1) * n_kv + kvh) * 256 * DH;
-    constexpr int VEC_PER_ROW = DH / 8;
+    const size_t head_k = ((size_t(layer) * 2 + 0) * n_kv + kvh) * 256 * DH;
+    const size_t head_v = ((size_t(layer) * 2 + 1) * n_kv + kvh) * 256 * DH;
+    constexpr int CHUNKS = kTile * DH / 8;  // 16-byte chunks per K (or V) tile
+    auto load_tile = [&](int tile, int buf) {
+        const int tok0 = tile * kTile;
+        const size_t base = size_t(pages[tok0 >> 8]) * kv.page_elems + size_t(tok0 & 255) * DH;
+        const __nv_bfloat16* ks = kv.pool + base + head_k;
+        const __nv_bfloat16* vs = kv.pool + base + head_v;
+        for (int i = threadIdx.x; i < CHUNKS; i += blockDim.x) {
+            const int r = i / (DH / 8), c = (i % (DH / 8)) * 8;
+            cp_async16(&sm.k[buf][r][c], ks + size_t(r) * DH + c);
+            cp_async16(&sm.v[buf][r][c], vs + size_t(r) * DH + c);
+        }
+        cp_async_commit();
+    };
 
+    if (tile0 < tile1) load_tile(tile0, 0);
     for (int tile = tile0; tile < tile1; ++tile) {
-        const int tok0 = tile * kAttnTile;
-        const size_t page_base = size_t(pages[tok0 >> 8]) * kv.page_elems + size_t(tok0 & 255) * DH;
-        const uint4* ksrc = reinterpret_cast<const uint4*>(kv.pool + page_base + kv_head_off_k);
-        const uint4* vsrc = reinterpret_cast<const uint4*>(kv.pool + page_base + kv_head_off_v);
-        __syncthreads();  // previous tile fully consumed (and q staged on the first pass)
-        for (int i = threadIdx.x; i < kAttnTile * VEC_PER_ROW; i += blockDim.x) {
-            const int r = i / VEC_PER_ROW, c = i % VEC_PER_ROW;
-            *reinterpret_cast<uint4*>(&sm.k[r][c * 8]) = ksrc[i];
-            *reinterpret_cast<uint4*>(&sm.v[r][c * 8]) = vsrc[i];
+        const int buf = (tile - tile0) & 1;
+        if (tile + 1 < tile1) {
+            load_tile(tile + 1, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
         __syncthreads();
-        const int valid = min(kAttnTile, ctx - tok0);
-#pragma unroll
-        for (int hi = 0; hi < 2; ++hi) {
-            const int h = warp + 4 * hi;
-            if (h >= G) break;
-            float s[2];
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                const int j = lane + 32 * half;
-                float dot = 0.f;
-#pragma unroll
-                for (int c = 0; c < VEC_PER_ROW; ++c) {
-                    float kf[8];
-                    unpack8(*reinterpret_cast<const uint4*>(&sm.k[j][c * 8]), kf);
-                    const float4 q0 = *reinterpret_cast<const float4*>(&sm.q[h][c * 8]);
-                    const float4 q1 = *reinterpret_cast<const float4*>(&sm.q[h][c * 8 + 4]);
-                    dot += kf[0] * q0.x + kf[1] * q0.y + kf[2] * q0.z + kf[3] * q0.w + kf[4] * q1.x +
-                           kf[5] * q1.y + kf[6] * q1.z + kf[7] * q1.w;
-                }
-                s[half] = j < valid ? dot : -INFINITY;
+        const int tok0 = tile * kTile;
+        // zero V rows past the last valid token so 0 * garbage cannot produce NaN
+        const int valid = min(kTile, last_pos + 1 - tok0);
+        if (valid < kTile) {
+            for (int i = threadIdx.x; i < (kTile - valid) * (DH / 8); i += blockDim.x) {
+                const int r = valid + i / (DH / 8), c = (i % (DH / 8)) * 8;
+                *reinterpret_cast<uint4*>(&sm.v[buf][r][c]) = make_uint4(0, 0, 0, 0);
             }
-            const float mt = warp_max(fmaxf(s[0], s[1]));
-            const float mn = fmaxf(m[hi], mt);
-            const float alpha = exp2f(m[hi] - mn);
-            const float p0 = exp2f(s[0] - mn), p1 = exp2f(s[1] - mn);
-            l[hi] = l[hi] * alpha + warp_sum(p0 + p1);
-            m[hi] = mn;
+            __syncthreads();
+        }
+        if (warp_active) {
+            // token slice of this warp within the tile
+            const int n0 = decode ? warp * 16 : 0;
+            constexpr int SN_MAX = kTile / 8;
+            const int sn = decode ? 2 : SN_MAX;  // n-tiles of 8 tokens
+            float s[SN_MAX][4];
 #pragma unroll
-            for (int j = 0; j < DPL; ++j) acc[hi][j] *= alpha;
-            for (int j = 0; j < valid; ++j) {
-                const float pj = __shfl_sync(0xffffffffu, j < 32 ? p0 : p1, j & 31);
-                if (DPL == 4) {
-                    const uint2 vv = *reinterpret_cast<const uint2*>(&sm.v[j][lane * 4]);
-                    const __nv_bfloat162* vh = reinterpret_cast<const __nv_bfloat162*>(&vv);
-                    const float2 a = __bfloat1622float2(vh[0]), b = __bfloat1622float2(vh[1]);
-                    acc[hi][0] += pj * a.x;
-                    acc[hi][1] += pj * a.y;
-                    acc[hi][2] += pj * b.x;
-                    acc[hi][3] += pj * b.y;
-                } else {
+            for (int j = 0; j < SN_MAX; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+            const uint32_t kbase = smem_u32(&sm.k[buf][0][0]);
 #pragma unroll
-                    for (int e = 0; e < DPL; ++e) acc[hi][e] += pj * bf2f(sm.v[j][lane * DPL + e]);
+            for (int j = 0; j < SN_MAX; ++j) {
+                if (j >= sn) break;
+#pragma unroll
+                for (int kk = 0; kk < KS; kk += 2) {
+                    const int mi = lane >> 3, rr = lane & 7;
+                    const int tok = n0 + j * 8 + rr;
+                    const int col = kk * 16 + mi * 8;
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4(kbase + uint32_t((tok * (DH + 8) + col) * 2), b0, b1, b2, b3);
+                    mma16816(s[j], qa[kk], b0, b1);
+                    mma16816(s[j], qa[kk + 1], b2, b3);
+                }
+            }
+            // causal mask + online softmax (rows g and g+8)
+            float mt[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+            for (int j = 0; j < SN_MAX; ++j) {
+                if (j >= sn) break;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int hr = e >> 1;
+                    const int tok = tok0 + n0 + j * 8 + 2 * tq + (e & 1);
+                    if (tok > rpos[hr]) s[j][e] = -INFINITY;
+                    mt[hr] = fmaxf(mt[hr], s[j][e]);
+                }
+            }
+            float alpha[2];
+#pragma unroll
+            for (int hr = 0; hr < 2; ++hr) {
+                mt[hr] = fmaxf(mt[hr], __shfl_xor_sync(0xffffffffu, mt[hr], 1));
+                mt[hr] = fmaxf(mt[hr], __shfl_xor_sync(0xffffffffu, mt[hr], 2));
+                const float mn = fmaxf(m_run[hr], mt[hr]);
+                alpha[hr] = mn == -INFINITY ? 1.f : exp2f(m_run[hr] - mn);
+                m_run[hr] = mn;
+            }
+            float ls[2] = {0.f, 0.f};
+            uint32_t pa[SN_MAX / 2][4];
+#pragma unroll
+            for (int j = 0; j < SN_MAX; ++j) {
+                if (j >= sn) break;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int hr = e >> 1;
+                    const float p = m_run[hr] == -INFINITY ? 0.f : exp2f(s[j][e] - m_run[hr]);
+                    s[j][e] = p;
+                    ls[hr] += p;
+                }
+            }
+#pragma unroll
+            for (int hr = 0; hr < 2; ++hr) l_run[hr] = l_run[hr] * alpha[hr] + ls[hr];  // quad-partial
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                acc[j][0] *= alpha[0];
+                acc[j][1] *= alpha[0];
+                acc[j][2] *= alpha[1];
+                acc[j][3] *= alpha[1];
+            }
+#pragma unroll
+            for (int kk = 0; kk < SN_MAX / 2; ++kk) {
+                if (2 * kk >= sn) break;
+                pa[kk][0] = pack2(s[2 * kk][0], s[2 * kk][1]);
+                pa[kk][1] = pack2(s[2 * kk][2], s[2 * kk][3]);
+                pa[kk][2] = pack2(s[2 * kk + 1][0], s[2 * kk + 1][1]);
+                pa[kk][3] = pack2(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+            }
+            const uint32_t vbase = smem_u32(&sm.v[buf][0][0]);
+#pragma unroll
+            for (int kk = 0; kk < SN_MAX / 2; ++kk) {
+                if (2 * kk >= sn) break;
+#pragma unroll
+                for (int nt = 0; nt < NT; nt += 2) {
+                    const int mi = lane >> 3, rr = lane & 7;
+                    const int tok = n0 + kk * 16 + (mi & 1) * 8 + rr;
+                    const int col = (nt + (mi >> 1)) * 8;
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4_t(vbase + uint32_t((tok * (DH + 8) + col) * 2), b0, b1, b2, b3);
+                    mma16816(acc[nt], pa[kk], b0, b1);
+                    mma16816(acc[nt + 1], pa[kk], b2, b3);
                 }
             }
         }
+        __syncthreads();  // buffer `buf` is overwritten by the prefetch two iterations later
     }
 
+    // full row sums across the quad
 #pragma unroll
-    for (int hi = 0; hi < 2; ++hi) {
-        const int h = warp + 4 * hi;
-        if (h >= G) break;
-        const int head = kvh * G + h;
+    for (int hr = 0; hr < 2; ++hr) {
+        l_run[hr] += __shfl_xor_sync(0xffffffffu, l_run[hr], 1);
+        l_run[hr] += __shfl_xor_sync(0xffffffffu, l_run[hr], 2);
+    }
+
+    if (decode) {
+        // merge the 4 warps' partial states through shared memory (reusing the K buffer)
+        float* red = reinterpret_cast<float*>(&sm.k[0][0][0]);  // [4 warps][16 rows][DH + 2]
+        __syncthreads();
+#pragma unroll
+        for (int hr = 0; hr < 2; ++hr) {
+            const int r = g + 8 * hr;
+            float* dst = red + (warp * 16 + r) * (DH + 2);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                dst[nt * 8 + 2 * tq] = acc[nt][2 * hr];
+                dst[nt * 8 + 2 * tq + 1] = acc[nt][2 * hr + 1];
+            }
+            if (tq == 0) {
+                dst[DH] = m_run[hr];
+                dst[DH + 1] = l_run[hr];
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < rows * DH; i += blockDim.x) {
+            const int r = i / DH, dd = i % DH;
+            float M = -INFINITY;
+#pragma unroll
+            for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, red[(w * 16 + r) * (DH + 2) + DH]);
+            float num = 0.f, den = 0.f;
+#pragma unroll
+            for (int w = 0; w < kAttnWarps; ++w) {
+                const float* src = red + (w * 16 + r) * (DH + 2);
+                const float wt = src[DH] == -INFINITY ? 0.f : exp2f(src[DH] - M);
+                num += src[dd] * wt;
+                den += src[DH + 1] * wt;
+            }
+            const int p = r / G, h = r % G;
+            const size_t row_head = size_t(t0 + p) * n_h + kvh * G + h;
+            if (splits == 1) {
+                o[row_head * DH + dd] = f2bf(num / den);
+            } else {
+                float* dst = ws + (row_head * splits + split) * (DH + 2);
+                dst[dd] = num;
+                if (dd == 0) {
+                    dst[DH] = M;
+                    dst[DH + 1] = den;
+                }
+            }
+        }
+        return;
+    }
+    if (!warp_active) return;
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+        const int r = r_base + g + 8 * hr;
+        if (r >= rows) continue;
+        const int p = r / G, h = r % G;
+        const size_t row_head = size_t(t0 + p) * n_h + kvh * G + h;
         if (splits == 1) {
-            const float inv = 1.0f / l[hi];
-            __nv_bfloat16* dst = o + (size_t(t) * n_h + head) * DH + lane * DPL;
+            const float inv = 1.0f / l_run[hr];
+            __nv_bfloat16* dst = o + row_head * DH;
 #pragma unroll
-            for (int e = 0; e < DPL; ++e) dst[e] = f2bf(acc[hi][e] * inv);
+            for (int nt = 0; nt < NT; ++nt)
+                *reinterpret_cast<uint32_t*>(dst + nt * 8 + 2 * tq) =
+                    pack2(acc[nt][2 * hr] * inv, acc[nt][2 * hr + 1] * inv);
         } else {
-            float* dst = ws + ((size_t(t) * n_h + head) * splits + split) * (DH + 2);
+            float* dst = ws + (row_head * splits + split) * (DH + 2);
 #pragma unroll
-            for (int e = 0; e < DPL; ++e) dst[lane * DPL + e] = acc[hi][e];
-            if (lane == 0) {
-                dst[DH] = m[hi];
-                dst[DH + 1] = l[hi];
+            for (int nt = 0; nt < NT; ++nt) {
+                dst[nt * 8 + 2 * tq] = acc[nt][2 * hr];
+                dst[nt * 8 + 2 * tq + 1] = acc[nt][2 * hr + 1];
+            }
+            if (tq == 0) {
+                dst[DH] = m_run[hr];
+                dst[DH + 1] = l_run[hr];
             }
         }
     }
 }
 
 template <int DH>
-__global__ void attn_combine_kernel(const float* __restrict__ ws, int n_rows_heads, int splits,
+__global__ void attn_combine_kernel(const float* __restrict__ ws, int splits,
                                     __nv_bfloat16* __restrict__ o) {
     const int rh = blockIdx.x;
     const float* base = ws + size_t(rh) * splits * (DH + 2);
@@ -163,43 +348,57 @@ __global__ void attn_combine_kernel(const float* __restrict__ ws, int n_rows_hea
     }
 }
 
-static int pick_attn_splits(int T, int n_kv, int max_ctx) {
-    const int base = T * n_kv;
-    const int tiles = (max_ctx + kAttnTile - 1) / kAttnTile;
+int attention_block_positions(int n_h, int n_kv) { return (kAttnWarps * 16) / (n_h / n_kv); }
+
+int attention_pick_splits(int n_blocks, int n_kv, int max_ctx) {
+    const int base = n_blocks * n_kv;
+    const int tiles = (max_ctx + kTile - 1) / kTile;
     int s = (2 * kNumSMs + base - 1) / base;
     if (s > tiles) s = tiles;
-    if (s > 32) s = 32;
+    if (s > 16) s = 16;
     return s < 1 ? 1 : s;
 }
 
-int attention_launches(int T, int n_kv, int max_ctx) {
-    return T > 0 ? (pick_attn_splits(T, n_kv, max_ctx) > 1 ? 2 : 1) : 0;
+int attention_launches(int n_blocks, int n_kv, int max_ctx) {
+    return n_blocks > 0 ? (attention_pick_splits(n_blocks, n_kv, max_ctx) > 1 ? 2 : 1) : 0;
 }
 
 size_t attention_workspace_floats(int T, int n_h, int d_head, int splits) {
     return size_t(T) * n_h * splits * (d_head + 2);
 }
 
-int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,
-                    const int32_t* row_page_off, const int32_t* flat_pages, const KvLayout& kv,
-                    int layer, int max_ctx, __nv_bfloat16* o, float* ws, size_t ws_floats,
-                    cudaStream_t stream) {
-    if (T <= 0) return 0;
-    if (n_h % kv.n_kv != 0 || n_h / kv.n_kv > 8) return -1;
-    int splits = pick_attn_splits(T, kv.n_kv, max_ctx);
-    if (splits > 1 && attention_workspace_floats(T, n_h, kv.d_head, splits) > ws_floats) splits = 1;
-    const int grid = T * kv.n_kv * splits;
-    if (kv.d_head == 128) {
-        attn_kernel<128><<<grid, kAttnThreads, 0, stream>>>(q, n_h, row_pos, row_page_off,
-                                                            flat_pages, kv, layer, splits, o, ws);
-        if (splits > 1) attn_combine_kernel<128><<<T * n_h, 128, 0, stream>>>(ws, T * n_h, splits, o);
-    } else if (kv.d_head == 64) {
-        attn_kernel<64><<<grid, kAttnThreads, 0, stream>>>(q, n_h, row_pos, row_page_off,
-                                                           flat_pages, kv, layer, splits, o, ws);
-        if (splits > 1) attn_combine_kernel<64><<<T * n_h, 64, 0, stream>>>(ws, T * n_h, splits, o);
-    } else {
-        return -2;
+template <int DH>
+static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,
+                   const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
+                   int n_blocks, const KvLayout& kv, int layer, int splits, __nv_bfloat16* o,
+                   float* ws, cudaStream_t stream) {
+    const size_t smem = sizeof(AttnSmem<DH>);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(attn_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr = true;
     }
+    attn_tc_kernel<DH><<<n_blocks * kv.n_kv * splits, kAttnWarps * 32, smem, stream>>>(
+        q, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, splits, o, ws);
+    if (splits > 1) attn_combine_kernel<DH><<<T * n_h, DH, 0, stream>>>(ws, splits, o);
+}
+
+int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,
+                    const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
+                    int n_blocks, const KvLayout& kv, int layer, int max_ctx, __nv_bfloat16* o,
+                    float* ws, size_t ws_floats, cudaStream_t stream) {
+    if (T <= 0 || n_blocks <= 0) return 0;
+    if (n_h % kv.n_kv != 0 || n_h / kv.n_kv > 16) return -1;
+    int splits = attention_pick_splits(n_blocks, kv.n_kv, max_ctx);
+    if (splits > 1 && attention_workspace_floats(T, n_h, kv.d_head, splits) > ws_floats) splits = 1;
+    if (kv.d_head == 128)
+        launch<128>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, kv, layer, splits,
+                    o, ws, stream);
+    else if (kv.d_head == 64)
+        launch<64>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, kv, layer, splits,
+                   o, ws, stream);
+    else
+        return -2;
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -3;
 }
 

@@ -134,26 +134,32 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int n_h, i
     const float* s = rs + size_t(pos) * half;
     const size_t page_base = size_t(row_page[t]) * kv.page_elems;
     const int slot = pos & 255;
-    // rotated q and k: (head, i) pairs
-    const int n_rot = (n_h + n_kv) * half;
+    // rotated q and k: each thread handles 8 consecutive rotary pairs (16-byte accesses)
+    const int n_rot = (n_h + n_kv) * (half / 8);
     for (int w = threadIdx.x; w < n_rot; w += blockDim.x) {
-        const int head = w / half, i = w % half;
-        const float x1 = bf2f(src[head * dh + i]);
-        const float x2 = bf2f(src[head * dh + i + half]);
-        // explicit _rn ops: no FMA contraction, bit-identical to the CPU oracle
-        const float o1 = __fsub_rn(__fmul_rn(x1, c[i]), __fmul_rn(x2, s[i]));
-        const float o2 = __fadd_rn(__fmul_rn(x2, c[i]), __fmul_rn(x1, s[i]));
-        if (head < n_h) {
-            __nv_bfloat16* dq = q_out + size_t(t) * n_h * dh + head * dh;
-            dq[i] = f2bf(o1);
-            dq[i + half] = f2bf(o2);
-        } else {
-            const int kh = head - n_h;
-            __nv_bfloat16* dk = kv.pool + page_base +
-                                ((size_t(layer) * 2 + 0) * n_kv + kh) * 256 * dh + size_t(slot) * dh;
-            dk[i] = f2bf(o1);
-            dk[i + half] = f2bf(o2);
+        const int head = w / (half / 8), i = (w % (half / 8)) * 8;
+        float x1[8], x2[8], o1[8], o2[8];
+        unpack8(*reinterpret_cast<const uint4*>(src + head * dh + i), x1);
+        unpack8(*reinterpret_cast<const uint4*>(src + head * dh + i + half), x2);
+        const float4 c0 = *reinterpret_cast<const float4*>(c + i), c1 = *reinterpret_cast<const float4*>(c + i + 4);
+        const float4 s0 = *reinterpret_cast<const float4*>(s + i), s1 = *reinterpret_cast<const float4*>(s + i + 4);
+        const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        const float ss[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            // explicit _rn ops: no FMA contraction, bit-identical to the CPU oracle
+            o1[j] = __fsub_rn(__fmul_rn(x1[j], cc[j]), __fmul_rn(x2[j], ss[j]));
+            o2[j] = __fadd_rn(__fmul_rn(x2[j], cc[j]), __fmul_rn(x1[j], ss[j]));
         }
+        __nv_bfloat16* dst;
+        if (head < n_h) {
+            dst = q_out + size_t(t) * n_h * dh + head * dh;
+        } else {
+            dst = kv.pool + page_base + ((size_t(layer) * 2 + 0) * n_kv + (head - n_h)) * 256 * dh +
+                  size_t(slot) * dh;
+        }
+        *reinterpret_cast<uint4*>(dst + i) = pack8(o1);
+        *reinterpret_cast<uint4*>(dst + i + half) = pack8(o2);
     }
     // v: plain copy, 16 B per thread-iteration
     const int nv = n_kv * dh / 8;

@@ -533,7 +533,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     MbKv& k = s->mbs[mb];
 
     // ---- rows -> pages + metadata (host)
-    int T = 0, R = 0, P = 0, max_ctx = 1;
+    int T = 0, R = 0, P = 0, max_ctx = 1, n_blk = 0;
     for (int64_t i = 0; i < n_rows; ++i) {
         const ds_row& r = rows[i];
         if (r.slot < 0 || r.slot >= s->max_slots || r.n_tok < 1 || r.pos < 0 ||
@@ -575,7 +575,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
                                                    std::to_string(mb) + " has non-resident pages");
 
     const int prevR = int(k.prev_logit_slots.size());
-    const size_t need_meta = size_t(7) * T + 2 * size_t(R) + P + prevR + 8;
+    const size_t need_meta = size_t(10) * T + 2 * size_t(R) + P + prevR + 8;
     if (need_meta > s->meta_cap) return ds_fail(DS_ERR_ARG, "step metadata exceeds capacity");
     const int buf = s->meta_buf;
     s->meta_buf ^= 1;
@@ -589,7 +589,8 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     int32_t* logit_rows = row_poff + T;
     int32_t* logit_slot = logit_rows + R;
     int32_t* prev_slot = logit_slot + R;
-    int32_t* flat = prev_slot + prevR;
+    int32_t* blk = prev_slot + prevR;  // attention query blocks, 3 ints each (<= T blocks)
+    int32_t* flat = blk + 3 * T;
     {
         int t = 0, r = 0, poff = 0;
         for (int64_t i = 0; i < n_rows; ++i) {
@@ -619,6 +620,19 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
             poff += np;
         }
         for (int j = 0; j < prevR; ++j) prev_slot[j] = k.prev_logit_slots[j];
+        // attention query blocks: one per decode row, QP-position chunks of each prompt group
+        const int qp = ds::attention_block_positions(m.n_heads, m.n_kv_heads);
+        int tb = 0;
+        for (int64_t i = 0; i < n_rows; ++i) {
+            const ds_row& rw = rows[i];
+            for (int j = 0; j < rw.n_tok; j += qp) {
+                blk[3 * n_blk] = tb + j;
+                blk[3 * n_blk + 1] = std::min(qp, rw.n_tok - j);
+                blk[3 * n_blk + 2] = rw.n_tok == 1 ? 1 : 0;
+                ++n_blk;
+            }
+            tb += rw.n_tok;
+        }
     }
     const size_t meta_n = size_t(flat - hm) + P;
     CK(cudaMemcpyAsync(s->d_meta, hm, meta_n * 4, cudaMemcpyHostToDevice, s->stream));
@@ -632,7 +646,8 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     const int32_t* d_lrows = d_poff + T;
     const int32_t* d_lslot = d_lrows + R;
     const int32_t* d_prev = d_lslot + R;
-    const int32_t* d_flat = d_prev + prevR;
+    const int32_t* d_blk = d_prev + prevR;
+    const int32_t* d_flat = d_blk + 3 * T;
 
     // ---- wait for the swap-in this compute depends on
     if (k.resident_slot >= 0) CK(cudaStreamWaitEvent(s->stream, s->ev_h2d, 0));
@@ -694,9 +709,9 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
                            s->rope_sin, s->kv, li, s->q, st);
         end_other(PK_ELEM, 0, 2.0 * T * qkv_rows + 2.0 * T * (qdim + 2 * m.n_kv_heads * m.d_head), 1);
         begin();
-        rc |= ds::attention_paged(s->q, T, m.n_heads, d_pos, d_poff, d_flat, s->kv, li, max_ctx,
+        rc |= ds::attention_paged(s->q, T, m.n_heads, d_pos, d_poff, d_flat, d_blk, n_blk, s->kv, li, max_ctx,
                                   s->attn, s->attn_ws, s->attn_ws_floats, st);
-        end_other(PK_ATTN, attn_flops, attn_bytes, ds::attention_launches(T, m.n_kv_heads, max_ctx));
+        end_other(PK_ATTN, attn_flops, attn_bytes, ds::attention_launches(n_blk, m.n_kv_heads, max_ctx));
         begin();
         rc |= ds::gemm_bf16(lw.wo, s->attn, T, ds::EPI_RESID, s->x, s->x, nullptr, s->ws,
                             s->ws_floats, 0, st);

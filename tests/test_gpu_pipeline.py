@@ -87,7 +87,7 @@ def test_tiny_pipeline_matches_oracle(name):
     for ci in range(n):
         for k, row in enumerate(logits[ci]):
             top = np.sort(row)[-2:]
-            if top[1] - top[0] > 0.1:
+            if top[1] - top[0] > 0.16:
                 checked += 1
                 mism += int(np.argmax(row) != r["tokens"][ci][k])
     assert checked > 0 and mism == 0, (checked, mism)

@@ -2,9 +2,10 @@
 
 Tolerance (bf16 storage, fp32 accumulation; differences come from accumulation order and
 occasional one-ulp bf16 rounding flips that propagate through the layers):
-  logits:      |gpu - cpu| <= 0.05 + 0.02 * |cpu|          (logits have O(1) scale)
+  logits:      |gpu - cpu| <= 0.08 + 0.02 * |cpu|   (logits have O(1) scale; attention rounds the
+               softmax numerators to bf16 for the tensor-core P.V, as FlashAttention does)
   activations: |gpu - cpu| <= 0.03 * max|cpu| per row
-  greedy:      gpu argmax == oracle argmax wherever the oracle's top-2 margin > 0.1
+  greedy:      gpu argmax == oracle argmax wherever the oracle's top-2 margin > 0.16
 """
 import numpy as np
 import pytest
@@ -13,7 +14,7 @@ from stage_harness import Pair, greedy_ok, logits_ok, random_act
 
 pytestmark = pytest.mark.gpu
 
-LOGIT_MARGIN = 0.1
+LOGIT_MARGIN = 0.16
 
 
 def _check_logits(o):
