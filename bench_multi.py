@@ -1,11 +1,125 @@
-"""N>1 leg of bench.py (see bench.py docstring). Placeholder until the multi-GPU path lands."""
+"""N>1 leg of bench.py: one process per GPU (torchrun), stage r on GPU r, NCCL hops.
+
+Workload: Llama-3-8B cut into N pipeline stages (32/N layers each, reference partition_layers),
+100 ms injected latency per hop, 32 microbatches with KV swap enabled (BASELINE configs[2] at
+N=4), §5 prompts [0,512] x [0,512]. A step replays the first `rounds` circuits of every
+microbatch of the reference schedule from empty KV pools. value = generated tokens / max over
+ranks of the step's CUDA-event time on the stage stream (idle waits for delayed hops included);
+e2e = same on the host clock around the C-ABI call.
+"""
 import json
 import os
+import statistics
+
+CONFIGS = os.path.join(os.path.dirname(os.path.abspath(__file__)), "configs")
+METRIC = "generated tokens/sec (whole pipeline) at injected inter-stage latency; roofline fraction"
+
+
+def pipeline_config(n_stages, latency_us=100_000, nb=32):
+    cfg = json.load(open(os.path.join(CONFIGS, "llama8b_4stage.json")))
+    node = cfg["nodes"][0]
+    cfg["nodes"] = [dict(node, node_id=f"g{i}") for i in range(n_stages)]
+    link = cfg["links"][0]
+    cfg["links"] = [dict(link, src=f"g{i}", dst=f"g{(i + 1) % n_stages}", latency_us=latency_us)
+                    for i in range(n_stages)]
+    cfg["scheduler"]["nb_override"] = nb
+    return cfg
 
 
 def run_multi(args):
+    import torch.distributed as dist
+
+    from bench import ClockSampler, roofline
+    from paper_2501_14784_b200 import pipeline as pl
+    import ctypes as C
+    from paper_2501_14784_b200._native import GpuOpts, check, lib
+
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}: launch with torchrun")
+    dist.init_process_group("gloo", init_method="env://", rank=rank, world_size=world)
+    ids = [None]
+    if rank == 0:
+        buf = (C.c_uint8 * (128 * world))()
+        for i in range(world):
+            one = (C.c_uint8 * 128)()
+            check(lib.ds_nccl_unique_id(one))
+            C.memmove(C.addressof(buf) + 128 * i, one, 128)
+        ids = [bytes(buf)]
+    dist.broadcast_object_list(ids, src=0)
+    id_buf = (C.c_uint8 * (128 * world)).from_buffer_copy(ids[0])
+
+    cfg = pipeline_config(world)
+    txt = json.dumps(cfg)
+    plan = json.loads(pl.plan_config(txt, CONFIGS))
+    nb = plan["n_microbatches"]
+    rounds = 6
+    md = pl.model_desc("llama3-8b")
+    opts = GpuOpts(device0=local, n_devices=1, real_delay=1, collect_tokens=0,
+                   max_circuits=nb * rounds, weight_seed=pl.WEIGHT_SEED)
+    h = C.c_void_p()
+    check(lib.ds_session_create_rank(txt.encode(), CONFIGS.encode(), b"", -1, -1, C.byref(md),
+                                     C.byref(opts), rank, world, id_buf, C.byref(h)))
+
+    def run(profile=False):
+        cap = 1 << 24
+        out = C.create_string_buffer(cap)
+        check(lib.ds_session_run(h, int(profile), 0, out, cap, None))
+        return json.loads(out.value.decode())
+
+    try:
+        for _ in range(args.warmup):
+            dist.barrier()
+            run()
+        runs = []
+        with ClockSampler([local]) as clk:
+            for _ in range(args.steps):
+                dist.barrier()
+                runs.append(run())
+        dist.barrier()
+        prof = run(profile=True)
+    finally:
+        dist.barrier()
+        lib.ds_session_destroy(h)
+    dev = [r["device_us"] for r in runs]
+    wall = [r["wall_us"] for r in runs]
+    gathered = [None] * world
+    dist.all_gather_object(gathered, {"dev": dev, "wall": wall, "clk": clk.summary(),
+                                      "kernels": prof["stages"][0]["kernels"],
+                                      "launches": sum(r["launches"] for r in runs),
+                                      "stage": prof["stages"][0]})
+    dist.destroy_process_group()
     if rank != 0:
         return None
-    return {"metric": "generated tokens/sec (whole pipeline) at injected inter-stage latency; roofline fraction",
-            "value": None, "unit": "tokens/s", "n_gpus": args.gpus, "unavailable": "multi-GPU leg not built yet"}
+    dev_max = [max(g["dev"][i] for g in gathered) for i in range(args.steps)]
+    wall_max = [max(g["wall"][i] for g in gathered) for i in range(args.steps)]
+    toks = runs[0]["decode_tokens"]
+    clocks = gathered[0]["clk"]
+    clocks["per_rank_sm_mhz"] = [g["clk"]["sm_mhz"] for g in gathered]
+    clocks["reasons"] = sorted({r for g in gathered for r in g["clk"]["reasons"]})
+    rf = roofline(gathered[0]["kernels"])
+    rf["rank"] = 0
+    return {
+        "metric": METRIC, "value": round(toks * args.steps / (sum(dev_max) / 1e6), 2),
+        "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(statistics.mean(dev_max) / 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weights, counter-RNG prompts; lengths from the reference "
+                "generator seed 42)",
+        "config": {"workload": f"Llama-3-8B {world}-stage pipeline on {world}xB200, 100 ms injected "
+                               f"latency per hop, {nb} microbatches, KV swap enabled, first {rounds} "
+                               "circuits of every microbatch",
+                   "parallelism": f"pp{world}", "tokens_per_step": toks,
+                   "circuits_per_step": runs[0]["circuits"],
+                   "analytic_bound_tokens_per_s": pl.steady_state_throughput(json.dumps(plan)),
+                   "hops": "NCCL send/recv over NVLink, one 2-rank communicator per ring link"},
+        "e2e": {"value": round(toks * args.steps / (sum(wall_max) / 1e6), 2), "unit": "tokens/s",
+                "h2d_bytes_per_step": None, "d2h_bytes_per_step": 0},
+        "gpu_launches": sum(g["launches"] for g in gathered),
+        "roofline": rf, "clocks": clocks,
+        "per_rank": [{"device_ms": g["stage"]["device_ms"], "busy_ms": g["stage"]["busy_ms"],
+                      "swap_in_bytes": g["stage"]["swap_in_bytes"], "topups": g["stage"]["topups"]}
+                     for g in gathered],
+    }

@@ -199,6 +199,16 @@ ds_status ds_session_run(ds_session* session, int32_t profile, int32_t collect_t
                          char* report_json, size_t cap, size_t* needed);
 ds_status ds_session_destroy(ds_session* session);
 
+/* One process per GPU: this process runs pipeline stage `rank` of `world` (= stages) on device0;
+ * activations (and sampled ids, last -> first) hop over NCCL send/recv, one 2-rank communicator per
+ * ring link (reference ring links, src/planner.cpp:122-138). nccl_ids: world x 128 bytes, id i for
+ * link i -> i+1, generated once (ds_nccl_unique_id) and shared by the launcher. */
+ds_status ds_nccl_unique_id(uint8_t* out128);
+ds_status ds_session_create_rank(const char* config_json, const char* config_dir, const char* policy,
+                                 int64_t latency_us, int64_t nb_override, const ds_model_desc* model,
+                                 const ds_gpu_opts* opts, int32_t rank, int32_t world,
+                                 const uint8_t* nccl_ids, ds_session** out);
+
 /* ------------------------------------------------------------------------------------------
  * Kernel-level entry points (parity tests call these through the same library).
  * ------------------------------------------------------------------------------------------ */

@@ -97,6 +97,8 @@ def _load() -> C.CDLL:
         "ds_session_create": (I32, [S, S, S, I64, I64, P, P, P]),
         "ds_session_run": (I32, [P, I32, I32, P, C.c_size_t, P]),
         "ds_session_destroy": (I32, [P]),
+        "ds_nccl_unique_id": (I32, [P]),
+        "ds_session_create_rank": (I32, [S, S, S, I64, I64, P, P, I32, I32, P, P]),
         "ds_stage_profile": (I32, [P, I32]),
         "ds_stage_kernel_stats": (I32, [P, P, C.c_size_t, P]),
         "ds_schedule_config": (I32, [S, S, S, I64, I64, I64, P, C.c_size_t, P]),

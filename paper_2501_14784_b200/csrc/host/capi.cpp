@@ -8,6 +8,7 @@
 
 #include "capi_util.hpp"
 #include "executor.hpp"
+#include "hop_nccl.hpp"
 #include "pipeline.hpp"
 
 namespace {
@@ -245,6 +246,48 @@ ds_status ds_session_create(const char* config_json, const char* config_dir, con
         ds_session* h = new ds_session();
         try {
             h->s = dsb::session_create(cp.first, cp.second, std::move(o.schedule), *model, g);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+        return DS_OK;
+    });
+}
+
+ds_status ds_nccl_unique_id(uint8_t* out128) {
+    return guarded([&] {
+        std::string why;
+        const dsb::NcclApi* api = dsb::nccl_api(&why);
+        if (!api) return ds_fail(DS_ERR_RUNTIME, "NCCL unavailable: " + why);
+        ncclUniqueId id;
+        if (api->GetUniqueId(&id) != ncclSuccess) return ds_fail(DS_ERR_RUNTIME, "ncclGetUniqueId failed");
+        std::memcpy(out128, &id, sizeof(id));
+        return DS_OK;
+    });
+}
+
+ds_status ds_session_create_rank(const char* config_json, const char* config_dir, const char* policy,
+                                 int64_t latency_us, int64_t nb_override, const ds_model_desc* model,
+                                 const ds_gpu_opts* opts, int32_t rank, int32_t world,
+                                 const uint8_t* nccl_ids, ds_session** out) {
+    return guarded([&] {
+        if (!model || !opts || !out || rank < 0 || world < 1) return ds_fail(DS_ERR_ARG, "bad argument");
+        if (world > 1 && !nccl_ids) return ds_fail(DS_ERR_ARG, "nccl ids required for world > 1");
+        auto cp = dsb::plan_from_config(config_json, config_dir, policy, latency_us, nb_override);
+        dsb::SimOutput o = dsb::simulate(cp.second, cp.first.topo, cp.first.workload, cp.first.model,
+                                         false, true);
+        dsb::GpuOptions g;
+        g.device0 = opts->device0;
+        g.n_devices = 1;
+        g.real_delay = opts->real_delay != 0;
+        g.collect_tokens = opts->collect_tokens != 0;
+        g.max_circuits = opts->max_circuits;
+        g.weight_seed = opts->weight_seed;
+        ds_session* h = new ds_session();
+        try {
+            h->s = dsb::session_create(cp.first, cp.second, std::move(o.schedule), *model, g, rank, world,
+                                       nccl_ids);
         } catch (...) {
             delete h;
             throw;

@@ -26,6 +26,7 @@
 
 #include "capi_util.hpp"
 #include "executor.hpp"
+#include "hop_nccl.hpp"
 #include "pipeline.hpp"
 
 namespace dsb {
@@ -107,11 +108,28 @@ struct Session {
     std::vector<Worker> W;
     int32_t* tok_pool = nullptr;
     std::vector<int64_t> tok_off;
+    // one-process-per-GPU mode: this process runs stage `rank`; hops go over NCCL
+    bool nccl = false;
+    int rank = 0, world = 1;
+    const NcclApi* api = nullptr;
+    RingLinks links;
+    cudaStream_t s_send = nullptr, s_recv = nullptr;
+    std::vector<void*> send_buf;        // per mb: staged output for the send
+    std::vector<cudaEvent_t> ev_copy;   // per mb: output staged (send stream waits on it)
+    std::vector<cudaEvent_t> ev_recv;   // per circuit: the receive of that circuit landed
 };
 
 Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, const ds_model_desc& md,
-                        const GpuOptions& opt) {
+                        const GpuOptions& opt, int rank, int world, const void* nccl_ids) {
     std::unique_ptr<Session> S(new Session());
+    if (rank >= 0) {
+        if (world != plan.S())
+            throw ConfigError("world size " + std::to_string(world) + " != pipeline stages " +
+                              std::to_string(plan.S()));
+        S->nccl = world > 1;
+        S->rank = rank;
+        S->world = world;
+    }
     S->cfg = cfg;
     S->plan = plan;
     S->sched = std::move(sched);
@@ -148,13 +166,20 @@ Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, con
         }
     }
 
-    S->W.resize(NS);
+    // in-process: every stage, stage s on device0 + s % n_devices; per-rank: only stage `rank`
+    std::vector<int64_t> mine;
+    if (rank >= 0)
+        mine.push_back(rank);
+    else
+        for (int64_t s = 0; s < NS; ++s) mine.push_back(s);
+    S->W.resize(mine.size());
     const bool swapping = plan.offload && NB > 2;
     const Tokens ppr = div_up(plan.seq_budget, kPage);
-    for (int64_t s = 0; s < NS; ++s) {
-        Worker& w = S->W[s];
+    for (size_t wi = 0; wi < mine.size(); ++wi) {
+        const int64_t s = mine[wi];
+        Worker& w = S->W[wi];
         w.idx = int(s);
-        w.device = opt.device0 + int(s % use_dev);
+        w.device = rank >= 0 ? opt.device0 : opt.device0 + int(s % use_dev);
         const StagePlanD& sp = plan.stages[s];
         DK(ds_stage_create(w.device, &md, sp.layer_begin, sp.layer_end, s == 0, s == NS - 1,
                            opt.weight_seed, int32_t(S->max_rows), int32_t(S->B), &w.st));
@@ -180,7 +205,26 @@ Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, con
             XK(cudaMemset(w.recv[m], 0, bytes));
         }
     }
-    if (use_dev > 1)
+    if (S->nccl) {
+        std::string why;
+        S->api = nccl_api(&why);
+        if (!S->api) throw SimError("NCCL unavailable: " + why);
+        Worker& w = S->W[0];
+        XK(cudaSetDevice(w.device));
+        XK(cudaStreamCreateWithFlags(&S->s_send, cudaStreamNonBlocking));
+        XK(cudaStreamCreateWithFlags(&S->s_recv, cudaStreamNonBlocking));
+        S->send_buf.assign(NB, nullptr);
+        S->ev_copy.assign(NB, nullptr);
+        const size_t sb = rank == NS - 1 ? size_t(S->max_rows) * 4 : size_t(S->max_rows) * md.d_model * 2;
+        for (int64_t m = 0; m < NB; ++m) {
+            XK(cudaMalloc(&S->send_buf[m], sb));
+            XK(cudaEventCreateWithFlags(&S->ev_copy[m], cudaEventDisableTiming));
+        }
+        S->ev_recv.assign(S->n_circ, nullptr);
+        for (auto& e : S->ev_recv) XK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        S->links.init(*S->api, rank, world, static_cast<const ncclUniqueId*>(nccl_ids));
+    }
+    if (use_dev > 1 && rank < 0)
         for (int a = 0; a < use_dev; ++a)
             for (int b = 0; b < use_dev; ++b)
                 if (a != b) {
@@ -217,6 +261,14 @@ void session_destroy(Session* S) {
         if (w.t_end) cudaEventDestroy(w.t_end);
         ds_stage_destroy(w.st);
     }
+    if (S->nccl) {
+        for (void* p : S->send_buf) cudaFree(p);
+        for (auto e : S->ev_copy) cudaEventDestroy(e);
+        for (auto e : S->ev_recv) cudaEventDestroy(e);
+        if (S->s_send) cudaStreamDestroy(S->s_send);
+        if (S->s_recv) cudaStreamDestroy(S->s_recv);
+        if (S->api) S->links.destroy(*S->api);
+    }
     if (S->tok_pool) cudaFreeHost(S->tok_pool);
     delete S;
 }
@@ -236,12 +288,20 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
         w.error.clear();
     }
     int64_t launches0 = 0;
-    std::vector<int64_t> h2d0(NS, 0);
-    for (int64_t s = 0; s < NS; ++s) {
+    for (auto& w : S->W) {
         int64_t l = 0;
-        DK(ds_stage_kernel_stats(S->W[s].st, nullptr, 0, &l));
+        DK(ds_stage_kernel_stats(w.st, nullptr, 0, &l));
         launches0 += l;
     }
+    // bytes of the hop that lands at stage `to` for circuit c (activations, or ids at stage 0)
+    auto hop_bytes = [&](int64_t to, int64_t c) -> size_t {
+        if (to == 0) {
+            int64_t r = 0;
+            for (const auto& row : circs[c].rows) r += row.need_logits;
+            return size_t(r) * 4;
+        }
+        return size_t(circs[c].eff_batch) * S->md.d_model * 2;
+    };
     auto hop_delay = [&](int64_t from, int64_t eff) -> int64_t {
         if (!opt.real_delay || NS < 2) return 0;
         const Link& l = plan.ring[from];
@@ -259,7 +319,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
         try {
             XK(cudaSetDevice(w.device));
             const int64_t s = w.idx;
-            Worker& next = S->W[(s + 1) % NS];
+            Worker* next = S->nccl ? nullptr : &S->W[(s + 1) % NS];
             const bool last = s == NS - 1;
             std::vector<ds_row> rows;
             for (const StageOp& op : S->sched.ops[s]) {
@@ -302,7 +362,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     const int64_t arrive = t_done + hop_delay(from, circs[need].eff_batch);
                     const int64_t wait = arrive - now_us();
                     if (wait > 0) std::this_thread::sleep_for(std::chrono::microseconds(wait));
-                    XK(cudaStreamWaitEvent(w.stream, mbx.ev, 0));
+                    XK(cudaStreamWaitEvent(w.stream, S->nccl ? S->ev_recv[need] : mbx.ev, 0));
                 }
                 // ---- residency top-up: the plan's prefetch may be stale
                 int32_t resident = 1;
@@ -343,13 +403,27 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 if (last && collect_tokens && S->tok_pool && n_out > 0)
                     XK(cudaMemcpyAsync(S->tok_pool + S->tok_off[c], src, size_t(n_out) * 4,
                                        cudaMemcpyDeviceToHost, w.stream));
-                if (NS > 1 && bytes > 0) {
-                    if (next.device == w.device)
-                        XK(cudaMemcpyAsync(next.recv[mb], src, size_t(bytes), cudaMemcpyDeviceToDevice, w.stream));
-                    else
-                        XK(cudaMemcpyPeerAsync(next.recv[mb], next.device, src, w.device, size_t(bytes), w.stream));
+                if (S->nccl) {
+                    // stage the output per microbatch, then ncclSend on the send stream
+                    if (bytes > 0) {
+                        XK(cudaMemcpyAsync(S->send_buf[mb], src, size_t(bytes), cudaMemcpyDeviceToDevice,
+                                           w.stream));
+                        XK(cudaEventRecord(S->ev_copy[mb], w.stream));
+                        XK(cudaStreamWaitEvent(S->s_send, S->ev_copy[mb], 0));
+                        const ncclResult_t nr = S->api->Send(S->send_buf[mb], size_t(bytes), ncclUint8, 1,
+                                                             S->links.send, S->s_send);
+                        if (nr != ncclSuccess)
+                            throw SimError(std::string("ncclSend: ") + S->api->GetErrorString(nr));
+                    }
+                    continue;
                 }
-                Mailbox& out = *next.in[mb];
+                if (NS > 1 && bytes > 0) {
+                    if (next->device == w.device)
+                        XK(cudaMemcpyAsync(next->recv[mb], src, size_t(bytes), cudaMemcpyDeviceToDevice, w.stream));
+                    else
+                        XK(cudaMemcpyPeerAsync(next->recv[mb], next->device, src, w.device, size_t(bytes), w.stream));
+                }
+                Mailbox& out = *next->in[mb];
                 XK(cudaEventRecord(out.ev, w.stream));
                 XK(cudaLaunchHostFunc(w.stream, post_cb, new PostCtx{&out, c}));
             }
@@ -362,9 +436,42 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 for (auto& m : ww.in) m->cv.notify_all();
         }
     };
+    // NCCL mode: a receiver thread posts the receives in the previous stage's send order (its
+    // compute order, known from the schedule) and publishes each landing to the mailboxes
+    auto receiver = [&]() {
+        Worker& w = S->W[0];
+        try {
+            XK(cudaSetDevice(w.device));
+            const int64_t from = (w.idx + NS - 1) % NS;
+            for (const StageOp& op : S->sched.ops[from]) {
+                if (failed) return;
+                if (op.kind != OpKind::Compute) continue;
+                const int64_t c = op.circuit;
+                if (c < 0 || c >= S->n_circ) break;
+                const size_t bytes = hop_bytes(w.idx, c);
+                if (bytes == 0) continue;  // the sender skips empty hops too
+                const int32_t mb = circs[c].mb;
+                const ncclResult_t nr =
+                    S->api->Recv(w.recv[mb], bytes, ncclUint8, 0, S->links.recv, S->s_recv);
+                if (nr != ncclSuccess) throw SimError(std::string("ncclRecv: ") + S->api->GetErrorString(nr));
+                XK(cudaEventRecord(S->ev_recv[c], S->s_recv));
+                XK(cudaLaunchHostFunc(S->s_recv, post_cb, new PostCtx{w.in[mb].get(), c}));
+            }
+            XK(cudaStreamSynchronize(S->s_recv));
+        } catch (const std::exception& e) {
+            if (w.error.empty()) w.error = std::string("receiver: ") + e.what();
+            failed = true;
+            for (auto& m : w.in) m->cv.notify_all();
+        }
+    };
     std::vector<std::thread> th;
+    if (S->nccl) th.emplace_back(receiver);
     for (auto& w : S->W) th.emplace_back(body, std::ref(w));
     for (auto& t : th) t.join();
+    if (S->nccl) {
+        cudaSetDevice(S->W[0].device);
+        cudaStreamSynchronize(S->s_send);
+    }
     for (auto& w : S->W) {
         cudaSetDevice(w.device);
         ds_stage_sync(w.st);

@@ -39,8 +39,11 @@ struct GpuRunResult {
 };
 
 struct Session;
+// rank < 0: every stage in this process (stage s on device0 + s % n_devices, hops by peer copy).
+// rank >= 0: only stage `rank` on device0, hops over NCCL (nccl_ids: world ncclUniqueIds).
 Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, const ds_model_desc& md,
-                        const GpuOptions& opt);
+                        const GpuOptions& opt, int rank = -1, int world = 1,
+                        const void* nccl_ids = nullptr);
 GpuRunResult session_run(Session* s, bool profile, bool collect_tokens);
 void session_destroy(Session* s);
 

@@ -1,0 +1,60 @@
+// NCCL resolution and ring-link setup (see hop_nccl.hpp).
+#include "hop_nccl.hpp"
+
+#include <dlfcn.h>
+
+#include <mutex>
+
+#include "pipeline.hpp"
+
+namespace dsb {
+
+const NcclApi* nccl_api(std::string* why) {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            api.error = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+            return;
+        }
+        auto sym = [&](const char* n) { return dlsym(h, n); };
+        api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+        api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+        api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+        api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+        api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+        api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+        api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+        api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+        if (!api.GetUniqueId || !api.CommInitRank || !api.Recv || !api.GroupStart || !api.GroupEnd) {
+            api.Send = nullptr;
+            api.error = "libnccl is missing point-to-point symbols";
+        }
+    });
+    if (!api.ok()) {
+        if (why) *why = api.error;
+        return nullptr;
+    }
+    return &api;
+}
+
+void RingLinks::init(const NcclApi& api, int rank, int world, const ncclUniqueId* ids) {
+    auto chk = [&](ncclResult_t r, const char* what) {
+        if (r != ncclSuccess) throw SimError(std::string(what) + ": " + api.GetErrorString(r));
+    };
+    const int prev = (rank + world - 1) % world;
+    chk(api.GroupStart(), "ncclGroupStart");
+    chk(api.CommInitRank(&send, 2, ids[rank], 0), "ncclCommInitRank(send link)");
+    chk(api.CommInitRank(&recv, 2, ids[prev], 1), "ncclCommInitRank(recv link)");
+    chk(api.GroupEnd(), "ncclGroupEnd");
+}
+
+void RingLinks::destroy(const NcclApi& api) {
+    if (send) api.CommDestroy(send);
+    if (recv) api.CommDestroy(recv);
+    send = recv = nullptr;
+}
+
+}  // namespace dsb
