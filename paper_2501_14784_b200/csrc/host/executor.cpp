@@ -18,6 +18,8 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -32,6 +34,8 @@
 namespace dsb {
 
 namespace {
+
+const bool g_trace = getenv("DS_TRACE") != nullptr;
 
 int64_t now_us() {
     return std::chrono::duration_cast<std::chrono::microseconds>(
@@ -354,6 +358,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     int64_t t_done;
                     {
                         std::unique_lock<std::mutex> lk(mbx.mu);
+                        if (g_trace) fprintf(stderr, "[ds r%lld] wait c=%lld mb=%d need=%lld posted=%lld\n", (long long)s, (long long)c, mb, (long long)need, (long long)mbx.posted);
                         mbx.cv.wait(lk, [&] { return mbx.posted >= need || failed.load(); });
                         t_done = mbx.t_done;
                     }
@@ -393,6 +398,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 const void* act_in = s == 0 ? (has_input ? w.recv[mb] : nullptr) : w.recv[mb];
                 void* act_out = (last && NS == 1) ? w.recv[mb] : nullptr;  // ids loop back
                 DK(ds_stage_step(w.st, mb, rows.data(), int64_t(rows.size()), act_in, act_out));
+                if (g_trace) fprintf(stderr, "[ds r%lld] step c=%lld mb=%d rows=%lld need=%lld\n", (long long)s, (long long)c, mb, (long long)circ.eff_batch, (long long)need);
                 if (tm) XK(cudaEventRecord(tm->b, w.stream));
                 w.computes++;
                 // ---- hop to the next stage (or ids back to stage 0)
@@ -456,6 +462,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 if (nr != ncclSuccess) throw SimError(std::string("ncclRecv: ") + S->api->GetErrorString(nr));
                 XK(cudaEventRecord(S->ev_recv[c], S->s_recv));
                 XK(cudaLaunchHostFunc(S->s_recv, post_cb, new PostCtx{w.in[mb].get(), c}));
+                if (g_trace) fprintf(stderr, "[ds r%lld] recv posted c=%lld mb=%d bytes=%zu\n", (long long)w.idx, (long long)c, mb, bytes);
             }
             XK(cudaStreamSynchronize(S->s_recv));
         } catch (const std::exception& e) {
