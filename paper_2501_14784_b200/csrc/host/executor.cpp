@@ -75,6 +75,7 @@ void CUDART_CB post_cb(void* p) {
         c->box->t_done = now_us();
     }
     c->box->cv.notify_all();
+    if (g_trace) fprintf(stderr, "[ds] posted circuit %lld\n", (long long)c->circuit);
     delete c;
 }
 
@@ -420,6 +421,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                                                              S->links.send, S->s_send);
                         if (nr != ncclSuccess)
                             throw SimError(std::string("ncclSend: ") + S->api->GetErrorString(nr));
+                        if (g_trace) fprintf(stderr, "[ds r%lld] send enqueued c=%lld mb=%d bytes=%lld\n", (long long)s, (long long)c, mb, (long long)bytes);
                     }
                     continue;
                 }
