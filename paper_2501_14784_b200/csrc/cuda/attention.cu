@@ -403,3 +403,17 @@ int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_p
 }
 
 }  // namespace ds
+
+namespace ds {
+void preload_attention() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, attn_tc_kernel<128>);
+    cudaFuncGetAttributes(&a, attn_tc_kernel<64>);
+    cudaFuncGetAttributes(&a, attn_combine_kernel<128>);
+    cudaFuncGetAttributes(&a, attn_combine_kernel<64>);
+    cudaFuncSetAttribute(attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(AttnSmem<128>)));
+    cudaFuncSetAttribute(attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(AttnSmem<64>)));
+}
+}  // namespace ds

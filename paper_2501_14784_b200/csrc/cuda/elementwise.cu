@@ -275,3 +275,20 @@ void resolve_tokens(const int32_t* prompt_tok, const int32_t* row_req, const int
 }
 
 }  // namespace ds
+
+namespace ds {
+void preload_elementwise() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, init_weights_kernel);
+    cudaFuncGetAttributes(&a, fill_bf16_kernel);
+    cudaFuncGetAttributes(&a, embed_kernel);
+    cudaFuncGetAttributes(&a, rmsnorm_kernel<1>);
+    cudaFuncGetAttributes(&a, rmsnorm_kernel<4>);
+    cudaFuncGetAttributes(&a, rmsnorm_kernel<8>);
+    cudaFuncGetAttributes(&a, rope_kv_kernel);
+    cudaFuncGetAttributes(&a, silu_mul_kernel);
+    cudaFuncGetAttributes(&a, argmax_kernel);
+    cudaFuncGetAttributes(&a, scatter_tokens_kernel);
+    cudaFuncGetAttributes(&a, resolve_tokens_kernel);
+}
+}  // namespace ds

@@ -337,3 +337,14 @@ int gemm_weight_init(GemmWeight* w, const __nv_bfloat16* data, int N, int K) {
 }
 
 }  // namespace ds
+
+namespace ds {
+// Forces the module holding these kernels to load now (lazy loading would otherwise load it at
+// the first launch, which can wait on in-flight work such as a spinning NCCL receive).
+void preload_gemm() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, gemm_tc_kernel);
+    cudaFuncGetAttributes(&a, splitk_reduce_kernel);
+    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
+}
+}  // namespace ds

@@ -81,4 +81,14 @@ void scatter_tokens(const int32_t* ids, const int32_t* req, int R, int32_t* last
 void resolve_tokens(const int32_t* prompt_tok, const int32_t* row_req, const int32_t* last_token,
                     int T, int32_t* tokens, cudaStream_t stream);
 
+// Eager module load of every kernel (see gemm_tc.cu preload_gemm).
+void preload_gemm();
+void preload_attention();
+void preload_elementwise();
+inline void preload_all() {
+    preload_gemm();
+    preload_attention();
+    preload_elementwise();
+}
+
 }  // namespace ds

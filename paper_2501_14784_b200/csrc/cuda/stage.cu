@@ -178,6 +178,7 @@ ds_status ds_stage_create(int32_t device, const ds_model_desc* md, int64_t layer
         return ds_fail(DS_ERR_NO_DEVICE, "no CUDA device: the B200 stage path has no CPU fallback");
     if (device < 0 || device >= ndev) return ds_fail(DS_ERR_ARG, "bad device index");
     CK(cudaSetDevice(device));
+    ds::preload_all();  // no lazy module load later, while e.g. an NCCL receive spins
 
     ds_stage* s = new ds_stage();
     *out = nullptr;
