@@ -122,7 +122,29 @@ struct Session {
     std::vector<void*> send_buf;        // per mb: staged output for the send
     std::vector<cudaEvent_t> ev_copy;   // per mb: output staged (send stream waits on it)
     std::vector<cudaEvent_t> ev_recv;   // per circuit: the receive of that circuit landed
+    std::mutex nccl_mu;                 // NCCL calls from the send and receive threads
+    // receives in flight are bounded: a receive posted far ahead spins on the GPU and, once
+    // NCCL's work queue fills, blocks the host inside ncclRecv while the peer waits on us
+    static constexpr int kRecvAhead = 2;
+    std::mutex land_mu;
+    std::condition_variable land_cv;
+    int64_t landed = 0;
 };
+
+namespace {
+struct LandCtx {
+    Session* s;
+};
+void CUDART_CB land_cb(void* p) {
+    Session* s = static_cast<LandCtx*>(p)->s;
+    {
+        std::lock_guard<std::mutex> lk(s->land_mu);
+        s->landed++;
+    }
+    s->land_cv.notify_all();
+    delete static_cast<LandCtx*>(p);
+}
+}  // namespace
 
 Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, const ds_model_desc& md,
                         const GpuOptions& opt, int rank, int world, const void* nccl_ids) {
@@ -288,6 +310,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
         DK(ds_kv_reset(w.st));
         DK(ds_stage_profile(w.st, profile ? 1 : 0));
         for (auto& m : w.in) m->posted = -1;
+        S->landed = 0;
         w.served = w.topups = w.moved_in = w.moved_out = w.plan_in = w.computes = 0;
         w.timing_used = 0;
         w.error.clear();
@@ -417,8 +440,12 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                                            w.stream));
                         XK(cudaEventRecord(S->ev_copy[mb], w.stream));
                         XK(cudaStreamWaitEvent(S->s_send, S->ev_copy[mb], 0));
-                        const ncclResult_t nr = S->api->Send(S->send_buf[mb], size_t(bytes), ncclUint8, 1,
-                                                             S->links.send, S->s_send);
+                        ncclResult_t nr;
+                        {
+                            std::lock_guard<std::mutex> lk(S->nccl_mu);
+                            nr = S->api->Send(S->send_buf[mb], size_t(bytes), ncclUint8, 1, S->links.send,
+                                              S->s_send);
+                        }
                         if (nr != ncclSuccess)
                             throw SimError(std::string("ncclSend: ") + S->api->GetErrorString(nr));
                         if (g_trace) fprintf(stderr, "[ds r%lld] send enqueued c=%lld mb=%d bytes=%lld\n", (long long)s, (long long)c, mb, (long long)bytes);
@@ -442,6 +469,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
             failed = true;
             for (auto& ww : S->W)
                 for (auto& m : ww.in) m->cv.notify_all();
+            S->land_cv.notify_all();
         }
     };
     // NCCL mode: a receiver thread posts the receives in the previous stage's send order (its
@@ -451,6 +479,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
         try {
             XK(cudaSetDevice(w.device));
             const int64_t from = (w.idx + NS - 1) % NS;
+            int64_t posted_n = 0;
             for (const StageOp& op : S->sched.ops[from]) {
                 if (failed) return;
                 if (op.kind != OpKind::Compute) continue;
@@ -459,10 +488,20 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 const size_t bytes = hop_bytes(w.idx, c);
                 if (bytes == 0) continue;  // the sender skips empty hops too
                 const int32_t mb = circs[c].mb;
-                const ncclResult_t nr =
-                    S->api->Recv(w.recv[mb], bytes, ncclUint8, 0, S->links.recv, S->s_recv);
+                {
+                    std::unique_lock<std::mutex> lk(S->land_mu);
+                    S->land_cv.wait(lk, [&] { return posted_n - S->landed < Session::kRecvAhead || failed.load(); });
+                }
+                if (failed) return;
+                ncclResult_t nr;
+                {
+                    std::lock_guard<std::mutex> lk(S->nccl_mu);
+                    nr = S->api->Recv(w.recv[mb], bytes, ncclUint8, 0, S->links.recv, S->s_recv);
+                }
+                ++posted_n;
                 if (nr != ncclSuccess) throw SimError(std::string("ncclRecv: ") + S->api->GetErrorString(nr));
                 XK(cudaEventRecord(S->ev_recv[c], S->s_recv));
+                XK(cudaLaunchHostFunc(S->s_recv, land_cb, new LandCtx{S}));
                 XK(cudaLaunchHostFunc(S->s_recv, post_cb, new PostCtx{w.in[mb].get(), c}));
                 if (g_trace) fprintf(stderr, "[ds r%lld] recv posted c=%lld mb=%d bytes=%zu\n", (long long)w.idx, (long long)c, mb, bytes);
             }
