@@ -122,7 +122,6 @@ struct Session {
     std::vector<void*> send_buf;        // per mb: staged output for the send
     std::vector<cudaEvent_t> ev_copy;   // per mb: output staged (send stream waits on it)
     std::vector<cudaEvent_t> ev_recv;   // per circuit: the receive of that circuit landed
-    std::mutex nccl_mu;                 // NCCL calls from the send and receive threads
     // receives in flight are bounded: a receive posted far ahead spins on the GPU and, once
     // NCCL's work queue fills, blocks the host inside ncclRecv while the peer waits on us
     static constexpr int kRecvAhead = 2;
@@ -250,6 +249,11 @@ Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, con
         S->ev_recv.assign(S->n_circ, nullptr);
         for (auto& e : S->ev_recv) XK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         S->links.init(*S->api, rank, world, static_cast<const ncclUniqueId*>(nccl_ids));
+        // NCCL connects p2p peers lazily and the first send/recv on a link blocks the calling
+        // host thread until the peer joins; warm both links up in one group so the send thread
+        // and the receive thread never block on connection setup later
+        S->links.warmup(*S->api, S->send_buf[0], w.recv[0], S->s_send);
+        XK(cudaStreamSynchronize(S->s_send));
     }
     if (use_dev > 1 && rank < 0)
         for (int a = 0; a < use_dev; ++a)
@@ -440,12 +444,8 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                                            w.stream));
                         XK(cudaEventRecord(S->ev_copy[mb], w.stream));
                         XK(cudaStreamWaitEvent(S->s_send, S->ev_copy[mb], 0));
-                        ncclResult_t nr;
-                        {
-                            std::lock_guard<std::mutex> lk(S->nccl_mu);
-                            nr = S->api->Send(S->send_buf[mb], size_t(bytes), ncclUint8, 1, S->links.send,
-                                              S->s_send);
-                        }
+                        const ncclResult_t nr = S->api->Send(S->send_buf[mb], size_t(bytes), ncclUint8, 1,
+                                                             S->links.send, S->s_send);
                         if (nr != ncclSuccess)
                             throw SimError(std::string("ncclSend: ") + S->api->GetErrorString(nr));
                         if (g_trace) fprintf(stderr, "[ds r%lld] send enqueued c=%lld mb=%d bytes=%lld\n", (long long)s, (long long)c, mb, (long long)bytes);
@@ -493,11 +493,8 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     S->land_cv.wait(lk, [&] { return posted_n - S->landed < Session::kRecvAhead || failed.load(); });
                 }
                 if (failed) return;
-                ncclResult_t nr;
-                {
-                    std::lock_guard<std::mutex> lk(S->nccl_mu);
-                    nr = S->api->Recv(w.recv[mb], bytes, ncclUint8, 0, S->links.recv, S->s_recv);
-                }
+                const ncclResult_t nr =
+                    S->api->Recv(w.recv[mb], bytes, ncclUint8, 0, S->links.recv, S->s_recv);
                 ++posted_n;
                 if (nr != ncclSuccess) throw SimError(std::string("ncclRecv: ") + S->api->GetErrorString(nr));
                 XK(cudaEventRecord(S->ev_recv[c], S->s_recv));

@@ -51,6 +51,16 @@ void RingLinks::init(const NcclApi& api, int rank, int world, const ncclUniqueId
     chk(api.GroupEnd(), "ncclGroupEnd");
 }
 
+void RingLinks::warmup(const NcclApi& api, void* send_buf, void* recv_buf, cudaStream_t stream) {
+    auto chk = [&](ncclResult_t r, const char* what) {
+        if (r != ncclSuccess) throw SimError(std::string(what) + ": " + api.GetErrorString(r));
+    };
+    chk(api.GroupStart(), "ncclGroupStart");
+    chk(api.Send(send_buf, 16, ncclUint8, 1, send, stream), "ncclSend(warmup)");
+    chk(api.Recv(recv_buf, 16, ncclUint8, 0, recv, stream), "ncclRecv(warmup)");
+    chk(api.GroupEnd(), "ncclGroupEnd");
+}
+
 void RingLinks::destroy(const NcclApi& api) {
     if (send) api.CommDestroy(send);
     if (recv) api.CommDestroy(recv);

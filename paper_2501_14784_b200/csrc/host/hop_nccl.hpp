@@ -33,6 +33,9 @@ const NcclApi* nccl_api(std::string* why);
 struct RingLinks {
     ncclComm_t send = nullptr, recv = nullptr;
     void init(const NcclApi& api, int rank, int world, const ncclUniqueId* ids);
+    // one tiny send on the send link and receive on the recv link, grouped: establishes both
+    // p2p connections on every rank at once
+    void warmup(const NcclApi& api, void* send_buf, void* recv_buf, cudaStream_t stream);
     void destroy(const NcclApi& api);
 };
 
