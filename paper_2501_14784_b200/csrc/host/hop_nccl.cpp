@@ -45,6 +45,8 @@ void RingLinks::init(const NcclApi& api, int rank, int world, const ncclUniqueId
         if (r != ncclSuccess) throw SimError(std::string(what) + ": " + api.GetErrorString(r));
     };
     const int prev = (rank + world - 1) % world;
+    rank_ = rank;
+    world_ = world;
     chk(api.GroupStart(), "ncclGroupStart");
     chk(api.CommInitRank(&send, 2, ids[rank], 0), "ncclCommInitRank(send link)");
     chk(api.CommInitRank(&recv, 2, ids[prev], 1), "ncclCommInitRank(recv link)");
@@ -61,9 +63,14 @@ void RingLinks::warmup(const NcclApi& api, void* send_buf, void* recv_buf, cudaS
     chk(api.GroupEnd(), "ncclGroupEnd");
 }
 
+// ncclCommDestroy finalizes with the peer, so every rank tears its two links down in global
+// link-index order (link i joins ranks i and i+1): the wait graph stays acyclic.
 void RingLinks::destroy(const NcclApi& api) {
-    if (send) api.CommDestroy(send);
-    if (recv) api.CommDestroy(recv);
+    const int send_link = rank_, recv_link = (rank_ + world_ - 1) % world_;
+    ncclComm_t first = send_link < recv_link ? send : recv;
+    ncclComm_t second = send_link < recv_link ? recv : send;
+    if (first) api.CommDestroy(first);
+    if (second) api.CommDestroy(second);
     send = recv = nullptr;
 }
 

@@ -37,6 +37,7 @@ struct RingLinks {
     // p2p connections on every rank at once
     void warmup(const NcclApi& api, void* send_buf, void* recv_buf, cudaStream_t stream);
     void destroy(const NcclApi& api);
+    int rank_ = 0, world_ = 1;
 };
 
 }  // namespace dsb
