@@ -2,7 +2,7 @@
 
 Workload: Llama-3-8B cut into N pipeline stages (32/N layers each, reference partition_layers),
 100 ms injected latency per hop, 32 microbatches with KV swap enabled (BASELINE configs[2] at
-N=4), §5 prompts [0,512] x [0,512]. A step replays the first `rounds` circuits of every
+N=4), §5 prompts [0,512] x [0,512], 4096-token prefill chunk. A step replays the first `rounds` circuits of every
 microbatch of the reference schedule from empty KV pools. value = generated tokens / max over
 ranks of the step's CUDA-event time on the stage stream (idle waits for delayed hops included);
 e2e = same on the host clock around the C-ABI call.
@@ -23,6 +23,9 @@ def pipeline_config(n_stages, latency_us=100_000, nb=32):
     cfg["links"] = [dict(link, src=f"g{i}", dst=f"g{(i + 1) % n_stages}", latency_us=latency_us)
                     for i in range(n_stages)]
     cfg["scheduler"]["nb_override"] = nb
+    # a 4096-token prefill chunk per circuit: with the reference default (256) the 32 x B requests
+    # admitted at t=0 need ~B circuits of prefill per microbatch before decode dominates
+    cfg["scheduler"]["prefill_chunk"] = 4096
     return cfg
 
 
@@ -55,7 +58,7 @@ def run_multi(args):
     txt = json.dumps(cfg)
     plan = json.loads(pl.plan_config(txt, CONFIGS))
     nb = plan["n_microbatches"]
-    rounds = 6
+    rounds = 30
     md = pl.model_desc("llama3-8b")
     opts = GpuOpts(device0=local, n_devices=1, real_delay=1, collect_tokens=0,
                    max_circuits=nb * rounds, weight_seed=pl.WEIGHT_SEED)
