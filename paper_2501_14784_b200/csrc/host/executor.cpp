@@ -225,11 +225,16 @@ Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, con
         w.recv.assign(NB, nullptr);
         for (int64_t m = 0; m < NB; ++m) {
             w.in[m].reset(new Mailbox());
-            XK(cudaEventCreateWithFlags(&w.in[m]->ev, cudaEventDisableTiming));
             const size_t bytes = s == 0 ? size_t(S->max_rows) * 4 : size_t(S->max_rows) * md.d_model * 2;
             XK(cudaMalloc(&w.recv[m], bytes));
             XK(cudaMemset(w.recv[m], 0, bytes));
         }
+    }
+    // a mailbox event is recorded on the PRODUCER's stream, so it must belong to that device
+    for (auto& w : S->W) {
+        const Worker& prod = S->nccl ? w : S->W[(w.idx + NS - 1) % NS];
+        XK(cudaSetDevice(prod.device));
+        for (auto& m : w.in) XK(cudaEventCreateWithFlags(&m->ev, cudaEventDisableTiming));
     }
     if (S->nccl) {
         std::string why;
