@@ -214,6 +214,8 @@ ds_status ds_session_create_rank(const char* config_json, const char* config_dir
  * ------------------------------------------------------------------------------------------ */
 ds_status ds_dbg_gemm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t N, int32_t K,
                       int32_t epi, const uint16_t* resid, int32_t k_splits, void* out);
+ds_status ds_dbg_gemm_bench(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters,
+                            int32_t k_splits, float* ms_out);
 ds_status ds_dbg_has_device(int32_t* n_devices);
 ds_status ds_dbg_alloc(int32_t device, int64_t bytes, void** out);
 ds_status ds_dbg_free(void* ptr);

@@ -105,6 +105,7 @@ def _load() -> C.CDLL:
         "ds_gpu_run_config": (I32, [S, S, S, I64, I64, P, P, P, C.c_size_t, P]),
         "ds_dbg_gemm": (I32, [P, P, I32, I32, I32, I32, P, I32, P]),
         "ds_dbg_has_device": (I32, [P]),
+        "ds_dbg_gemm_bench": (I32, [I32, I32, I32, I32, I32, I32, P]),
         "ds_dbg_alloc": (I32, [I32, I64, P]),
         "ds_dbg_free": (I32, [P]),
         "ds_dbg_copy": (I32, [P, P, I64]),

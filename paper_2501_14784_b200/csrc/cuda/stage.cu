@@ -867,6 +867,56 @@ ds_status ds_dbg_copy(void* dst, const void* src, int64_t bytes) {
     return DS_OK;
 }
 
+// Times gemm_bf16 on device-resident random operands: ms per launch (CUDA events, `iters`
+// back-to-back launches after 3 warm-ups; weights larger than L2 are rotated through `n_w`
+// copies so every launch streams its weights from HBM).
+ds_status ds_dbg_gemm_bench(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters,
+                            int32_t k_splits, float* ms_out) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return ds_fail(DS_ERR_NO_DEVICE, "no CUDA device");
+    ds::preload_all();
+    const size_t wbytes = size_t(N) * K * 2;
+    const int n_w = int(std::max<size_t>(1, std::min<size_t>(16, (size_t(512) << 20) / wbytes + 1)));
+    bf16 *dx = nullptr, *dw = nullptr, *dout = nullptr;
+    float *dws = nullptr, *df = nullptr;
+    CK(cudaMalloc(&dx, size_t(T) * K * 2));
+    CK(cudaMalloc(&dw, wbytes * n_w));
+    CK(cudaMalloc(&dout, size_t(T) * N * 2));
+    CK(cudaMalloc(&df, size_t(T) * N * 4));
+    const size_t wsf = size_t(8) * T * N;
+    CK(cudaMalloc(&dws, wsf * 4));
+    ds::init_weights(dx, 1, 1, T, K, 1.0f, -1, 0);
+    ds::init_weights(dw, 1, 2, int64_t(N) * n_w, K, 0.02f, -1, 0);
+    CK(cudaMemset(dout, 0, size_t(T) * N * 2));
+    std::vector<GemmWeight> gw(n_w);
+    for (int i = 0; i < n_w; ++i)
+        if (ds::gemm_weight_init(&gw[i], dw + size_t(i) * N * K, N, K))
+            return ds_fail(DS_ERR_RUNTIME, "tensor map");
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    for (int i = 0; i < 3; ++i)
+        ds::gemm_bf16(gw[i % n_w], dx, T, epi, dout, dout, df, dws, wsf, k_splits, 0);
+    CK(cudaEventRecord(a, 0));
+    for (int i = 0; i < iters; ++i)
+        ds::gemm_bf16(gw[i % n_w], dx, T, epi, dout, dout, df, dws, wsf, k_splits, 0);
+    CK(cudaEventRecord(b, 0));
+    CK(cudaEventSynchronize(b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    *ms_out = ms / float(iters);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(dx);
+    cudaFree(dw);
+    cudaFree(dout);
+    cudaFree(df);
+    cudaFree(dws);
+    CK(cudaGetLastError());
+    return DS_OK;
+}
+
 ds_status ds_dbg_gemm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t N, int32_t K,
                       int32_t epi, const uint16_t* resid, int32_t k_splits, void* out) {
     int ndev = 0;
