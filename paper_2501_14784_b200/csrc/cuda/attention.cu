@@ -60,6 +60,8 @@ attn_tc_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __re
                const int32_t* __restrict__ row_page_off, const int32_t* __restrict__ flat_pages,
                const int32_t* __restrict__ blocks, KvLayout kv, int layer, int splits,
                __nv_bfloat16* __restrict__ o, float* __restrict__ ws) {
+    pdl_launch_dependents();
+    pdl_wait();
     extern __shared__ __align__(16) uint8_t attn_smem[];
     AttnSmem<DH>& sm = *reinterpret_cast<AttnSmem<DH>*>(attn_smem);
     constexpr int NT = DH / 8;   // output n-tiles
@@ -331,6 +333,8 @@ attn_tc_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __re
 template <int DH>
 __global__ void attn_combine_kernel(const float* __restrict__ ws, int splits,
                                     __nv_bfloat16* __restrict__ o) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int rh = blockIdx.x;
     const float* base = ws + size_t(rh) * splits * (DH + 2);
     float M = -INFINITY;
@@ -378,9 +382,11 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
         cudaFuncSetAttribute(attn_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         attr = true;
     }
-    attn_tc_kernel<DH><<<n_blocks * kv.n_kv * splits, kAttnWarps * 32, smem, stream>>>(
-        q, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, splits, o, ws);
-    if (splits > 1) attn_combine_kernel<DH><<<T * n_h, DH, 0, stream>>>(ws, splits, o);
+    launch_pdl(attn_tc_kernel<DH>, dim3(n_blocks * kv.n_kv * splits), dim3(kAttnWarps * 32), smem,
+               stream, q, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, splits, o, ws);
+    if (splits > 1)
+        launch_pdl(attn_combine_kernel<DH>, dim3(T * n_h), dim3(DH), 0, stream, (const float*)ws,
+                   splits, o);
 }
 
 int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,

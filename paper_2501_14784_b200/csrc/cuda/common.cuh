@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #define DS_DEVICE __device__ __forceinline__
 
 namespace ds {
@@ -180,6 +182,12 @@ DS_DEVICE void tmem_ld16(uint32_t taddr, uint32_t* r) {
 }
 DS_DEVICE void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// Programmatic dependent launch: every stage-forward kernel is launched with
+// programmaticStreamSerialization, lets its successor start its prologue early
+// (launch_dependents) and waits for its predecessor's results before reading them (wait).
+DS_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+DS_DEVICE void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 DS_DEVICE bool elect_one() {
     uint32_t pred = 0;
     asm volatile(
@@ -191,6 +199,23 @@ DS_DEVICE bool elect_one() {
         "}\n"
         : "=r"(pred));
     return pred != 0;
+}
+
+// Host: launch with the programmatic-stream-serialization attribute (PDL).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 }  // namespace ds

@@ -50,6 +50,8 @@ void fill_bf16(__nv_bfloat16* dst, int64_t n, float v, cudaStream_t stream) {
 // ---------------------------------------------------------- embedding ----
 __global__ void embed_kernel(const __nv_bfloat16* __restrict__ emb, const int32_t* __restrict__ tok,
                              int d, __nv_bfloat16* __restrict__ x) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int t = blockIdx.x;
     const uint4* src = reinterpret_cast<const uint4*>(emb + size_t(tok[t]) * d);
     uint4* dst = reinterpret_cast<uint4*>(x + size_t(t) * d);
@@ -57,7 +59,7 @@ __global__ void embed_kernel(const __nv_bfloat16* __restrict__ emb, const int32_
 }
 void embed_rows(const __nv_bfloat16* emb, const int32_t* tokens, int T, int d, __nv_bfloat16* x,
                 cudaStream_t stream) {
-    if (T > 0) embed_kernel<<<T, 128, 0, stream>>>(emb, tokens, d, x);
+    if (T > 0) launch_pdl(embed_kernel, dim3(T), dim3(128), 0, stream, emb, tokens, d, x);
 }
 
 // ------------------------------------------------------------ RMSNorm ----
@@ -66,6 +68,8 @@ template <int VPT>
 __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ rows,
                                int d, const __nv_bfloat16* __restrict__ g, float eps,
                                __nv_bfloat16* __restrict__ y) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int i = blockIdx.x;
     const int src_row = rows ? rows[i] : i;
     const uint4* xr = reinterpret_cast<const uint4*>(x + size_t(src_row) * d);
@@ -112,11 +116,11 @@ void rmsnorm_rows(const __nv_bfloat16* x, const int32_t* rows, int n_rows, int d
     if (n_rows <= 0) return;
     const int nv = d / 8;
     if (nv <= 128)
-        rmsnorm_kernel<1><<<n_rows, 128, 0, stream>>>(x, rows, d, g, eps, y);
+        launch_pdl(rmsnorm_kernel<1>, dim3(n_rows), dim3(128), 0, stream, x, rows, d, g, eps, y);
     else if (nv <= 512)
-        rmsnorm_kernel<4><<<n_rows, 128, 0, stream>>>(x, rows, d, g, eps, y);
+        launch_pdl(rmsnorm_kernel<4>, dim3(n_rows), dim3(128), 0, stream, x, rows, d, g, eps, y);
     else
-        rmsnorm_kernel<8><<<n_rows, 128, 0, stream>>>(x, rows, d, g, eps, y);
+        launch_pdl(rmsnorm_kernel<8>, dim3(n_rows), dim3(128), 0, stream, x, rows, d, g, eps, y);
 }
 
 // ------------------------------------------------- RoPE + KV append ----
@@ -125,6 +129,8 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int n_h, i
                                const int32_t* __restrict__ row_page, const float* __restrict__ rc,
                                const float* __restrict__ rs, KvLayout kv, int layer,
                                __nv_bfloat16* __restrict__ q_out) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int t = blockIdx.x;
     const int pos = row_pos[t];
     const int half = dh / 2;
@@ -177,13 +183,14 @@ void rope_kv_append(const __nv_bfloat16* qkv, int T, int n_h, int n_kv, int d_he
                     const float* rope_sin, const KvLayout& kv, int layer, __nv_bfloat16* q_out,
                     cudaStream_t stream) {
     if (T > 0)
-        rope_kv_kernel<<<T, 256, 0, stream>>>(qkv, n_h, n_kv, d_head, row_pos, row_page, rope_cos,
-                                              rope_sin, kv, layer, q_out);
+        launch_pdl(rope_kv_kernel, dim3(T), dim3(256), 0, stream, qkv, n_h, n_kv, d_head, row_pos, row_page, rope_cos, rope_sin, kv, layer, q_out);
 }
 
 // ----------------------------------------------------------- SiLU*mul ----
 __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, int T, int ffn,
                                 __nv_bfloat16* __restrict__ h) {
+    pdl_launch_dependents();
+    pdl_wait();
     const size_t total = size_t(T) * ffn / 8;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
          i += size_t(gridDim.x) * blockDim.x) {
@@ -208,11 +215,13 @@ void silu_mul(const __nv_bfloat16* gu, int T, int ffn, __nv_bfloat16* h, cudaStr
     const size_t total = size_t(T) * ffn / 8;
     int blocks = int((total + 255) / 256);
     if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
-    silu_mul_kernel<<<blocks, 256, 0, stream>>>(gu, T, ffn, h);
+    launch_pdl(silu_mul_kernel, dim3(blocks), dim3(256), 0, stream, gu, T, ffn, h);
 }
 
 // ------------------------------------------------------------- argmax ----
 __global__ void argmax_kernel(const float* __restrict__ logits, int V, int32_t* __restrict__ ids) {
+    pdl_launch_dependents();
+    pdl_wait();
     const float* row = logits + size_t(blockIdx.x) * V;
     float best = -INFINITY;
     int bi = 0x7fffffff;
@@ -250,28 +259,31 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int V, int32_t* 
     }
 }
 void argmax_rows(const float* logits, int R, int V, int32_t* ids, cudaStream_t stream) {
-    if (R > 0) argmax_kernel<<<R, 512, 0, stream>>>(logits, V, ids);
+    if (R > 0) launch_pdl(argmax_kernel, dim3(R), dim3(512), 0, stream, logits, V, ids);
 }
 
 __global__ void scatter_tokens_kernel(const int32_t* ids, const int32_t* req, int R, int32_t* last) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < R) last[req[i]] = ids[i];
 }
 void scatter_tokens(const int32_t* ids, const int32_t* req, int R, int32_t* last_token,
                     cudaStream_t stream) {
-    if (R > 0) scatter_tokens_kernel<<<(R + 255) / 256, 256, 0, stream>>>(ids, req, R, last_token);
+    if (R > 0) launch_pdl(scatter_tokens_kernel, dim3((R + 255) / 256), dim3(256), 0, stream, ids, req, R, last_token);
 }
 
 __global__ void resolve_tokens_kernel(const int32_t* prompt_tok, const int32_t* row_req,
                                       const int32_t* last, int T, int32_t* tokens) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < T) tokens[i] = prompt_tok[i] >= 0 ? prompt_tok[i] : last[row_req[i]];
 }
 void resolve_tokens(const int32_t* prompt_tok, const int32_t* row_req, const int32_t* last_token,
                     int T, int32_t* tokens, cudaStream_t stream) {
     if (T > 0)
-        resolve_tokens_kernel<<<(T + 255) / 256, 256, 0, stream>>>(prompt_tok, row_req, last_token,
-                                                                    T, tokens);
+        launch_pdl(resolve_tokens_kernel, dim3((T + 255) / 256), dim3(256), 0, stream, prompt_tok, row_req, last_token, T, tokens);
 }
 
 }  // namespace ds

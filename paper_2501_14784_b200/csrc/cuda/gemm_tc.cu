@@ -79,9 +79,26 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
     const int total_kb = p.K / kBK;
     const int units = p.t_blocks * p.m_tiles * p.k_splits;
 
+    pdl_launch_dependents();  // the next kernel may start its prologue on SMs we free
+
     if (warp == 0) {
         if (elect_one()) {
             const uint64_t pol_w = policy_evict_first();
+            // The weights do not depend on the previous kernel: issue the first `stages` weight
+            // tiles before waiting for it (programmatic dependent launch), the activations after.
+            int pre = 0;
+            for (int u = blockIdx.x; u < units && pre < p.stages; u += gridDim.x) {
+                const int ks = u % p.k_splits;
+                const int mt = (u / p.k_splits) % p.m_tiles;
+                const int kb0 = ks * total_kb / p.k_splits;
+                const int kb1 = (ks + 1) * total_kb / p.k_splits;
+                for (int kb = kb0; kb < kb1 && pre < p.stages; ++kb, ++pre) {
+                    uint8_t* sa = smem + pre * stage_bytes;
+                    mbar_arrive_expect_tx(&full_bar[pre], stage_bytes);
+                    tma_load_2d_hint(sa, &tmap_w, &full_bar[pre], kb * kBK, mt * kBM, pol_w);
+                }
+            }
+            pdl_wait();
             int it = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
                 const int ks = u % p.k_splits;
@@ -92,11 +109,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % p.stages;
                     const uint32_t round = it / p.stages;
-                    mbar_wait(&empty_bar[s], (round & 1) ^ 1);
                     uint8_t* sa = smem + s * stage_bytes;
                     uint8_t* sb = sa + a_bytes;
-                    mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
-                    tma_load_2d_hint(sa, &tmap_w, &full_bar[s], kb * kBK, mt * kBM, pol_w);
+                    if (it >= pre) {
+                        mbar_wait(&empty_bar[s], (round & 1) ^ 1);
+                        mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
+                        tma_load_2d_hint(sa, &tmap_w, &full_bar[s], kb * kBK, mt * kBM, pol_w);
+                    }
                     for (int j = 0; j < p.b_loads; ++j)
                         tma_load_2d(sb + j * p.bbox * kBK * 2, &tmap_x, &full_bar[s], kb * kBK,
                                     tbk * p.tb + j * p.bbox);
@@ -143,6 +162,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
             }
         }
     } else if (warp >= 4) {
+        pdl_wait();
         const int q = warp & 3;
         int uc = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
@@ -190,6 +210,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int T, int N, int epi,
                                      __nv_bfloat16* out_bf16, const __nv_bfloat16* resid,
                                      float* out_f32) {
+    pdl_launch_dependents();
+    pdl_wait();
     const size_t total = size_t(T) * N / 4;
     const size_t plane = size_t(T) * N;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
@@ -317,14 +339,14 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
     }
     const int units = p.t_blocks * p.m_tiles * p.k_splits;
     const int grid = units < kNumSMs ? units : kNumSMs;
-    gemm_tc_kernel<<<grid, kGemmThreads, smem, stream>>>(
-        *reinterpret_cast<const CUtensorMap*>(w.tmap), tx, p);
+    launch_pdl(gemm_tc_kernel, dim3(grid), dim3(kGemmThreads), smem, stream,
+               *reinterpret_cast<const CUtensorMap*>(w.tmap), tx, p);
     if (k_splits > 1) {
         const size_t total4 = size_t(T) * N / 4;
         int blocks = int((total4 + 255) / 256);
         if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
-        splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(workspace, k_splits, T, N, epi, out_bf16,
-                                                          resid, out_f32);
+        launch_pdl(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, stream, (const float*)workspace,
+                   k_splits, T, N, epi, out_bf16, resid, out_f32);
     }
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
 }
