@@ -2,16 +2,28 @@
 //
 //   out[t, n] = epilogue( sum_k X[t, k] * W[n, k] )        X: [T, K], W: [N, K], both K-major
 //
-// Orientation: the weight matrix is the UMMA "A" operand (M = 128 output features per tile)
-// and the stage's token rows are the "B" operand (N = up to 256 tokens per instruction, two
-// instructions side by side for up to 512 tokens). A decode/prefill stage step has T = rows of
-// the circuit (eff_batch, reference sim.cpp:406) which is small and ragged, so each CTA streams
-// a 128-row weight panel from HBM exactly once per token block while the activations (tiny,
-// L2-resident) are re-read. The fp32 accumulator lives in TMEM (lanes = features, columns =
-// tokens); the epilogue warps drain it with tcgen05.ld and apply the fused epilogue.
+// Orientation: the weight matrix is the UMMA "A" operand (M = 128 output features per CTA tile)
+// and the stage step's token rows are the "B" operand (N <= 256 tokens per instruction, two
+// instructions side by side for <= 512 tokens per token block). A stage step has T = eff_batch
+// rows (reference sim.cpp:406): small and ragged, so weights are streamed from HBM exactly once
+// per token block, the fp32 accumulator lives in TMEM (lanes = features, columns = tokens).
+//
+// * 2-CTA clusters: the two CTAs of a cluster own adjacent 128-feature tiles and the same token
+//   block; each loads half of the activation tile and multicasts it to both (TMA .multicast), so
+//   the per-SM activation traffic from L2 is halved. Each CTA's MMA releases a stage in both
+//   CTAs (tcgen05.commit .multicast::cluster).
+// * Stream-K: the (token block x cluster tile x k-block) iteration space is cut into equal
+//   contiguous ranges, one per cluster (no wave quantisation). A tile split across clusters is
+//   finished by whichever CTA arrives last (atomic counter): it sums every fp32 partial in
+//   segment order (deterministic) and applies the epilogue. No separate reduction kernel.
+// * TMEM holds two accumulators when the token block fits 256 columns, so a tile's epilogue
+//   overlaps the next tile's MMAs.
+// * Epilogue: tcgen05.ld -> shared-memory transpose -> 16-byte coalesced stores, fused
+//   bf16 / residual-add (x = bf16(x + bf16(acc))) / fp32 (logits).
+// * Programmatic dependent launch: the first weight tiles are fetched before waiting on the
+//   previous kernel; the activations after.
 //
 // Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w4..w7 epilogue.
-// Work units = (token block, 128-feature tile, K split); persistent CTAs loop over units.
 #include <cuda.h>
 
 #include "common.cuh"
@@ -19,124 +31,215 @@
 
 namespace ds {
 
-constexpr int kBM = 128;   // weight rows per tile (UMMA M)
-constexpr int kBK = 64;    // K elements per stage = one 128-byte swizzle row
-constexpr int kMaxTB = 512;  // tokens per block (TMEM columns)
+constexpr int kBM = 128;      // weight rows per CTA tile (UMMA M)
+constexpr int kBK = 64;       // K elements per stage = one 128-byte swizzle row
+constexpr int kMaxTB = 512;   // tokens per block (TMEM columns)
+constexpr int kCN = 2;        // CTAs per cluster
 constexpr int kGemmThreads = 256;
 constexpr int kSmemBudget = 200 * 1024;
+constexpr int kStageStride = 36;  // floats per row of the epilogue transpose buffer
+constexpr int kMaxCounters = 16384;
 
 struct GemmParams {
     int T, N, K;
-    int k_splits;
-    int t_blocks, m_tiles;
-    int tb;        // tokens per block (<= 512)
-    int bbox;      // TMA box rows for X (<= 256)
-    int b_loads;   // X boxes per stage
+    int m_tiles;  // N / 128
+    int t_blocks;
+    int tb;       // tokens per block (<= 512)
+    int tb_pad;   // tb rounded up to 16
+    int brows;    // activation rows each CTA of the cluster loads per stage (tb_pad / 2)
     int stages;
-    uint32_t tmem_cols;
+    int n_acc;    // TMEM accumulators
+    int KB;       // k-blocks per tile
+    int n_clusters;
+    long long total;  // cluster-tile k-block iterations
     int epi;
     __nv_bfloat16* out_bf16;
     const __nv_bfloat16* resid;
-    float* out_f32;  // EPI_F32 output or split-K workspace [k_splits][T][N]
+    float* out_f32;
+    float* partial;  // [n_clusters * 2 CTAs][2 slots][tb_pad cols][128 lanes]
+    int* counters;   // per CTA tile, zero between launches
 };
+
+DS_DEVICE uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+DS_DEVICE void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+DS_DEVICE void tma_load_2d_mc(void* smem_dst, const void* tmap, uint64_t* bar, int c0, int c1,
+                              uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+        : "memory");
+}
+DS_DEVICE void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+DS_DEVICE void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__host__ __device__ inline long long range_start(long long total, int n, int c) {
+    return total * c / n;
+}
+DS_DEVICE int cluster_of(long long total, int n, long long x) {
+    int c = int((x * n) / total);
+    while (c + 1 < n && range_start(total, n, c + 1) <= x) ++c;
+    while (c > 0 && range_start(total, n, c) > x) --c;
+    return c;
+}
+
+// Applies the epilogue to 16 consecutive token columns of one 32-feature slice held as vals[16]
+// (this thread's feature, columns c0..c0+15), through a per-warp transpose buffer.
+DS_DEVICE void epilogue16(const GemmParams& p, float* stage, const float* vals, int lane, int t0,
+                          int c0, int t_here, int f_base) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) stage[j * kStageStride + lane] = vals[j];
+    __syncwarp();
+    const int row = lane >> 1, half = lane & 1;
+    if (c0 + row < t_here) {
+        const int t = t0 + c0 + row;
+        const int f0 = f_base + half * 16;
+        const float4* src = reinterpret_cast<const float4*>(stage + row * kStageStride + half * 16);
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float4 x = src[i];
+            v[4 * i] = x.x;
+            v[4 * i + 1] = x.y;
+            v[4 * i + 2] = x.z;
+            v[4 * i + 3] = x.w;
+        }
+        const size_t o = size_t(t) * p.N + f0;
+        if (p.epi == EPI_F32) {
+            float4* dst = reinterpret_cast<float4*>(p.out_f32 + o);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        } else {
+            if (p.epi == EPI_RESID) {
+                float r[16];
+                unpack8(reinterpret_cast<const uint4*>(p.resid + o)[0], r);
+                unpack8(reinterpret_cast<const uint4*>(p.resid + o)[1], r + 8);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = r[j] + round_bf(v[j]);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(p.out_bf16 + o);
+            dst[0] = pack8(v);
+            dst[1] = pack8(v + 8);
+        }
+    }
+    __syncwarp();
+}
 
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
                const GemmParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // 1024-byte alignment for SWIZZLE_128B tiles.
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     const int a_bytes = kBM * kBK * 2;
-    const int b_bytes = p.b_loads * p.bbox * kBK * 2;
+    const int b_bytes = p.tb_pad * kBK * 2;
     const int stage_bytes = a_bytes + b_bytes;
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
+    float* ep_stage = reinterpret_cast<float*>(smem + p.stages * stage_bytes);  // 4 x 16 x 36 floats
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(ep_stage + 4 * 16 * kStageStride);
     uint64_t* empty_bar = full_bar + p.stages;
-    uint64_t* tfull_bar = empty_bar + p.stages;
-    uint64_t* tempty_bar = tfull_bar + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 1);
+    uint64_t* tfull_bar = empty_bar + p.stages;  // [2]
+    uint64_t* tempty_bar = tfull_bar + 2;        // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int cluster = blockIdx.x / kCN;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmap_w);
         tma_prefetch_desc(&tmap_x);
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], 1);
+            mbar_init(&empty_bar[s], kCN);
         }
-        mbar_init(tfull_bar, 1);
-        mbar_init(tempty_bar, 4);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull_bar[a], 1);
+            mbar_init(&tempty_bar[a], 4);
+        }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, p.tmem_cols);
+    if (warp == 2) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
+    cluster_sync();  // remote barriers initialised before any multicast lands
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_launch_dependents();
 
-    const int total_kb = p.K / kBK;
-    const int units = p.t_blocks * p.m_tiles * p.k_splits;
-
-    pdl_launch_dependents();  // the next kernel may start its prologue on SMs we free
+    const long long beg = range_start(p.total, p.n_clusters, cluster);
+    const long long end = range_start(p.total, p.n_clusters, cluster + 1);
+    const int cl_tiles = p.m_tiles / kCN;
 
     if (warp == 0) {
         if (elect_one()) {
             const uint64_t pol_w = policy_evict_first();
-            // The weights do not depend on the previous kernel: issue the first `stages` weight
-            // tiles before waiting for it (programmatic dependent launch), the activations after.
+            const uint16_t mask = (1u << kCN) - 1;
+            auto coords = [&](long long it, int& kb, int& mt, int& tbk) {
+                const long long ut = it / p.KB;
+                kb = int(it % p.KB);
+                tbk = int(ut / cl_tiles);
+                mt = int(ut % cl_tiles) * kCN + int(rank);
+            };
+            // weights first (independent of the previous kernel), activations after pdl_wait
             int pre = 0;
-            for (int u = blockIdx.x; u < units && pre < p.stages; u += gridDim.x) {
-                const int ks = u % p.k_splits;
-                const int mt = (u / p.k_splits) % p.m_tiles;
-                const int kb0 = ks * total_kb / p.k_splits;
-                const int kb1 = (ks + 1) * total_kb / p.k_splits;
-                for (int kb = kb0; kb < kb1 && pre < p.stages; ++kb, ++pre) {
-                    uint8_t* sa = smem + pre * stage_bytes;
-                    mbar_arrive_expect_tx(&full_bar[pre], stage_bytes);
-                    tma_load_2d_hint(sa, &tmap_w, &full_bar[pre], kb * kBK, mt * kBM, pol_w);
-                }
+            for (long long it = beg; it < end && pre < p.stages; ++it, ++pre) {
+                int kb, mt, tbk;
+                coords(it, kb, mt, tbk);
+                mbar_arrive_expect_tx(&full_bar[pre], stage_bytes);
+                tma_load_2d_hint(smem + pre * stage_bytes, &tmap_w, &full_bar[pre], kb * kBK, mt * kBM, pol_w);
             }
             pdl_wait();
-            int it = 0;
-            for (int u = blockIdx.x; u < units; u += gridDim.x) {
-                const int ks = u % p.k_splits;
-                const int mt = (u / p.k_splits) % p.m_tiles;
-                const int tbk = u / (p.k_splits * p.m_tiles);
-                const int kb0 = ks * total_kb / p.k_splits;
-                const int kb1 = (ks + 1) * total_kb / p.k_splits;
-                for (int kb = kb0; kb < kb1; ++kb, ++it) {
-                    const int s = it % p.stages;
-                    const uint32_t round = it / p.stages;
-                    uint8_t* sa = smem + s * stage_bytes;
-                    uint8_t* sb = sa + a_bytes;
-                    if (it >= pre) {
-                        mbar_wait(&empty_bar[s], (round & 1) ^ 1);
-                        mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
-                        tma_load_2d_hint(sa, &tmap_w, &full_bar[s], kb * kBK, mt * kBM, pol_w);
-                    }
-                    for (int j = 0; j < p.b_loads; ++j)
-                        tma_load_2d(sb + j * p.bbox * kBK * 2, &tmap_x, &full_bar[s], kb * kBK,
-                                    tbk * p.tb + j * p.bbox);
+            int i = 0;
+            for (long long it = beg; it < end; ++it, ++i) {
+                int kb, mt, tbk;
+                coords(it, kb, mt, tbk);
+                const int s = i % p.stages;
+                const uint32_t round = i / p.stages;
+                uint8_t* sa = smem + s * stage_bytes;
+                uint8_t* sb = sa + a_bytes;
+                if (i >= pre) {
+                    mbar_wait(&empty_bar[s], (round & 1) ^ 1);
+                    mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
+                    tma_load_2d_hint(sa, &tmap_w, &full_bar[s], kb * kBK, mt * kBM, pol_w);
                 }
+                tma_load_2d_mc(sb + rank * p.brows * kBK * 2, &tmap_x, &full_bar[s], kb * kBK,
+                               tbk * p.tb + int(rank) * p.brows, mask);
             }
+            // drain: every stage released by both CTAs (no remote arrival after we exit)
+            const int n = i;
+            for (int k = (n > p.stages ? n - p.stages : 0); k < n; ++k)
+                mbar_wait(&empty_bar[k % p.stages], (uint32_t(k / p.stages) & 1));
         }
     } else if (warp == 1) {
-        int it = 0;
-        int uc = 0;
-        for (int u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
-            const int ks = u % p.k_splits;
-            const int tbk = u / (p.k_splits * p.m_tiles);
-            const int kb0 = ks * total_kb / p.k_splits;
-            const int kb1 = (ks + 1) * total_kb / p.k_splits;
+        int i = 0, seg = 0;
+        long long it = beg;
+        while (it < end) {
+            const long long ut = it / p.KB;
+            const int kb0 = int(it % p.KB);
+            const int kb1 = int(end - it < (long long)(p.KB - kb0) ? kb0 + (end - it) : p.KB);
+            const int tbk = int(ut / cl_tiles);
             const int t_here = min(p.tb, p.T - tbk * p.tb);
-            mbar_wait(tempty_bar, (uc & 1) ^ 1);
+            const int a = seg % p.n_acc;
+            const uint32_t acc = tmem_base + uint32_t(a * 256);
+            mbar_wait(&tempty_bar[a], ((seg / p.n_acc) & 1) ^ 1);
             tc_fence_after();
-            for (int kb = kb0; kb < kb1; ++kb, ++it) {
-                const int s = it % p.stages;
-                const uint32_t round = it / p.stages;
-                mbar_wait(&full_bar[s], round & 1);
+            for (int kb = kb0; kb < kb1; ++kb, ++i) {
+                const int s = i % p.stages;
+                mbar_wait(&full_bar[s], (i / p.stages) & 1);
                 tc_fence_after();
                 if (elect_one()) {
                     const uint32_t sa = smem_u32(smem + s * stage_bytes);
@@ -145,105 +248,104 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                     for (int c = 0; c < 2; ++c) {
                         const int n_c = min(256, t_here - 256 * c);
                         if (n_c <= 0) break;
-                        const int n_pad = (n_c + 15) & ~15;
-                        const uint32_t idesc = umma_idesc_bf16(kBM, n_pad);
+                        const uint32_t idesc = umma_idesc_bf16(kBM, (n_c + 15) & ~15);
 #pragma unroll
-                        for (int k = 0; k < kBK / 16; ++k) {
-                            const uint64_t ad = umma_sdesc_sw128(sa + k * 32);
-                            const uint64_t bd = umma_sdesc_sw128(sb + c * 256 * 128 + k * 32);
-                            umma_bf16(tmem_base + c * 256, ad, bd, idesc,
+                        for (int k = 0; k < kBK / 16; ++k)
+                            umma_bf16(acc + c * 256, umma_sdesc_sw128(sa + k * 32),
+                                      umma_sdesc_sw128(sb + c * 256 * 128 + k * 32), idesc,
                                       (kb > kb0 || k > 0) ? 1u : 0u);
-                        }
                     }
-                    umma_commit(&empty_bar[s]);
-                    if (kb == kb1 - 1) umma_commit(tfull_bar);
+                    umma_commit_mc(&empty_bar[s], (1u << kCN) - 1);
+                    if (kb == kb1 - 1) umma_commit(&tfull_bar[a]);
                 }
                 __syncwarp();
             }
+            it += kb1 - kb0;
+            ++seg;
         }
     } else if (warp >= 4) {
         pdl_wait();
         const int q = warp & 3;
-        int uc = 0;
-        for (int u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
-            const int ks = u % p.k_splits;
-            const int mt = (u / p.k_splits) % p.m_tiles;
-            const int tbk = u / (p.k_splits * p.m_tiles);
+        const int tid = threadIdx.x - 128;  // 0..127, = TMEM lane
+        float* stage = ep_stage + q * 16 * kStageStride;
+        int seg = 0;
+        long long it = beg;
+        while (it < end) {
+            const long long ut = it / p.KB;
+            const int kb0 = int(it % p.KB);
+            const int kb1 = int(end - it < (long long)(p.KB - kb0) ? kb0 + (end - it) : p.KB);
+            const int tbk = int(ut / cl_tiles);
+            const int mt = int(ut % cl_tiles) * kCN + int(rank);
             const int t0 = tbk * p.tb;
             const int t_here = min(p.tb, p.T - t0);
-            const int n = mt * kBM + q * 32 + lane;
-            mbar_wait(tfull_bar, uc & 1);
+            const int a = seg % p.n_acc;
+            const uint32_t acc = tmem_base + uint32_t(a * 256) + (uint32_t(q * 32) << 16);
+            mbar_wait(&tfull_bar[a], (seg / p.n_acc) & 1);
             tc_fence_after();
-            for (int c0 = 0; c0 < t_here; c0 += 16) {
-                uint32_t r[16];
-                tmem_ld16(tmem_base + (uint32_t(q * 32) << 16) + c0, r);
-                tmem_ld_wait();
-                const int tmax = min(16, t_here - c0);
-                if (p.epi == EPI_BF16) {
-                    for (int j = 0; j < tmax; ++j)
-                        p.out_bf16[size_t(t0 + c0 + j) * p.N + n] = f2bf(__uint_as_float(r[j]));
-                } else if (p.epi == EPI_RESID) {
-                    for (int j = 0; j < tmax; ++j) {
-                        const size_t o = size_t(t0 + c0 + j) * p.N + n;
-                        const float y = bf2f(p.resid[o]) + round_bf(__uint_as_float(r[j]));
-                        p.out_bf16[o] = f2bf(y);
+            const bool full = kb0 == 0 && kb1 == p.KB;
+            if (full) {
+                for (int c0 = 0; c0 < t_here; c0 += 16) {
+                    uint32_t r[16];
+                    tmem_ld16(acc + c0, r);
+                    tmem_ld_wait();
+                    epilogue16(p, stage, reinterpret_cast<float*>(r), lane, t0, c0, t_here,
+                               mt * kBM + q * 32);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty_bar[a]);
+            } else {
+                // partial: park it (coalesced [col][lane]) and count the tile's segments in
+                const int slot = seg == 0 ? 0 : 1;
+                float* mine = p.partial + (size_t(cluster * kCN + rank) * 2 + slot) * size_t(p.tb_pad) * kBM;
+                for (int c0 = 0; c0 < t_here; c0 += 16) {
+                    uint32_t r[16];
+                    tmem_ld16(acc + c0, r);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (c0 + j < t_here) mine[size_t(c0 + j) * kBM + tid] = __uint_as_float(r[j]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty_bar[a]);  // accumulator free for the next tile
+                __threadfence();
+                named_bar(1, 128);
+                const long long t_lo = ut * p.KB, t_hi = (ut + 1) * p.KB - 1;
+                const int c_lo = cluster_of(p.total, p.n_clusters, t_lo);
+                const int c_hi = cluster_of(p.total, p.n_clusters, t_hi);
+                const int ctr = int(ut) * kCN + int(rank);
+                if (tid == 0) *last_flag = atomicAdd(&p.counters[ctr], 1) == c_hi - c_lo;
+                named_bar(1, 128);
+                if (*last_flag) {
+                    __threadfence();
+                    // sum every segment's partial in cluster order (deterministic), then epilogue
+                    for (int c0 = 0; c0 < t_here; c0 += 16) {
+                        float v[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+                        for (int c = c_lo; c <= c_hi; ++c) {
+                            const int sl = range_start(p.total, p.n_clusters, c) >= t_lo ? 0 : 1;
+                            const float* src = p.partial + (size_t(c * kCN + rank) * 2 + sl) *
+                                                               size_t(p.tb_pad) * kBM;
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                if (c0 + j < t_here) v[j] += __ldcg(src + size_t(c0 + j) * kBM + tid);
+                        }
+                        epilogue16(p, stage, v, lane, t0, c0, t_here, mt * kBM + q * 32);
                     }
-                } else {
-                    float* dst = p.out_f32 + (p.epi == EPI_PARTIAL ? size_t(ks) * p.T * p.N : 0);
-                    for (int j = 0; j < tmax; ++j)
-                        dst[size_t(t0 + c0 + j) * p.N + n] = __uint_as_float(r[j]);
+                    if (tid == 0) p.counters[ctr] = 0;  // ready for the next launch
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tempty_bar);
+            it += kb1 - kb0;
+            ++seg;
         }
     }
     __syncthreads();
+    cluster_sync();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, p.tmem_cols);
-    }
-}
-
-// Deterministic split-K reduction (splits summed in order) + the same epilogues.
-__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int T, int N, int epi,
-                                     __nv_bfloat16* out_bf16, const __nv_bfloat16* resid,
-                                     float* out_f32) {
-    pdl_launch_dependents();
-    pdl_wait();
-    const size_t total = size_t(T) * N / 4;
-    const size_t plane = size_t(T) * N;
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
-         i += size_t(gridDim.x) * blockDim.x) {
-        float4 acc = reinterpret_cast<const float4*>(ws)[i];
-        for (int s = 1; s < splits; ++s) {
-            const float4 v = reinterpret_cast<const float4*>(ws + s * plane)[i];
-            acc.x += v.x;
-            acc.y += v.y;
-            acc.z += v.z;
-            acc.w += v.w;
-        }
-        const size_t o = i * 4;
-        if (epi == EPI_F32) {
-            reinterpret_cast<float4*>(out_f32)[i] = acc;
-        } else {
-            float a[4] = {acc.x, acc.y, acc.z, acc.w};
-            if (epi == EPI_RESID) {
-                const uint2 rv = *reinterpret_cast<const uint2*>(resid + o);
-                const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
-                const float2 r0 = __bfloat1622float2(rh[0]);
-                const float2 r1 = __bfloat1622float2(rh[1]);
-                a[0] = r0.x + round_bf(a[0]);
-                a[1] = r0.y + round_bf(a[1]);
-                a[2] = r1.x + round_bf(a[2]);
-                a[3] = r1.y + round_bf(a[3]);
-            }
-            uint2 ov;
-            ov.x = pack2(a[0], a[1]);
-            ov.y = pack2(a[2], a[3]);
-            *reinterpret_cast<uint2*>(out_bf16 + o) = ov;
-        }
+        tmem_dealloc(tmem_base, 512);
     }
 }
 
@@ -258,9 +360,9 @@ static EncodeTiledFn get_encode_fn() {
     static EncodeTiledFn fn = nullptr;
     if (!fn) {
         cudaDriverEntryPointQueryResult q;
-        void* p = nullptr;
-        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
-        fn = reinterpret_cast<EncodeTiledFn>(p);
+        void* ptr = nullptr;
+        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q);
+        fn = reinterpret_cast<EncodeTiledFn>(ptr);
     }
     return fn;
 }
@@ -280,75 +382,66 @@ int make_tmap_2d_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t 
     return r == CUDA_SUCCESS ? 0 : -2;
 }
 
-size_t gemm_workspace_floats(int T, int N, int k_splits) { return size_t(k_splits) * T * N; }
-
-int gemm_pick_splits(int T, int N, int K) {
-    const int tiles = ((T + kMaxTB - 1) / kMaxTB) * (N / kBM);
-    const int kb = K / kBK;
-    if (tiles >= kNumSMs / 2) return 1;
-    int s = kNumSMs / tiles;
-    s = min(s, 8);
-    s = min(s, kb / 4);
-    return max(s, 1);
-}
+// partials for every CTA (2 slots of 128 x 512 fp32) + per-tile counters (zero-initialised)
+size_t gemm_workspace_floats() { return size_t(kNumSMs) * 2 * kBM * kMaxTB + kMaxCounters; }
 
 int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_bfloat16* out_bf16,
               const __nv_bfloat16* resid, float* out_f32, float* workspace, size_t workspace_floats,
-              int k_splits, cudaStream_t stream) {
+              int max_clusters, cudaStream_t stream) {
     const int N = w.N, K = w.K;
     if (T <= 0) return 0;
-    if (K % kBK != 0 || N % kBM != 0) return -3;
+    if (K % kBK != 0 || N % (kBM * kCN) != 0) return -3;
+    if (!workspace || workspace_floats < gemm_workspace_floats()) return -7;
     GemmParams p{};
     p.T = T;
     p.N = N;
     p.K = K;
-    p.t_blocks = (T + kMaxTB - 1) / kMaxTB;
-    p.tb = T < kMaxTB ? T : kMaxTB;
-    const int tb_pad = (p.tb + 15) & ~15;
-    p.bbox = tb_pad < 256 ? tb_pad : 256;
-    p.b_loads = (tb_pad + p.bbox - 1) / p.bbox;
     p.m_tiles = N / kBM;
-    if (k_splits <= 0) k_splits = gemm_pick_splits(T, N, K);
-    if (k_splits > 1 && (size_t(k_splits) * T * N > workspace_floats || workspace == nullptr))
-        k_splits = 1;
-    p.k_splits = k_splits;
-    const int stage_bytes = kBM * kBK * 2 + p.b_loads * p.bbox * kBK * 2;
-    p.stages = (kSmemBudget - 2048) / stage_bytes;
+    p.t_blocks = (T + kMaxTB - 1) / kMaxTB;
+    if (p.t_blocks * p.m_tiles > kMaxCounters) return -8;
+    p.tb = T < kMaxTB ? T : kMaxTB;
+    p.tb_pad = (p.tb + 15) & ~15;
+    p.brows = p.tb_pad / kCN;
+    p.KB = K / kBK;
+    const int stage_bytes = kBM * kBK * 2 + p.tb_pad * kBK * 2;
+    const int fixed = 4 * 16 * kStageStride * 4 + 256 + 1024;
+    p.stages = (kSmemBudget - fixed) / stage_bytes;
     if (p.stages > 8) p.stages = 8;
     if (p.stages < 2) return -4;
-    uint32_t cols = 32;
-    while (cols < uint32_t(tb_pad > 256 ? 512 : tb_pad)) cols <<= 1;
-    p.tmem_cols = cols;
-    if (k_splits > 1) {
-        p.epi = EPI_PARTIAL;
-        p.out_f32 = workspace;
-    } else {
-        p.epi = epi;
-        p.out_bf16 = out_bf16;
-        p.resid = resid;
-        p.out_f32 = out_f32;
-    }
+    p.n_acc = p.tb_pad <= 256 ? 2 : 1;
+    p.total = (long long)p.t_blocks * (p.m_tiles / kCN) * p.KB;
+    int nc = kNumSMs / kCN;
+    // keep at least ~4 k-blocks per cluster so tiny GEMMs do not shred into partials
+    const long long min_work = 4;
+    if (p.total / min_work < nc) nc = int(p.total / min_work > 0 ? p.total / min_work : 1);
+    if (max_clusters > 0 && nc > max_clusters) nc = max_clusters;
+    p.n_clusters = nc;
+    p.epi = epi;
+    p.out_bf16 = out_bf16;
+    p.resid = resid;
+    p.out_f32 = out_f32;
+    p.partial = workspace;
+    p.counters = reinterpret_cast<int*>(workspace + size_t(kNumSMs) * 2 * kBM * kMaxTB);
     alignas(64) CUtensorMap tx;
-    if (make_tmap_2d_bf16(&tx, x, T, K, p.bbox, kBK) != 0) return -5;
-    const size_t smem = size_t(p.stages) * stage_bytes + 1024 + 256;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kSmemBudget + 2048);
-        attr_set = true;
-    }
-    const int units = p.t_blocks * p.m_tiles * p.k_splits;
-    const int grid = units < kNumSMs ? units : kNumSMs;
-    launch_pdl(gemm_tc_kernel, dim3(grid), dim3(kGemmThreads), smem, stream,
-               *reinterpret_cast<const CUtensorMap*>(w.tmap), tx, p);
-    if (k_splits > 1) {
-        const size_t total4 = size_t(T) * N / 4;
-        int blocks = int((total4 + 255) / 256);
-        if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
-        launch_pdl(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, stream, (const float*)workspace,
-                   k_splits, T, N, epi, out_bf16, resid, out_f32);
-    }
-    return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
+    if (make_tmap_2d_bf16(&tx, x, T, K, p.brows, kBK) != 0) return -5;
+    const size_t smem = size_t(p.stages) * stage_bytes + fixed;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(nc * kCN);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kCN;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel,
+                                       *reinterpret_cast<const CUtensorMap*>(w.tmap), tx, p);
+    return e == cudaSuccess ? 0 : -6;
 }
 
 int gemm_weight_init(GemmWeight* w, const __nv_bfloat16* data, int N, int K) {
@@ -358,15 +451,12 @@ int gemm_weight_init(GemmWeight* w, const __nv_bfloat16* data, int N, int K) {
     return make_tmap_2d_bf16(w->tmap, data, N, K, kBM, kBK);
 }
 
-}  // namespace ds
-
-namespace ds {
-// Forces the module holding these kernels to load now (lazy loading would otherwise load it at
-// the first launch, which can wait on in-flight work such as a spinning NCCL receive).
+// Forces the module holding the kernel to load now (lazy loading would otherwise load it at the
+// first launch, which can wait on in-flight work such as a spinning NCCL receive).
 void preload_gemm() {
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, gemm_tc_kernel);
-    cudaFuncGetAttributes(&a, splitk_reduce_kernel);
     cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
 }
+
 }  // namespace ds

@@ -23,9 +23,10 @@ struct GemmWeight {
 };
 
 int gemm_weight_init(GemmWeight* w, const __nv_bfloat16* data, int N, int K);
-int gemm_pick_splits(int T, int N, int K);
-size_t gemm_workspace_floats(int T, int N, int k_splits);
-// out[T, N] = epi(X[T, K] . W[N, K]^T). k_splits <= 0 picks automatically.
+// Stream-K partials + per-tile counters; allocate once, zero-initialised, one per stream.
+size_t gemm_workspace_floats();
+// out[T, N] = epi(X[T, K] . W[N, K]^T). max_clusters > 0 caps the 2-CTA clusters (tests use it
+// to force tiles split across clusters); 0 = all SMs.
 int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_bfloat16* out_bf16,
               const __nv_bfloat16* resid, float* out_f32, float* workspace, size_t workspace_floats,
               int k_splits, cudaStream_t stream);

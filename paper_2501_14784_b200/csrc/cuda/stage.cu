@@ -287,15 +287,9 @@ ds_status ds_stage_create(int32_t device, const ds_model_desc* md, int64_t layer
     }
     if (s->last && (st = A((void**)&s->logits, R * size_t(m.vocab) * 4))) { delete s; return st; }
     {
-        size_t wsf = 0;
-        const int shapes[4][2] = {{qkv_rows, d}, {d, qdim}, {2 * m.ffn, d}, {d, m.ffn}};
-        for (int T = 1; T <= max_rows; T = (T < 64 ? T + 1 : T + 16))
-            for (auto& sh : shapes) {
-                const int ks = ds::gemm_pick_splits(T, sh[0], sh[1]);
-                if (ks > 1) wsf = std::max(wsf, ds::gemm_workspace_floats(T, sh[0], ks));
-            }
-        s->ws_floats = wsf;
-        if (wsf && (st = A((void**)&s->ws, wsf * 4))) { delete s; return st; }
+        s->ws_floats = ds::gemm_workspace_floats();
+        if ((st = A((void**)&s->ws, s->ws_floats * 4))) { delete s; return st; }
+        CK(cudaMemset(s->ws, 0, s->ws_floats * 4));
         s->attn_ws_floats = (R + 320) * m.n_heads * size_t(m.d_head + 2);
         if ((st = A((void**)&s->attn_ws, s->attn_ws_floats * 4))) { delete s; return st; }
     }
@@ -684,7 +678,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     size_t mark = 0;
     auto begin = [&]() { if (s->prof) mark = prof_mark(s); };
     auto end_gemm = [&](int kind, int rows_, int N, int K, int out_bytes) {
-        s->launches += ds::gemm_pick_splits(rows_, N, K) > 1 ? 2 : 1;
+        s->launches += 1;
         if (!s->prof) return;
         const size_t e1 = prof_mark(s);
         s->recs.push_back({kind, rows_, 2.0 * rows_ * N * K,
@@ -884,8 +878,9 @@ ds_status ds_dbg_gemm_bench(int32_t T, int32_t N, int32_t K, int32_t epi, int32_
     CK(cudaMalloc(&dw, wbytes * n_w));
     CK(cudaMalloc(&dout, size_t(T) * N * 2));
     CK(cudaMalloc(&df, size_t(T) * N * 4));
-    const size_t wsf = size_t(8) * T * N;
+    const size_t wsf = ds::gemm_workspace_floats();
     CK(cudaMalloc(&dws, wsf * 4));
+    CK(cudaMemset(dws, 0, wsf * 4));
     ds::init_weights(dx, 1, 1, T, K, 1.0f, -1, 0);
     ds::init_weights(dw, 1, 2, int64_t(N) * n_w, K, 0.02f, -1, 0);
     CK(cudaMemset(dout, 0, size_t(T) * N * 2));
@@ -929,8 +924,9 @@ ds_status ds_dbg_gemm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t N
     CK(cudaMalloc(&dw, size_t(N) * K * 2));
     CK(cudaMalloc(&dout, out_elems * 2));
     CK(cudaMalloc(&df, out_elems * 4));
-    const size_t wsf = size_t(8) * T * N;
+    const size_t wsf = ds::gemm_workspace_floats();
     CK(cudaMalloc(&dws, wsf * 4));
+    CK(cudaMemset(dws, 0, wsf * 4));
     CK(cudaMemcpy(dx, x, size_t(T) * K * 2, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dw, w, size_t(N) * K * 2, cudaMemcpyHostToDevice));
     if (resid) CK(cudaMemcpy(dout, resid, out_elems * 2, cudaMemcpyHostToDevice));
