@@ -12,10 +12,11 @@
 //   block; each loads half of the activation tile and multicasts it to both (TMA .multicast), so
 //   the per-SM activation traffic from L2 is halved. Each CTA's MMA releases a stage in both
 //   CTAs (tcgen05.commit .multicast::cluster).
-// * Stream-K: the (token block x cluster tile x k-block) iteration space is cut into equal
-//   contiguous ranges, one per cluster (no wave quantisation). A tile split across clusters is
-//   finished by whichever CTA arrives last (atomic counter): it sums every fp32 partial in
-//   segment order (deterministic) and applies the epilogue. No separate reduction kernel.
+// * Data-parallel + stream-K: whole waves of cluster tiles go to clusters round-robin; the
+//   remaining tiles' (tile x k-block) iterations are cut into equal contiguous ranges, one per
+//   cluster (no wave quantisation). A tile split across clusters is finished by whichever CTA
+//   arrives last (atomic counter): it sums every fp32 partial in segment order (deterministic)
+//   and applies the epilogue. No separate reduction kernel.
 // * TMEM holds two accumulators when the token block fits 256 columns, so a tile's epilogue
 //   overlaps the next tile's MMAs.
 // * Epilogue: tcgen05.ld -> shared-memory transpose -> 16-byte coalesced stores, fused
@@ -51,12 +52,13 @@ struct GemmParams {
     int n_acc;    // TMEM accumulators
     int KB;       // k-blocks per tile
     int n_clusters;
-    long long total;  // cluster-tile k-block iterations
+    long long dp_tiles;  // cluster tiles handled whole, round-robin
+    long long sk_total;  // stream-K iterations (tiles after dp_tiles, x KB)
     int epi;
     __nv_bfloat16* out_bf16;
     const __nv_bfloat16* resid;
     float* out_f32;
-    float* partial;  // [n_clusters * 2 CTAs][2 slots][tb_pad cols][128 lanes]
+    float* partial;  // [n_clusters * 2 CTAs][2 slots][tb_pad/4][128 lanes][4]
     int* counters;   // per CTA tile, zero between launches
 };
 
@@ -94,6 +96,42 @@ DS_DEVICE int cluster_of(long long total, int n, long long x) {
     while (c > 0 && range_start(total, n, c) > x) --c;
     return c;
 }
+
+// A cluster's work in order: its data-parallel tiles, then its stream-K range.
+struct Seg {
+    long long ut;
+    int kb0, kb1;
+    bool sk;
+};
+struct SegIter {
+    long long dp_next, dp_end, it, end, sk_base;
+    int nc, KB;
+    DS_DEVICE SegIter(const GemmParams& p, int c) {
+        nc = p.n_clusters;
+        KB = p.KB;
+        dp_next = c;
+        dp_end = p.dp_tiles;
+        sk_base = p.dp_tiles * p.KB;
+        it = sk_base + range_start(p.sk_total, nc, c);
+        end = sk_base + range_start(p.sk_total, nc, c + 1);
+    }
+    DS_DEVICE bool next(Seg& s) {
+        if (dp_next < dp_end) {
+            s = {dp_next, 0, KB, false};
+            dp_next += nc;
+            return true;
+        }
+        if (it < end) {
+            s.ut = it / KB;
+            s.kb0 = int(it - s.ut * KB);
+            s.kb1 = int(end - it < (long long)(KB - s.kb0) ? s.kb0 + (end - it) : KB);
+            s.sk = true;
+            it += s.kb1 - s.kb0;
+            return true;
+        }
+        return false;
+    }
+};
 
 // Applies the epilogue to 16 consecutive token columns of one 32-feature slice held as vals[16]
 // (this thread's feature, columns c0..c0+15), through a per-warp transpose buffer.
@@ -180,44 +218,46 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
     const uint32_t tmem_base = *tmem_slot;
     pdl_launch_dependents();
 
-    const long long beg = range_start(p.total, p.n_clusters, cluster);
-    const long long end = range_start(p.total, p.n_clusters, cluster + 1);
     const int cl_tiles = p.m_tiles / kCN;
 
     if (warp == 0) {
         if (elect_one()) {
             const uint64_t pol_w = policy_evict_first();
             const uint16_t mask = (1u << kCN) - 1;
-            auto coords = [&](long long it, int& kb, int& mt, int& tbk) {
-                const long long ut = it / p.KB;
-                kb = int(it % p.KB);
-                tbk = int(ut / cl_tiles);
-                mt = int(ut % cl_tiles) * kCN + int(rank);
-            };
             // weights first (independent of the previous kernel), activations after pdl_wait
             int pre = 0;
-            for (long long it = beg; it < end && pre < p.stages; ++it, ++pre) {
-                int kb, mt, tbk;
-                coords(it, kb, mt, tbk);
-                mbar_arrive_expect_tx(&full_bar[pre], stage_bytes);
-                tma_load_2d_hint(smem + pre * stage_bytes, &tmap_w, &full_bar[pre], kb * kBK, mt * kBM, pol_w);
+            {
+                SegIter si(p, cluster);
+                Seg sg;
+                while (pre < p.stages && si.next(sg)) {
+                    const int mt = int(sg.ut % cl_tiles) * kCN + int(rank);
+                    for (int kb = sg.kb0; kb < sg.kb1 && pre < p.stages; ++kb, ++pre) {
+                        mbar_arrive_expect_tx(&full_bar[pre], stage_bytes);
+                        tma_load_2d_hint(smem + pre * stage_bytes, &tmap_w, &full_bar[pre], kb * kBK,
+                                         mt * kBM, pol_w);
+                    }
+                }
             }
             pdl_wait();
             int i = 0;
-            for (long long it = beg; it < end; ++it, ++i) {
-                int kb, mt, tbk;
-                coords(it, kb, mt, tbk);
-                const int s = i % p.stages;
-                const uint32_t round = i / p.stages;
-                uint8_t* sa = smem + s * stage_bytes;
-                uint8_t* sb = sa + a_bytes;
-                if (i >= pre) {
-                    mbar_wait(&empty_bar[s], (round & 1) ^ 1);
-                    mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
-                    tma_load_2d_hint(sa, &tmap_w, &full_bar[s], kb * kBK, mt * kBM, pol_w);
+            SegIter si(p, cluster);
+            Seg sg;
+            while (si.next(sg)) {
+                const int tbk = int(sg.ut / cl_tiles);
+                const int mt = int(sg.ut % cl_tiles) * kCN + int(rank);
+                for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++i) {
+                    const int s = i % p.stages;
+                    const uint32_t round = i / p.stages;
+                    uint8_t* sa = smem + s * stage_bytes;
+                    uint8_t* sb = sa + a_bytes;
+                    if (i >= pre) {
+                        mbar_wait(&empty_bar[s], (round & 1) ^ 1);
+                        mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
+                        tma_load_2d_hint(sa, &tmap_w, &full_bar[s], kb * kBK, mt * kBM, pol_w);
+                    }
+                    tma_load_2d_mc(sb + rank * p.brows * kBK * 2, &tmap_x, &full_bar[s], kb * kBK,
+                                   tbk * p.tb + int(rank) * p.brows, mask);
                 }
-                tma_load_2d_mc(sb + rank * p.brows * kBK * 2, &tmap_x, &full_bar[s], kb * kBK,
-                               tbk * p.tb + int(rank) * p.brows, mask);
             }
             // drain: every stage released by both CTAs (no remote arrival after we exit)
             const int n = i;
@@ -226,18 +266,16 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         }
     } else if (warp == 1) {
         int i = 0, seg = 0;
-        long long it = beg;
-        while (it < end) {
-            const long long ut = it / p.KB;
-            const int kb0 = int(it % p.KB);
-            const int kb1 = int(end - it < (long long)(p.KB - kb0) ? kb0 + (end - it) : p.KB);
-            const int tbk = int(ut / cl_tiles);
+        SegIter si(p, cluster);
+        Seg sg;
+        while (si.next(sg)) {
+            const int tbk = int(sg.ut / cl_tiles);
             const int t_here = min(p.tb, p.T - tbk * p.tb);
             const int a = seg % p.n_acc;
             const uint32_t acc = tmem_base + uint32_t(a * 256);
             mbar_wait(&tempty_bar[a], ((seg / p.n_acc) & 1) ^ 1);
             tc_fence_after();
-            for (int kb = kb0; kb < kb1; ++kb, ++i) {
+            for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++i) {
                 const int s = i % p.stages;
                 mbar_wait(&full_bar[s], (i / p.stages) & 1);
                 tc_fence_after();
@@ -253,14 +291,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                         for (int k = 0; k < kBK / 16; ++k)
                             umma_bf16(acc + c * 256, umma_sdesc_sw128(sa + k * 32),
                                       umma_sdesc_sw128(sb + c * 256 * 128 + k * 32), idesc,
-                                      (kb > kb0 || k > 0) ? 1u : 0u);
+                                      (kb > sg.kb0 || k > 0) ? 1u : 0u);
                     }
                     umma_commit_mc(&empty_bar[s], (1u << kCN) - 1);
-                    if (kb == kb1 - 1) umma_commit(&tfull_bar[a]);
+                    if (kb == sg.kb1 - 1) umma_commit(&tfull_bar[a]);
                 }
                 __syncwarp();
             }
-            it += kb1 - kb0;
             ++seg;
         }
     } else if (warp >= 4) {
@@ -268,22 +305,21 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         const int q = warp & 3;
         const int tid = threadIdx.x - 128;  // 0..127, = TMEM lane
         float* stage = ep_stage + q * 16 * kStageStride;
+        const size_t slot_floats = size_t(p.tb_pad) * kBM;
         int seg = 0;
-        long long it = beg;
-        while (it < end) {
-            const long long ut = it / p.KB;
-            const int kb0 = int(it % p.KB);
-            const int kb1 = int(end - it < (long long)(p.KB - kb0) ? kb0 + (end - it) : p.KB);
-            const int tbk = int(ut / cl_tiles);
-            const int mt = int(ut % cl_tiles) * kCN + int(rank);
+        bool first_sk = true;
+        SegIter si(p, cluster);
+        Seg sg;
+        while (si.next(sg)) {
+            const int tbk = int(sg.ut / cl_tiles);
+            const int mt = int(sg.ut % cl_tiles) * kCN + int(rank);
             const int t0 = tbk * p.tb;
             const int t_here = min(p.tb, p.T - t0);
             const int a = seg % p.n_acc;
             const uint32_t acc = tmem_base + uint32_t(a * 256) + (uint32_t(q * 32) << 16);
             mbar_wait(&tfull_bar[a], (seg / p.n_acc) & 1);
             tc_fence_after();
-            const bool full = kb0 == 0 && kb1 == p.KB;
-            if (full) {
+            if (sg.kb0 == 0 && sg.kb1 == p.KB) {
                 for (int c0 = 0; c0 < t_here; c0 += 16) {
                     uint32_t r[16];
                     tmem_ld16(acc + c0, r);
@@ -295,26 +331,30 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty_bar[a]);
             } else {
-                // partial: park it (coalesced [col][lane]) and count the tile's segments in
-                const int slot = seg == 0 ? 0 : 1;
-                float* mine = p.partial + (size_t(cluster * kCN + rank) * 2 + slot) * size_t(p.tb_pad) * kBM;
+                // park the partial as [col/4][lane][4] (16-byte stores, 512 B per warp)
+                const int slot = first_sk ? 0 : 1;
+                float4* mine = reinterpret_cast<float4*>(
+                    p.partial + (size_t(cluster * kCN + rank) * 2 + slot) * slot_floats);
                 for (int c0 = 0; c0 < t_here; c0 += 16) {
                     uint32_t r[16];
                     tmem_ld16(acc + c0, r);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        if (c0 + j < t_here) mine[size_t(c0 + j) * kBM + tid] = __uint_as_float(r[j]);
+                    for (int jj = 0; jj < 4; ++jj)
+                        mine[size_t(c0 / 4 + jj) * kBM + tid] =
+                            make_float4(__uint_as_float(r[4 * jj]), __uint_as_float(r[4 * jj + 1]),
+                                        __uint_as_float(r[4 * jj + 2]), __uint_as_float(r[4 * jj + 3]));
                 }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty_bar[a]);  // accumulator free for the next tile
                 __threadfence();
                 named_bar(1, 128);
-                const long long t_lo = ut * p.KB, t_hi = (ut + 1) * p.KB - 1;
-                const int c_lo = cluster_of(p.total, p.n_clusters, t_lo);
-                const int c_hi = cluster_of(p.total, p.n_clusters, t_hi);
-                const int ctr = int(ut) * kCN + int(rank);
+                const long long x_lo = sg.ut * p.KB - p.dp_tiles * p.KB;
+                const long long x_hi = x_lo + p.KB - 1;
+                const int c_lo = cluster_of(p.sk_total, p.n_clusters, x_lo);
+                const int c_hi = cluster_of(p.sk_total, p.n_clusters, x_hi);
+                const int ctr = int(sg.ut) * kCN + int(rank);
                 if (tid == 0) *last_flag = atomicAdd(&p.counters[ctr], 1) == c_hi - c_lo;
                 named_bar(1, 128);
                 if (*last_flag) {
@@ -324,20 +364,37 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                         float v[16];
 #pragma unroll
                         for (int j = 0; j < 16; ++j) v[j] = 0.f;
-                        for (int c = c_lo; c <= c_hi; ++c) {
-                            const int sl = range_start(p.total, p.n_clusters, c) >= t_lo ? 0 : 1;
-                            const float* src = p.partial + (size_t(c * kCN + rank) * 2 + sl) *
-                                                               size_t(p.tb_pad) * kBM;
+                        for (int cb = c_lo; cb <= c_hi; cb += 4) {
+                            float4 buf[4][4];
 #pragma unroll
-                            for (int j = 0; j < 16; ++j)
-                                if (c0 + j < t_here) v[j] += __ldcg(src + size_t(c0 + j) * kBM + tid);
+                            for (int u = 0; u < 4; ++u) {
+                                const int c = cb + u;
+                                if (c > c_hi) break;
+                                const int sl = range_start(p.sk_total, p.n_clusters, c) >= x_lo ? 0 : 1;
+                                const float4* src = reinterpret_cast<const float4*>(
+                                    p.partial + (size_t(c * kCN + rank) * 2 + sl) * slot_floats);
+#pragma unroll
+                                for (int jj = 0; jj < 4; ++jj)
+                                    buf[u][jj] = __ldcg(src + size_t(c0 / 4 + jj) * kBM + tid);
+                            }
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                if (cb + u > c_hi) break;
+#pragma unroll
+                                for (int jj = 0; jj < 4; ++jj) {
+                                    v[4 * jj] += buf[u][jj].x;
+                                    v[4 * jj + 1] += buf[u][jj].y;
+                                    v[4 * jj + 2] += buf[u][jj].z;
+                                    v[4 * jj + 3] += buf[u][jj].w;
+                                }
+                            }
                         }
                         epilogue16(p, stage, v, lane, t0, c0, t_here, mt * kBM + q * 32);
                     }
                     if (tid == 0) p.counters[ctr] = 0;  // ready for the next launch
                 }
             }
-            it += kb1 - kb0;
+            if (sg.sk) first_sk = false;
             ++seg;
         }
     }
@@ -409,13 +466,22 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
     if (p.stages > 8) p.stages = 8;
     if (p.stages < 2) return -4;
     p.n_acc = p.tb_pad <= 256 ? 2 : 1;
-    p.total = (long long)p.t_blocks * (p.m_tiles / kCN) * p.KB;
+    const long long tiles = (long long)p.t_blocks * (p.m_tiles / kCN);
     int nc = kNumSMs / kCN;
-    // keep at least ~4 k-blocks per cluster so tiny GEMMs do not shred into partials
-    const long long min_work = 4;
-    if (p.total / min_work < nc) nc = int(p.total / min_work > 0 ? p.total / min_work : 1);
     if (max_clusters > 0 && nc > max_clusters) nc = max_clusters;
+    // whole waves data-parallel; the remainder stream-K with >= 8 k-blocks per cluster
+    long long dp = tiles >= nc ? (tiles / nc) * nc : 0;
+    if (dp == tiles) {
+        // exact waves: nothing to split
+    } else if ((tiles - dp) * p.KB < 8LL * nc && dp >= nc) {
+        dp -= nc;  // tiny remainder: fold the last full wave into the stream-K part
+    }
+    long long sk = (tiles - dp) * p.KB;
+    if (dp == 0 && sk > 0 && sk / 4 < nc) nc = int(sk / 4 > 0 ? sk / 4 : 1);  // tiny GEMM: fewer clusters
+    if (dp > 0 && nc > tiles) nc = int(tiles);
     p.n_clusters = nc;
+    p.dp_tiles = dp;
+    p.sk_total = sk;
     p.epi = epi;
     p.out_bf16 = out_bf16;
     p.resid = resid;
