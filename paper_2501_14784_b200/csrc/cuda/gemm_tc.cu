@@ -14,9 +14,10 @@
 //   CTAs (tcgen05.commit .multicast::cluster).
 // * Data-parallel + stream-K: whole waves of cluster tiles go to clusters round-robin; the
 //   remaining tiles' (tile x k-block) iterations are cut into equal contiguous ranges, one per
-//   cluster (no wave quantisation). A tile split across clusters is finished by whichever CTA
-//   arrives last (atomic counter): it sums every fp32 partial in segment order (deterministic)
-//   and applies the epilogue. No separate reduction kernel.
+//   cluster (no wave quantisation). A tile split across clusters parks fp32 partials; after
+//   their main loops its contributors wait for the tile's counter, then each reduces its share
+//   of the tile's columns (partials summed in cluster order: deterministic) and applies the
+//   epilogue. No separate reduction kernel.
 // * TMEM holds two accumulators when the token block fits 256 columns, so a tile's epilogue
 //   overlaps the next tile's MMAs.
 // * Epilogue: tcgen05.ld -> shared-memory transpose -> 16-byte coalesced stores, fused
@@ -308,6 +309,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         const size_t slot_floats = size_t(p.tb_pad) * kBM;
         int seg = 0;
         bool first_sk = true;
+        long long pending[2];  // split tiles this CTA parked a partial for (<= 2 per range)
+        int n_pending = 0;
         SegIter si(p, cluster);
         Seg sg;
         while (si.next(sg)) {
@@ -350,17 +353,40 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                 if (lane == 0) mbar_arrive(&tempty_bar[a]);  // accumulator free for the next tile
                 __threadfence();
                 named_bar(1, 128);
-                const long long x_lo = sg.ut * p.KB - p.dp_tiles * p.KB;
-                const long long x_hi = x_lo + p.KB - 1;
-                const int c_lo = cluster_of(p.sk_total, p.n_clusters, x_lo);
-                const int c_hi = cluster_of(p.sk_total, p.n_clusters, x_hi);
-                const int ctr = int(sg.ut) * kCN + int(rank);
-                if (tid == 0) *last_flag = atomicAdd(&p.counters[ctr], 1) == c_hi - c_lo;
-                named_bar(1, 128);
-                if (*last_flag) {
-                    __threadfence();
-                    // sum every segment's partial in cluster order (deterministic), then epilogue
-                    for (int c0 = 0; c0 < t_here; c0 += 16) {
+                if (tid == 0) atomicAdd(&p.counters[int(sg.ut) * kCN + int(rank)], 1);
+                pending[n_pending++] = sg.ut;  // reduced after the main loop, in parallel
+            }
+            if (sg.sk) first_sk = false;
+            ++seg;
+        }
+        // Deferred, parallel fixup: every contributor of a split tile waits until all partials
+        // are parked, then reduces its share of the tile's 16-column chunks (partials summed in
+        // cluster order: deterministic) and applies the epilogue. Waiting only at the end keeps
+        // the stream-K ranges from serialising on each other.
+        for (int pi = 0; pi < n_pending; ++pi) {
+            const long long ut = pending[pi];
+            const int tbk = int(ut / cl_tiles);
+            const int mt = int(ut % cl_tiles) * kCN + int(rank);
+            const int t0 = tbk * p.tb;
+            const int t_here = min(p.tb, p.T - t0);
+            const long long x_lo = ut * p.KB - p.dp_tiles * p.KB;
+            const long long x_hi = x_lo + p.KB - 1;
+            const int c_lo = cluster_of(p.sk_total, p.n_clusters, x_lo);
+            const int c_hi = cluster_of(p.sk_total, p.n_clusters, x_hi);
+            const int nseg = c_hi - c_lo + 1;
+            const int ctr = int(ut) * kCN + int(rank);
+            if (tid == 0) {
+                volatile int* cnt = p.counters + ctr;
+                while (*cnt < nseg) __nanosleep(100);
+            }
+            named_bar(1, 128);
+            __threadfence();
+            const int nch = (t_here + 15) / 16;
+            const int k = cluster - c_lo;
+            const int ch0 = k * nch / nseg, ch1 = (k + 1) * nch / nseg;
+            {
+                {
+                    for (int c0 = ch0 * 16; c0 < ch1 * 16; c0 += 16) {
                         float v[16];
 #pragma unroll
                         for (int j = 0; j < 16; ++j) v[j] = 0.f;
@@ -391,11 +417,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                         }
                         epilogue16(p, stage, v, lane, t0, c0, t_here, mt * kBM + q * 32);
                     }
-                    if (tid == 0) p.counters[ctr] = 0;  // ready for the next launch
                 }
             }
-            if (sg.sk) first_sk = false;
-            ++seg;
+            // the last contributor to finish resets both counters for the next launch
+            named_bar(1, 128);
+            if (tid == 0) {
+                int* done = p.counters + kMaxCounters;
+                if (atomicAdd(done + ctr, 1) == nseg - 1) {
+                    p.counters[ctr] = 0;
+                    done[ctr] = 0;
+                }
+            }
         }
     }
     __syncthreads();
@@ -440,7 +472,7 @@ int make_tmap_2d_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t 
 }
 
 // partials for every CTA (2 slots of 128 x 512 fp32) + per-tile counters (zero-initialised)
-size_t gemm_workspace_floats() { return size_t(kNumSMs) * 2 * kBM * kMaxTB + kMaxCounters; }
+size_t gemm_workspace_floats() { return size_t(kNumSMs) * 2 * kBM * kMaxTB + 2 * kMaxCounters; }
 
 int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_bfloat16* out_bf16,
               const __nv_bfloat16* resid, float* out_f32, float* workspace, size_t workspace_floats,
