@@ -28,6 +28,8 @@
 // Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w4..w7 epilogue.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -176,6 +178,7 @@ DS_DEVICE void epilogue16(const GemmParams& p, float* stage, const float* vals, 
     __syncwarp();
 }
 
+template <int CN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
                const GemmParams p) {
@@ -196,14 +199,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
-    const int cluster = blockIdx.x / kCN;
+    const int cluster = blockIdx.x / CN;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmap_w);
         tma_prefetch_desc(&tmap_x);
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], kCN);
+            mbar_init(&empty_bar[s], CN);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull_bar[a], 1);
@@ -219,19 +222,19 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
     const uint32_t tmem_base = *tmem_slot;
     pdl_launch_dependents();
 
-    const int cl_tiles = p.m_tiles / kCN;
+    const int cl_tiles = p.m_tiles / CN;
 
     if (warp == 0) {
         if (elect_one()) {
             const uint64_t pol_w = policy_evict_first();
-            const uint16_t mask = (1u << kCN) - 1;
+            const uint16_t mask = (1u << CN) - 1;
             // weights first (independent of the previous kernel), activations after pdl_wait
             int pre = 0;
             {
                 SegIter si(p, cluster);
                 Seg sg;
                 while (pre < p.stages && si.next(sg)) {
-                    const int mt = int(sg.ut % cl_tiles) * kCN + int(rank);
+                    const int mt = int(sg.ut % cl_tiles) * CN + int(rank);
                     for (int kb = sg.kb0; kb < sg.kb1 && pre < p.stages; ++kb, ++pre) {
                         mbar_arrive_expect_tx(&full_bar[pre], stage_bytes);
                         tma_load_2d_hint(smem + pre * stage_bytes, &tmap_w, &full_bar[pre], kb * kBK,
@@ -245,7 +248,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
             Seg sg;
             while (si.next(sg)) {
                 const int tbk = int(sg.ut / cl_tiles);
-                const int mt = int(sg.ut % cl_tiles) * kCN + int(rank);
+                const int mt = int(sg.ut % cl_tiles) * CN + int(rank);
                 for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++i) {
                     const int s = i % p.stages;
                     const uint32_t round = i / p.stages;
@@ -294,7 +297,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                                       umma_sdesc_sw128(sb + c * 256 * 128 + k * 32), idesc,
                                       (kb > sg.kb0 || k > 0) ? 1u : 0u);
                     }
-                    umma_commit_mc(&empty_bar[s], (1u << kCN) - 1);
+                    umma_commit_mc(&empty_bar[s], (1u << CN) - 1);
                     if (kb == sg.kb1 - 1) umma_commit(&tfull_bar[a]);
                 }
                 __syncwarp();
@@ -315,7 +318,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         Seg sg;
         while (si.next(sg)) {
             const int tbk = int(sg.ut / cl_tiles);
-            const int mt = int(sg.ut % cl_tiles) * kCN + int(rank);
+            const int mt = int(sg.ut % cl_tiles) * CN + int(rank);
             const int t0 = tbk * p.tb;
             const int t_here = min(p.tb, p.T - t0);
             const int a = seg % p.n_acc;
@@ -337,7 +340,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                 // park the partial as [col/4][lane][4] (16-byte stores, 512 B per warp)
                 const int slot = first_sk ? 0 : 1;
                 float4* mine = reinterpret_cast<float4*>(
-                    p.partial + (size_t(cluster * kCN + rank) * 2 + slot) * slot_floats);
+                    p.partial + (size_t(cluster * CN + rank) * 2 + slot) * slot_floats);
                 for (int c0 = 0; c0 < t_here; c0 += 16) {
                     uint32_t r[16];
                     tmem_ld16(acc + c0, r);
@@ -353,7 +356,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                 if (lane == 0) mbar_arrive(&tempty_bar[a]);  // accumulator free for the next tile
                 __threadfence();
                 named_bar(1, 128);
-                if (tid == 0) atomicAdd(&p.counters[int(sg.ut) * kCN + int(rank)], 1);
+                if (tid == 0) atomicAdd(&p.counters[int(sg.ut) * CN + int(rank)], 1);
                 pending[n_pending++] = sg.ut;  // reduced after the main loop, in parallel
             }
             if (sg.sk) first_sk = false;
@@ -366,7 +369,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         for (int pi = 0; pi < n_pending; ++pi) {
             const long long ut = pending[pi];
             const int tbk = int(ut / cl_tiles);
-            const int mt = int(ut % cl_tiles) * kCN + int(rank);
+            const int mt = int(ut % cl_tiles) * CN + int(rank);
             const int t0 = tbk * p.tb;
             const int t_here = min(p.tb, p.T - t0);
             const long long x_lo = ut * p.KB - p.dp_tiles * p.KB;
@@ -374,7 +377,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
             const int c_lo = cluster_of(p.sk_total, p.n_clusters, x_lo);
             const int c_hi = cluster_of(p.sk_total, p.n_clusters, x_hi);
             const int nseg = c_hi - c_lo + 1;
-            const int ctr = int(ut) * kCN + int(rank);
+            const int ctr = int(ut) * CN + int(rank);
             if (tid == 0) {
                 volatile int* cnt = p.counters + ctr;
                 while (*cnt < nseg) __nanosleep(100);
@@ -398,7 +401,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                                 if (c > c_hi) break;
                                 const int sl = range_start(p.sk_total, p.n_clusters, c) >= x_lo ? 0 : 1;
                                 const float4* src = reinterpret_cast<const float4*>(
-                                    p.partial + (size_t(c * kCN + rank) * 2 + sl) * slot_floats);
+                                    p.partial + (size_t(c * CN + rank) * 2 + sl) * slot_floats);
 #pragma unroll
                                 for (int jj = 0; jj < 4; ++jj)
                                     buf[u][jj] = __ldcg(src + size_t(c0 / 4 + jj) * kBM + tid);
@@ -479,7 +482,9 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
               int max_clusters, cudaStream_t stream) {
     const int N = w.N, K = w.K;
     if (T <= 0) return 0;
-    if (K % kBK != 0 || N % (kBM * kCN) != 0) return -3;
+    static const int cn_env = getenv("DS_GEMM_CN") ? atoi(getenv("DS_GEMM_CN")) : kCN;
+    const int cn = (cn_env == 1 || (N / kBM) % 2 != 0) ? 1 : 2;
+    if (K % kBK != 0 || N % kBM != 0) return -3;
     if (!workspace || workspace_floats < gemm_workspace_floats()) return -7;
     GemmParams p{};
     p.T = T;
@@ -490,7 +495,7 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
     if (p.t_blocks * p.m_tiles > kMaxCounters) return -8;
     p.tb = T < kMaxTB ? T : kMaxTB;
     p.tb_pad = (p.tb + 15) & ~15;
-    p.brows = p.tb_pad / kCN;
+    p.brows = p.tb_pad / cn;
     p.KB = K / kBK;
     const int stage_bytes = kBM * kBK * 2 + p.tb_pad * kBK * 2;
     const int fixed = 4 * 16 * kStageStride * 4 + 256 + 1024;
@@ -498,8 +503,8 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
     if (p.stages > 8) p.stages = 8;
     if (p.stages < 2) return -4;
     p.n_acc = p.tb_pad <= 256 ? 2 : 1;
-    const long long tiles = (long long)p.t_blocks * (p.m_tiles / kCN);
-    int nc = kNumSMs / kCN;
+    const long long tiles = (long long)p.t_blocks * (p.m_tiles / cn);
+    int nc = kNumSMs / cn;
     if (max_clusters > 0 && nc > max_clusters) nc = max_clusters;
     // whole waves data-parallel; the remainder stream-K with >= 8 k-blocks per cluster
     long long dp = tiles >= nc ? (tiles / nc) * nc : 0;
@@ -524,21 +529,23 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
     if (make_tmap_2d_bf16(&tx, x, T, K, p.brows, kBK) != 0) return -5;
     const size_t smem = size_t(p.stages) * stage_bytes + fixed;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(nc * kCN);
+    cfg.gridDim = dim3(nc * cn);
     cfg.blockDim = dim3(kGemmThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = kCN;
+    attr[0].val.clusterDim.x = cn;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel,
-                                       *reinterpret_cast<const CUtensorMap*>(w.tmap), tx, p);
+    cudaError_t e = cn == 2 ? cudaLaunchKernelEx(&cfg, gemm_tc_kernel<2>,
+                                                 *reinterpret_cast<const CUtensorMap*>(w.tmap), tx, p)
+                            : cudaLaunchKernelEx(&cfg, gemm_tc_kernel<1>,
+                                                 *reinterpret_cast<const CUtensorMap*>(w.tmap), tx, p);
     return e == cudaSuccess ? 0 : -6;
 }
 
@@ -553,8 +560,10 @@ int gemm_weight_init(GemmWeight* w, const __nv_bfloat16* data, int N, int K) {
 // first launch, which can wait on in-flight work such as a spinning NCCL receive).
 void preload_gemm() {
     cudaFuncAttributes a;
-    cudaFuncGetAttributes(&a, gemm_tc_kernel);
-    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
+    cudaFuncGetAttributes(&a, gemm_tc_kernel<1>);
+    cudaFuncGetAttributes(&a, gemm_tc_kernel<2>);
+    cudaFuncSetAttribute(gemm_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
+    cudaFuncSetAttribute(gemm_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
 }
 
 }  // namespace ds

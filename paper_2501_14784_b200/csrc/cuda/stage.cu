@@ -917,6 +917,7 @@ ds_status ds_dbg_gemm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t N
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return ds_fail(DS_ERR_NO_DEVICE, "no CUDA device");
+    ds::preload_all();
     bf16 *dx = nullptr, *dw = nullptr, *dout = nullptr;
     float *dws = nullptr, *df = nullptr;
     const size_t out_elems = size_t(T) * N;
