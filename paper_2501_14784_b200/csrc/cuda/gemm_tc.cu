@@ -12,22 +12,22 @@
 //   block; each loads half of the activation tile and multicasts it to both (TMA .multicast), so
 //   the per-SM activation traffic from L2 is halved. Each CTA's MMA releases a stage in both
 //   CTAs (tcgen05.commit .multicast::cluster).
-// * Data-parallel + stream-K: whole waves of cluster tiles go to clusters round-robin; the
-//   remaining tiles' (tile x k-block) iterations are cut into equal contiguous ranges, one per
-//   cluster (no wave quantisation). A tile split across clusters parks fp32 partials; after
-//   their main loops its contributors wait for the tile's counter, then each reduces its share
-//   of the tile's columns (partials summed in cluster order: deterministic) and applies the
-//   epilogue. No separate reduction kernel.
-// * TMEM holds two accumulators when the token block fits 256 columns, so a tile's epilogue
-//   overlaps the next tile's MMAs.
+// * Work units = (cluster tile, K split), handed to clusters round-robin (persistent CTAs). Wide
+//   GEMMs (>= one wave of cluster tiles) run unsplit; narrow ones (q/k/v, o, down at 8B) split K
+//   so every SM streams weights, parking fp32 partials that a PDL-chained reduction kernel sums
+//   in split order (deterministic) with the same fused epilogue. (An in-kernel stream-K fixup was
+//   measured slower here: its contributors idle while the tile's last partial lands.)
+// * TMEM holds two accumulators when the token block fits 256 columns, so a unit's epilogue
+//   overlaps the next unit's MMAs.
 // * Epilogue: tcgen05.ld -> shared-memory transpose -> 16-byte coalesced stores, fused
-//   bf16 / residual-add (x = bf16(x + bf16(acc))) / fp32 (logits).
+//   bf16 / residual-add (x = bf16(x + bf16(acc))) / fp32 (logits, split partials).
 // * Programmatic dependent launch: the first weight tiles are fetched before waiting on the
 //   previous kernel; the activations after.
 //
 // Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w4..w7 epilogue.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -38,11 +38,10 @@ namespace ds {
 constexpr int kBM = 128;      // weight rows per CTA tile (UMMA M)
 constexpr int kBK = 64;       // K elements per stage = one 128-byte swizzle row
 constexpr int kMaxTB = 512;   // tokens per block (TMEM columns)
-constexpr int kCN = 2;        // CTAs per cluster
 constexpr int kGemmThreads = 256;
-constexpr int kSmemBudget = 200 * 1024;
+constexpr int kSmemBudget = 222 * 1024;
 constexpr int kStageStride = 36;  // floats per row of the epilogue transpose buffer
-constexpr int kMaxCounters = 16384;
+constexpr size_t kWorkspaceFloats = size_t(16) << 20;  // split-K partials
 
 struct GemmParams {
     int T, N, K;
@@ -50,20 +49,33 @@ struct GemmParams {
     int t_blocks;
     int tb;       // tokens per block (<= 512)
     int tb_pad;   // tb rounded up to 16
-    int brows;    // activation rows each CTA of the cluster loads per stage (tb_pad / 2)
+    int brows;    // activation rows each CTA of the cluster loads per stage (tb_pad / CN)
     int stages;
     int n_acc;    // TMEM accumulators
     int KB;       // k-blocks per tile
+    int splits;   // K splits per tile
     int n_clusters;
-    long long dp_tiles;  // cluster tiles handled whole, round-robin
-    long long sk_total;  // stream-K iterations (tiles after dp_tiles, x KB)
+    int units;    // cluster tiles x splits
     int epi;
     __nv_bfloat16* out_bf16;
     const __nv_bfloat16* resid;
     float* out_f32;
-    float* partial;  // [n_clusters * 2 CTAs][2 slots][tb_pad/4][128 lanes][4]
-    int* counters;   // per CTA tile, zero between launches
+    float* partial;  // [splits][T][N] fp32 when splits > 1
+    unsigned long long* trace;  // optional per-CTA phase timestamps (gemm_set_trace)
 };
+
+DS_DEVICE unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define GEMM_TRACE(k)                                             \
+    do {                                                          \
+        if (p.trace) p.trace[blockIdx.x * 8 + (k)] = gtime();    \
+    } while (0)
+
+static unsigned long long* g_gemm_trace = nullptr;
+void gemm_set_trace(unsigned long long* buf) { g_gemm_trace = buf; }
 
 DS_DEVICE uint32_t cluster_rank() {
     uint32_t r;
@@ -88,58 +100,24 @@ DS_DEVICE void umma_commit_mc(uint64_t* bar, uint16_t mask) {
         "h"(mask)
         : "memory");
 }
-DS_DEVICE void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-__host__ __device__ inline long long range_start(long long total, int n, int c) {
-    return total * c / n;
-}
-DS_DEVICE int cluster_of(long long total, int n, long long x) {
-    int c = int((x * n) / total);
-    while (c + 1 < n && range_start(total, n, c + 1) <= x) ++c;
-    while (c > 0 && range_start(total, n, c) > x) --c;
-    return c;
-}
-
-// A cluster's work in order: its data-parallel tiles, then its stream-K range.
-struct Seg {
-    long long ut;
-    int kb0, kb1;
-    bool sk;
+// A unit: cluster tile ut (token block x feature pair) and its K range [kb0, kb1).
+struct Unit {
+    int ut, split, kb0, kb1;
 };
-struct SegIter {
-    long long dp_next, dp_end, it, end, sk_base;
-    int nc, KB;
-    DS_DEVICE SegIter(const GemmParams& p, int c) {
-        nc = p.n_clusters;
-        KB = p.KB;
-        dp_next = c;
-        dp_end = p.dp_tiles;
-        sk_base = p.dp_tiles * p.KB;
-        it = sk_base + range_start(p.sk_total, nc, c);
-        end = sk_base + range_start(p.sk_total, nc, c + 1);
-    }
-    DS_DEVICE bool next(Seg& s) {
-        if (dp_next < dp_end) {
-            s = {dp_next, 0, KB, false};
-            dp_next += nc;
-            return true;
-        }
-        if (it < end) {
-            s.ut = it / KB;
-            s.kb0 = int(it - s.ut * KB);
-            s.kb1 = int(end - it < (long long)(KB - s.kb0) ? s.kb0 + (end - it) : KB);
-            s.sk = true;
-            it += s.kb1 - s.kb0;
-            return true;
-        }
-        return false;
-    }
-};
+DS_DEVICE Unit unit_of(const GemmParams& p, int u) {
+    Unit x;
+    x.ut = u / p.splits;
+    x.split = u % p.splits;
+    x.kb0 = x.split * p.KB / p.splits;
+    x.kb1 = (x.split + 1) * p.KB / p.splits;
+    return x;
+}
 
 // Applies the epilogue to 16 consecutive token columns of one 32-feature slice held as vals[16]
 // (this thread's feature, columns c0..c0+15), through a per-warp transpose buffer.
-DS_DEVICE void epilogue16(const GemmParams& p, float* stage, const float* vals, int lane, int t0,
-                          int c0, int t_here, int f_base) {
+DS_DEVICE void epilogue16(const GemmParams& p, int epi, float* out_f32, float* stage,
+                          const float* vals, int lane, int t0, int c0, int t_here, int f_base) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) stage[j * kStageStride + lane] = vals[j];
     __syncwarp();
@@ -158,12 +136,12 @@ DS_DEVICE void epilogue16(const GemmParams& p, float* stage, const float* vals, 
             v[4 * i + 3] = x.w;
         }
         const size_t o = size_t(t) * p.N + f0;
-        if (p.epi == EPI_F32) {
-            float4* dst = reinterpret_cast<float4*>(p.out_f32 + o);
+        if (epi == EPI_F32) {
+            float4* dst = reinterpret_cast<float4*>(out_f32 + o);
 #pragma unroll
             for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
         } else {
-            if (p.epi == EPI_RESID) {
+            if (epi == EPI_RESID) {
                 float r[16];
                 unpack8(reinterpret_cast<const uint4*>(p.resid + o)[0], r);
                 unpack8(reinterpret_cast<const uint4*>(p.resid + o)[1], r + 8);
@@ -194,11 +172,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
     uint64_t* tfull_bar = empty_bar + p.stages;  // [2]
     uint64_t* tempty_bar = tfull_bar + 2;        // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-    int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
+    const uint32_t rank = CN > 1 ? cluster_rank() : 0;
     const int cluster = blockIdx.x / CN;
 
     if (warp == 0 && lane == 0) {
@@ -217,9 +194,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
     if (warp == 2) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
-    cluster_sync();  // remote barriers initialised before any multicast lands
+    if (CN > 1) cluster_sync();  // remote barriers initialised before any multicast lands
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) GEMM_TRACE(0);
     pdl_launch_dependents();
 
     const int cl_tiles = p.m_tiles / CN;
@@ -230,26 +208,22 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
             const uint16_t mask = (1u << CN) - 1;
             // weights first (independent of the previous kernel), activations after pdl_wait
             int pre = 0;
-            {
-                SegIter si(p, cluster);
-                Seg sg;
-                while (pre < p.stages && si.next(sg)) {
-                    const int mt = int(sg.ut % cl_tiles) * CN + int(rank);
-                    for (int kb = sg.kb0; kb < sg.kb1 && pre < p.stages; ++kb, ++pre) {
-                        mbar_arrive_expect_tx(&full_bar[pre], stage_bytes);
-                        tma_load_2d_hint(smem + pre * stage_bytes, &tmap_w, &full_bar[pre], kb * kBK,
-                                         mt * kBM, pol_w);
-                    }
+            for (int u = cluster; u < p.units && pre < p.stages; u += p.n_clusters) {
+                const Unit w = unit_of(p, u);
+                const int mt = (w.ut % cl_tiles) * CN + int(rank);
+                for (int kb = w.kb0; kb < w.kb1 && pre < p.stages; ++kb, ++pre) {
+                    mbar_arrive_expect_tx(&full_bar[pre], stage_bytes);
+                    tma_load_2d_hint(smem + pre * stage_bytes, &tmap_w, &full_bar[pre], kb * kBK,
+                                     mt * kBM, pol_w);
                 }
             }
             pdl_wait();
             int i = 0;
-            SegIter si(p, cluster);
-            Seg sg;
-            while (si.next(sg)) {
-                const int tbk = int(sg.ut / cl_tiles);
-                const int mt = int(sg.ut % cl_tiles) * CN + int(rank);
-                for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++i) {
+            for (int u = cluster; u < p.units; u += p.n_clusters) {
+                const Unit w = unit_of(p, u);
+                const int tbk = w.ut / cl_tiles;
+                const int mt = (w.ut % cl_tiles) * CN + int(rank);
+                for (int kb = w.kb0; kb < w.kb1; ++kb, ++i) {
                     const int s = i % p.stages;
                     const uint32_t round = i / p.stages;
                     uint8_t* sa = smem + s * stage_bytes;
@@ -259,27 +233,30 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                         mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
                         tma_load_2d_hint(sa, &tmap_w, &full_bar[s], kb * kBK, mt * kBM, pol_w);
                     }
-                    tma_load_2d_mc(sb + rank * p.brows * kBK * 2, &tmap_x, &full_bar[s], kb * kBK,
-                                   tbk * p.tb + int(rank) * p.brows, mask);
+                    if (CN > 1)
+                        tma_load_2d_mc(sb + rank * p.brows * kBK * 2, &tmap_x, &full_bar[s], kb * kBK,
+                                       tbk * p.tb + int(rank) * p.brows, mask);
+                    else
+                        tma_load_2d(sb, &tmap_x, &full_bar[s], kb * kBK, tbk * p.tb);
                 }
             }
-            // drain: every stage released by both CTAs (no remote arrival after we exit)
+            GEMM_TRACE(1);
+            // drain: every stage released by every CTA (no remote arrival after we exit)
             const int n = i;
             for (int k = (n > p.stages ? n - p.stages : 0); k < n; ++k)
                 mbar_wait(&empty_bar[k % p.stages], (uint32_t(k / p.stages) & 1));
         }
     } else if (warp == 1) {
         int i = 0, seg = 0;
-        SegIter si(p, cluster);
-        Seg sg;
-        while (si.next(sg)) {
-            const int tbk = int(sg.ut / cl_tiles);
+        for (int u = cluster; u < p.units; u += p.n_clusters, ++seg) {
+            const Unit w = unit_of(p, u);
+            const int tbk = w.ut / cl_tiles;
             const int t_here = min(p.tb, p.T - tbk * p.tb);
             const int a = seg % p.n_acc;
             const uint32_t acc = tmem_base + uint32_t(a * 256);
             mbar_wait(&tempty_bar[a], ((seg / p.n_acc) & 1) ^ 1);
             tc_fence_after();
-            for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++i) {
+            for (int kb = w.kb0; kb < w.kb1; ++kb, ++i) {
                 const int s = i % p.stages;
                 mbar_wait(&full_bar[s], (i / p.stages) & 1);
                 tc_fence_after();
@@ -295,149 +272,95 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                         for (int k = 0; k < kBK / 16; ++k)
                             umma_bf16(acc + c * 256, umma_sdesc_sw128(sa + k * 32),
                                       umma_sdesc_sw128(sb + c * 256 * 128 + k * 32), idesc,
-                                      (kb > sg.kb0 || k > 0) ? 1u : 0u);
+                                      (kb > w.kb0 || k > 0) ? 1u : 0u);
                     }
-                    umma_commit_mc(&empty_bar[s], (1u << CN) - 1);
-                    if (kb == sg.kb1 - 1) umma_commit(&tfull_bar[a]);
+                    if (CN > 1)
+                        umma_commit_mc(&empty_bar[s], (1u << CN) - 1);
+                    else
+                        umma_commit(&empty_bar[s]);
+                    if (kb == w.kb1 - 1) umma_commit(&tfull_bar[a]);
                 }
                 __syncwarp();
             }
-            ++seg;
         }
+        if (lane == 0) GEMM_TRACE(2);
     } else if (warp >= 4) {
         pdl_wait();
         const int q = warp & 3;
-        const int tid = threadIdx.x - 128;  // 0..127, = TMEM lane
         float* stage = ep_stage + q * 16 * kStageStride;
-        const size_t slot_floats = size_t(p.tb_pad) * kBM;
         int seg = 0;
-        bool first_sk = true;
-        long long pending[2];  // split tiles this CTA parked a partial for (<= 2 per range)
-        int n_pending = 0;
-        SegIter si(p, cluster);
-        Seg sg;
-        while (si.next(sg)) {
-            const int tbk = int(sg.ut / cl_tiles);
-            const int mt = int(sg.ut % cl_tiles) * CN + int(rank);
+        for (int u = cluster; u < p.units; u += p.n_clusters, ++seg) {
+            const Unit w = unit_of(p, u);
+            const int tbk = w.ut / cl_tiles;
+            const int mt = (w.ut % cl_tiles) * CN + int(rank);
             const int t0 = tbk * p.tb;
             const int t_here = min(p.tb, p.T - t0);
             const int a = seg % p.n_acc;
             const uint32_t acc = tmem_base + uint32_t(a * 256) + (uint32_t(q * 32) << 16);
             mbar_wait(&tfull_bar[a], (seg / p.n_acc) & 1);
             tc_fence_after();
-            if (sg.kb0 == 0 && sg.kb1 == p.KB) {
-                for (int c0 = 0; c0 < t_here; c0 += 16) {
-                    uint32_t r[16];
-                    tmem_ld16(acc + c0, r);
-                    tmem_ld_wait();
-                    epilogue16(p, stage, reinterpret_cast<float*>(r), lane, t0, c0, t_here,
-                               mt * kBM + q * 32);
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty_bar[a]);
-            } else {
-                // park the partial as [col/4][lane][4] (16-byte stores, 512 B per warp)
-                const int slot = first_sk ? 0 : 1;
-                float4* mine = reinterpret_cast<float4*>(
-                    p.partial + (size_t(cluster * CN + rank) * 2 + slot) * slot_floats);
-                for (int c0 = 0; c0 < t_here; c0 += 16) {
-                    uint32_t r[16];
-                    tmem_ld16(acc + c0, r);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj)
-                        mine[size_t(c0 / 4 + jj) * kBM + tid] =
-                            make_float4(__uint_as_float(r[4 * jj]), __uint_as_float(r[4 * jj + 1]),
-                                        __uint_as_float(r[4 * jj + 2]), __uint_as_float(r[4 * jj + 3]));
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty_bar[a]);  // accumulator free for the next tile
-                __threadfence();
-                named_bar(1, 128);
-                if (tid == 0) atomicAdd(&p.counters[int(sg.ut) * CN + int(rank)], 1);
-                pending[n_pending++] = sg.ut;  // reduced after the main loop, in parallel
+            // unsplit: the fused epilogue; split: an fp32 partial into its split plane
+            const int epi = p.splits > 1 ? EPI_F32 : p.epi;
+            float* out_f32 = p.splits > 1 ? p.partial + size_t(w.split) * p.T * p.N : p.out_f32;
+            for (int c0 = 0; c0 < t_here; c0 += 16) {
+                uint32_t r[16];
+                tmem_ld16(acc + c0, r);
+                tmem_ld_wait();
+                epilogue16(p, epi, out_f32, stage, reinterpret_cast<float*>(r), lane, t0, c0, t_here,
+                           mt * kBM + q * 32);
             }
-            if (sg.sk) first_sk = false;
-            ++seg;
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty_bar[a]);
         }
-        // Deferred, parallel fixup: every contributor of a split tile waits until all partials
-        // are parked, then reduces its share of the tile's 16-column chunks (partials summed in
-        // cluster order: deterministic) and applies the epilogue. Waiting only at the end keeps
-        // the stream-K ranges from serialising on each other.
-        for (int pi = 0; pi < n_pending; ++pi) {
-            const long long ut = pending[pi];
-            const int tbk = int(ut / cl_tiles);
-            const int mt = int(ut % cl_tiles) * CN + int(rank);
-            const int t0 = tbk * p.tb;
-            const int t_here = min(p.tb, p.T - t0);
-            const long long x_lo = ut * p.KB - p.dp_tiles * p.KB;
-            const long long x_hi = x_lo + p.KB - 1;
-            const int c_lo = cluster_of(p.sk_total, p.n_clusters, x_lo);
-            const int c_hi = cluster_of(p.sk_total, p.n_clusters, x_hi);
-            const int nseg = c_hi - c_lo + 1;
-            const int ctr = int(ut) * CN + int(rank);
-            if (tid == 0) {
-                volatile int* cnt = p.counters + ctr;
-                while (*cnt < nseg) __nanosleep(100);
-            }
-            named_bar(1, 128);
-            __threadfence();
-            const int nch = (t_here + 15) / 16;
-            const int k = cluster - c_lo;
-            const int ch0 = k * nch / nseg, ch1 = (k + 1) * nch / nseg;
-            {
-                {
-                    for (int c0 = ch0 * 16; c0 < ch1 * 16; c0 += 16) {
-                        float v[16];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) v[j] = 0.f;
-                        for (int cb = c_lo; cb <= c_hi; cb += 4) {
-                            float4 buf[4][4];
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                const int c = cb + u;
-                                if (c > c_hi) break;
-                                const int sl = range_start(p.sk_total, p.n_clusters, c) >= x_lo ? 0 : 1;
-                                const float4* src = reinterpret_cast<const float4*>(
-                                    p.partial + (size_t(c * CN + rank) * 2 + sl) * slot_floats);
-#pragma unroll
-                                for (int jj = 0; jj < 4; ++jj)
-                                    buf[u][jj] = __ldcg(src + size_t(c0 / 4 + jj) * kBM + tid);
-                            }
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                if (cb + u > c_hi) break;
-#pragma unroll
-                                for (int jj = 0; jj < 4; ++jj) {
-                                    v[4 * jj] += buf[u][jj].x;
-                                    v[4 * jj + 1] += buf[u][jj].y;
-                                    v[4 * jj + 2] += buf[u][jj].z;
-                                    v[4 * jj + 3] += buf[u][jj].w;
-                                }
-                            }
-                        }
-                        epilogue16(p, stage, v, lane, t0, c0, t_here, mt * kBM + q * 32);
-                    }
-                }
-            }
-            // the last contributor to finish resets both counters for the next launch
-            named_bar(1, 128);
-            if (tid == 0) {
-                int* done = p.counters + kMaxCounters;
-                if (atomicAdd(done + ctr, 1) == nseg - 1) {
-                    p.counters[ctr] = 0;
-                    done[ctr] = 0;
-                }
-            }
-        }
+        if (threadIdx.x == 128) GEMM_TRACE(3);
     }
     __syncthreads();
-    cluster_sync();
+    if (CN > 1) cluster_sync();
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(tmem_base, 512);
+    }
+}
+
+// Split-K reduction: splits summed in order (deterministic) + the same epilogues.
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int T, int N, int epi,
+                                     __nv_bfloat16* out_bf16, const __nv_bfloat16* resid,
+                                     float* out_f32) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const size_t total = size_t(T) * N / 4;
+    const size_t plane = size_t(T) * N;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
+         i += size_t(gridDim.x) * blockDim.x) {
+        float4 acc = reinterpret_cast<const float4*>(ws)[i];
+        for (int s = 1; s < splits; ++s) {
+            const float4 v = reinterpret_cast<const float4*>(ws + s * plane)[i];
+            acc.x += v.x;
+            acc.y += v.y;
+            acc.z += v.z;
+            acc.w += v.w;
+        }
+        const size_t o = i * 4;
+        if (epi == EPI_F32) {
+            reinterpret_cast<float4*>(out_f32)[i] = acc;
+        } else {
+            float a[4] = {acc.x, acc.y, acc.z, acc.w};
+            if (epi == EPI_RESID) {
+                const uint2 rv = *reinterpret_cast<const uint2*>(resid + o);
+                const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
+                const float2 r0 = __bfloat1622float2(rh[0]);
+                const float2 r1 = __bfloat1622float2(rh[1]);
+                a[0] = r0.x + round_bf(a[0]);
+                a[1] = r0.y + round_bf(a[1]);
+                a[2] = r1.x + round_bf(a[2]);
+                a[3] = r1.y + round_bf(a[3]);
+            }
+            uint2 ov;
+            ov.x = pack2(a[0], a[1]);
+            ov.y = pack2(a[2], a[3]);
+            *reinterpret_cast<uint2*>(out_bf16 + o) = ov;
+        }
     }
 }
 
@@ -474,62 +397,74 @@ int make_tmap_2d_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t 
     return r == CUDA_SUCCESS ? 0 : -2;
 }
 
-// partials for every CTA (2 slots of 128 x 512 fp32) + per-tile counters (zero-initialised)
-size_t gemm_workspace_floats() { return size_t(kNumSMs) * 2 * kBM * kMaxTB + 2 * kMaxCounters; }
+size_t gemm_workspace_floats() { return kWorkspaceFloats; }
+
+// launches issued by gemm_bf16 for this shape (1, or 2 with the split-K reduction)
+int gemm_launch_count(int T, int N, int K);
+
+static int pick_splits(int T, int N, int K, int cn, int n_clusters) {
+    const int tiles = ((T + kMaxTB - 1) / kMaxTB) * (N / kBM / cn);
+    if (tiles >= n_clusters) return 1;
+    int s = n_clusters / tiles;
+    s = std::min(s, 8);
+    s = std::min(s, (K / kBK) / 4);
+    while (s > 1 && size_t(s) * T * N > kWorkspaceFloats) --s;
+    return std::max(s, 1);
+}
+
+static int pick_cn(int N) {
+    static const int cn_env = getenv("DS_GEMM_CN") ? atoi(getenv("DS_GEMM_CN")) : 2;
+    return (cn_env == 1 || (N / kBM) % 2 != 0) ? 1 : 2;
+}
+
+int gemm_launch_count(int T, int N, int K) {
+    const int cn = pick_cn(N);
+    return pick_splits(T, N, K, cn, kNumSMs / cn) > 1 ? 2 : 1;
+}
 
 int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_bfloat16* out_bf16,
               const __nv_bfloat16* resid, float* out_f32, float* workspace, size_t workspace_floats,
               int max_clusters, cudaStream_t stream) {
     const int N = w.N, K = w.K;
     if (T <= 0) return 0;
-    static const int cn_env = getenv("DS_GEMM_CN") ? atoi(getenv("DS_GEMM_CN")) : kCN;
-    const int cn = (cn_env == 1 || (N / kBM) % 2 != 0) ? 1 : 2;
+    int cn = pick_cn(N);
     if (K % kBK != 0 || N % kBM != 0) return -3;
-    if (!workspace || workspace_floats < gemm_workspace_floats()) return -7;
     GemmParams p{};
     p.T = T;
     p.N = N;
     p.K = K;
     p.m_tiles = N / kBM;
     p.t_blocks = (T + kMaxTB - 1) / kMaxTB;
-    if (p.t_blocks * p.m_tiles > kMaxCounters) return -8;
     p.tb = T < kMaxTB ? T : kMaxTB;
     p.tb_pad = (p.tb + 15) & ~15;
+    if (cn == 1 && p.tb_pad > 256) cn = (p.m_tiles % 2 == 0) ? 2 : 1;  // TMA box rows <= 256
+    if (cn == 1 && p.tb_pad > 256) return -9;
     p.brows = p.tb_pad / cn;
     p.KB = K / kBK;
     const int stage_bytes = kBM * kBK * 2 + p.tb_pad * kBK * 2;
     const int fixed = 4 * 16 * kStageStride * 4 + 256 + 1024;
     p.stages = (kSmemBudget - fixed) / stage_bytes;
-    if (p.stages > 8) p.stages = 8;
+    if (p.stages > 12) p.stages = 12;
     if (p.stages < 2) return -4;
     p.n_acc = p.tb_pad <= 256 ? 2 : 1;
-    const long long tiles = (long long)p.t_blocks * (p.m_tiles / cn);
     int nc = kNumSMs / cn;
     if (max_clusters > 0 && nc > max_clusters) nc = max_clusters;
-    // whole waves data-parallel; the remainder stream-K with >= 8 k-blocks per cluster
-    long long dp = tiles >= nc ? (tiles / nc) * nc : 0;
-    if (dp == tiles) {
-        // exact waves: nothing to split
-    } else if ((tiles - dp) * p.KB < 8LL * nc && dp >= nc) {
-        dp -= nc;  // tiny remainder: fold the last full wave into the stream-K part
-    }
-    long long sk = (tiles - dp) * p.KB;
-    if (dp == 0 && sk > 0 && sk / 4 < nc) nc = int(sk / 4 > 0 ? sk / 4 : 1);  // tiny GEMM: fewer clusters
-    if (dp > 0 && nc > tiles) nc = int(tiles);
-    p.n_clusters = nc;
-    p.dp_tiles = dp;
-    p.sk_total = sk;
+    p.splits = pick_splits(T, N, K, cn, nc);
+    if (p.splits > 1 && (!workspace || workspace_floats < size_t(p.splits) * T * N)) p.splits = 1;
+    const int tiles = p.t_blocks * (p.m_tiles / cn);
+    p.units = tiles * p.splits;
+    p.n_clusters = std::min(nc, p.units);
     p.epi = epi;
     p.out_bf16 = out_bf16;
     p.resid = resid;
     p.out_f32 = out_f32;
     p.partial = workspace;
-    p.counters = reinterpret_cast<int*>(workspace + size_t(kNumSMs) * 2 * kBM * kMaxTB);
+    p.trace = g_gemm_trace;
     alignas(64) CUtensorMap tx;
     if (make_tmap_2d_bf16(&tx, x, T, K, p.brows, kBK) != 0) return -5;
     const size_t smem = size_t(p.stages) * stage_bytes + fixed;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(nc * cn);
+    cfg.gridDim = dim3(p.n_clusters * cn);
     cfg.blockDim = dim3(kGemmThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
@@ -542,11 +477,19 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    cudaError_t e = cn == 2 ? cudaLaunchKernelEx(&cfg, gemm_tc_kernel<2>,
-                                                 *reinterpret_cast<const CUtensorMap*>(w.tmap), tx, p)
-                            : cudaLaunchKernelEx(&cfg, gemm_tc_kernel<1>,
-                                                 *reinterpret_cast<const CUtensorMap*>(w.tmap), tx, p);
-    return e == cudaSuccess ? 0 : -6;
+    const CUtensorMap& tw = *reinterpret_cast<const CUtensorMap*>(w.tmap);
+    cudaError_t e = cn == 2 ? cudaLaunchKernelEx(&cfg, gemm_tc_kernel<2>, tw, tx, p)
+                            : cudaLaunchKernelEx(&cfg, gemm_tc_kernel<1>, tw, tx, p);
+    if (e != cudaSuccess) return -6;
+    if (p.splits > 1) {
+        const size_t total4 = size_t(T) * N / 4;
+        int blocks = int((total4 + 255) / 256);
+        if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+        e = launch_pdl(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, stream, (const float*)workspace,
+                       p.splits, T, N, epi, out_bf16, resid, out_f32);
+        if (e != cudaSuccess) return -6;
+    }
+    return 0;
 }
 
 int gemm_weight_init(GemmWeight* w, const __nv_bfloat16* data, int N, int K) {
@@ -556,12 +499,13 @@ int gemm_weight_init(GemmWeight* w, const __nv_bfloat16* data, int N, int K) {
     return make_tmap_2d_bf16(w->tmap, data, N, K, kBM, kBK);
 }
 
-// Forces the module holding the kernel to load now (lazy loading would otherwise load it at the
+// Forces the module holding the kernels to load now (lazy loading would otherwise load it at the
 // first launch, which can wait on in-flight work such as a spinning NCCL receive).
 void preload_gemm() {
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, gemm_tc_kernel<1>);
     cudaFuncGetAttributes(&a, gemm_tc_kernel<2>);
+    cudaFuncGetAttributes(&a, splitk_reduce_kernel);
     cudaFuncSetAttribute(gemm_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
     cudaFuncSetAttribute(gemm_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
 }

@@ -25,6 +25,10 @@ struct GemmWeight {
 int gemm_weight_init(GemmWeight* w, const __nv_bfloat16* data, int N, int K);
 // Stream-K partials + per-tile counters; allocate once, zero-initialised, one per stream.
 size_t gemm_workspace_floats();
+// Debug: per-CTA phase timestamps (globaltimer ns, 8 slots per CTA) for subsequent launches.
+void gemm_set_trace(unsigned long long* device_buf);
+// Kernel launches gemm_bf16 issues for a shape (2 when K is split and reduced).
+int gemm_launch_count(int T, int N, int K);
 // out[T, N] = epi(X[T, K] . W[N, K]^T). max_clusters > 0 caps the 2-CTA clusters (tests use it
 // to force tiles split across clusters); 0 = all SMs.
 int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_bfloat16* out_bf16,

@@ -18,6 +18,7 @@
 using ds::GemmWeight;
 using ds::KvLayout;
 using bf16 = __nv_bfloat16;
+constexpr int kNumSMsHost = 148;
 
 #define CK(call)                                                                            \
     do {                                                                                    \
@@ -678,7 +679,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     size_t mark = 0;
     auto begin = [&]() { if (s->prof) mark = prof_mark(s); };
     auto end_gemm = [&](int kind, int rows_, int N, int K, int out_bytes) {
-        s->launches += 1;
+        s->launches += ds::gemm_launch_count(rows_, N, K);
         if (!s->prof) return;
         const size_t e1 = prof_mark(s);
         s->recs.push_back({kind, rows_, 2.0 * rows_ * N * K,
@@ -901,6 +902,32 @@ ds_status ds_dbg_gemm_bench(int32_t T, int32_t N, int32_t K, int32_t epi, int32_
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, a, b));
     *ms_out = ms / float(iters);
+    if (getenv("DS_GEMM_TRACE")) {
+        // one traced launch: per-CTA phase times relative to the earliest CTA start (us)
+        unsigned long long* dtr = nullptr;
+        CK(cudaMalloc(&dtr, kNumSMsHost * 8 * 8));
+        CK(cudaMemset(dtr, 0, kNumSMsHost * 8 * 8));
+        ds::gemm_set_trace(dtr);
+        ds::gemm_bf16(gw[0], dx, T, epi, dout, dout, df, dws, wsf, k_splits, 0);
+        CK(cudaDeviceSynchronize());
+        ds::gemm_set_trace(nullptr);
+        std::vector<unsigned long long> h(kNumSMsHost * 8);
+        CK(cudaMemcpy(h.data(), dtr, h.size() * 8, cudaMemcpyDeviceToHost));
+        cudaFree(dtr);
+        unsigned long long t0 = ~0ull;
+        for (int c = 0; c < kNumSMsHost; ++c)
+            if (h[c * 8]) t0 = std::min(t0, h[c * 8]);
+        const char* names[6] = {"start", "loads_issued", "mma_done", "epi_main_done", "fixup_done", "end"};
+        for (int k = 0; k < 6; ++k) {
+            std::vector<double> v;
+            for (int c = 0; c < kNumSMsHost; ++c)
+                if (h[c * 8 + k]) v.push_back(double(h[c * 8 + k] - t0) / 1000.0);
+            std::sort(v.begin(), v.end());
+            if (!v.empty())
+                fprintf(stderr, "trace T=%d N=%d K=%d %-14s n=%zu min %.2f med %.2f max %.2f us\n", T, N,
+                        K, names[k], v.size(), v.front(), v[v.size() / 2], v.back());
+        }
+    }
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     cudaFree(dx);
