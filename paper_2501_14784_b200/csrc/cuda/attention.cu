@@ -352,6 +352,219 @@ __global__ void attn_combine_kernel(const float* __restrict__ ws, int splits,
     }
 }
 
+// ------------------------------------------------------------------ decode rows ----
+// One decode row x one KV head x one context split per CTA. The split's context is cut into
+// 16-token chunks dealt round-robin to the 4 warps; every warp streams its chunks through its
+// own kDecStages-deep cp.async ring (no CTA-wide barrier in the loop), computes S = Q.K^T and
+// O += P.V with mma.sync (the G <= 16 query heads of the KV head are the M rows), and the 4
+// partial softmax states merge through shared memory at the end. Memory-level parallelism:
+// 4 warps x kDecStages x 8 KB of K/V in flight per CTA.
+constexpr int kDecChunk = 16;
+constexpr int kDecStages = 4;
+
+template <int DH>
+struct DecSmem {
+    __nv_bfloat16 k[kAttnWarps][kDecStages][kDecChunk][DH + 8];
+    __nv_bfloat16 v[kAttnWarps][kDecStages][kDecChunk][DH + 8];
+};
+
+template <int DH>
+__global__ void __launch_bounds__(kAttnWarps * 32)
+attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __restrict__ row_pos,
+                   const int32_t* __restrict__ row_page_off, const int32_t* __restrict__ flat_pages,
+                   const int32_t* __restrict__ drows, KvLayout kv, int layer, int splits,
+                   __nv_bfloat16* __restrict__ o, float* __restrict__ ws) {
+    pdl_launch_dependents();
+    pdl_wait();
+    extern __shared__ __align__(16) uint8_t dec_smem[];
+    DecSmem<DH>& sm = *reinterpret_cast<DecSmem<DH>*>(dec_smem);
+    constexpr int NT = DH / 8, KS = DH / 16;
+    const int n_kv = kv.n_kv;
+    const int G = n_h / n_kv;
+    const int split = blockIdx.x % splits;
+    const int kvh = (blockIdx.x / splits) % n_kv;
+    const int t = drows[blockIdx.x / (splits * n_kv)];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, tq = lane & 3;
+    const int ctx = row_pos[t] + 1;
+    const int n_chunks = (ctx + kDecChunk - 1) / kDecChunk;
+    const int ch0 = split * n_chunks / splits, ch1 = (split + 1) * n_chunks / splits;
+    const int32_t* pages = flat_pages + row_page_off[t];
+
+    uint32_t qa[KS][4];
+    const float qs = rsqrtf(float(DH)) * 1.4426950408889634f;
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = g + ((i & 1) ? 8 : 0);
+            const int col = kk * 16 + 2 * tq + ((i & 2) ? 8 : 0);
+            float x0 = 0.f, x1 = 0.f;
+            if (r < G) {
+                const __nv_bfloat162 v2 = *reinterpret_cast<const __nv_bfloat162*>(
+                    q + (size_t(t) * n_h + kvh * G + r) * DH + col);
+                x0 = __bfloat162float(v2.x) * qs;
+                x1 = __bfloat162float(v2.y) * qs;
+            }
+            qa[kk][i] = pack2(x0, x1);
+        }
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+    float acc[NT][4];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+
+    const size_t head_k = ((size_t(layer) * 2 + 0) * n_kv + kvh) * 256 * DH;
+    const size_t head_v = ((size_t(layer) * 2 + 1) * n_kv + kvh) * 256 * DH;
+    // this warp's chunks: ch0 + warp, ch0 + warp + 4, ...
+    const int my_n = ch1 - ch0 > warp ? (ch1 - ch0 - warp + kAttnWarps - 1) / kAttnWarps : 0;
+    auto load = [&](int j, int buf) {
+        const int tok0 = (ch0 + warp + j * kAttnWarps) * kDecChunk;
+        const size_t base = size_t(pages[tok0 >> 8]) * kv.page_elems + size_t(tok0 & 255) * DH;
+        const __nv_bfloat16* ksrc = kv.pool + base + head_k;
+        const __nv_bfloat16* vsrc = kv.pool + base + head_v;
+#pragma unroll
+        for (int i = lane; i < kDecChunk * DH / 8; i += 32) {
+            const int r = i / (DH / 8), c = (i % (DH / 8)) * 8;
+            cp_async16(&sm.k[warp][buf][r][c], ksrc + size_t(r) * DH + c);
+            cp_async16(&sm.v[warp][buf][r][c], vsrc + size_t(r) * DH + c);
+        }
+    };
+#pragma unroll
+    for (int j = 0; j < kDecStages - 1; ++j) {
+        if (j < my_n) load(j, j);
+        cp_async_commit();
+    }
+    for (int j = 0; j < my_n; ++j) {
+        const int buf = j % kDecStages;
+        cp_async_wait<kDecStages - 2>();
+        __syncwarp();
+        const int tok0 = (ch0 + warp + j * kAttnWarps) * kDecChunk;
+        const int valid = min(kDecChunk, ctx - tok0);
+        if (valid < kDecChunk) {  // no 0 * garbage = NaN from rows past the context
+            for (int i = lane; i < (kDecChunk - valid) * (DH / 8); i += 32) {
+                const int r = valid + i / (DH / 8), c = (i % (DH / 8)) * 8;
+                *reinterpret_cast<uint4*>(&sm.v[warp][buf][r][c]) = make_uint4(0, 0, 0, 0);
+            }
+            __syncwarp();
+        }
+        float s[2][4];
+#pragma unroll
+        for (int jn = 0; jn < 2; ++jn) {
+            s[jn][0] = s[jn][1] = s[jn][2] = s[jn][3] = 0.f;
+            const uint32_t kbase = smem_u32(&sm.k[warp][buf][0][0]);
+#pragma unroll
+            for (int kk = 0; kk < KS; kk += 2) {
+                const int mi = lane >> 3, rr = lane & 7;
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(kbase + uint32_t(((jn * 8 + rr) * (DH + 8) + kk * 16 + mi * 8) * 2), b0, b1, b2, b3);
+                mma16816(s[jn], qa[kk], b0, b1);
+                mma16816(s[jn], qa[kk + 1], b2, b3);
+            }
+        }
+        float mt[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int jn = 0; jn < 2; ++jn)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int tok = tok0 + jn * 8 + 2 * tq + (e & 1);
+                if (tok >= ctx) s[jn][e] = -INFINITY;
+                mt[e >> 1] = fmaxf(mt[e >> 1], s[jn][e]);
+            }
+        float alpha[2];
+#pragma unroll
+        for (int hr = 0; hr < 2; ++hr) {
+            mt[hr] = fmaxf(mt[hr], __shfl_xor_sync(0xffffffffu, mt[hr], 1));
+            mt[hr] = fmaxf(mt[hr], __shfl_xor_sync(0xffffffffu, mt[hr], 2));
+            const float mn = fmaxf(m_run[hr], mt[hr]);
+            alpha[hr] = mn == -INFINITY ? 1.f : exp2f(m_run[hr] - mn);
+            m_run[hr] = mn;
+        }
+#pragma unroll
+        for (int jn = 0; jn < 2; ++jn)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int hr = e >> 1;
+                s[jn][e] = m_run[hr] == -INFINITY ? 0.f : exp2f(s[jn][e] - m_run[hr]);
+            }
+        float ls[2];
+        ls[0] = s[0][0] + s[0][1] + s[1][0] + s[1][1];
+        ls[1] = s[0][2] + s[0][3] + s[1][2] + s[1][3];
+        l_run[0] = l_run[0] * alpha[0] + ls[0];
+        l_run[1] = l_run[1] * alpha[1] + ls[1];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            acc[nt][0] *= alpha[0];
+            acc[nt][1] *= alpha[0];
+            acc[nt][2] *= alpha[1];
+            acc[nt][3] *= alpha[1];
+        }
+        uint32_t pa[4] = {pack2(s[0][0], s[0][1]), pack2(s[0][2], s[0][3]), pack2(s[1][0], s[1][1]),
+                          pack2(s[1][2], s[1][3])};
+        const uint32_t vbase = smem_u32(&sm.v[warp][buf][0][0]);
+#pragma unroll
+        for (int nt = 0; nt < NT; nt += 2) {
+            const int mi = lane >> 3, rr = lane & 7;
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_t(vbase + uint32_t((((mi & 1) * 8 + rr) * (DH + 8) + (nt + (mi >> 1)) * 8) * 2), b0, b1,
+                      b2, b3);
+            mma16816(acc[nt], pa, b0, b1);
+            mma16816(acc[nt + 1], pa, b2, b3);
+        }
+        __syncwarp();
+        if (j + kDecStages - 1 < my_n) load(j + kDecStages - 1, (j + kDecStages - 1) % kDecStages);
+        cp_async_commit();
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+        l_run[hr] += __shfl_xor_sync(0xffffffffu, l_run[hr], 1);
+        l_run[hr] += __shfl_xor_sync(0xffffffffu, l_run[hr], 2);
+    }
+    // merge the 4 warps' states through shared memory (reusing the K ring)
+    __syncthreads();
+    float* red = reinterpret_cast<float*>(&sm.k[0][0][0][0]);  // [4 warps][16 rows][DH + 2]
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+        const int r = g + 8 * hr;
+        float* dst = red + (warp * 16 + r) * (DH + 2);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            dst[nt * 8 + 2 * tq] = acc[nt][2 * hr];
+            dst[nt * 8 + 2 * tq + 1] = acc[nt][2 * hr + 1];
+        }
+        if (tq == 0) {
+            dst[DH] = m_run[hr];
+            dst[DH + 1] = l_run[hr];
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < G * DH; i += blockDim.x) {
+        const int r = i / DH, dd = i % DH;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, red[(w * 16 + r) * (DH + 2) + DH]);
+        float num = 0.f, den = 0.f;
+#pragma unroll
+        for (int w = 0; w < kAttnWarps; ++w) {
+            const float* src = red + (w * 16 + r) * (DH + 2);
+            const float wt = src[DH] == -INFINITY ? 0.f : exp2f(src[DH] - M);
+            num += src[dd] * wt;
+            den += src[DH + 1] * wt;
+        }
+        const size_t row_head = size_t(t) * n_h + kvh * G + r;
+        if (splits == 1) {
+            o[row_head * DH + dd] = f2bf(num / den);
+        } else {
+            float* dst = ws + (row_head * splits + split) * (DH + 2);
+            dst[dd] = num;
+            if (dd == 0) {
+                dst[DH] = M;
+                dst[DH + 1] = den;
+            }
+        }
+    }
+}
+
 int attention_block_positions(int n_h, int n_kv) { return (kAttnWarps * 16) / (n_h / n_kv); }
 
 int attention_pick_splits(int n_blocks, int n_kv, int max_ctx) {
@@ -363,8 +576,10 @@ int attention_pick_splits(int n_blocks, int n_kv, int max_ctx) {
     return s < 1 ? 1 : s;
 }
 
-int attention_launches(int n_blocks, int n_kv, int max_ctx) {
-    return n_blocks > 0 ? (attention_pick_splits(n_blocks, n_kv, max_ctx) > 1 ? 2 : 1) : 0;
+int attention_launches(int n_blocks, int n_drows, int n_kv, int max_ctx) {
+    if (n_blocks + n_drows <= 0) return 0;
+    return (n_blocks > 0) + (n_drows > 0) +
+           (attention_pick_splits(n_blocks + n_drows, n_kv, max_ctx) > 1 ? 1 : 0);
 }
 
 size_t attention_workspace_floats(int T, int n_h, int d_head, int splits) {
@@ -374,16 +589,16 @@ size_t attention_workspace_floats(int T, int n_h, int d_head, int splits) {
 template <int DH>
 static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,
                    const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
-                   int n_blocks, const KvLayout& kv, int layer, int splits, __nv_bfloat16* o,
-                   float* ws, cudaStream_t stream) {
-    const size_t smem = sizeof(AttnSmem<DH>);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(attn_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr = true;
-    }
-    launch_pdl(attn_tc_kernel<DH>, dim3(n_blocks * kv.n_kv * splits), dim3(kAttnWarps * 32), smem,
-               stream, q, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, splits, o, ws);
+                   int n_blocks, const int32_t* drows, int n_drows, const KvLayout& kv, int layer,
+                   int splits, __nv_bfloat16* o, float* ws, cudaStream_t stream) {
+    if (n_blocks > 0)
+        launch_pdl(attn_tc_kernel<DH>, dim3(n_blocks * kv.n_kv * splits), dim3(kAttnWarps * 32),
+                   sizeof(AttnSmem<DH>), stream, q, n_h, row_pos, row_page_off, flat_pages, blocks, kv,
+                   layer, splits, o, ws);
+    if (n_drows > 0)
+        launch_pdl(attn_decode_kernel<DH>, dim3(n_drows * kv.n_kv * splits), dim3(kAttnWarps * 32),
+                   sizeof(DecSmem<DH>), stream, q, n_h, row_pos, row_page_off, flat_pages, drows, kv,
+                   layer, splits, o, ws);
     if (splits > 1)
         launch_pdl(attn_combine_kernel<DH>, dim3(T * n_h), dim3(DH), 0, stream, (const float*)ws,
                    splits, o);
@@ -391,18 +606,18 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
 
 int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,
                     const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
-                    int n_blocks, const KvLayout& kv, int layer, int max_ctx, __nv_bfloat16* o,
-                    float* ws, size_t ws_floats, cudaStream_t stream) {
-    if (T <= 0 || n_blocks <= 0) return 0;
+                    int n_blocks, const int32_t* drows, int n_drows, const KvLayout& kv, int layer,
+                    int max_ctx, __nv_bfloat16* o, float* ws, size_t ws_floats, cudaStream_t stream) {
+    if (T <= 0 || n_blocks + n_drows <= 0) return 0;
     if (n_h % kv.n_kv != 0 || n_h / kv.n_kv > 16) return -1;
-    int splits = attention_pick_splits(n_blocks, kv.n_kv, max_ctx);
+    int splits = attention_pick_splits(n_blocks + n_drows, kv.n_kv, max_ctx);
     if (splits > 1 && attention_workspace_floats(T, n_h, kv.d_head, splits) > ws_floats) splits = 1;
     if (kv.d_head == 128)
-        launch<128>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, kv, layer, splits,
-                    o, ws, stream);
+        launch<128>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, drows, n_drows, kv,
+                    layer, splits, o, ws, stream);
     else if (kv.d_head == 64)
-        launch<64>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, kv, layer, splits,
-                   o, ws, stream);
+        launch<64>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, drows, n_drows, kv,
+                   layer, splits, o, ws, stream);
     else
         return -2;
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -3;
@@ -421,5 +636,11 @@ void preload_attention() {
                          int(sizeof(AttnSmem<128>)));
     cudaFuncSetAttribute(attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(sizeof(AttnSmem<64>)));
+    cudaFuncGetAttributes(&a, attn_decode_kernel<128>);
+    cudaFuncGetAttributes(&a, attn_decode_kernel<64>);
+    cudaFuncSetAttribute(attn_decode_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(DecSmem<128>)));
+    cudaFuncSetAttribute(attn_decode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(DecSmem<64>)));
 }
 }  // namespace ds

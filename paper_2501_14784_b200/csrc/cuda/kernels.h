@@ -64,15 +64,17 @@ void rope_kv_append(const __nv_bfloat16* qkv, int T, int n_h, int n_kv, int d_he
 
 // Paged causal attention: row t attends positions [0, row_pos[t]] of its request, whose pages
 // are flat_pages[row_page_off[t] ...]. Output o[T, n_h * d_head] bf16.
-// Query blocks: blocks[3*i] = first row, [3*i+1] = consecutive positions (1 for a decode row,
-// <= attention_block_positions() for prompt rows of one request), [3*i+2] = 1 for decode mode.
+// Prompt query blocks: blocks[3*i] = first row, [3*i+1] = consecutive positions
+// (<= attention_block_positions() rows of one request), [3*i+2] = 0. Decode rows (one query
+// position each) are listed separately in drows[] and go to the decode kernel.
 int attention_block_positions(int n_h, int n_kv);
-int attention_launches(int n_blocks, int n_kv, int max_ctx);
+int attention_launches(int n_blocks, int n_drows, int n_kv, int max_ctx);
 size_t attention_workspace_floats(int T, int n_h, int d_head, int splits);
 int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,
                     const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
-                    int n_blocks, const KvLayout& kv, int layer, int max_ctx, __nv_bfloat16* o,
-                    float* ws, size_t ws_floats, cudaStream_t stream);
+                    int n_blocks, const int32_t* drows, int n_drows, const KvLayout& kv, int layer,
+                    int max_ctx, __nv_bfloat16* o, float* ws, size_t ws_floats,
+                    cudaStream_t stream);
 
 // h[t, f] = bf16(bf16(silu(g)) * u) from the gate/up interleaved GEMM output [T, 2*ffn].
 void silu_mul(const __nv_bfloat16* gu, int T, int ffn, __nv_bfloat16* h, cudaStream_t stream);

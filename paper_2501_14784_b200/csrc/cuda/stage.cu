@@ -529,7 +529,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     MbKv& k = s->mbs[mb];
 
     // ---- rows -> pages + metadata (host)
-    int T = 0, R = 0, P = 0, max_ctx = 1, n_blk = 0;
+    int T = 0, R = 0, P = 0, max_ctx = 1, n_blk = 0, n_drow = 0;
     for (int64_t i = 0; i < n_rows; ++i) {
         const ds_row& r = rows[i];
         if (r.slot < 0 || r.slot >= s->max_slots || r.n_tok < 1 || r.pos < 0 ||
@@ -616,18 +616,25 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
             poff += np;
         }
         for (int j = 0; j < prevR; ++j) prev_slot[j] = k.prev_logit_slots[j];
-        // attention query blocks: one per decode row, QP-position chunks of each prompt group
+        // attention work: QP-position query blocks of each prompt group, then the list of
+        // single-position (decode) rows, packed behind the blocks in the same 3*T ints
         const int qp = ds::attention_block_positions(m.n_heads, m.n_kv_heads);
         int tb = 0;
         for (int64_t i = 0; i < n_rows; ++i) {
             const ds_row& rw = rows[i];
-            for (int j = 0; j < rw.n_tok; j += qp) {
-                blk[3 * n_blk] = tb + j;
-                blk[3 * n_blk + 1] = std::min(qp, rw.n_tok - j);
-                blk[3 * n_blk + 2] = rw.n_tok == 1 ? 1 : 0;
-                ++n_blk;
-            }
+            if (rw.n_tok > 1)
+                for (int j = 0; j < rw.n_tok; j += qp) {
+                    blk[3 * n_blk] = tb + j;
+                    blk[3 * n_blk + 1] = std::min(qp, rw.n_tok - j);
+                    blk[3 * n_blk + 2] = 0;
+                    ++n_blk;
+                }
             tb += rw.n_tok;
+        }
+        tb = 0;
+        for (int64_t i = 0; i < n_rows; ++i) {
+            if (rows[i].n_tok == 1) blk[3 * n_blk + n_drow++] = tb;
+            tb += rows[i].n_tok;
         }
     }
     const size_t meta_n = size_t(flat - hm) + P;
@@ -705,9 +712,11 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
                            s->rope_sin, s->kv, li, s->q, st);
         end_other(PK_ELEM, 0, 2.0 * T * qkv_rows + 2.0 * T * (qdim + 2 * m.n_kv_heads * m.d_head), 1);
         begin();
-        rc |= ds::attention_paged(s->q, T, m.n_heads, d_pos, d_poff, d_flat, d_blk, n_blk, s->kv, li, max_ctx,
-                                  s->attn, s->attn_ws, s->attn_ws_floats, st);
-        end_other(PK_ATTN, attn_flops, attn_bytes, ds::attention_launches(n_blk, m.n_kv_heads, max_ctx));
+        rc |= ds::attention_paged(s->q, T, m.n_heads, d_pos, d_poff, d_flat, d_blk, n_blk,
+                                  d_blk + 3 * n_blk, n_drow, s->kv, li, max_ctx, s->attn, s->attn_ws,
+                                  s->attn_ws_floats, st);
+        end_other(PK_ATTN, attn_flops, attn_bytes,
+                  ds::attention_launches(n_blk, n_drow, m.n_kv_heads, max_ctx));
         begin();
         rc |= ds::gemm_bf16(lw.wo, s->attn, T, ds::EPI_RESID, s->x, s->x, nullptr, s->ws,
                             s->ws_floats, 0, st);
