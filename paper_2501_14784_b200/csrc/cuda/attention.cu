@@ -13,6 +13,8 @@
 //
 // HBM roofline: each (block, kv head) reads its request's KV once: ctx * d_head * 2 (K,V) * 2 B
 // per kv head.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -355,20 +357,20 @@ __global__ void attn_combine_kernel(const float* __restrict__ ws, int splits,
 // ------------------------------------------------------------------ decode rows ----
 // One decode row x one KV head x one context split per CTA. The split's context is cut into
 // 16-token chunks dealt round-robin to the 4 warps; every warp streams its chunks through its
-// own kDecStages-deep cp.async ring (no CTA-wide barrier in the loop), computes S = Q.K^T and
+// own ST-deep cp.async ring (no CTA-wide barrier in the loop), computes S = Q.K^T and
 // O += P.V with mma.sync (the G <= 16 query heads of the KV head are the M rows), and the 4
 // partial softmax states merge through shared memory at the end. Memory-level parallelism:
-// 4 warps x kDecStages x 8 KB of K/V in flight per CTA.
+// (ST - 1) x 8 KB of K/V in flight per warp while it computes on the previous chunk.
 constexpr int kDecChunk = 16;
-constexpr int kDecStages = 4;
+constexpr int kDecStages = 2;  // per-warp ring depth; 2 keeps 3 CTAs (12 warps) resident per SM
 
-template <int DH>
+template <int DH, int ST = kDecStages>
 struct DecSmem {
-    __nv_bfloat16 k[kAttnWarps][kDecStages][kDecChunk][DH + 8];
-    __nv_bfloat16 v[kAttnWarps][kDecStages][kDecChunk][DH + 8];
+    __nv_bfloat16 k[kAttnWarps][ST][kDecChunk][DH + 8];
+    __nv_bfloat16 v[kAttnWarps][ST][kDecChunk][DH + 8];
 };
 
-template <int DH>
+template <int DH, int ST = kDecStages>
 __global__ void __launch_bounds__(kAttnWarps * 32)
 attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __restrict__ row_pos,
                    const int32_t* __restrict__ row_page_off, const int32_t* __restrict__ flat_pages,
@@ -377,7 +379,7 @@ attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
     pdl_launch_dependents();
     pdl_wait();
     extern __shared__ __align__(16) uint8_t dec_smem[];
-    DecSmem<DH>& sm = *reinterpret_cast<DecSmem<DH>*>(dec_smem);
+    DecSmem<DH, ST>& sm = *reinterpret_cast<DecSmem<DH, ST>*>(dec_smem);
     constexpr int NT = DH / 8, KS = DH / 16;
     const int n_kv = kv.n_kv;
     const int G = n_h / n_kv;
@@ -430,13 +432,16 @@ attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
         }
     };
 #pragma unroll
-    for (int j = 0; j < kDecStages - 1; ++j) {
+    for (int j = 0; j < ST - 1; ++j) {
         if (j < my_n) load(j, j);
         cp_async_commit();
     }
     for (int j = 0; j < my_n; ++j) {
-        const int buf = j % kDecStages;
-        cp_async_wait<kDecStages - 2>();
+        const int buf = j % ST;
+        // refill the slot chunk j-1 used (consumed: __syncwarp at the end of the last iteration)
+        if (j + ST - 1 < my_n) load(j + ST - 1, (j + ST - 1) % ST);
+        cp_async_commit();
+        cp_async_wait<ST - 1>();
         __syncwarp();
         const int tok0 = (ch0 + warp + j * kAttnWarps) * kDecChunk;
         const int valid = min(kDecChunk, ctx - tok0);
@@ -511,8 +516,6 @@ attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
             mma16816(acc[nt + 1], pa, b2, b3);
         }
         __syncwarp();
-        if (j + kDecStages - 1 < my_n) load(j + kDecStages - 1, (j + kDecStages - 1) % kDecStages);
-        cp_async_commit();
     }
     cp_async_wait<0>();
 #pragma unroll
@@ -586,6 +589,16 @@ size_t attention_workspace_floats(int T, int n_h, int d_head, int splits) {
     return size_t(T) * n_h * splits * (d_head + 2);
 }
 
+// Decode ring depth (DS_ATTN_STAGES=2|3|4 for tuning experiments; default kDecStages).
+static int decode_stages() {
+    static const int st = [] {
+        const char* e = getenv("DS_ATTN_STAGES");
+        const int v = e ? atoi(e) : kDecStages;
+        return (v >= 2 && v <= 4) ? v : kDecStages;
+    }();
+    return st;
+}
+
 template <int DH>
 static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,
                    const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
@@ -595,10 +608,22 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
         launch_pdl(attn_tc_kernel<DH>, dim3(n_blocks * kv.n_kv * splits), dim3(kAttnWarps * 32),
                    sizeof(AttnSmem<DH>), stream, q, n_h, row_pos, row_page_off, flat_pages, blocks, kv,
                    layer, splits, o, ws);
-    if (n_drows > 0)
-        launch_pdl(attn_decode_kernel<DH>, dim3(n_drows * kv.n_kv * splits), dim3(kAttnWarps * 32),
-                   sizeof(DecSmem<DH>), stream, q, n_h, row_pos, row_page_off, flat_pages, drows, kv,
-                   layer, splits, o, ws);
+    if (n_drows > 0) {
+        const dim3 grid(n_drows * kv.n_kv * splits), block(kAttnWarps * 32);
+        switch (decode_stages()) {
+            case 3:
+                launch_pdl(attn_decode_kernel<DH, 3>, grid, block, sizeof(DecSmem<DH, 3>), stream, q,
+                           n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, splits, o, ws);
+                break;
+            case 4:
+                launch_pdl(attn_decode_kernel<DH, 4>, grid, block, sizeof(DecSmem<DH, 4>), stream, q,
+                           n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, splits, o, ws);
+                break;
+            default:
+                launch_pdl(attn_decode_kernel<DH, 2>, grid, block, sizeof(DecSmem<DH, 2>), stream, q,
+                           n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, splits, o, ws);
+        }
+    }
     if (splits > 1)
         launch_pdl(attn_combine_kernel<DH>, dim3(T * n_h), dim3(DH), 0, stream, (const float*)ws,
                    splits, o);
@@ -626,6 +651,14 @@ int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_p
 }  // namespace ds
 
 namespace ds {
+template <int DH, int ST>
+static void preload_decode() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, attn_decode_kernel<DH, ST>);
+    cudaFuncSetAttribute(attn_decode_kernel<DH, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(DecSmem<DH, ST>)));
+}
+
 void preload_attention() {
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, attn_tc_kernel<128>);
@@ -636,11 +669,11 @@ void preload_attention() {
                          int(sizeof(AttnSmem<128>)));
     cudaFuncSetAttribute(attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(sizeof(AttnSmem<64>)));
-    cudaFuncGetAttributes(&a, attn_decode_kernel<128>);
-    cudaFuncGetAttributes(&a, attn_decode_kernel<64>);
-    cudaFuncSetAttribute(attn_decode_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(sizeof(DecSmem<128>)));
-    cudaFuncSetAttribute(attn_decode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(sizeof(DecSmem<64>)));
+    preload_decode<128, 2>();
+    preload_decode<128, 3>();
+    preload_decode<128, 4>();
+    preload_decode<64, 2>();
+    preload_decode<64, 3>();
+    preload_decode<64, 4>();
 }
 }  // namespace ds

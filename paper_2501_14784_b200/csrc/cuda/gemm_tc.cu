@@ -12,11 +12,13 @@
 //   block; each loads half of the activation tile and multicasts it to both (TMA .multicast), so
 //   the per-SM activation traffic from L2 is halved. Each CTA's MMA releases a stage in both
 //   CTAs (tcgen05.commit .multicast::cluster).
-// * Work units = (cluster tile, K split), handed to clusters round-robin (persistent CTAs). Wide
-//   GEMMs (>= one wave of cluster tiles) run unsplit; narrow ones (q/k/v, o, down at 8B) split K
-//   so every SM streams weights, parking fp32 partials that a PDL-chained reduction kernel sums
-//   in split order (deterministic) with the same fused epilogue. (An in-kernel stream-K fixup was
-//   measured slower here: its contributors idle while the tile's last partial lands.)
+// * Persistent clusters, hybrid data-parallel + stream-K schedule: whole waves of cluster tiles
+//   are dealt one per cluster; the remaining (tile, k-block) iteration space is cut into equal
+//   contiguous ranges, one per cluster, so every SM streams the same number of weight bytes.
+//   A tile split across clusters is finished by its LAST-arriving CTA (per-tile arrival counter):
+//   the others park fp32 pieces in a workspace slot and move on; nobody waits, and the finisher
+//   sums the pieces in k order (deterministic) into the fused epilogue. (A designated-owner fixup
+//   and a separate split-K reduction kernel were both measured slower.)
 // * TMEM holds two accumulators when the token block fits 256 columns, so a unit's epilogue
 //   overlaps the next unit's MMAs.
 // * Epilogue: tcgen05.ld -> shared-memory transpose -> 16-byte coalesced stores, fused
@@ -41,7 +43,9 @@ constexpr int kMaxTB = 512;   // tokens per block (TMEM columns)
 constexpr int kGemmThreads = 256;
 constexpr int kSmemBudget = 222 * 1024;
 constexpr int kStageStride = 36;  // floats per row of the epilogue transpose buffer
-constexpr size_t kWorkspaceFloats = size_t(16) << 20;  // split-K partials
+constexpr size_t kWorkspaceFloats = size_t(24) << 20;  // arrival counters + stream-K pieces
+constexpr size_t kCounterInts = size_t(64) << 10;
+constexpr int kFixedSmem = 4 * 16 * kStageStride * 4 + 256 + 1024;  // transpose buffers, barriers, align
 
 struct GemmParams {
     int T, N, K;
@@ -53,14 +57,18 @@ struct GemmParams {
     int stages;
     int n_acc;    // TMEM accumulators
     int KB;       // k-blocks per tile
-    int splits;   // K splits per tile
     int n_clusters;
-    int units;    // cluster tiles x splits
+    int dp_rounds;  // whole-tile rounds (tile = round * n_clusters + cluster)
+    int sk_tiles;   // tiles after the data-parallel rounds, shared out by k-block ranges
+    int n_sk;       // clusters taking a stream-K range (<= sk_tiles * KB: no empty range)
+    int defer;      // 1: split tiles are summed by splitk_finish_kernel instead of the last arriver
+    int planes;     // > 0: aligned narrow GEMM, partials in [planes][T][N] for splitk_reduce_kernel
     int epi;
     __nv_bfloat16* out_bf16;
     const __nv_bfloat16* resid;
     float* out_f32;
-    float* partial;  // [splits][T][N] fp32 when splits > 1
+    float* slots;   // [n_clusters][2][CN][tb_pad][128] fp32 pieces of split tiles
+    int* counters;  // [tiles][CN] arrivals (self-resetting)
     unsigned long long* trace;  // optional per-CTA phase timestamps (gemm_set_trace)
 };
 
@@ -101,32 +109,47 @@ DS_DEVICE void umma_commit_mc(uint64_t* bar, uint16_t mask) {
         : "memory");
 }
 
-// A unit: cluster tile ut (token block x feature pair) and its K range [kb0, kb1).
-struct Unit {
-    int ut, split, kb0, kb1;
+// A segment: cluster tile ut, k-blocks [kb0, kb1), and (stream-K part) which of this cluster's two
+// piece slots it would use.
+struct Seg {
+    int ut, kb0, kb1, which;
 };
-DS_DEVICE Unit unit_of(const GemmParams& p, int u) {
-    Unit x;
-    x.ut = u / p.splits;
-    x.split = u % p.splits;
-    x.kb0 = x.split * p.KB / p.splits;
-    x.kb1 = (x.split + 1) * p.KB / p.splits;
-    return x;
+// Stream-K range of cluster c over the sk_tiles * KB iteration space.
+DS_DEVICE int sk_begin(const GemmParams& p, int c) {
+    return int((long long)c * p.sk_tiles * p.KB / p.n_sk);
+}
+// Cluster whose stream-K range holds iteration g.
+DS_DEVICE int sk_owner(const GemmParams& p, int g) {
+    const long long G = (long long)p.sk_tiles * p.KB;
+    return int(((long long)(g + 1) * p.n_sk + G - 1) / G) - 1;
+}
+// Iterates this cluster's segments: its stream-K range over tiles [0, sk_tiles) first (so split
+// tiles are finished while the data-parallel tiles stream), then one tile per data-parallel round.
+template <typename F>
+DS_DEVICE void for_each_seg(const GemmParams& p, int cluster, F&& f) {
+    if (cluster < p.n_sk) {
+        const int g0 = sk_begin(p, cluster), g1 = sk_begin(p, cluster + 1);
+        for (int g = g0; g < g1;) {
+            const int t = g / p.KB, kb0 = g % p.KB;
+            const int kb1 = min(p.KB, kb0 + (g1 - g));
+            f(Seg{t, kb0, kb1, g == g0 ? 0 : 1});
+            g += kb1 - kb0;
+        }
+    }
+    for (int r = 0; r < p.dp_rounds; ++r) f(Seg{p.sk_tiles + r * p.n_clusters + cluster, 0, p.KB, 0});
 }
 
-// Applies the epilogue to 16 consecutive token columns of one 32-feature slice held as vals[16]
-// (this thread's feature, columns c0..c0+15), through a per-warp transpose buffer.
-DS_DEVICE void epilogue16(const GemmParams& p, int epi, float* out_f32, float* stage,
-                          const float* vals, int lane, int t0, int c0, int t_here, int f_base) {
+// Transposes 16 consecutive token columns of one 32-feature slice (vals[16]: this thread's
+// feature, columns c0..c0+15) through a per-warp buffer: afterwards the thread holds token row
+// lane/2, features (lane&1)*16 .. +15 of the slice in v[16]. Returns false for padding rows.
+DS_DEVICE bool transpose16(float* stage, const float* vals, int lane, int c0, int t_here, float* v) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) stage[j * kStageStride + lane] = vals[j];
     __syncwarp();
     const int row = lane >> 1, half = lane & 1;
-    if (c0 + row < t_here) {
-        const int t = t0 + c0 + row;
-        const int f0 = f_base + half * 16;
+    const bool ok = c0 + row < t_here;
+    if (ok) {
         const float4* src = reinterpret_cast<const float4*>(stage + row * kStageStride + half * 16);
-        float v[16];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const float4 x = src[i];
@@ -135,29 +158,82 @@ DS_DEVICE void epilogue16(const GemmParams& p, int epi, float* out_f32, float* s
             v[4 * i + 2] = x.z;
             v[4 * i + 3] = x.w;
         }
-        const size_t o = size_t(t) * p.N + f0;
-        if (epi == EPI_F32) {
-            float4* dst = reinterpret_cast<float4*>(out_f32 + o);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        } else {
-            if (epi == EPI_RESID) {
-                float r[16];
-                unpack8(reinterpret_cast<const uint4*>(p.resid + o)[0], r);
-                unpack8(reinterpret_cast<const uint4*>(p.resid + o)[1], r + 8);
-#pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = r[j] + round_bf(v[j]);
-            }
-            uint4* dst = reinterpret_cast<uint4*>(p.out_bf16 + o);
-            dst[0] = pack8(v);
-            dst[1] = pack8(v + 8);
-        }
     }
     __syncwarp();
+    return ok;
+}
+
+// Final epilogue of 16 features f0.. of token row t: bf16 / residual-add / fp32 store.
+DS_DEVICE void store16(const GemmParams& p, float* v, int t, int f0) {
+    const size_t o = size_t(t) * p.N + f0;
+    if (p.epi == EPI_F32) {
+        float4* dst = reinterpret_cast<float4*>(p.out_f32 + o);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        return;
+    }
+    if (p.epi == EPI_RESID) {
+        float r[16];
+        unpack8(reinterpret_cast<const uint4*>(p.resid + o)[0], r);
+        unpack8(reinterpret_cast<const uint4*>(p.resid + o)[1], r + 8);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = r[j] + round_bf(v[j]);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(p.out_bf16 + o);
+    dst[0] = pack8(v);
+    dst[1] = pack8(v + 8);
+}
+
+DS_DEVICE void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Piece slot of cluster c for the split tile starting at k-block tile_g0 (its first or last
+// stream-K segment), plus this thread's offset.
+DS_DEVICE const float* piece_ptr(const GemmParams& p, int cn, int rank, int c, int tile_g0, size_t off) {
+    const int which = sk_begin(p, c) >= tile_g0 ? 0 : 1;
+    return p.slots + ((size_t(c) * 2 + which) * cn + rank) * (size_t(p.tb_pad) * kBM) + off;
+}
+
+// sum[16] = the 16 values at `off` of every piece of a split tile, added in cluster (= k) order;
+// the finishing cluster `self` contributes `own` (its TMEM values) at its position; kPieceBatch
+// pieces' loads are in flight at a time.
+constexpr int kPieceBatch = 2;
+DS_DEVICE void sum_pieces(const GemmParams& p, int cn, int rank, int tile_g0, int c_lo, int c_hi,
+                          size_t off, int self, const float* own, float* sum) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sum[j] = 0.f;
+    for (int cb = c_lo; cb <= c_hi; cb += kPieceBatch) {
+        float4 x[kPieceBatch][4];
+#pragma unroll
+        for (int i = 0; i < kPieceBatch; ++i) {
+            const int c = cb + i;
+            if (c <= c_hi && c != self) {
+                const float4* src = reinterpret_cast<const float4*>(piece_ptr(p, cn, rank, c, tile_g0, off));
+#pragma unroll
+                for (int k = 0; k < 4; ++k) x[i][k] = __ldcg(src + k);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kPieceBatch; ++i) {
+            const int c = cb + i;
+            if (c > c_hi) break;
+            if (c == self) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) sum[j] += own[j];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    sum[4 * k] += x[i][k].x;
+                    sum[4 * k + 1] += x[i][k].y;
+                    sum[4 * k + 2] += x[i][k].z;
+                    sum[4 * k + 3] += x[i][k].w;
+                }
+            }
+        }
+    }
 }
 
 template <int CN>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __maxnreg__(168)  // leaves registers for the co-resident finish kernel
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
                const GemmParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -208,19 +284,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
             const uint16_t mask = (1u << CN) - 1;
             // weights first (independent of the previous kernel), activations after pdl_wait
             int pre = 0;
-            for (int u = cluster; u < p.units && pre < p.stages; u += p.n_clusters) {
-                const Unit w = unit_of(p, u);
+            for_each_seg(p, cluster, [&](const Seg& w) {
                 const int mt = (w.ut % cl_tiles) * CN + int(rank);
                 for (int kb = w.kb0; kb < w.kb1 && pre < p.stages; ++kb, ++pre) {
                     mbar_arrive_expect_tx(&full_bar[pre], stage_bytes);
                     tma_load_2d_hint(smem + pre * stage_bytes, &tmap_w, &full_bar[pre], kb * kBK,
                                      mt * kBM, pol_w);
                 }
-            }
+            });
             pdl_wait();
             int i = 0;
-            for (int u = cluster; u < p.units; u += p.n_clusters) {
-                const Unit w = unit_of(p, u);
+            for_each_seg(p, cluster, [&](const Seg& w) {
                 const int tbk = w.ut / cl_tiles;
                 const int mt = (w.ut % cl_tiles) * CN + int(rank);
                 for (int kb = w.kb0; kb < w.kb1; ++kb, ++i) {
@@ -239,7 +313,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                     else
                         tma_load_2d(sb, &tmap_x, &full_bar[s], kb * kBK, tbk * p.tb);
                 }
-            }
+            });
             GEMM_TRACE(1);
             // drain: every stage released by every CTA (no remote arrival after we exit)
             const int n = i;
@@ -248,8 +322,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         }
     } else if (warp == 1) {
         int i = 0, seg = 0;
-        for (int u = cluster; u < p.units; u += p.n_clusters, ++seg) {
-            const Unit w = unit_of(p, u);
+        for_each_seg(p, cluster, [&](const Seg& w) {
             const int tbk = w.ut / cl_tiles;
             const int t_here = min(p.tb, p.T - tbk * p.tb);
             const int a = seg % p.n_acc;
@@ -282,37 +355,101 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                 }
                 __syncwarp();
             }
-        }
+            ++seg;
+        });
         if (lane == 0) GEMM_TRACE(2);
     } else if (warp >= 4) {
         pdl_wait();
         const int q = warp & 3;
         float* stage = ep_stage + q * 16 * kStageStride;
+        volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+        const int row = lane >> 1, half = lane & 1;
+        const size_t slot_elems = size_t(p.tb_pad) * kBM;
         int seg = 0;
-        for (int u = cluster; u < p.units; u += p.n_clusters, ++seg) {
-            const Unit w = unit_of(p, u);
+        for_each_seg(p, cluster, [&](const Seg& w) {
             const int tbk = w.ut / cl_tiles;
             const int mt = (w.ut % cl_tiles) * CN + int(rank);
             const int t0 = tbk * p.tb;
             const int t_here = min(p.tb, p.T - t0);
             const int a = seg % p.n_acc;
             const uint32_t acc = tmem_base + uint32_t(a * 256) + (uint32_t(q * 32) << 16);
+            const int f_slice = mt * kBM + q * 32;
             mbar_wait(&tfull_bar[a], (seg / p.n_acc) & 1);
             tc_fence_after();
-            // unsplit: the fused epilogue; split: an fp32 partial into its split plane
-            const int epi = p.splits > 1 ? EPI_F32 : p.epi;
-            float* out_f32 = p.splits > 1 ? p.partial + size_t(w.split) * p.T * p.N : p.out_f32;
-            for (int c0 = 0; c0 < t_here; c0 += 16) {
-                uint32_t r[16];
-                tmem_ld16(acc + c0, r);
-                tmem_ld_wait();
-                epilogue16(p, epi, out_f32, stage, reinterpret_cast<float*>(r), lane, t0, c0, t_here,
-                           mt * kBM + q * 32);
+            float v[16];
+            uint32_t r[16];
+            if (w.kb0 == 0 && w.kb1 == p.KB) {  // whole tile: fused epilogue straight from TMEM
+                for (int c0 = 0; c0 < t_here; c0 += 16) {
+                    tmem_ld16(acc + c0, r);
+                    tmem_ld_wait();
+                    if (transpose16(stage, reinterpret_cast<float*>(r), lane, c0, t_here, v))
+                        store16(p, v, t0 + c0 + row, f_slice + half * 16);
+                }
+            } else {
+                // split tile: park this piece (TMEM-native layout [chunk][feature][16 tokens]: each
+                // thread stores / loads its own 64 contiguous bytes), count the arrival; the last
+                // arriver sums all pieces in k order (deterministic) and runs the epilogue.
+                if (p.planes) {  // narrow GEMM: fp32 partial into plane (k range) [T][N]
+                    float* plane = p.slots + size_t(cluster % p.planes) * p.T * p.N;
+                    for (int c0 = 0; c0 < t_here; c0 += 16) {
+                        tmem_ld16(acc + c0, r);
+                        tmem_ld_wait();
+                        if (transpose16(stage, reinterpret_cast<float*>(r), lane, c0, t_here, v)) {
+                            float4* dst = reinterpret_cast<float4*>(plane + size_t(t0 + c0 + row) * p.N +
+                                                                    f_slice + half * 16);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                __stcg(dst + i, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+                        }
+                    }
+                    goto seg_done;  // planes summed by splitk_reduce_kernel
+                }
+                const size_t fo = size_t(q * 32 + lane) * 16;
+                const int n_chunks = (t_here + 15) / 16;
+                float* mine = p.slots + ((size_t(cluster) * 2 + w.which) * CN + rank) * slot_elems;
+                for (int ch = 0; ch < n_chunks; ++ch) {
+                    tmem_ld16(acc + ch * 16, r);
+                    tmem_ld_wait();
+                    float4* dst = reinterpret_cast<float4*>(mine + size_t(ch) * kBM * 16 + fo);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        __stcg(dst + i, make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                                    __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3])));
+                }
+                if (p.defer) goto seg_done;  // pieces summed by splitk_finish_kernel
+                __threadfence();
+                epi_bar();
+                const int tile_g0 = w.ut * p.KB;
+                const int c_lo = sk_owner(p, tile_g0), c_hi = sk_owner(p, tile_g0 + p.KB - 1);
+                if (threadIdx.x == 128) {
+                    int* cnt = p.counters + size_t(w.ut) * CN + rank;
+                    const int old = atomicAdd(cnt, 1);
+                    const int last = old == c_hi - c_lo;
+                    if (last) *cnt = 0;  // ready for the next launch
+                    *last_flag = last;
+                }
+                epi_bar();
+                const bool last = *last_flag != 0;
+                epi_bar();  // flag read by all before the next segment rewrites it
+                if (last) {
+                    __threadfence();
+                    for (int ch = 0; ch < n_chunks; ++ch) {
+                        float own[16], sum[16];
+                        tmem_ld16(acc + ch * 16, reinterpret_cast<uint32_t*>(own));
+                        tmem_ld_wait();
+                        sum_pieces(p, CN, rank, tile_g0, c_lo, c_hi, size_t(ch) * kBM * 16 + fo, cluster,
+                                   own, sum);
+                        if (transpose16(stage, sum, lane, ch * 16, t_here, v))
+                            store16(p, v, t0 + ch * 16 + row, f_slice + half * 16);
+                    }
+                }
             }
+        seg_done:
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty_bar[a]);
-        }
+            ++seg;
+        });
         if (threadIdx.x == 128) GEMM_TRACE(3);
     }
     __syncthreads();
@@ -323,44 +460,72 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
     }
 }
 
-// Split-K reduction: splits summed in order (deterministic) + the same epilogues.
-__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int T, int N, int epi,
-                                     __nv_bfloat16* out_bf16, const __nv_bfloat16* resid,
-                                     float* out_f32) {
+// Deferred stream-K finish: block = (split tile, CTA rank, 16-token chunk); sums the tile's pieces
+// in k order (same order as the in-kernel last arriver) and applies the fused epilogue. Spreads
+// the reduction of narrow GEMMs (every tile split) over all SMs.
+template <int CN>
+__global__ void __launch_bounds__(128) splitk_finish_kernel(const GemmParams p) {
     pdl_launch_dependents();
     pdl_wait();
-    const size_t total = size_t(T) * N / 4;
-    const size_t plane = size_t(T) * N;
+    __shared__ float stage_all[4][16 * kStageStride];
+    const int n_chunks = (p.tb + 15) / 16;
+    const int ch = blockIdx.x % n_chunks;
+    const int rank = (blockIdx.x / n_chunks) % CN;
+    const int ut = blockIdx.x / (n_chunks * CN);
+    const int cl_tiles = p.m_tiles / CN;
+    const int tbk = ut / cl_tiles;
+    const int mt = (ut % cl_tiles) * CN + rank;
+    const int t0 = tbk * p.tb;
+    const int t_here = min(p.tb, p.T - t0);
+    if (ch * 16 >= t_here) return;
+    const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile_g0 = ut * p.KB;
+    const int c_lo = sk_owner(p, tile_g0), c_hi = sk_owner(p, tile_g0 + p.KB - 1);
+    if (c_lo == c_hi) return;  // one cluster covered the whole tile and finished it in-kernel
+    float sum[16], v[16];
+    sum_pieces(p, CN, rank, tile_g0, c_lo, c_hi, size_t(ch) * kBM * 16 + size_t(q * 32 + lane) * 16, -1,
+               nullptr, sum);
+    if (transpose16(stage_all[q], sum, lane, ch * 16, t_here, v))
+        store16(p, v, t0 + ch * 16 + (lane >> 1), mt * kBM + q * 32 + (lane & 1) * 16);
+}
+
+// Narrow-GEMM reduction: the k-range planes summed in order (deterministic) + the fused epilogue,
+// grid-stride over float4s of [T][N] (no shared memory: co-resides with the GEMM CTAs and waits
+// at griddepcontrol.wait, so it runs the moment the GEMM retires).
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const GemmParams p) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const size_t total = size_t(p.T) * p.N / 4;
+    const size_t plane = size_t(p.T) * p.N;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
          i += size_t(gridDim.x) * blockDim.x) {
-        float4 acc = reinterpret_cast<const float4*>(ws)[i];
-        for (int s = 1; s < splits; ++s) {
-            const float4 v = reinterpret_cast<const float4*>(ws + s * plane)[i];
-            acc.x += v.x;
-            acc.y += v.y;
-            acc.z += v.z;
-            acc.w += v.w;
+        float4 a = __ldcg(reinterpret_cast<const float4*>(p.slots) + i);
+        for (int k = 1; k < p.planes; ++k) {
+            const float4 b = __ldcg(reinterpret_cast<const float4*>(p.slots + k * plane) + i);
+            a.x += b.x;
+            a.y += b.y;
+            a.z += b.z;
+            a.w += b.w;
         }
         const size_t o = i * 4;
-        if (epi == EPI_F32) {
-            reinterpret_cast<float4*>(out_f32)[i] = acc;
-        } else {
-            float a[4] = {acc.x, acc.y, acc.z, acc.w};
-            if (epi == EPI_RESID) {
-                const uint2 rv = *reinterpret_cast<const uint2*>(resid + o);
-                const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
-                const float2 r0 = __bfloat1622float2(rh[0]);
-                const float2 r1 = __bfloat1622float2(rh[1]);
-                a[0] = r0.x + round_bf(a[0]);
-                a[1] = r0.y + round_bf(a[1]);
-                a[2] = r1.x + round_bf(a[2]);
-                a[3] = r1.y + round_bf(a[3]);
-            }
-            uint2 ov;
-            ov.x = pack2(a[0], a[1]);
-            ov.y = pack2(a[2], a[3]);
-            *reinterpret_cast<uint2*>(out_bf16 + o) = ov;
+        if (p.epi == EPI_F32) {
+            reinterpret_cast<float4*>(p.out_f32)[i] = a;
+            continue;
         }
+        float v[4] = {a.x, a.y, a.z, a.w};
+        if (p.epi == EPI_RESID) {
+            const uint2 rv = *reinterpret_cast<const uint2*>(p.resid + o);
+            const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
+            const float2 r0 = __bfloat1622float2(rh[0]), r1 = __bfloat1622float2(rh[1]);
+            v[0] = r0.x + round_bf(v[0]);
+            v[1] = r0.y + round_bf(v[1]);
+            v[2] = r1.x + round_bf(v[2]);
+            v[3] = r1.y + round_bf(v[3]);
+        }
+        uint2 ov;
+        ov.x = pack2(v[0], v[1]);
+        ov.y = pack2(v[2], v[3]);
+        *reinterpret_cast<uint2*>(p.out_bf16 + o) = ov;
     }
 }
 
@@ -399,27 +564,68 @@ int make_tmap_2d_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t 
 
 size_t gemm_workspace_floats() { return kWorkspaceFloats; }
 
-// launches issued by gemm_bf16 for this shape (1, or 2 with the split-K reduction)
-int gemm_launch_count(int T, int N, int K);
-
-static int pick_splits(int T, int N, int K, int cn, int n_clusters) {
-    const int tiles = ((T + kMaxTB - 1) / kMaxTB) * (N / kBM / cn);
-    if (tiles >= n_clusters) return 1;
-    int s = n_clusters / tiles;
-    s = std::min(s, 8);
-    s = std::min(s, (K / kBK) / 4);
-    while (s > 1 && size_t(s) * T * N > kWorkspaceFloats) --s;
-    return std::max(s, 1);
-}
-
 static int pick_cn(int N) {
     static const int cn_env = getenv("DS_GEMM_CN") ? atoi(getenv("DS_GEMM_CN")) : 2;
     return (cn_env == 1 || (N / kBM) % 2 != 0) ? 1 : 2;
 }
 
+static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out);
+
 int gemm_launch_count(int T, int N, int K) {
-    const int cn = pick_cn(N);
-    return pick_splits(T, N, K, cn, kNumSMs / cn) > 1 ? 2 : 1;
+    int cn = 0;
+    const GemmParams p = plan_gemm(T, N, K, 0, &cn);
+    return 1 + p.defer;
+}
+
+// Tile shape, pipeline depth and the data-parallel / stream-K partition of one GEMM (a negative
+// p.T is the error code of an unsupported shape).
+static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) {
+    GemmParams p{};
+    int cn = pick_cn(N);
+    p.T = T;
+    p.N = N;
+    p.K = K;
+    if (K % kBK != 0 || N % kBM != 0) { p.T = -3; return p; }
+    p.m_tiles = N / kBM;
+    p.t_blocks = (T + kMaxTB - 1) / kMaxTB;
+    p.tb = T < kMaxTB ? T : kMaxTB;
+    p.tb_pad = (p.tb + 15) & ~15;
+    if (cn == 1 && p.tb_pad > 256) cn = (p.m_tiles % 2 == 0) ? 2 : 1;  // TMA box rows <= 256
+    if (cn == 1 && p.tb_pad > 256) { p.T = -9; return p; }
+    p.brows = p.tb_pad / cn;
+    p.KB = K / kBK;
+    const int stage_bytes = kBM * kBK * 2 + p.tb_pad * kBK * 2;
+    p.stages = (kSmemBudget - kFixedSmem) / stage_bytes;
+    if (p.stages > 12) p.stages = 12;
+    if (p.stages < 2) { p.T = -4; return p; }
+    p.n_acc = p.tb_pad <= 256 ? 2 : 1;
+    int nc = kNumSMs / cn;
+    if (max_clusters > 0 && nc > max_clusters) nc = max_clusters;
+    const int tiles = p.t_blocks * (p.m_tiles / cn);
+    // whole waves data-parallel, the remainder stream-K over all clusters
+    static const bool no_sk = getenv("DS_GEMM_NOSK") != nullptr;  // debug: whole tiles only
+    p.n_clusters = std::min(nc, no_sk ? tiles : tiles * p.KB);
+    p.dp_rounds = tiles / p.n_clusters;
+    p.sk_tiles = tiles - p.dp_rounds * p.n_clusters;
+    p.n_sk = std::min(p.n_clusters, p.sk_tiles * p.KB);
+    static const int align_env = getenv("DS_GEMM_ALIGN") ? atoi(getenv("DS_GEMM_ALIGN")) : 1;
+    if (align_env && p.dp_rounds == 0 && p.sk_tiles * 2 <= p.n_sk) {
+        // narrow GEMM: every tile split into the same number of k ranges, one piece per cluster
+        // (no range straddles two tiles: half the pieces of a free partition, a few idle SMs)
+        p.n_sk = p.sk_tiles * std::min(p.n_sk / p.sk_tiles, p.KB);
+        p.n_clusters = p.n_sk;
+        // one plane per k range while they fit the workspace (else TMEM-layout pieces)
+        if (size_t(p.n_sk / p.sk_tiles) * T * N <= kWorkspaceFloats - kCounterInts)
+            p.planes = p.n_sk / p.sk_tiles;
+    }
+    // single TMEM accumulator: the remainder tiles run whole (a last arriver's reads would stall
+    // the next tile's MMAs), i.e. n_sk = sk_tiles gives every remainder cluster one whole tile
+    if (p.dp_rounds > 0 && p.tb_pad > 256) p.n_sk = p.sk_tiles;
+    // the in-kernel last arriver pays off when its reads overlap the next tile's MMAs (data-
+    // parallel tiles follow, accumulator double-buffered); otherwise a finish kernel spreads them
+    p.defer = (p.sk_tiles > 0 && p.dp_rounds == 0) ? 1 : 0;
+    *cn_out = cn;
+    return p;
 }
 
 int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_bfloat16* out_bf16,
@@ -427,38 +633,25 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
               int max_clusters, cudaStream_t stream) {
     const int N = w.N, K = w.K;
     if (T <= 0) return 0;
-    int cn = pick_cn(N);
-    if (K % kBK != 0 || N % kBM != 0) return -3;
-    GemmParams p{};
-    p.T = T;
-    p.N = N;
-    p.K = K;
-    p.m_tiles = N / kBM;
-    p.t_blocks = (T + kMaxTB - 1) / kMaxTB;
-    p.tb = T < kMaxTB ? T : kMaxTB;
-    p.tb_pad = (p.tb + 15) & ~15;
-    if (cn == 1 && p.tb_pad > 256) cn = (p.m_tiles % 2 == 0) ? 2 : 1;  // TMA box rows <= 256
-    if (cn == 1 && p.tb_pad > 256) return -9;
-    p.brows = p.tb_pad / cn;
-    p.KB = K / kBK;
-    const int stage_bytes = kBM * kBK * 2 + p.tb_pad * kBK * 2;
-    const int fixed = 4 * 16 * kStageStride * 4 + 256 + 1024;
-    p.stages = (kSmemBudget - fixed) / stage_bytes;
-    if (p.stages > 12) p.stages = 12;
-    if (p.stages < 2) return -4;
-    p.n_acc = p.tb_pad <= 256 ? 2 : 1;
-    int nc = kNumSMs / cn;
-    if (max_clusters > 0 && nc > max_clusters) nc = max_clusters;
-    p.splits = pick_splits(T, N, K, cn, nc);
-    if (p.splits > 1 && (!workspace || workspace_floats < size_t(p.splits) * T * N)) p.splits = 1;
+    int cn = 1;
+    GemmParams p = plan_gemm(T, N, K, max_clusters, &cn);
+    if (p.T < 0) return p.T;
     const int tiles = p.t_blocks * (p.m_tiles / cn);
-    p.units = tiles * p.splits;
-    p.n_clusters = std::min(nc, p.units);
+    const int stage_bytes = kBM * kBK * 2 + p.tb_pad * kBK * 2;
+    const int fixed = kFixedSmem;
+    // workspace: [counters: kCounterInts, shared by every shape: a launch leaves them all 0]
+    //            [slots: n_clusters * 2 * cn * tb_pad * 128 floats]
+    const size_t n_cnt = kCounterInts;
+    const size_t need = n_cnt + (p.planes ? size_t(p.planes) * T * N
+                                          : size_t(p.n_clusters) * 2 * cn * p.tb_pad * kBM);
+    if (p.sk_tiles > 0 && (!workspace || workspace_floats < need || size_t(tiles) * cn > n_cnt))
+        return -7;
     p.epi = epi;
     p.out_bf16 = out_bf16;
     p.resid = resid;
     p.out_f32 = out_f32;
-    p.partial = workspace;
+    p.counters = reinterpret_cast<int*>(workspace);
+    p.slots = workspace + n_cnt;
     p.trace = g_gemm_trace;
     alignas(64) CUtensorMap tx;
     if (make_tmap_2d_bf16(&tx, x, T, K, p.brows, kBK) != 0) return -5;
@@ -481,12 +674,16 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
     cudaError_t e = cn == 2 ? cudaLaunchKernelEx(&cfg, gemm_tc_kernel<2>, tw, tx, p)
                             : cudaLaunchKernelEx(&cfg, gemm_tc_kernel<1>, tw, tx, p);
     if (e != cudaSuccess) return -6;
-    if (p.splits > 1) {
+    static const bool no_finish = getenv("DS_GEMM_NOFINISH") != nullptr;  // debug: timing only
+    if (p.planes && !no_finish) {
         const size_t total4 = size_t(T) * N / 4;
-        int blocks = int((total4 + 255) / 256);
-        if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
-        e = launch_pdl(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, stream, (const float*)workspace,
-                       p.splits, T, N, epi, out_bf16, resid, out_f32);
+        const int blocks = int(std::min<size_t>((total4 + 255) / 256, size_t(kNumSMs) * 8));
+        e = launch_pdl(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, stream, p);
+        if (e != cudaSuccess) return -6;
+    } else if (p.defer && !no_finish) {
+        const dim3 grid(p.sk_tiles * cn * ((p.tb + 15) / 16));
+        e = cn == 2 ? launch_pdl(splitk_finish_kernel<2>, grid, dim3(128), 0, stream, p)
+                    : launch_pdl(splitk_finish_kernel<1>, grid, dim3(128), 0, stream, p);
         if (e != cudaSuccess) return -6;
     }
     return 0;
@@ -506,6 +703,8 @@ void preload_gemm() {
     cudaFuncGetAttributes(&a, gemm_tc_kernel<1>);
     cudaFuncGetAttributes(&a, gemm_tc_kernel<2>);
     cudaFuncGetAttributes(&a, splitk_reduce_kernel);
+    cudaFuncGetAttributes(&a, splitk_finish_kernel<1>);
+    cudaFuncGetAttributes(&a, splitk_finish_kernel<2>);
     cudaFuncSetAttribute(gemm_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
     cudaFuncSetAttribute(gemm_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
 }

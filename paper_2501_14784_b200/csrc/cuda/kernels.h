@@ -12,7 +12,6 @@ enum GemmEpilogue : int {
     EPI_BF16 = 0,     // out = bf16(acc)
     EPI_RESID = 1,    // out = bf16(resid + bf16(acc))   (residual add fused; out may alias resid)
     EPI_F32 = 2,      // out = acc (fp32, logits)
-    EPI_PARTIAL = 3,  // internal: split-K fp32 partial
 };
 
 // A weight matrix [N, K] (row-major, K contiguous) with its TMA descriptor.
@@ -23,17 +22,17 @@ struct GemmWeight {
 };
 
 int gemm_weight_init(GemmWeight* w, const __nv_bfloat16* data, int N, int K);
-// Stream-K partials + per-tile counters; allocate once, zero-initialised, one per stream.
+// Stream-K pieces + per-tile arrival counters; allocate once, zero-initialised, one per stream.
 size_t gemm_workspace_floats();
 // Debug: per-CTA phase timestamps (globaltimer ns, 8 slots per CTA) for subsequent launches.
 void gemm_set_trace(unsigned long long* device_buf);
-// Kernel launches gemm_bf16 issues for a shape (2 when K is split and reduced).
+// Kernel launches gemm_bf16 issues for a shape (always 1: split tiles finish in-kernel).
 int gemm_launch_count(int T, int N, int K);
 // out[T, N] = epi(X[T, K] . W[N, K]^T). max_clusters > 0 caps the 2-CTA clusters (tests use it
-// to force tiles split across clusters); 0 = all SMs.
+// to force other data-parallel / stream-K partitions); 0 = all SMs.
 int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_bfloat16* out_bf16,
               const __nv_bfloat16* resid, float* out_f32, float* workspace, size_t workspace_floats,
-              int k_splits, cudaStream_t stream);
+              int max_clusters, cudaStream_t stream);
 
 // Counter-based weight init (bf16(uniform(-1,1) * scale)); see oracle/llama_ref.c ds_ref_weight.
 // If interleave64 != 0 the [rows, cols] tensor is written into the gate/up interleaved

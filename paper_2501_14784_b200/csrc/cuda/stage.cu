@@ -954,23 +954,28 @@ ds_status ds_dbg_gemm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t N
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return ds_fail(DS_ERR_NO_DEVICE, "no CUDA device");
     ds::preload_all();
-    bf16 *dx = nullptr, *dw = nullptr, *dout = nullptr;
+    bf16 *dx = nullptr, *dw = nullptr, *dout = nullptr, *dres = nullptr;
     float *dws = nullptr, *df = nullptr;
     const size_t out_elems = size_t(T) * N;
     CK(cudaMalloc(&dx, size_t(T) * K * 2));
     CK(cudaMalloc(&dw, size_t(N) * K * 2));
     CK(cudaMalloc(&dout, out_elems * 2));
+    CK(cudaMalloc(&dres, out_elems * 2));
     CK(cudaMalloc(&df, out_elems * 4));
     const size_t wsf = ds::gemm_workspace_floats();
     CK(cudaMalloc(&dws, wsf * 4));
     CK(cudaMemset(dws, 0, wsf * 4));
     CK(cudaMemcpy(dx, x, size_t(T) * K * 2, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dw, w, size_t(N) * K * 2, cudaMemcpyHostToDevice));
-    if (resid) CK(cudaMemcpy(dout, resid, out_elems * 2, cudaMemcpyHostToDevice));
+    if (resid) CK(cudaMemcpy(dres, resid, out_elems * 2, cudaMemcpyHostToDevice));
     GemmWeight gw;
     if (ds::gemm_weight_init(&gw, dw, N, K)) return ds_fail(DS_ERR_RUNTIME, "tensor map");
-    const int rc = ds::gemm_bf16(gw, dx, T, epi, dout, dout, df, dws, wsf, k_splits, 0);
-    if (rc) return ds_fail(DS_ERR_RUNTIME, "gemm launch rc=" + std::to_string(rc));
+    // three back-to-back (PDL-chained) launches on one workspace: the result must not depend on
+    // leftovers of the previous launch (stream-K arrival counters reset themselves)
+    for (int rep = 0; rep < 3; ++rep) {
+        const int rc = ds::gemm_bf16(gw, dx, T, epi, dout, dres, df, dws, wsf, k_splits, 0);
+        if (rc) return ds_fail(DS_ERR_RUNTIME, "gemm launch rc=" + std::to_string(rc));
+    }
     CK(cudaDeviceSynchronize());
     if (epi == ds::EPI_F32)
         CK(cudaMemcpy(out, df, out_elems * 4, cudaMemcpyDeviceToHost));
@@ -979,6 +984,7 @@ ds_status ds_dbg_gemm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t N
     cudaFree(dx);
     cudaFree(dw);
     cudaFree(dout);
+    cudaFree(dres);
     cudaFree(df);
     cudaFree(dws);
     return DS_OK;

@@ -33,15 +33,30 @@ def test_gemm_shapes(T):
 
 
 @pytest.mark.parametrize("epi", [0, 1, 2])
-@pytest.mark.parametrize("splits", [1, 3])
-def test_gemm_epilogues_and_splits(epi, splits):
-    # splits = cap on 2-CTA clusters: 1 -> one cluster owns whole tiles; 3 -> every tile is
-    # split across clusters and finished by the last-arriving CTA (stream-K fixup)
-    got, ref = _run(64, 256, 1024, epi=epi, splits=splits, seed=3)
+@pytest.mark.parametrize("clusters", [1, 3, 5, 0])
+def test_gemm_epilogues_and_partitions(epi, clusters):
+    # clusters = cap on 2-CTA clusters: 1 -> one cluster owns whole tiles; 3, 5 -> data-parallel
+    # rounds plus a stream-K remainder whose split tiles the last-arriving CTA finishes; 0 -> all
+    # SMs (every tile split across several clusters)
+    got, ref = _run(64, 256 * 3, 1024, epi=epi, splits=clusters, seed=3)
     tol = (1e-4 if epi == 2 else 2e-2) * np.abs(ref).max() + 1e-3
     assert np.abs(got - ref).max() <= tol
+
+
+@pytest.mark.parametrize("T,clusters", [(600, 2), (777, 0), (300, 7)])
+def test_gemm_two_token_blocks_stream_k(T, clusters):
+    got, ref = _run(T, 1024, 512, epi=1, splits=clusters, seed=T)
+    assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max() + 1e-3
 
 
 def test_gemm_llama8b_qkv_shape():
     got, ref = _run(200, 6144, 4096, seed=5)
     assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("N,K", [(512, 256), (256, 256), (1536, 256), (256, 768), (128256, 256)])
+@pytest.mark.parametrize("T", [1, 17, 300])
+def test_gemm_tiny_model_shapes(N, K, T):
+    got, ref = _run(T, N, K, epi=2 if N == 128256 else 1, seed=N + T)
+    assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max() + 1e-3
+
