@@ -1,7 +1,9 @@
-// HBM-bound stage-forward kernels: weight init, embedding gather, RMSNorm, RoPE + paged KV
-// append, SiLU*mul, greedy argmax and the token plumbing between circuits. All vectorised
+// HBM-bound stage-forward kernels: weight init, embedding gather, RMSNorm (+ deferred residual),
+// RoPE + paged KV append (+ deferred q/k/v epilogue), greedy argmax and the token plumbing between circuits. All vectorised
 // 16-byte accesses; grids sized in multiples of the SM count where the row count allows.
 // Numerics follow oracle/llama_ref.c exactly (bf16 storage, fp32 math, same rounding points).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -26,7 +28,7 @@ __global__ void init_weights_kernel(__nv_bfloat16* dst, uint64_t seed, uint64_t 
         int64_t o = i;
         if (part >= 0) {
             const int64_t r = i / cols, c = i % cols;
-            o = ((r / 64) * 128 + part * 64 + (r % 64)) * cols + c;
+            o = ((r / 16) * 32 + part * 16 + (r % 16)) * cols + c;
         }
         dst[o] = f2bf(v);
     }
@@ -64,10 +66,33 @@ void embed_rows(const __nv_bfloat16* emb, const int32_t* tokens, int T, int d, _
 
 // ------------------------------------------------------------ RMSNorm ----
 // One CTA per row; d/8 16-byte vectors, at most 8 per thread kept in registers.
+// Sum of 8 consecutive plane values (plane order) at element offset e; the loads of four planes
+// are in flight at a time.
+DS_DEVICE void sum_planes8(const Planes& pl, size_t e, float* acc) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    for (int k0 = 0; k0 < pl.n; k0 += 4) {
+        float4 a[4][2];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k0 + k < pl.n) {
+                const float4* pk = reinterpret_cast<const float4*>(pl.p + (k0 + k) * pl.stride + e);
+                a[k][0] = __ldcg(pk);
+                a[k][1] = __ldcg(pk + 1);
+            }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k0 + k < pl.n) {
+                acc[0] += a[k][0].x; acc[1] += a[k][0].y; acc[2] += a[k][0].z; acc[3] += a[k][0].w;
+                acc[4] += a[k][1].x; acc[5] += a[k][1].y; acc[6] += a[k][1].z; acc[7] += a[k][1].w;
+            }
+    }
+}
+
 template <int VPT>
-__global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(512) rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ rows,
                                int d, const __nv_bfloat16* __restrict__ g, float eps,
-                               __nv_bfloat16* __restrict__ y) {
+                               __nv_bfloat16* __restrict__ y, Planes pl) {
     pdl_launch_dependents();
     pdl_wait();
     const int i = blockIdx.x;
@@ -81,10 +106,18 @@ __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_
         const int idx = threadIdx.x + k * blockDim.x;
         if (idx < nv) {
             unpack8(xr[idx], v[k]);
+            if (pl.n > 0) {  // deferred residual epilogue: x = bf16(x + bf16(acc))
+                float acc[8];
+                sum_planes8(pl, size_t(src_row) * d + idx * 8, acc);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[k][j] = round_bf(v[k][j] + round_bf(acc[j]));
+                reinterpret_cast<uint4*>(const_cast<__nv_bfloat16*>(x) + size_t(src_row) * d)[idx] = pack8(v[k]);
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j) ss += v[k][j] * v[k][j];
         }
     }
+    if (y == nullptr) return;
     __shared__ float red[32];
     ss = warp_sum(ss);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
@@ -112,23 +145,26 @@ __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int32_
 }
 
 void rmsnorm_rows(const __nv_bfloat16* x, const int32_t* rows, int n_rows, int d,
-                  const __nv_bfloat16* g, float eps, __nv_bfloat16* y, cudaStream_t stream) {
+                  const __nv_bfloat16* g, float eps, __nv_bfloat16* y, cudaStream_t stream,
+                  const Planes& pending) {
     if (n_rows <= 0) return;
+    // one 16-byte vector per thread (d <= 4096) so every load of the row is in flight at once
     const int nv = d / 8;
-    if (nv <= 128)
-        launch_pdl(rmsnorm_kernel<1>, dim3(n_rows), dim3(128), 0, stream, x, rows, d, g, eps, y);
-    else if (nv <= 512)
-        launch_pdl(rmsnorm_kernel<4>, dim3(n_rows), dim3(128), 0, stream, x, rows, d, g, eps, y);
+    const int threads = std::min(512, std::max(32, (nv + 31) / 32 * 32));
+    if (nv <= threads)
+        launch_pdl(rmsnorm_kernel<1>, dim3(n_rows), dim3(threads), 0, stream, x, rows, d, g, eps, y, pending);
+    else if (nv <= 4 * threads)
+        launch_pdl(rmsnorm_kernel<4>, dim3(n_rows), dim3(threads), 0, stream, x, rows, d, g, eps, y, pending);
     else
-        launch_pdl(rmsnorm_kernel<8>, dim3(n_rows), dim3(128), 0, stream, x, rows, d, g, eps, y);
+        launch_pdl(rmsnorm_kernel<8>, dim3(n_rows), dim3(threads), 0, stream, x, rows, d, g, eps, y, pending);
 }
 
 // ------------------------------------------------- RoPE + KV append ----
-__global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int n_h, int n_kv, int dh,
+__global__ void __launch_bounds__(512) rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int n_h, int n_kv, int dh,
                                const int32_t* __restrict__ row_pos,
                                const int32_t* __restrict__ row_page, const float* __restrict__ rc,
                                const float* __restrict__ rs, KvLayout kv, int layer,
-                               __nv_bfloat16* __restrict__ q_out) {
+                               __nv_bfloat16* __restrict__ q_out, Planes pl) {
     pdl_launch_dependents();
     pdl_wait();
     const int t = blockIdx.x;
@@ -145,8 +181,18 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int n_h, i
     for (int w = threadIdx.x; w < n_rot; w += blockDim.x) {
         const int head = w / (half / 8), i = (w % (half / 8)) * 8;
         float x1[8], x2[8], o1[8], o2[8];
-        unpack8(*reinterpret_cast<const uint4*>(src + head * dh + i), x1);
-        unpack8(*reinterpret_cast<const uint4*>(src + head * dh + i + half), x2);
+        if (pl.n > 0) {  // deferred GEMM epilogue: bf16(sum of planes)
+            sum_planes8(pl, size_t(t) * width + head * dh + i, x1);
+            sum_planes8(pl, size_t(t) * width + head * dh + i + half, x2);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                x1[j] = round_bf(x1[j]);
+                x2[j] = round_bf(x2[j]);
+            }
+        } else {
+            unpack8(*reinterpret_cast<const uint4*>(src + head * dh + i), x1);
+            unpack8(*reinterpret_cast<const uint4*>(src + head * dh + i + half), x2);
+        }
         const float4 c0 = *reinterpret_cast<const float4*>(c + i), c1 = *reinterpret_cast<const float4*>(c + i + 4);
         const float4 s0 = *reinterpret_cast<const float4*>(s + i), s1 = *reinterpret_cast<const float4*>(s + i + 4);
         const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
@@ -171,7 +217,14 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int n_h, i
     const int nv = n_kv * dh / 8;
     for (int w = threadIdx.x; w < nv; w += blockDim.x) {
         const int kh = (w * 8) / dh, i = (w * 8) % dh;
-        const uint4 val = *reinterpret_cast<const uint4*>(src + (n_h + n_kv) * dh + kh * dh + i);
+        uint4 val;
+        if (pl.n > 0) {
+            float a[8];
+            sum_planes8(pl, size_t(t) * width + (n_h + n_kv) * dh + kh * dh + i, a);
+            val = pack8(a);
+        } else {
+            val = *reinterpret_cast<const uint4*>(src + (n_h + n_kv) * dh + kh * dh + i);
+        }
         __nv_bfloat16* dv = kv.pool + page_base + ((size_t(layer) * 2 + 1) * n_kv + kh) * 256 * dh +
                             size_t(slot) * dh + i;
         *reinterpret_cast<uint4*>(dv) = val;
@@ -181,41 +234,13 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int n_h, i
 void rope_kv_append(const __nv_bfloat16* qkv, int T, int n_h, int n_kv, int d_head,
                     const int32_t* row_pos, const int32_t* row_page, const float* rope_cos,
                     const float* rope_sin, const KvLayout& kv, int layer, __nv_bfloat16* q_out,
-                    cudaStream_t stream) {
+                    cudaStream_t stream, const Planes& planes) {
+    // one rotary 8-pair group (and one v vector) per thread: all loads of the row in flight
+    const int work = std::max((n_h + n_kv) * (d_head / 16), n_kv * d_head / 8);
+    const int threads = std::min(512, (work + 31) / 32 * 32);
     if (T > 0)
-        launch_pdl(rope_kv_kernel, dim3(T), dim3(256), 0, stream, qkv, n_h, n_kv, d_head, row_pos, row_page, rope_cos, rope_sin, kv, layer, q_out);
-}
-
-// ----------------------------------------------------------- SiLU*mul ----
-__global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, int T, int ffn,
-                                __nv_bfloat16* __restrict__ h) {
-    pdl_launch_dependents();
-    pdl_wait();
-    const size_t total = size_t(T) * ffn / 8;
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
-         i += size_t(gridDim.x) * blockDim.x) {
-        const size_t e = i * 8;
-        const size_t t = e / ffn;
-        const int f = int(e % ffn);
-        const __nv_bfloat16* row = gu + t * size_t(2 * ffn);
-        const int gcol = (f / 64) * 128 + (f % 64);
-        float g[8], u[8], o[8];
-        unpack8(*reinterpret_cast<const uint4*>(row + gcol), g);
-        unpack8(*reinterpret_cast<const uint4*>(row + gcol + 64), u);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const float sg = round_bf(g[j] / (1.0f + expf(-g[j])));
-            o[j] = sg * u[j];
-        }
-        *reinterpret_cast<uint4*>(h + e) = pack8(o);
-    }
-}
-void silu_mul(const __nv_bfloat16* gu, int T, int ffn, __nv_bfloat16* h, cudaStream_t stream) {
-    if (T <= 0) return;
-    const size_t total = size_t(T) * ffn / 8;
-    int blocks = int((total + 255) / 256);
-    if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
-    launch_pdl(silu_mul_kernel, dim3(blocks), dim3(256), 0, stream, gu, T, ffn, h);
+        launch_pdl(rope_kv_kernel, dim3(T), dim3(threads), 0, stream, qkv, n_h, n_kv, d_head, row_pos,
+                   row_page, rope_cos, rope_sin, kv, layer, q_out, planes);
 }
 
 // ------------------------------------------------------------- argmax ----
@@ -298,7 +323,6 @@ void preload_elementwise() {
     cudaFuncGetAttributes(&a, rmsnorm_kernel<4>);
     cudaFuncGetAttributes(&a, rmsnorm_kernel<8>);
     cudaFuncGetAttributes(&a, rope_kv_kernel);
-    cudaFuncGetAttributes(&a, silu_mul_kernel);
     cudaFuncGetAttributes(&a, argmax_kernel);
     cudaFuncGetAttributes(&a, scatter_tokens_kernel);
     cudaFuncGetAttributes(&a, resolve_tokens_kernel);

@@ -184,6 +184,38 @@ DS_DEVICE void store16(const GemmParams& p, float* v, int t, int f0) {
     dst[1] = pack8(v + 8);
 }
 
+// SiLU epilogue of one transposed 32-feature slice f_slice.. (16 gate + the matching 16 up rows
+// of the interleaved weight): lane 2r holds the gate, lane 2r+1 the up features of token row r;
+// they swap halves and each writes 8 of the 16 ffn columns. Every lane must call (shuffles).
+DS_DEVICE void store_silu(const GemmParams& p, const float* v, bool ok, int lane, int t, int f_slice) {
+    const int half = lane & 1;
+    float send[8], recv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) send[j] = half ? v[j] : v[8 + j];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) recv[j] = __shfl_xor_sync(0xffffffffu, send[j], 1);
+    if (!ok) return;
+    const float* g = half ? recv : v;
+    const float* u = half ? v + 8 : recv;
+    float o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const float gb = round_bf(g[j]);
+        o[j] = round_bf(__fdividef(gb, 1.0f + __expf(-gb))) * round_bf(u[j]);  // fast math: bf16-rounded
+    }
+    const int ld = p.N / 2;
+    *reinterpret_cast<uint4*>(p.out_bf16 + size_t(t) * ld + (f_slice / 32) * 16 + half * 8) = pack8(o);
+}
+
+// Final epilogue of a transposed chunk (all lanes call; `ok` = this lane's token row is real).
+DS_DEVICE void epi_store(const GemmParams& p, float* v, bool ok, int lane, int t, int f_slice) {
+    if (p.epi == EPI_SILU) {
+        store_silu(p, v, ok, lane, t, f_slice);
+        return;
+    }
+    if (ok) store16(p, v, t, f_slice + (lane & 1) * 16);
+}
+
 DS_DEVICE void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 // Piece slot of cluster c for the split tile starting at k-block tile_g0 (its first or last
@@ -382,8 +414,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                 for (int c0 = 0; c0 < t_here; c0 += 16) {
                     tmem_ld16(acc + c0, r);
                     tmem_ld_wait();
-                    if (transpose16(stage, reinterpret_cast<float*>(r), lane, c0, t_here, v))
-                        store16(p, v, t0 + c0 + row, f_slice + half * 16);
+                    const bool ok = transpose16(stage, reinterpret_cast<float*>(r), lane, c0, t_here, v);
+                    epi_store(p, v, ok, lane, t0 + c0 + row, f_slice);
                 }
             } else {
                 // split tile: park this piece (TMEM-native layout [chunk][feature][16 tokens]: each
@@ -439,8 +471,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                         tmem_ld_wait();
                         sum_pieces(p, CN, rank, tile_g0, c_lo, c_hi, size_t(ch) * kBM * 16 + fo, cluster,
                                    own, sum);
-                        if (transpose16(stage, sum, lane, ch * 16, t_here, v))
-                            store16(p, v, t0 + ch * 16 + row, f_slice + half * 16);
+                        const bool ok = transpose16(stage, sum, lane, ch * 16, t_here, v);
+                        epi_store(p, v, ok, lane, t0 + ch * 16 + row, f_slice);
                     }
                 }
             }
@@ -485,8 +517,8 @@ __global__ void __launch_bounds__(128) splitk_finish_kernel(const GemmParams p) 
     float sum[16], v[16];
     sum_pieces(p, CN, rank, tile_g0, c_lo, c_hi, size_t(ch) * kBM * 16 + size_t(q * 32 + lane) * 16, -1,
                nullptr, sum);
-    if (transpose16(stage_all[q], sum, lane, ch * 16, t_here, v))
-        store16(p, v, t0 + ch * 16 + (lane >> 1), mt * kBM + q * 32 + (lane & 1) * 16);
+    const bool ok = transpose16(stage_all[q], sum, lane, ch * 16, t_here, v);
+    epi_store(p, v, ok, lane, t0 + ch * 16 + (lane >> 1), mt * kBM + q * 32);
 }
 
 // Narrow-GEMM reduction: the k-range planes summed in order (deterministic) + the fused epilogue,
@@ -510,6 +542,31 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const GemmParams p) 
         const size_t o = i * 4;
         if (p.epi == EPI_F32) {
             reinterpret_cast<float4*>(p.out_f32)[i] = a;
+            continue;
+        }
+        if (p.epi == EPI_SILU) {  // gate columns pair with the up columns 16 further on
+            const int c = int(o % p.N);
+            if (c % 32 >= 16) continue;
+            float4 u = __ldcg(reinterpret_cast<const float4*>(p.slots) + i + 4);
+            for (int k = 1; k < p.planes; ++k) {
+                const float4 b = __ldcg(reinterpret_cast<const float4*>(p.slots + k * plane) + i + 4);
+                u.x += b.x;
+                u.y += b.y;
+                u.z += b.z;
+                u.w += b.w;
+            }
+            const float g4[4] = {a.x, a.y, a.z, a.w}, u4[4] = {u.x, u.y, u.z, u.w};
+            float h[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float gb = round_bf(g4[j]);
+                h[j] = round_bf(__fdividef(gb, 1.0f + __expf(-gb))) * round_bf(u4[j]);
+            }
+            uint2 hv;
+            hv.x = pack2(h[0], h[1]);
+            hv.y = pack2(h[2], h[3]);
+            const size_t t = o / p.N;
+            *reinterpret_cast<uint2*>(p.out_bf16 + t * (p.N / 2) + (c / 32) * 16 + c % 32) = hv;
             continue;
         }
         float v[4] = {a.x, a.y, a.z, a.w};
@@ -571,10 +628,10 @@ static int pick_cn(int N) {
 
 static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out);
 
-int gemm_launch_count(int T, int N, int K) {
+int gemm_launch_count(int T, int N, int K, bool deferred) {
     int cn = 0;
     const GemmParams p = plan_gemm(T, N, K, 0, &cn);
-    return 1 + p.defer;
+    return 1 + ((p.defer && !(deferred && p.planes)) ? 1 : 0);
 }
 
 // Tile shape, pipeline depth and the data-parallel / stream-K partition of one GEMM (a negative
@@ -630,8 +687,9 @@ static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) 
 
 int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_bfloat16* out_bf16,
               const __nv_bfloat16* resid, float* out_f32, float* workspace, size_t workspace_floats,
-              int max_clusters, cudaStream_t stream) {
+              int max_clusters, cudaStream_t stream, Planes* defer) {
     const int N = w.N, K = w.K;
+    if (defer) *defer = Planes{};
     if (T <= 0) return 0;
     int cn = 1;
     GemmParams p = plan_gemm(T, N, K, max_clusters, &cn);
@@ -675,7 +733,11 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
                             : cudaLaunchKernelEx(&cfg, gemm_tc_kernel<1>, tw, tx, p);
     if (e != cudaSuccess) return -6;
     static const bool no_finish = getenv("DS_GEMM_NOFINISH") != nullptr;  // debug: timing only
-    if (p.planes && !no_finish) {
+    if (p.planes && defer) {
+        defer->p = p.slots;
+        defer->n = p.planes;
+        defer->stride = size_t(T) * N;
+    } else if (p.planes && !no_finish) {
         const size_t total4 = size_t(T) * N / 4;
         const int blocks = int(std::min<size_t>((total4 + 255) / 256, size_t(kNumSMs) * 8));
         e = launch_pdl(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, stream, p);

@@ -12,6 +12,8 @@ enum GemmEpilogue : int {
     EPI_BF16 = 0,     // out = bf16(acc)
     EPI_RESID = 1,    // out = bf16(resid + bf16(acc))   (residual add fused; out may alias resid)
     EPI_F32 = 2,      // out = acc (fp32, logits)
+    EPI_SILU = 3,     // gate/up GEMM (16-row interleaved weight): out[t, N/2] =
+                      //   bf16(bf16(silu(bf16(gate))) * bf16(up))
 };
 
 // A weight matrix [N, K] (row-major, K contiguous) with its TMA descriptor.
@@ -21,22 +23,36 @@ struct GemmWeight {
     alignas(64) unsigned char tmap[128];
 };
 
+// Split-K partial planes a narrow GEMM leaves for its consumer kernel to sum (in plane order,
+// then the GEMM's epilogue rounding) instead of a separate reduction: plane k of row t, column
+// c is p[k * stride + t * ld + c]. n == 0: no planes, the GEMM wrote its final output.
+struct Planes {
+    const float* p = nullptr;
+    int n = 0;
+    size_t stride = 0;
+};
+
 int gemm_weight_init(GemmWeight* w, const __nv_bfloat16* data, int N, int K);
 // Stream-K pieces + per-tile arrival counters; allocate once, zero-initialised, one per stream.
 size_t gemm_workspace_floats();
 // Debug: per-CTA phase timestamps (globaltimer ns, 8 slots per CTA) for subsequent launches.
 void gemm_set_trace(unsigned long long* device_buf);
-// Kernel launches gemm_bf16 issues for a shape (always 1: split tiles finish in-kernel).
-int gemm_launch_count(int T, int N, int K);
+// Kernel launches gemm_bf16 issues for a shape (2 with a reduction / finish kernel; `deferred`:
+// called with a Planes out-parameter).
+int gemm_launch_count(int T, int N, int K, bool deferred = false);
 // out[T, N] = epi(X[T, K] . W[N, K]^T). max_clusters > 0 caps the 2-CTA clusters (tests use it
 // to force other data-parallel / stream-K partitions); 0 = all SMs.
+// With `defer` != nullptr, a GEMM that would end in the split-K reduction kernel instead leaves
+// its planes in the workspace and describes them in *defer (the consumer kernel finishes it);
+// otherwise *defer = {} and the output is final.
 int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_bfloat16* out_bf16,
               const __nv_bfloat16* resid, float* out_f32, float* workspace, size_t workspace_floats,
-              int max_clusters, cudaStream_t stream);
+              int max_clusters, cudaStream_t stream, Planes* defer = nullptr);
 
 // Counter-based weight init (bf16(uniform(-1,1) * scale)); see oracle/llama_ref.c ds_ref_weight.
-// If interleave64 != 0 the [rows, cols] tensor is written into the gate/up interleaved
-// layout: canonical row r of tensor `part` (0 gate, 1 up) lands at row 128*(r/64) + 64*part + r%64.
+// interleave_part >= 0 writes the [rows, cols] tensor into the gate/up interleaved layout:
+// canonical row r of tensor `part` (0 gate, 1 up) lands at row 32*(r/16) + 16*part + r%16, so a
+// 32-row TMEM slice holds 16 gate and the matching 16 up features (EPI_SILU).
 void init_weights(__nv_bfloat16* dst, uint64_t seed, uint64_t tensor_id, int64_t rows, int64_t cols,
                   float scale, int interleave_part, cudaStream_t stream);
 void fill_bf16(__nv_bfloat16* dst, int64_t n, float v, cudaStream_t stream);
@@ -45,8 +61,11 @@ void fill_bf16(__nv_bfloat16* dst, int64_t n, float v, cudaStream_t stream);
 void embed_rows(const __nv_bfloat16* emb, const int32_t* tokens, int T, int d, __nv_bfloat16* x,
                 cudaStream_t stream);
 // y[i] = bf16(g * bf16(x[row_i] * rsqrt(mean(x^2) + eps))); rows = index list or identity.
+// With pending planes (identity rows only): first x[i] = bf16(x[i] + bf16(sum of planes)) (the
+// deferred residual GEMM epilogue), written back to x; y == nullptr skips the normalisation.
 void rmsnorm_rows(const __nv_bfloat16* x, const int32_t* rows, int n_rows, int d,
-                  const __nv_bfloat16* g, float eps, __nv_bfloat16* y, cudaStream_t stream);
+                  const __nv_bfloat16* g, float eps, __nv_bfloat16* y, cudaStream_t stream,
+                  const Planes& pending = Planes{});
 
 struct KvLayout {
     __nv_bfloat16* pool = nullptr;  // [n_pages][L_stage][2][n_kv][256][d_head]
@@ -56,10 +75,11 @@ struct KvLayout {
 
 // Rotary embedding on q and k (rotate-half, table [max_pos][d_head/2] cos / sin) and
 // the paged KV append of k, v for every row at row_pos[t] into page row_page[t].
+// With planes, the qkv values are bf16(sum of planes) (the deferred GEMM epilogue).
 void rope_kv_append(const __nv_bfloat16* qkv, int T, int n_h, int n_kv, int d_head,
                     const int32_t* row_pos, const int32_t* row_page, const float* rope_cos,
                     const float* rope_sin, const KvLayout& kv, int layer, __nv_bfloat16* q_out,
-                    cudaStream_t stream);
+                    cudaStream_t stream, const Planes& planes = Planes{});
 
 // Paged causal attention: row t attends positions [0, row_pos[t]] of its request, whose pages
 // are flat_pages[row_page_off[t] ...]. Output o[T, n_h * d_head] bf16.
@@ -74,9 +94,6 @@ int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_p
                     int n_blocks, const int32_t* drows, int n_drows, const KvLayout& kv, int layer,
                     int max_ctx, __nv_bfloat16* o, float* ws, size_t ws_floats,
                     cudaStream_t stream);
-
-// h[t, f] = bf16(bf16(silu(g)) * u) from the gate/up interleaved GEMM output [T, 2*ffn].
-void silu_mul(const __nv_bfloat16* gu, int T, int ffn, __nv_bfloat16* h, cudaStream_t stream);
 
 // ids[r] = argmax_v logits[r, v] (lowest index wins ties).
 void argmax_rows(const float* logits, int R, int V, int32_t* ids, cudaStream_t stream);

@@ -75,8 +75,7 @@ struct ds_stage {
     float* rope_cos = nullptr;
     float* rope_sin = nullptr;
 
-    bf16 *x = nullptr, *xn = nullptr, *qkv = nullptr, *q = nullptr, *attn = nullptr, *gu = nullptr,
-         *h = nullptr;
+    bf16 *x = nullptr, *xn = nullptr, *qkv = nullptr, *q = nullptr, *attn = nullptr, *h = nullptr;
     float* logits = nullptr;
     int32_t* ids = nullptr;
     float* ws = nullptr;
@@ -281,7 +280,7 @@ ds_status ds_stage_create(int32_t device, const ds_model_desc* md, int64_t layer
     auto A = [&](void** p, size_t bytes) { return alloc_dev(p, bytes); };
     if ((st = A((void**)&s->x, R * d * 2)) || (st = A((void**)&s->xn, R * d * 2)) ||
         (st = A((void**)&s->qkv, R * qkv_rows * 2)) || (st = A((void**)&s->q, R * qdim * 2)) ||
-        (st = A((void**)&s->attn, R * qdim * 2)) || (st = A((void**)&s->gu, R * 2 * m.ffn * 2)) ||
+        (st = A((void**)&s->attn, R * qdim * 2)) ||
         (st = A((void**)&s->h, R * m.ffn * 2)) || (st = A((void**)&s->ids, R * 4))) {
         delete s;
         return st;
@@ -310,7 +309,7 @@ ds_status ds_stage_destroy(ds_stage* s) {
     cudaSetDevice(s->device);
     cudaDeviceSynchronize();
     for (void* p : {(void*)s->wbuf, (void*)s->rope_cos, (void*)s->rope_sin, (void*)s->x, (void*)s->xn,
-                    (void*)s->qkv, (void*)s->q, (void*)s->attn, (void*)s->gu, (void*)s->h,
+                    (void*)s->qkv, (void*)s->q, (void*)s->attn, (void*)s->h,
                     (void*)s->logits, (void*)s->ids, (void*)s->ws, (void*)s->attn_ws,
                     (void*)s->d_meta, (void*)s->kv.pool, (void*)s->last_token,
                     (void*)s->pending_ids})
@@ -685,8 +684,11 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     attn_bytes += double(T) * qdim * 4.0;
     size_t mark = 0;
     auto begin = [&]() { if (s->prof) mark = prof_mark(s); };
-    auto end_gemm = [&](int kind, int rows_, int N, int K, int out_bytes) {
-        s->launches += ds::gemm_launch_count(rows_, N, K);
+    static const bool check_each = getenv("DS_CHECK_LAUNCH") != nullptr;  // debug: name the failing group
+    auto end_gemm = [&](int kind, int rows_, int N, int K, int out_bytes, bool deferred = false) {
+        s->launches += ds::gemm_launch_count(rows_, N, K, deferred);
+        if (check_each && cudaPeekAtLastError() != cudaSuccess)
+            fprintf(stderr, "launch error after %s: %s\n", kPkName[kind], cudaGetErrorString(cudaPeekAtLastError()));
         if (!s->prof) return;
         const size_t e1 = prof_mark(s);
         s->recs.push_back({kind, rows_, 2.0 * rows_ * N * K,
@@ -694,48 +696,69 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     };
     auto end_other = [&](int kind, double flops, double bytes, int n_launch) {
         s->launches += n_launch;
+        if (check_each && cudaPeekAtLastError() != cudaSuccess)
+            fprintf(stderr, "launch error after %s: %s\n", kPkName[kind], cudaGetErrorString(cudaPeekAtLastError()));
         if (!s->prof) return;
         const size_t e1 = prof_mark(s);
         s->recs.push_back({kind, T, flops, bytes, mark, e1});
     };
+    // timing experiments only (results invalid): DS_SKIP bit 0 rmsnorm, 1 rope/KV, 2 attention,
+    // 4 GEMMs
+    static const int skip = getenv("DS_SKIP") ? atoi(getenv("DS_SKIP")) : 0;
+    // Narrow GEMMs (q/k/v, o, down) leave split-K planes that their consumer sums: RoPE/KV append
+    // for q/k/v, the next RMSNorm (with the residual add) for o and down.
+    ds::Planes pend;  // deferred residual of the previous down projection
     for (int li = 0; li < s->L; ++li) {
         LayerW& lw = s->layers[li];
+        ds::Planes pq, po;
         begin();
-        ds::rmsnorm_rows(s->x, nullptr, T, d, lw.attn_norm, m.norm_eps, s->xn, st);
-        end_other(PK_ELEM, 0, 4.0 * T * d, 1);
+        if (!(skip & 1))
+            ds::rmsnorm_rows(s->x, nullptr, T, d, lw.attn_norm, m.norm_eps, s->xn, st, pend);
+        end_other(PK_ELEM, 0, (4.0 + 4.0 * pend.n) * T * d, 1);
         begin();
-        int rc = ds::gemm_bf16(lw.wqkv, s->xn, T, ds::EPI_BF16, s->qkv, nullptr, nullptr, s->ws,
-                               s->ws_floats, 0, st);
-        end_gemm(PK_QKV, T, qkv_rows, d, 2);
+        int rc = (skip & 16) ? 0 : ds::gemm_bf16(lw.wqkv, s->xn, T, ds::EPI_BF16, s->qkv, nullptr,
+                                                  nullptr, s->ws, s->ws_floats, 0, st, &pq);
+        end_gemm(PK_QKV, T, qkv_rows, d, 2, true);
         begin();
-        ds::rope_kv_append(s->qkv, T, m.n_heads, m.n_kv_heads, m.d_head, d_pos, d_page, s->rope_cos,
-                           s->rope_sin, s->kv, li, s->q, st);
+        if (!(skip & 2))
+            ds::rope_kv_append(s->qkv, T, m.n_heads, m.n_kv_heads, m.d_head, d_pos, d_page,
+                               s->rope_cos, s->rope_sin, s->kv, li, s->q, st, pq);
         end_other(PK_ELEM, 0, 2.0 * T * qkv_rows + 2.0 * T * (qdim + 2 * m.n_kv_heads * m.d_head), 1);
         begin();
-        rc |= ds::attention_paged(s->q, T, m.n_heads, d_pos, d_poff, d_flat, d_blk, n_blk,
-                                  d_blk + 3 * n_blk, n_drow, s->kv, li, max_ctx, s->attn, s->attn_ws,
-                                  s->attn_ws_floats, st);
+        if (!(skip & 4))
+            rc |= ds::attention_paged(s->q, T, m.n_heads, d_pos, d_poff, d_flat, d_blk, n_blk,
+                                      d_blk + 3 * n_blk, n_drow, s->kv, li, max_ctx, s->attn,
+                                      s->attn_ws, s->attn_ws_floats, st);
         end_other(PK_ATTN, attn_flops, attn_bytes,
                   ds::attention_launches(n_blk, n_drow, m.n_kv_heads, max_ctx));
         begin();
-        rc |= ds::gemm_bf16(lw.wo, s->attn, T, ds::EPI_RESID, s->x, s->x, nullptr, s->ws,
+        if (!(skip & 16))
+            rc |= ds::gemm_bf16(lw.wo, s->attn, T, ds::EPI_RESID, s->x, s->x, nullptr, s->ws,
+                                s->ws_floats, 0, st, &po);
+        end_gemm(PK_O, T, d, qdim, 4, true);
+        begin();
+        if (!(skip & 1))
+            ds::rmsnorm_rows(s->x, nullptr, T, d, lw.mlp_norm, m.norm_eps, s->xn, st, po);
+        end_other(PK_ELEM, 0, (4.0 + 4.0 * po.n) * T * d, 1);
+        begin();
+        if (!(skip & 16))
+            rc |= ds::gemm_bf16(lw.wgu, s->xn, T, ds::EPI_SILU, s->h, nullptr, nullptr, s->ws,
                             s->ws_floats, 0, st);
-        end_gemm(PK_O, T, d, qdim, 4);
+        end_gemm(PK_GU, T, 2 * m.ffn, d, 1);  // SiLU fused: writes h[T, ffn]
         begin();
-        ds::rmsnorm_rows(s->x, nullptr, T, d, lw.mlp_norm, m.norm_eps, s->xn, st);
-        end_other(PK_ELEM, 0, 4.0 * T * d, 1);
+        if (!(skip & 16))
+            rc |= ds::gemm_bf16(lw.wd, s->h, T, ds::EPI_RESID, s->x, s->x, nullptr, s->ws,
+                                s->ws_floats, 0, st, &pend);
+        end_gemm(PK_DOWN, T, d, m.ffn, 4, true);
+        if (rc)
+            return ds_fail(DS_ERR_RUNTIME, "kernel launch failed in layer " + std::to_string(li) +
+                                               " (T=" + std::to_string(T) + ", rc " + std::to_string(rc) +
+                                               ", " + cudaGetErrorString(cudaGetLastError()) + ")");
+    }
+    if (pend.n > 0) {  // last layer's deferred residual: x final for the LM head / next stage
         begin();
-        rc |= ds::gemm_bf16(lw.wgu, s->xn, T, ds::EPI_BF16, s->gu, nullptr, nullptr, s->ws,
-                            s->ws_floats, 0, st);
-        end_gemm(PK_GU, T, 2 * m.ffn, d, 2);
-        begin();
-        ds::silu_mul(s->gu, T, m.ffn, s->h, st);
-        end_other(PK_ELEM, 0, 6.0 * T * m.ffn, 1);
-        begin();
-        rc |= ds::gemm_bf16(lw.wd, s->h, T, ds::EPI_RESID, s->x, s->x, nullptr, s->ws, s->ws_floats,
-                            0, st);
-        end_gemm(PK_DOWN, T, d, m.ffn, 4);
-        if (rc) return ds_fail(DS_ERR_RUNTIME, "kernel launch failed in layer " + std::to_string(li));
+        ds::rmsnorm_rows(s->x, nullptr, T, d, nullptr, m.norm_eps, nullptr, st, pend);
+        end_other(PK_ELEM, 0, (4.0 + 4.0 * pend.n) * T * d, 1);
     }
     if (s->last) {
         int32_t* ids_out = act_out ? static_cast<int32_t*>(act_out)
@@ -980,7 +1003,8 @@ ds_status ds_dbg_gemm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t N
     if (epi == ds::EPI_F32)
         CK(cudaMemcpy(out, df, out_elems * 4, cudaMemcpyDeviceToHost));
     else
-        CK(cudaMemcpy(out, dout, out_elems * 2, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(out, dout, (epi == ds::EPI_SILU ? out_elems / 2 : out_elems) * 2,
+                      cudaMemcpyDeviceToHost));
     cudaFree(dx);
     cudaFree(dw);
     cudaFree(dout);

@@ -60,3 +60,31 @@ def test_gemm_tiny_model_shapes(N, K, T):
     got, ref = _run(T, N, K, epi=2 if N == 128256 else 1, seed=N + T)
     assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max() + 1e-3
 
+
+def _silu_ref(acc):
+    """h[t, 16G + j] from the 16-row interleaved gate/up accumulator (EPI_SILU)."""
+    from paper_2501_14784_b200.bf16 import from_bf16, to_bf16
+    T, N = acc.shape
+    a = acc.reshape(T, N // 32, 2, 16)
+    g = from_bf16(to_bf16(a[:, :, 0, :].astype(np.float32))).astype(np.float64)
+    u = from_bf16(to_bf16(a[:, :, 1, :].astype(np.float32))).astype(np.float64)
+    sg = from_bf16(to_bf16((g / (1.0 + np.exp(-g))).astype(np.float32))).astype(np.float64)
+    return (sg * u).reshape(T, N // 2)
+
+
+@pytest.mark.parametrize("T,clusters", [(1, 0), (33, 0), (180, 0), (300, 0), (64, 3), (40, 1)])
+def test_gemm_silu_epilogue(T, clusters):
+    from paper_2501_14784_b200 import _native as nat
+    from paper_2501_14784_b200.bf16 import from_bf16, to_bf16
+    N, K = 2048, 512
+    rng = np.random.default_rng(T)
+    x = to_bf16(rng.standard_normal((T, K)).astype(np.float32))
+    w = to_bf16((rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32))
+    acc = from_bf16(x).astype(np.float64) @ from_bf16(w).astype(np.float64).T
+    ref = _silu_ref(acc)
+    out = np.zeros((T, N // 2), dtype=np.uint16)
+    nat.check(nat.lib.ds_dbg_gemm(x.ctypes.data, w.ctypes.data, T, N, K, 3, None, clusters,
+                                  out.ctypes.data))
+    got = from_bf16(out).astype(np.float64)
+    assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max() + 1e-3
+
