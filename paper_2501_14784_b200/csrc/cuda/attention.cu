@@ -570,11 +570,17 @@ attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
 
 int attention_block_positions(int n_h, int n_kv) { return (kAttnWarps * 16) / (n_h / n_kv); }
 
+// Context splits (flash-decoding): at least kSplitTarget CTAs per SM when the (block, kv head)
+// count alone is short of that, each split keeping >= 2 tiles (128 tokens) of the longest context.
+static int split_target() {
+    static const int v = getenv("DS_ATTN_TARGET") ? atoi(getenv("DS_ATTN_TARGET")) : 2;
+    return v;
+}
 int attention_pick_splits(int n_blocks, int n_kv, int max_ctx) {
     const int base = n_blocks * n_kv;
     const int tiles = (max_ctx + kTile - 1) / kTile;
-    int s = (2 * kNumSMs + base - 1) / base;
-    if (s > tiles) s = tiles;
+    int s = (split_target() * kNumSMs + base - 1) / base;
+    if (s > tiles / 2) s = tiles / 2;
     if (s > 16) s = 16;
     return s < 1 ? 1 : s;
 }

@@ -63,6 +63,8 @@ struct GemmParams {
     int n_sk;       // clusters taking a stream-K range (<= sk_tiles * KB: no empty range)
     int defer;      // 1: split tiles are summed by splitk_finish_kernel instead of the last arriver
     int planes;     // > 0: aligned narrow GEMM, partials in [planes][T][N] for splitk_reduce_kernel
+    int ks;         // > 1: narrow GEMM, K split ks ways INSIDE each cluster (CN x ks CTAs, one
+                    // tile per cluster), partials summed through distributed shared memory
     int epi;
     __nv_bfloat16* out_bf16;
     const __nv_bfloat16* resid;
@@ -126,7 +128,11 @@ DS_DEVICE int sk_owner(const GemmParams& p, int g) {
 // Iterates this cluster's segments: its stream-K range over tiles [0, sk_tiles) first (so split
 // tiles are finished while the data-parallel tiles stream), then one tile per data-parallel round.
 template <typename F>
-DS_DEVICE void for_each_seg(const GemmParams& p, int cluster, F&& f) {
+DS_DEVICE void for_each_seg(const GemmParams& p, int cluster, int kidx, F&& f) {
+    if (p.ks > 1) {  // k-split cluster: tile `cluster`, this CTA's share of its k-blocks
+        f(Seg{cluster, kidx * p.KB / p.ks, (kidx + 1) * p.KB / p.ks, 0});
+        return;
+    }
     if (cluster < p.n_sk) {
         const int g0 = sk_begin(p, cluster), g1 = sk_begin(p, cluster + 1);
         for (int g = g0; g < g1;) {
@@ -264,6 +270,102 @@ DS_DEVICE void sum_pieces(const GemmParams& p, int cn, int rank, int tile_g0, in
     }
 }
 
+DS_DEVICE uint32_t mapa_shared(uint32_t addr, uint32_t cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(cta));
+    return r;
+}
+DS_DEVICE float4 ld_dsmem_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+DS_DEVICE void add4(float4& a, const float4& b) {
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+}
+
+// k-split cluster epilogue (all 256 threads): the ks CTAs holding the same 128 features park
+// their fp32 accumulators in their (now idle) pipeline shared memory, 256 token columns at a
+// time, and each sums its 1/ks share of the token rows over the cluster's CTAs in k order
+// (ld.shared::cluster), then applies the fused epilogue 4 features per thread.
+template <int CN>
+DS_DEVICE void ksplit_epilogue(const GemmParams& p, uint8_t* smem, uint32_t tmem_base, int cluster,
+                               int kidx, int rank, int warp, int lane) {
+    const int cl_tiles = p.m_tiles / CN;
+    const int tbk = cluster / cl_tiles;
+    const int mt = (cluster % cl_tiles) * CN + rank;
+    const int t0 = tbk * p.tb;
+    const int t_here = min(p.tb, p.T - t0);
+    float* part = reinterpret_cast<float*>(smem);  // [256 tokens][128 features]
+    const uint32_t part_u32 = smem_u32(part);
+    const int quarter = warp & 3, cgrp = warp >> 2;
+    const bool silu = p.epi == EPI_SILU;
+    const int ipr = silu ? 16 : 32;  // 4-feature items per token row (SiLU: gate quads only)
+    for (int w0 = 0; w0 < t_here; w0 += 256) {
+        const int wn = min(256, t_here - w0);
+        for (int c = cgrp * 16; c < wn; c += 32) {
+            uint32_t r[16];
+            tmem_ld16(tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(w0 + c), r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) part[(c + j) * kBM + quarter * 32 + lane] = __uint_as_float(r[j]);
+        }
+        cluster_sync();  // every CTA's window parked and visible cluster-wide
+        const int r0 = kidx * wn / p.ks, r1 = (kidx + 1) * wn / p.ks;
+        for (int it = threadIdx.x; it < (r1 - r0) * ipr; it += kGemmThreads) {
+            const int row = r0 + it / ipr, q4 = it % ipr;
+            const int f = silu ? (q4 >> 2) * 32 + (q4 & 3) * 4 : q4 * 4;
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f), u = a;
+            const uint32_t off = part_u32 + uint32_t((row * kBM + f) * 4);
+            for (int k = 0; k < p.ks; ++k) {  // k order: deterministic
+                const uint32_t peer = uint32_t(k * CN + rank);
+                add4(a, ld_dsmem_f4(mapa_shared(off, peer)));
+                if (silu) add4(u, ld_dsmem_f4(mapa_shared(off + 64, peer)));
+            }
+            const int t = t0 + w0 + row, fg = mt * kBM + f;
+            const float v[4] = {a.x, a.y, a.z, a.w};
+            if (p.epi == EPI_F32) {
+                *reinterpret_cast<float4*>(p.out_f32 + size_t(t) * p.N + fg) = a;
+            } else if (silu) {
+                const float uu[4] = {u.x, u.y, u.z, u.w};
+                float h[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float gb = round_bf(v[j]);
+                    h[j] = round_bf(__fdividef(gb, 1.0f + __expf(-gb))) * round_bf(uu[j]);
+                }
+                uint2 hv;
+                hv.x = pack2(h[0], h[1]);
+                hv.y = pack2(h[2], h[3]);
+                *reinterpret_cast<uint2*>(p.out_bf16 + size_t(t) * (p.N / 2) + (fg / 32) * 16 + fg % 32) = hv;
+            } else {
+                float o[4] = {v[0], v[1], v[2], v[3]};
+                const size_t oi = size_t(t) * p.N + fg;
+                if (p.epi == EPI_RESID) {
+                    const uint2 rv = *reinterpret_cast<const uint2*>(p.resid + oi);
+                    const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
+                    const float2 x0 = __bfloat1622float2(rh[0]), x1 = __bfloat1622float2(rh[1]);
+                    o[0] = x0.x + round_bf(o[0]);
+                    o[1] = x0.y + round_bf(o[1]);
+                    o[2] = x1.x + round_bf(o[2]);
+                    o[3] = x1.y + round_bf(o[3]);
+                }
+                uint2 ov;
+                ov.x = pack2(o[0], o[1]);
+                ov.y = pack2(o[2], o[3]);
+                *reinterpret_cast<uint2*>(p.out_bf16 + oi) = ov;
+            }
+        }
+        cluster_sync();  // peers done reading before the next window overwrites it
+    }
+}
+
 template <int CN>
 __global__ void __maxnreg__(168)  // leaves registers for the co-resident finish kernel
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
@@ -283,8 +385,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t rank = CN > 1 ? cluster_rank() : 0;
-    const int cluster = blockIdx.x / CN;
+    const int csize = CN * p.ks;
+    const uint32_t crank = csize > 1 ? cluster_rank() : 0;
+    const uint32_t rank = crank % CN;  // feature tile within the multicast pair
+    const int kidx = int(crank) / CN;  // k share (k-split clusters)
+    const int cluster = blockIdx.x / csize;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmap_w);
@@ -302,7 +407,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
     if (warp == 2) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
-    if (CN > 1) cluster_sync();  // remote barriers initialised before any multicast lands
+    if (csize > 1) cluster_sync();  // remote barriers initialised before any multicast lands
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) GEMM_TRACE(0);
@@ -313,10 +418,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
     if (warp == 0) {
         if (elect_one()) {
             const uint64_t pol_w = policy_evict_first();
-            const uint16_t mask = (1u << CN) - 1;
+            const uint16_t mask = uint16_t(((1u << CN) - 1) << (kidx * CN));
             // weights first (independent of the previous kernel), activations after pdl_wait
             int pre = 0;
-            for_each_seg(p, cluster, [&](const Seg& w) {
+            for_each_seg(p, cluster, kidx, [&](const Seg& w) {
                 const int mt = (w.ut % cl_tiles) * CN + int(rank);
                 for (int kb = w.kb0; kb < w.kb1 && pre < p.stages; ++kb, ++pre) {
                     mbar_arrive_expect_tx(&full_bar[pre], stage_bytes);
@@ -326,7 +431,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
             });
             pdl_wait();
             int i = 0;
-            for_each_seg(p, cluster, [&](const Seg& w) {
+            for_each_seg(p, cluster, kidx, [&](const Seg& w) {
                 const int tbk = w.ut / cl_tiles;
                 const int mt = (w.ut % cl_tiles) * CN + int(rank);
                 for (int kb = w.kb0; kb < w.kb1; ++kb, ++i) {
@@ -354,7 +459,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         }
     } else if (warp == 1) {
         int i = 0, seg = 0;
-        for_each_seg(p, cluster, [&](const Seg& w) {
+        for_each_seg(p, cluster, kidx, [&](const Seg& w) {
             const int tbk = w.ut / cl_tiles;
             const int t_here = min(p.tb, p.T - tbk * p.tb);
             const int a = seg % p.n_acc;
@@ -380,7 +485,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                                       (kb > w.kb0 || k > 0) ? 1u : 0u);
                     }
                     if (CN > 1)
-                        umma_commit_mc(&empty_bar[s], (1u << CN) - 1);
+                        umma_commit_mc(&empty_bar[s], uint16_t(((1u << CN) - 1) << (kidx * CN)));
                     else
                         umma_commit(&empty_bar[s]);
                     if (kb == w.kb1 - 1) umma_commit(&tfull_bar[a]);
@@ -390,7 +495,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
             ++seg;
         });
         if (lane == 0) GEMM_TRACE(2);
-    } else if (warp >= 4) {
+    } else if (warp >= 4 && p.ks == 1) {
         pdl_wait();
         const int q = warp & 3;
         float* stage = ep_stage + q * 16 * kStageStride;
@@ -398,7 +503,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         const int row = lane >> 1, half = lane & 1;
         const size_t slot_elems = size_t(p.tb_pad) * kBM;
         int seg = 0;
-        for_each_seg(p, cluster, [&](const Seg& w) {
+        for_each_seg(p, cluster, kidx, [&](const Seg& w) {
             const int tbk = w.ut / cl_tiles;
             const int mt = (w.ut % cl_tiles) * CN + int(rank);
             const int t0 = tbk * p.tb;
@@ -485,7 +590,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         if (threadIdx.x == 128) GEMM_TRACE(3);
     }
     __syncthreads();
-    if (CN > 1) cluster_sync();
+    if (p.ks > 1) {
+        pdl_wait();
+        mbar_wait(&tfull_bar[0], 0);
+        tc_fence_after();
+        ksplit_epilogue<CN>(p, smem, tmem_base, cluster, kidx, int(rank), warp, lane);
+        tc_fence_before();
+    }
+    if (csize > 1) cluster_sync();
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(tmem_base, 512);
@@ -681,6 +793,25 @@ static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) 
     // the in-kernel last arriver pays off when its reads overlap the next tile's MMAs (data-
     // parallel tiles follow, accumulator double-buffered); otherwise a finish kernel spreads them
     p.defer = (p.sk_tiles > 0 && p.dp_rounds == 0) ? 1 : 0;
+    p.ks = 1;
+    // Very narrow GEMM (<= 1/4 of the SMs busy with whole 128-feature tiles, <= 256 tokens): no
+    // multicast pair; K split 4 ways inside clusters of 4 CTAs that sum through distributed
+    // shared memory (no workspace round trip, no second kernel). Measured: clusters of 3, 6 or 8
+    // CTAs do not all fit at once on the GPCs, 4 do.
+    static const int ksplit_env = getenv("DS_GEMM_KSPLIT") ? atoi(getenv("DS_GEMM_KSPLIT")) : 1;
+    const int tiles1 = p.t_blocks * p.m_tiles;
+    if (ksplit_env && max_clusters <= 0 && p.tb_pad <= 256 && p.KB >= 8 && kNumSMs / tiles1 >= 4) {
+        const int sb1 = kBM * kBK * 2 + p.tb_pad * kBK * 2;
+        const int st1 = std::min(12, (kSmemBudget - kFixedSmem) / sb1);
+        if (size_t(st1) * sb1 >= size_t(p.tb_pad) * kBM * 4) {
+            cn = 1;
+            p.brows = p.tb_pad;
+            p.stages = st1;
+            p.ks = 4;
+            p.n_clusters = tiles1;
+            p.dp_rounds = p.sk_tiles = p.n_sk = p.defer = p.planes = 0;
+        }
+    }
     *cn_out = cn;
     return p;
 }
@@ -715,13 +846,13 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
     if (make_tmap_2d_bf16(&tx, x, T, K, p.brows, kBK) != 0) return -5;
     const size_t smem = size_t(p.stages) * stage_bytes + fixed;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(p.n_clusters * cn);
+    cfg.gridDim = dim3(p.n_clusters * cn * p.ks);
     cfg.blockDim = dim3(kGemmThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cn;
+    attr[0].val.clusterDim.x = cn * p.ks;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
