@@ -53,7 +53,9 @@ struct GemmParams {
     int t_blocks;
     int tb;       // tokens per block (<= 512)
     int tb_pad;   // tb rounded up to 16
-    int brows;    // activation rows each CTA of the cluster loads per stage (tb_pad / CN)
+    int brows;    // activation rows per TMA box (tb_pad / CN; 2-SM: half an instruction's N)
+    int b_bytes;  // activation bytes per stage in each CTA's shared memory
+    int two_sm;   // 1: CTA pair runs tcgen05.mma.cta_group::2 (M = 256, B split by columns)
     int stages;
     int n_acc;    // TMEM accumulators
     int KB;       // k-blocks per tile
@@ -366,7 +368,15 @@ DS_DEVICE void ksplit_epilogue(const GemmParams& p, uint8_t* smem, uint32_t tmem
     }
 }
 
-template <int CN>
+DS_DEVICE void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+                 : "memory");
+}
+
+// TWO (CN == 2): the pair runs 2-SM MMAs issued by the even CTA; each CTA stages its own 128
+// weight rows and HALF of each instruction's token columns, so a stage costs 16 KB + T/2 rows
+// instead of 16 KB + T rows: about twice the pipeline depth at T >= 256.
+template <int CN, bool TWO>
 __global__ void __maxnreg__(168)  // leaves registers for the co-resident finish kernel
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
                const GemmParams p) {
@@ -374,7 +384,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     const int a_bytes = kBM * kBK * 2;
-    const int b_bytes = p.tb_pad * kBK * 2;
+    const int b_bytes = p.b_bytes;
     const int stage_bytes = a_bytes + b_bytes;
     float* ep_stage = reinterpret_cast<float*>(smem + p.stages * stage_bytes);  // 4 x 16 x 36 floats
     uint64_t* full_bar = reinterpret_cast<uint64_t*>(ep_stage + 4 * 16 * kStageStride);
@@ -396,15 +406,20 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         tma_prefetch_desc(&tmap_x);
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], CN);
+            mbar_init(&empty_bar[s], TWO ? 1 : CN);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull_bar[a], 1);
-            mbar_init(&tempty_bar[a], 4);
+            mbar_init(&tempty_bar[a], TWO ? 8 : 4);  // 2-SM: both CTAs' epilogue warps
         }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    if (warp == 2) {
+        if constexpr (TWO)
+            tmem_alloc_2sm(tmem_slot, 512);
+        else
+            tmem_alloc(tmem_slot, 512);
+    }
     tc_fence_before();
     __syncthreads();
     if (csize > 1) cluster_sync();  // remote barriers initialised before any multicast lands
@@ -414,20 +429,29 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
     pdl_launch_dependents();
 
     const int cl_tiles = p.m_tiles / CN;
+    const bool leader = !TWO || rank == 0;
 
     if (warp == 0) {
         if (elect_one()) {
             const uint64_t pol_w = policy_evict_first();
+            const uint64_t pol_x = policy_evict_last();
             const uint16_t mask = uint16_t(((1u << CN) - 1) << (kidx * CN));
+            // 2-SM: every TMA completes on the leader's full barrier, which expects both CTAs' bytes
+            auto load_w = [&](int s, int kb, int mt) {
+                if constexpr (TWO) {
+                    if (leader) mbar_arrive_expect_tx(&full_bar[s], 2 * stage_bytes);
+                    tma_load_2d_2sm(smem + s * stage_bytes, &tmap_w, mapa_shared(smem_u32(&full_bar[s]), 0),
+                                    kb * kBK, mt * kBM, pol_w);
+                } else {
+                    mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
+                    tma_load_2d_hint(smem + s * stage_bytes, &tmap_w, &full_bar[s], kb * kBK, mt * kBM, pol_w);
+                }
+            };
             // weights first (independent of the previous kernel), activations after pdl_wait
             int pre = 0;
             for_each_seg(p, cluster, kidx, [&](const Seg& w) {
                 const int mt = (w.ut % cl_tiles) * CN + int(rank);
-                for (int kb = w.kb0; kb < w.kb1 && pre < p.stages; ++kb, ++pre) {
-                    mbar_arrive_expect_tx(&full_bar[pre], stage_bytes);
-                    tma_load_2d_hint(smem + pre * stage_bytes, &tmap_w, &full_bar[pre], kb * kBK,
-                                     mt * kBM, pol_w);
-                }
+                for (int kb = w.kb0; kb < w.kb1 && pre < p.stages; ++kb, ++pre) load_w(pre, kb, mt);
             });
             pdl_wait();
             int i = 0;
@@ -441,14 +465,22 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                     uint8_t* sb = sa + a_bytes;
                     if (i >= pre) {
                         mbar_wait(&empty_bar[s], (round & 1) ^ 1);
-                        mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
-                        tma_load_2d_hint(sa, &tmap_w, &full_bar[s], kb * kBK, mt * kBM, pol_w);
+                        load_w(s, kb, mt);
                     }
-                    if (CN > 1)
+                    if constexpr (TWO) {
+                        // this CTA's half of each instruction's token columns (<= 2 instructions)
+                        const uint32_t lb = mapa_shared(smem_u32(&full_bar[s]), 0);
+                        const int n0 = min(256, p.tb_pad);
+                        tma_load_2d_2sm(sb, &tmap_x, lb, kb * kBK, tbk * p.tb + int(rank) * (n0 / 2), pol_x);
+                        if (p.tb_pad > 256)
+                            tma_load_2d_2sm(sb + 128 * 128, &tmap_x, lb, kb * kBK,
+                                            tbk * p.tb + 256 + int(rank) * ((p.tb_pad - 256) / 2), pol_x);
+                    } else if (CN > 1) {
                         tma_load_2d_mc(sb + rank * p.brows * kBK * 2, &tmap_x, &full_bar[s], kb * kBK,
                                        tbk * p.tb + int(rank) * p.brows, mask);
-                    else
+                    } else {
                         tma_load_2d(sb, &tmap_x, &full_bar[s], kb * kBK, tbk * p.tb);
+                    }
                 }
             });
             GEMM_TRACE(1);
@@ -457,7 +489,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
             for (int k = (n > p.stages ? n - p.stages : 0); k < n; ++k)
                 mbar_wait(&empty_bar[k % p.stages], (uint32_t(k / p.stages) & 1));
         }
-    } else if (warp == 1) {
+    } else if (warp == 1 && leader) {
         int i = 0, seg = 0;
         for_each_seg(p, cluster, kidx, [&](const Seg& w) {
             const int tbk = w.ut / cl_tiles;
@@ -475,20 +507,37 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                     const uint32_t sb = sa + a_bytes;
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {
-                        const int n_c = min(256, t_here - 256 * c);
-                        if (n_c <= 0) break;
-                        const uint32_t idesc = umma_idesc_bf16(kBM, (n_c + 15) & ~15);
+                        if constexpr (TWO) {
+                            // fixed split of the padded token block (matches the producer's halves)
+                            const int n_c = c == 0 ? min(256, p.tb_pad) : p.tb_pad - 256;
+                            if (n_c <= 0) break;
+                            const uint32_t idesc = umma_idesc_bf16(2 * kBM, n_c);
 #pragma unroll
-                        for (int k = 0; k < kBK / 16; ++k)
-                            umma_bf16(acc + c * 256, umma_sdesc_sw128(sa + k * 32),
-                                      umma_sdesc_sw128(sb + c * 256 * 128 + k * 32), idesc,
-                                      (kb > w.kb0 || k > 0) ? 1u : 0u);
+                            for (int k = 0; k < kBK / 16; ++k)
+                                umma_bf16_2sm(acc + c * 256, umma_sdesc_sw128(sa + k * 32),
+                                              umma_sdesc_sw128(sb + c * 128 * 128 + k * 32), idesc,
+                                              (kb > w.kb0 || k > 0) ? 1u : 0u);
+                        } else {
+                            const int n_c = min(256, t_here - 256 * c);
+                            if (n_c <= 0) break;
+                            const uint32_t idesc = umma_idesc_bf16(kBM, (n_c + 15) & ~15);
+#pragma unroll
+                            for (int k = 0; k < kBK / 16; ++k)
+                                umma_bf16(acc + c * 256, umma_sdesc_sw128(sa + k * 32),
+                                          umma_sdesc_sw128(sb + c * 256 * 128 + k * 32), idesc,
+                                          (kb > w.kb0 || k > 0) ? 1u : 0u);
+                        }
                     }
-                    if (CN > 1)
-                        umma_commit_mc(&empty_bar[s], uint16_t(((1u << CN) - 1) << (kidx * CN)));
-                    else
-                        umma_commit(&empty_bar[s]);
-                    if (kb == w.kb1 - 1) umma_commit(&tfull_bar[a]);
+                    if constexpr (TWO) {
+                        umma_commit_2sm(&empty_bar[s], 0x3);
+                        if (kb == w.kb1 - 1) umma_commit_2sm(&tfull_bar[a], 0x3);
+                    } else {
+                        if (CN > 1)
+                            umma_commit_mc(&empty_bar[s], uint16_t(((1u << CN) - 1) << (kidx * CN)));
+                        else
+                            umma_commit(&empty_bar[s]);
+                        if (kb == w.kb1 - 1) umma_commit(&tfull_bar[a]);
+                    }
                 }
                 __syncwarp();
             }
@@ -584,7 +633,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         seg_done:
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty_bar[a]);
+            if (lane == 0) {
+                if constexpr (TWO)
+                    mbar_arrive_remote(mapa_shared(smem_u32(&tempty_bar[a]), 0));  // leader's MMA
+                else
+                    mbar_arrive(&tempty_bar[a]);
+            }
             ++seg;
         });
         if (threadIdx.x == 128) GEMM_TRACE(3);
@@ -600,7 +654,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
     if (csize > 1) cluster_sync();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, 512);
+        if constexpr (TWO)
+            tmem_dealloc_2sm(tmem_base, 512);
+        else
+            tmem_dealloc(tmem_base, 512);
     }
 }
 
@@ -763,7 +820,14 @@ static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) 
     if (cn == 1 && p.tb_pad > 256) { p.T = -9; return p; }
     p.brows = p.tb_pad / cn;
     p.KB = K / kBK;
-    const int stage_bytes = kBM * kBK * 2 + p.tb_pad * kBK * 2;
+    p.b_bytes = p.tb_pad * kBK * 2;
+    static const int two_sm_env = getenv("DS_GEMM_2SM") ? atoi(getenv("DS_GEMM_2SM")) : 1;
+    if (cn == 2 && two_sm_env) {  // 2-SM MMA: half of each instruction's tokens per CTA
+        p.two_sm = 1;
+        p.brows = p.tb_pad <= 256 ? p.tb_pad / 2 : 128;
+        p.b_bytes = p.tb_pad <= 256 ? p.tb_pad / 2 * 128 : 2 * 128 * 128;
+    }
+    const int stage_bytes = kBM * kBK * 2 + p.b_bytes;
     p.stages = (kSmemBudget - kFixedSmem) / stage_bytes;
     if (p.stages > 12) p.stages = 12;
     if (p.stages < 2) { p.T = -4; return p; }
@@ -805,6 +869,8 @@ static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) 
         const int st1 = std::min(12, (kSmemBudget - kFixedSmem) / sb1);
         if (size_t(st1) * sb1 >= size_t(p.tb_pad) * kBM * 4) {
             cn = 1;
+            p.two_sm = 0;
+            p.b_bytes = p.tb_pad * kBK * 2;
             p.brows = p.tb_pad;
             p.stages = st1;
             p.ks = 4;
@@ -826,7 +892,7 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
     GemmParams p = plan_gemm(T, N, K, max_clusters, &cn);
     if (p.T < 0) return p.T;
     const int tiles = p.t_blocks * (p.m_tiles / cn);
-    const int stage_bytes = kBM * kBK * 2 + p.tb_pad * kBK * 2;
+    const int stage_bytes = kBM * kBK * 2 + p.b_bytes;
     const int fixed = kFixedSmem;
     // workspace: [counters: kCounterInts, shared by every shape: a launch leaves them all 0]
     //            [slots: n_clusters * 2 * cn * tb_pad * 128 floats]
@@ -860,8 +926,9 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     const CUtensorMap& tw = *reinterpret_cast<const CUtensorMap*>(w.tmap);
-    cudaError_t e = cn == 2 ? cudaLaunchKernelEx(&cfg, gemm_tc_kernel<2>, tw, tx, p)
-                            : cudaLaunchKernelEx(&cfg, gemm_tc_kernel<1>, tw, tx, p);
+    cudaError_t e = p.two_sm ? cudaLaunchKernelEx(&cfg, gemm_tc_kernel<2, true>, tw, tx, p)
+                    : cn == 2 ? cudaLaunchKernelEx(&cfg, gemm_tc_kernel<2, false>, tw, tx, p)
+                              : cudaLaunchKernelEx(&cfg, gemm_tc_kernel<1, false>, tw, tx, p);
     if (e != cudaSuccess) return -6;
     static const bool no_finish = getenv("DS_GEMM_NOFINISH") != nullptr;  // debug: timing only
     if (p.planes && defer) {
@@ -893,13 +960,15 @@ int gemm_weight_init(GemmWeight* w, const __nv_bfloat16* data, int N, int K) {
 // first launch, which can wait on in-flight work such as a spinning NCCL receive).
 void preload_gemm() {
     cudaFuncAttributes a;
-    cudaFuncGetAttributes(&a, gemm_tc_kernel<1>);
-    cudaFuncGetAttributes(&a, gemm_tc_kernel<2>);
+    cudaFuncGetAttributes(&a, gemm_tc_kernel<1, false>);
+    cudaFuncGetAttributes(&a, gemm_tc_kernel<2, false>);
+    cudaFuncGetAttributes(&a, gemm_tc_kernel<2, true>);
     cudaFuncGetAttributes(&a, splitk_reduce_kernel);
     cudaFuncGetAttributes(&a, splitk_finish_kernel<1>);
     cudaFuncGetAttributes(&a, splitk_finish_kernel<2>);
-    cudaFuncSetAttribute(gemm_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
-    cudaFuncSetAttribute(gemm_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
+    cudaFuncSetAttribute(gemm_tc_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
+    cudaFuncSetAttribute(gemm_tc_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
+    cudaFuncSetAttribute(gemm_tc_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
 }
 
 }  // namespace ds

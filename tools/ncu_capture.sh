@@ -9,7 +9,7 @@ mkdir -p "$OUT"
 what=${1:-all}
 DRV="python tools/step_driver.py --circuits 300"
 if [[ $what == launches || $what == all ]]; then
-  ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 115000 --launch-count 900 \
+  ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 70000 --launch-count 600 \
       --csv --log-file "$OUT/launches.csv" $DRV > "$OUT/ncu_launches.log" 2>&1 || true
 fi
 if [[ $what == full || $what == all ]]; then
