@@ -851,9 +851,13 @@ static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) 
         if (size_t(p.n_sk / p.sk_tiles) * T * N <= kWorkspaceFloats - kCounterInts)
             p.planes = p.n_sk / p.sk_tiles;
     }
-    // single TMEM accumulator: the remainder tiles run whole (a last arriver's reads would stall
-    // the next tile's MMAs), i.e. n_sk = sk_tiles gives every remainder cluster one whole tile
-    if (p.dp_rounds > 0 && p.tb_pad > 256) p.n_sk = p.sk_tiles;
+    // Remainder tiles run whole (n_sk = sk_tiles: one whole tile per remainder cluster) above
+    // 128 tokens: half the SMs still saturate HBM in the last round, while the last arriver's
+    // piece reads delay its next epilogue (measured at T = 180 / 256: 49 / 55 us whole vs 55 / 64
+    // stream-K); at <= 128 tokens stream-K balancing wins (e.g. 40.9 vs 44.0 us at T = 16).
+    static const int whole_env = getenv("DS_GEMM_WHOLE") ? atoi(getenv("DS_GEMM_WHOLE")) : -1;
+    const bool whole = whole_env >= 0 ? whole_env != 0 : p.tb_pad > 128;
+    if (p.dp_rounds > 0 && whole) p.n_sk = p.sk_tiles;
     // the in-kernel last arriver pays off when its reads overlap the next tile's MMAs (data-
     // parallel tiles follow, accumulator double-buffered); otherwise a finish kernel spreads them
     p.defer = (p.sk_tiles > 0 && p.dp_rounds == 0) ? 1 : 0;
