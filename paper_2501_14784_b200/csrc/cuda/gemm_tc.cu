@@ -56,6 +56,8 @@ struct GemmParams {
     int brows;    // activation rows per TMA box (tb_pad / CN; 2-SM: half an instruction's N)
     int b_bytes;  // activation bytes per stage in each CTA's shared memory
     int two_sm;   // 1: CTA pair runs tcgen05.mma.cta_group::2 (M = 256, B split by columns)
+    int tb_fast;  // 1: tile index runs token blocks fastest (token-split narrow GEMMs: the blocks
+                  //    sharing a weight tile stream it concurrently, L2 serves the re-reads)
     int stages;
     int n_acc;    // TMEM accumulators
     int KB;       // k-blocks per tile
@@ -118,6 +120,14 @@ DS_DEVICE void umma_commit_mc(uint64_t* bar, uint16_t mask) {
 struct Seg {
     int ut, kb0, kb1, which;
 };
+// Token block and (cluster-level) feature tile of tile index ut.
+DS_DEVICE int tile_tbk(const GemmParams& p, int ut, int cl_tiles) {
+    return p.tb_fast ? ut % p.t_blocks : ut / cl_tiles;
+}
+DS_DEVICE int tile_mtc(const GemmParams& p, int ut, int cl_tiles) {
+    return p.tb_fast ? ut / p.t_blocks : ut % cl_tiles;
+}
+
 // Stream-K range of cluster c over the sk_tiles * KB iteration space.
 DS_DEVICE int sk_begin(const GemmParams& p, int c) {
     return int((long long)c * p.sk_tiles * p.KB / p.n_sk);
@@ -300,8 +310,8 @@ template <int CN>
 DS_DEVICE void ksplit_epilogue(const GemmParams& p, uint8_t* smem, uint32_t tmem_base, int cluster,
                                int kidx, int rank, int warp, int lane) {
     const int cl_tiles = p.m_tiles / CN;
-    const int tbk = cluster / cl_tiles;
-    const int mt = (cluster % cl_tiles) * CN + rank;
+    const int tbk = tile_tbk(p, cluster, cl_tiles);
+    const int mt = tile_mtc(p, cluster, cl_tiles) * CN + rank;
     const int t0 = tbk * p.tb;
     const int t_here = min(p.tb, p.T - t0);
     float* part = reinterpret_cast<float*>(smem);  // [256 tokens][128 features]
@@ -450,14 +460,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
             // weights first (independent of the previous kernel), activations after pdl_wait
             int pre = 0;
             for_each_seg(p, cluster, kidx, [&](const Seg& w) {
-                const int mt = (w.ut % cl_tiles) * CN + int(rank);
+                const int mt = tile_mtc(p, w.ut, cl_tiles) * CN + int(rank);
                 for (int kb = w.kb0; kb < w.kb1 && pre < p.stages; ++kb, ++pre) load_w(pre, kb, mt);
             });
             pdl_wait();
             int i = 0;
             for_each_seg(p, cluster, kidx, [&](const Seg& w) {
-                const int tbk = w.ut / cl_tiles;
-                const int mt = (w.ut % cl_tiles) * CN + int(rank);
+                const int tbk = tile_tbk(p, w.ut, cl_tiles);
+                const int mt = tile_mtc(p, w.ut, cl_tiles) * CN + int(rank);
                 for (int kb = w.kb0; kb < w.kb1; ++kb, ++i) {
                     const int s = i % p.stages;
                     const uint32_t round = i / p.stages;
@@ -492,7 +502,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
     } else if (warp == 1 && leader) {
         int i = 0, seg = 0;
         for_each_seg(p, cluster, kidx, [&](const Seg& w) {
-            const int tbk = w.ut / cl_tiles;
+            const int tbk = tile_tbk(p, w.ut, cl_tiles);
             const int t_here = min(p.tb, p.T - tbk * p.tb);
             const int a = seg % p.n_acc;
             const uint32_t acc = tmem_base + uint32_t(a * 256);
@@ -553,8 +563,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         const size_t slot_elems = size_t(p.tb_pad) * kBM;
         int seg = 0;
         for_each_seg(p, cluster, kidx, [&](const Seg& w) {
-            const int tbk = w.ut / cl_tiles;
-            const int mt = (w.ut % cl_tiles) * CN + int(rank);
+            const int tbk = tile_tbk(p, w.ut, cl_tiles);
+            const int mt = tile_mtc(p, w.ut, cl_tiles) * CN + int(rank);
             const int t0 = tbk * p.tb;
             const int t_here = min(p.tb, p.T - t0);
             const int a = seg % p.n_acc;
@@ -674,8 +684,8 @@ __global__ void __launch_bounds__(128) splitk_finish_kernel(const GemmParams p) 
     const int rank = (blockIdx.x / n_chunks) % CN;
     const int ut = blockIdx.x / (n_chunks * CN);
     const int cl_tiles = p.m_tiles / CN;
-    const int tbk = ut / cl_tiles;
-    const int mt = (ut % cl_tiles) * CN + rank;
+    const int tbk = tile_tbk(p, ut, cl_tiles);
+    const int mt = tile_mtc(p, ut, cl_tiles) * CN + rank;
     const int t0 = tbk * p.tb;
     const int t_here = min(p.tb, p.T - t0);
     if (ch * 16 >= t_here) return;
@@ -803,8 +813,35 @@ int gemm_launch_count(int T, int N, int K, bool deferred) {
     return 1 + ((p.defer && !(deferred && p.planes)) ? 1 : 0);
 }
 
-// Tile shape, pipeline depth and the data-parallel / stream-K partition of one GEMM (a negative
-// p.T is the error code of an unsupported shape).
+// Token block `tb` with `cn` CTAs per cluster: padding, TMA box, shared-memory stage and depth.
+static bool set_block(GemmParams& p, int tb, int cn) {
+    static const int two_sm_env = getenv("DS_GEMM_2SM") ? atoi(getenv("DS_GEMM_2SM")) : 1;
+    p.tb = tb;
+    p.t_blocks = (p.T + tb - 1) / tb;
+    p.tb_pad = (tb + 15) & ~15;
+    p.brows = p.tb_pad / cn;
+    p.b_bytes = p.tb_pad * kBK * 2;
+    p.two_sm = 0;
+    if (cn == 2 && two_sm_env) {  // 2-SM MMA: half of each instruction's tokens per CTA
+        p.two_sm = 1;
+        p.brows = p.tb_pad <= 256 ? p.tb_pad / 2 : 128;
+        p.b_bytes = p.tb_pad <= 256 ? p.tb_pad / 2 * 128 : 2 * 128 * 128;
+    }
+    const int stage_bytes = kBM * kBK * 2 + p.b_bytes;
+    p.stages = std::min(12, (kSmemBudget - kFixedSmem) / stage_bytes);
+    p.n_acc = p.tb_pad <= 256 ? 2 : 1;
+    return p.stages >= 2 && p.brows <= 256;
+}
+
+// Tile shape, pipeline depth and the work partition of one GEMM (a negative p.T is the error code
+// of an unsupported shape). Modes, by how many 128-feature tiles there are per SM:
+//  * wide (>= one wave of tiles): whole tiles data-parallel, the remainder wave stream-K split
+//    (<= 128 tokens, last-arriver fixup) or whole;
+//  * very narrow, <= 256 tokens (o / down at 8B): K split 4 ways inside 4-CTA clusters reduced
+//    through distributed shared memory;
+//  * narrow with >= 64 tokens per block: token blocks split instead of K (no partial sums; the
+//    blocks sharing a weight tile stream it at the same time, L2 serves the re-reads);
+//  * otherwise: K split into planes summed by the consumer kernel (or a reduction kernel).
 static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) {
     GemmParams p{};
     int cn = pick_cn(N);
@@ -813,36 +850,54 @@ static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) 
     p.K = K;
     if (K % kBK != 0 || N % kBM != 0) { p.T = -3; return p; }
     p.m_tiles = N / kBM;
-    p.t_blocks = (T + kMaxTB - 1) / kMaxTB;
-    p.tb = T < kMaxTB ? T : kMaxTB;
-    p.tb_pad = (p.tb + 15) & ~15;
-    if (cn == 1 && p.tb_pad > 256) cn = (p.m_tiles % 2 == 0) ? 2 : 1;  // TMA box rows <= 256
-    if (cn == 1 && p.tb_pad > 256) { p.T = -9; return p; }
-    p.brows = p.tb_pad / cn;
     p.KB = K / kBK;
-    p.b_bytes = p.tb_pad * kBK * 2;
-    static const int two_sm_env = getenv("DS_GEMM_2SM") ? atoi(getenv("DS_GEMM_2SM")) : 1;
-    if (cn == 2 && two_sm_env) {  // 2-SM MMA: half of each instruction's tokens per CTA
-        p.two_sm = 1;
-        p.brows = p.tb_pad <= 256 ? p.tb_pad / 2 : 128;
-        p.b_bytes = p.tb_pad <= 256 ? p.tb_pad / 2 * 128 : 2 * 128 * 128;
-    }
-    const int stage_bytes = kBM * kBK * 2 + p.b_bytes;
-    p.stages = (kSmemBudget - kFixedSmem) / stage_bytes;
-    if (p.stages > 12) p.stages = 12;
-    if (p.stages < 2) { p.T = -4; return p; }
-    p.n_acc = p.tb_pad <= 256 ? 2 : 1;
+    p.ks = 1;
+    if (cn == 1 && ((T < kMaxTB ? T : kMaxTB) + 15) / 16 * 16 > 256)
+        cn = (p.m_tiles % 2 == 0) ? 2 : 1;  // TMA box rows <= 256
+    if (!set_block(p, T < kMaxTB ? T : kMaxTB, cn)) { p.T = cn == 1 ? -9 : -4; return p; }
     int nc = kNumSMs / cn;
     if (max_clusters > 0 && nc > max_clusters) nc = max_clusters;
-    const int tiles = p.t_blocks * (p.m_tiles / cn);
+    const int cl_tiles = p.m_tiles / cn;
+    int tiles = p.t_blocks * cl_tiles;
+
+    static const int ksplit_env = getenv("DS_GEMM_KSPLIT") ? atoi(getenv("DS_GEMM_KSPLIT")) : 1;
+    static const int ts_min = getenv("DS_GEMM_TS_MIN") ? atoi(getenv("DS_GEMM_TS_MIN")) : 257;
+    const int tiles1 = p.t_blocks * p.m_tiles;
+    if (ksplit_env && max_clusters <= 0 && p.tb_pad <= 256 && p.KB >= 8 && kNumSMs / tiles1 >= 4 &&
+        T < ts_min) {
+        GemmParams q = p;
+        if (set_block(q, p.tb, 1) && size_t(q.stages) * (kBM * kBK * 2 + q.b_bytes) >= size_t(q.tb_pad) * kBM * 4) {
+            q.ks = 4;
+            q.n_clusters = tiles1;
+            *cn_out = 1;
+            return q;
+        }
+    }
+    // (weights must stay L2-resident across the concurrent blocks: measured at T = 320..456,
+    // q/k/v 50 MB and o 32 MB gain 25-30%, down 117 MB loses 25%; below 257 tokens the k-split
+    // cluster / plane modes win)
+    if (tiles < nc && max_clusters <= 0 && T >= ts_min && T >= 128 &&
+        size_t(N) * K * 2 <= (size_t(64) << 20)) {
+        // token split: s blocks of >= 64 tokens per weight tile, at most one wave of tiles
+        const int s_t = std::min(nc / cl_tiles, T / 64);
+        if (s_t >= 2) {
+            GemmParams q = p;
+            const int tb = std::min(kMaxTB, ((T + s_t - 1) / s_t + 15) / 16 * 16);
+            if (set_block(q, tb, cn)) {
+                q.tb_fast = 1;
+                q.n_clusters = q.t_blocks * cl_tiles;
+                q.dp_rounds = 1;
+                *cn_out = cn;
+                return q;
+            }
+        }
+    }
     // whole waves data-parallel, the remainder stream-K over all clusters
-    static const bool no_sk = getenv("DS_GEMM_NOSK") != nullptr;  // debug: whole tiles only
-    p.n_clusters = std::min(nc, no_sk ? tiles : tiles * p.KB);
+    p.n_clusters = std::min(nc, tiles * p.KB);
     p.dp_rounds = tiles / p.n_clusters;
     p.sk_tiles = tiles - p.dp_rounds * p.n_clusters;
     p.n_sk = std::min(p.n_clusters, p.sk_tiles * p.KB);
-    static const int align_env = getenv("DS_GEMM_ALIGN") ? atoi(getenv("DS_GEMM_ALIGN")) : 1;
-    if (align_env && p.dp_rounds == 0 && p.sk_tiles * 2 <= p.n_sk) {
+    if (p.dp_rounds == 0 && p.sk_tiles * 2 <= p.n_sk) {
         // narrow GEMM: every tile split into the same number of k ranges, one piece per cluster
         // (no range straddles two tiles: half the pieces of a free partition, a few idle SMs)
         p.n_sk = p.sk_tiles * std::min(p.n_sk / p.sk_tiles, p.KB);
@@ -861,27 +916,6 @@ static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) 
     // the in-kernel last arriver pays off when its reads overlap the next tile's MMAs (data-
     // parallel tiles follow, accumulator double-buffered); otherwise a finish kernel spreads them
     p.defer = (p.sk_tiles > 0 && p.dp_rounds == 0) ? 1 : 0;
-    p.ks = 1;
-    // Very narrow GEMM (<= 1/4 of the SMs busy with whole 128-feature tiles, <= 256 tokens): no
-    // multicast pair; K split 4 ways inside clusters of 4 CTAs that sum through distributed
-    // shared memory (no workspace round trip, no second kernel). Measured: clusters of 3, 6 or 8
-    // CTAs do not all fit at once on the GPCs, 4 do.
-    static const int ksplit_env = getenv("DS_GEMM_KSPLIT") ? atoi(getenv("DS_GEMM_KSPLIT")) : 1;
-    const int tiles1 = p.t_blocks * p.m_tiles;
-    if (ksplit_env && max_clusters <= 0 && p.tb_pad <= 256 && p.KB >= 8 && kNumSMs / tiles1 >= 4) {
-        const int sb1 = kBM * kBK * 2 + p.tb_pad * kBK * 2;
-        const int st1 = std::min(12, (kSmemBudget - kFixedSmem) / sb1);
-        if (size_t(st1) * sb1 >= size_t(p.tb_pad) * kBM * 4) {
-            cn = 1;
-            p.two_sm = 0;
-            p.b_bytes = p.tb_pad * kBK * 2;
-            p.brows = p.tb_pad;
-            p.stages = st1;
-            p.ks = 4;
-            p.n_clusters = tiles1;
-            p.dp_rounds = p.sk_tiles = p.n_sk = p.defer = p.planes = 0;
-        }
-    }
     *cn_out = cn;
     return p;
 }
