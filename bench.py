@@ -121,6 +121,34 @@ def roofline(kernels):
                         for k, x in kinds.items()}}
 
 
+def stage_roofline(cfg_txt, model="llama3-8b"):
+    """SURVEY.md 8(d) stage roofline of the schedule the run executes: per circuit
+    t_roof = max(FLOPs / F_sustained, bytes / BW) with FLOPs = 2·T·P_L·L + Σ_positions 4·n_h·d_h·c·L
+    + 2·R·d·V and bytes = weights + KV read once per request row group (c = group end) + KV
+    append + LM head + activations; returns the per-step sum."""
+    from paper_2501_14784_b200 import pipeline as pl
+    hbm, _, tf_sus, _ = load_peaks()
+    dm = pl.MODEL_DIMS[model]
+    d, L, nh, nkv, dh, ffn, V = (dm["d_model"], dm["n_layers"], dm["n_heads"], dm["n_kv_heads"],
+                                 dm["d_head"], dm["ffn"], dm["vocab"])
+    P_L = d * (nh + 2 * nkv) * dh + nh * dh * d + 3 * d * ffn
+    sched = pl.schedule_config(cfg_txt, CONFIGS)
+    t = fl_all = by_all = 0.0
+    for c in sched["circuits"]:
+        rows = c["rows"]
+        T = sum(r[2] for r in rows)
+        R = sum(r[3] for r in rows)
+        ctx = sum(r[1] * r[2] + r[2] * (r[2] + 1) // 2 for r in rows)
+        fl = 2.0 * T * P_L * L + 4.0 * nh * dh * ctx * L + 2.0 * R * d * V
+        by = (2.0 * P_L * L + sum(r[1] + r[2] for r in rows) * 4.0 * nkv * dh * L
+              + T * 4.0 * nkv * dh * L + 2.0 * d * V + 4.0 * T * d)
+        t += max(fl / (tf_sus * 1e12), by / (hbm * 1e9))
+        fl_all += fl
+        by_all += by
+    return {"t_roof_s_per_step": round(t, 4), "flops_per_step": fl_all, "bytes_per_step": by_all,
+            "peaks": {"tflops_sustained": tf_sus, "hbm_gbs": hbm}}
+
+
 def cpu_baseline(budget_s=20.0):
     """Oracle port (oracle/llama_ref.c, OpenMP on all host cores) on a bounded sample of the
     config-2 workload: one Llama-3-8B layer + the LM head at a 64-row decode circuit with
@@ -211,6 +239,12 @@ def run_single(args):
         "roofline": rf,
         "clocks": clk.summary(),
     }
+    try:
+        sr = stage_roofline(txt)
+        sr["frac"] = round(sr["t_roof_s_per_step"] / (dev_s / args.steps), 4)
+        out["stage_roofline"] = sr
+    except Exception as e:
+        out["stage_roofline"] = {"error": str(e)[:200]}
     if not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline()

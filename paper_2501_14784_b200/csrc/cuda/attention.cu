@@ -15,6 +15,8 @@
 // per kv head.
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -60,7 +62,7 @@ template <int DH>
 __global__ void __launch_bounds__(kAttnWarps * 32)
 attn_tc_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __restrict__ row_pos,
                const int32_t* __restrict__ row_page_off, const int32_t* __restrict__ flat_pages,
-               const int32_t* __restrict__ blocks, KvLayout kv, int layer, int splits,
+               const int32_t* __restrict__ blocks, KvLayout kv, int layer, int splits, int stride,
                __nv_bfloat16* __restrict__ o, float* __restrict__ ws) {
     pdl_launch_dependents();
     pdl_wait();
@@ -293,7 +295,7 @@ attn_tc_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __re
             if (splits == 1) {
                 o[row_head * DH + dd] = f2bf(num / den);
             } else {
-                float* dst = ws + (row_head * splits + split) * (DH + 2);
+                float* dst = ws + (row_head * stride + split) * (DH + 2);
                 dst[dd] = num;
                 if (dd == 0) {
                     dst[DH] = M;
@@ -318,7 +320,7 @@ attn_tc_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __re
                 *reinterpret_cast<uint32_t*>(dst + nt * 8 + 2 * tq) =
                     pack2(acc[nt][2 * hr] * inv, acc[nt][2 * hr + 1] * inv);
         } else {
-            float* dst = ws + (row_head * splits + split) * (DH + 2);
+            float* dst = ws + (row_head * stride + split) * (DH + 2);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
                 dst[nt * 8 + 2 * tq] = acc[nt][2 * hr];
@@ -332,13 +334,18 @@ attn_tc_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __re
     }
 }
 
+// Merges the (o, m, l) context-split partials of every row-head with row_splits[row] > 1
+// (partials at ws[(row_head * stride + split) * (DH + 2)]).
 template <int DH>
-__global__ void attn_combine_kernel(const float* __restrict__ ws, int splits,
+__global__ void attn_combine_kernel(const float* __restrict__ ws, int stride, int n_h,
+                                    const int32_t* __restrict__ row_splits,
                                     __nv_bfloat16* __restrict__ o) {
     pdl_launch_dependents();
     pdl_wait();
     const int rh = blockIdx.x;
-    const float* base = ws + size_t(rh) * splits * (DH + 2);
+    const int splits = row_splits[rh / n_h];
+    if (splits <= 1) return;  // written directly by the attention kernel
+    const float* base = ws + size_t(rh) * stride * (DH + 2);
     float M = -INFINITY;
     for (int s = 0; s < splits; ++s) M = fmaxf(M, base[s * (DH + 2) + DH]);
     for (int dd = threadIdx.x; dd < DH; dd += blockDim.x) {
@@ -374,7 +381,7 @@ template <int DH, int ST = kDecStages>
 __global__ void __launch_bounds__(kAttnWarps * 32)
 attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __restrict__ row_pos,
                    const int32_t* __restrict__ row_page_off, const int32_t* __restrict__ flat_pages,
-                   const int32_t* __restrict__ drows, KvLayout kv, int layer, int splits,
+                   const int32_t* __restrict__ drows, KvLayout kv, int layer, int splits, int stride,
                    __nv_bfloat16* __restrict__ o, float* __restrict__ ws) {
     pdl_launch_dependents();
     pdl_wait();
@@ -558,7 +565,7 @@ attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
         if (splits == 1) {
             o[row_head * DH + dd] = f2bf(num / den);
         } else {
-            float* dst = ws + (row_head * splits + split) * (DH + 2);
+            float* dst = ws + (row_head * stride + split) * (DH + 2);
             dst[dd] = num;
             if (dd == 0) {
                 dst[DH] = M;
@@ -585,10 +592,26 @@ int attention_pick_splits(int n_blocks, int n_kv, int max_ctx) {
     return s < 1 ? 1 : s;
 }
 
-int attention_launches(int n_blocks, int n_drows, int n_kv, int max_ctx) {
+// Context splits: decode rows by the CTA-count heuristic above; prompt blocks so that no CTA
+// walks more than 2 tiles (128 tokens) of the longest context (their mma.sync work, not HBM,
+// bounds a long prompt chunk). Both shrink until T x max(splits) partials fit the workspace.
+void attention_splits(int T, int n_h, int d_head, int n_blocks, int n_drows, int n_kv, int max_ctx,
+                      size_t ws_floats, int* s_prompt, int* s_decode) {
+    int sd = n_drows > 0 ? attention_pick_splits(n_blocks + n_drows, n_kv, max_ctx) : 1;
+    const int tiles = (max_ctx + kTile - 1) / kTile;
+    static const int sp_tiles = getenv("DS_ATTN_PROMPT_TILES") ? atoi(getenv("DS_ATTN_PROMPT_TILES")) : 0;
+    int sp = (n_blocks > 0 && sp_tiles > 0) ? std::min(8, std::max(1, (tiles + sp_tiles - 1) / sp_tiles)) : 1;
+    while (std::max(sp, sd) > 1 && attention_workspace_floats(T, n_h, d_head, std::max(sp, sd)) > ws_floats) {
+        if (sp >= sd) --sp; else --sd;
+    }
+    *s_prompt = sp;
+    *s_decode = sd;
+}
+
+int attention_launches(int n_blocks, int n_drows, int s_prompt, int s_decode) {
     if (n_blocks + n_drows <= 0) return 0;
     return (n_blocks > 0) + (n_drows > 0) +
-           (attention_pick_splits(n_blocks + n_drows, n_kv, max_ctx) > 1 ? 1 : 0);
+           (((n_blocks > 0 && s_prompt > 1) || (n_drows > 0 && s_decode > 1)) ? 1 : 0);
 }
 
 size_t attention_workspace_floats(int T, int n_h, int d_head, int splits) {
@@ -608,52 +631,60 @@ static int decode_stages() {
 template <int DH>
 static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,
                    const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
-                   int n_blocks, const int32_t* drows, int n_drows, const KvLayout& kv, int layer,
-                   int splits, __nv_bfloat16* o, float* ws, cudaStream_t stream) {
+                   int n_blocks, const int32_t* drows, int n_drows, const int32_t* row_splits,
+                   const KvLayout& kv, int layer, int sp, int sd, __nv_bfloat16* o, float* ws,
+                   cudaStream_t stream) {
+    // timing experiments only (results invalid): DS_ATTN_SKIP bit 0 prompt blocks, 1 decode rows,
+    // 2 combine
+    static const int skip = getenv("DS_ATTN_SKIP") ? atoi(getenv("DS_ATTN_SKIP")) : 0;
+    if (skip & 1) n_blocks = 0;
+    if (skip & 2) n_drows = 0;
+    const int stride = std::max(sp, sd);
     if (n_blocks > 0)
-        launch_pdl(attn_tc_kernel<DH>, dim3(n_blocks * kv.n_kv * splits), dim3(kAttnWarps * 32),
+        launch_pdl(attn_tc_kernel<DH>, dim3(n_blocks * kv.n_kv * sp), dim3(kAttnWarps * 32),
                    sizeof(AttnSmem<DH>), stream, q, n_h, row_pos, row_page_off, flat_pages, blocks, kv,
-                   layer, splits, o, ws);
+                   layer, sp, stride, o, ws);
     if (n_drows > 0) {
-        const dim3 grid(n_drows * kv.n_kv * splits), block(kAttnWarps * 32);
+        const dim3 grid(n_drows * kv.n_kv * sd), block(kAttnWarps * 32);
         switch (decode_stages()) {
             case 3:
                 launch_pdl(attn_decode_kernel<DH, 3>, grid, block, sizeof(DecSmem<DH, 3>), stream, q,
-                           n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, splits, o, ws);
+                           n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws);
                 break;
             case 4:
                 launch_pdl(attn_decode_kernel<DH, 4>, grid, block, sizeof(DecSmem<DH, 4>), stream, q,
-                           n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, splits, o, ws);
+                           n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws);
                 break;
             default:
                 launch_pdl(attn_decode_kernel<DH, 2>, grid, block, sizeof(DecSmem<DH, 2>), stream, q,
-                           n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, splits, o, ws);
+                           n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws);
         }
     }
-    if (splits > 1)
+    if (((n_blocks > 0 && sp > 1) || (n_drows > 0 && sd > 1)) && !(skip & 4))
         launch_pdl(attn_combine_kernel<DH>, dim3(T * n_h), dim3(DH), 0, stream, (const float*)ws,
-                   splits, o);
+                   stride, n_h, row_splits, o);
 }
 
 int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,
                     const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
-                    int n_blocks, const int32_t* drows, int n_drows, const KvLayout& kv, int layer,
-                    int max_ctx, __nv_bfloat16* o, float* ws, size_t ws_floats, cudaStream_t stream) {
+                    int n_blocks, const int32_t* drows, int n_drows, const int32_t* row_splits,
+                    const KvLayout& kv, int layer, int s_prompt, int s_decode, __nv_bfloat16* o,
+                    float* ws, size_t ws_floats, cudaStream_t stream) {
     if (T <= 0 || n_blocks + n_drows <= 0) return 0;
     if (n_h % kv.n_kv != 0 || n_h / kv.n_kv > 16) return -1;
-    int splits = attention_pick_splits(n_blocks + n_drows, kv.n_kv, max_ctx);
-    if (splits > 1 && attention_workspace_floats(T, n_h, kv.d_head, splits) > ws_floats) splits = 1;
+    if (attention_workspace_floats(T, n_h, kv.d_head, std::max(s_prompt, s_decode)) > ws_floats &&
+        std::max(s_prompt, s_decode) > 1)
+        return -4;
     if (kv.d_head == 128)
-        launch<128>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, drows, n_drows, kv,
-                    layer, splits, o, ws, stream);
+        launch<128>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, drows, n_drows,
+                    row_splits, kv, layer, s_prompt, s_decode, o, ws, stream);
     else if (kv.d_head == 64)
-        launch<64>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, drows, n_drows, kv,
-                   layer, splits, o, ws, stream);
+        launch<64>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, drows, n_drows,
+                   row_splits, kv, layer, s_prompt, s_decode, o, ws, stream);
     else
         return -2;
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -3;
 }
-
 }  // namespace ds
 
 namespace ds {

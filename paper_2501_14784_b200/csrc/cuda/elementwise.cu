@@ -280,7 +280,7 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int V, int32_t* 
             const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
             if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
         }
-        if (threadIdx.x == 0) ids[blockIdx.x] = bi;
+        if (threadIdx.x == 0) ids[blockIdx.x] = bi < V ? bi : 0;  // all-NaN row: stay in range
     }
 }
 void argmax_rows(const float* logits, int R, int V, int32_t* ids, cudaStream_t stream) {

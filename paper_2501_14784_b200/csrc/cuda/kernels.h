@@ -86,14 +86,18 @@ void rope_kv_append(const __nv_bfloat16* qkv, int T, int n_h, int n_kv, int d_he
 // Prompt query blocks: blocks[3*i] = first row, [3*i+1] = consecutive positions
 // (<= attention_block_positions() rows of one request), [3*i+2] = 0. Decode rows (one query
 // position each) are listed separately in drows[] and go to the decode kernel.
+// Context splits: s_prompt for the prompt blocks, s_decode for the decode rows; row_splits[t]
+// (device) = the split count of row t's kind, read by the combine kernel.
 int attention_block_positions(int n_h, int n_kv);
-int attention_launches(int n_blocks, int n_drows, int n_kv, int max_ctx);
+void attention_splits(int T, int n_h, int d_head, int n_blocks, int n_drows, int n_kv, int max_ctx,
+                      size_t ws_floats, int* s_prompt, int* s_decode);
+int attention_launches(int n_blocks, int n_drows, int s_prompt, int s_decode);
 size_t attention_workspace_floats(int T, int n_h, int d_head, int splits);
 int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,
                     const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
-                    int n_blocks, const int32_t* drows, int n_drows, const KvLayout& kv, int layer,
-                    int max_ctx, __nv_bfloat16* o, float* ws, size_t ws_floats,
-                    cudaStream_t stream);
+                    int n_blocks, const int32_t* drows, int n_drows, const int32_t* row_splits,
+                    const KvLayout& kv, int layer, int s_prompt, int s_decode, __nv_bfloat16* o,
+                    float* ws, size_t ws_floats, cudaStream_t stream);
 
 // ids[r] = argmax_v logits[r, v] (lowest index wins ties).
 void argmax_rows(const float* logits, int R, int V, int32_t* ids, cudaStream_t stream);

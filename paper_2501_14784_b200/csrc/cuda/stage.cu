@@ -290,7 +290,8 @@ ds_status ds_stage_create(int32_t device, const ds_model_desc* md, int64_t layer
         s->ws_floats = ds::gemm_workspace_floats();
         if ((st = A((void**)&s->ws, s->ws_floats * 4))) { delete s; return st; }
         CK(cudaMemset(s->ws, 0, s->ws_floats * 4));
-        s->attn_ws_floats = (R + 320) * m.n_heads * size_t(m.d_head + 2);
+        // context-split partials: up to 4 per row (prompt chunks split up to 8 ways when short)
+        s->attn_ws_floats = (4 * R + 1184) * m.n_heads * size_t(m.d_head + 2);
         if ((st = A((void**)&s->attn_ws, s->attn_ws_floats * 4))) { delete s; return st; }
     }
     s->meta_cap = 16 * R + size_t(max_slots) * 64 + R * size_t((m.max_seq_len + 255) / 256) + 64;
@@ -528,7 +529,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     MbKv& k = s->mbs[mb];
 
     // ---- rows -> pages + metadata (host)
-    int T = 0, R = 0, P = 0, max_ctx = 1, n_blk = 0, n_drow = 0;
+    int T = 0, R = 0, P = 0, max_ctx = 1, n_blk = 0, n_drow = 0, s_prompt = 1, s_decode = 1;
     for (int64_t i = 0; i < n_rows; ++i) {
         const ds_row& r = rows[i];
         if (r.slot < 0 || r.slot >= s->max_slots || r.n_tok < 1 || r.pos < 0 ||
@@ -570,7 +571,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
                                                    std::to_string(mb) + " has non-resident pages");
 
     const int prevR = int(k.prev_logit_slots.size());
-    const size_t need_meta = size_t(10) * T + 2 * size_t(R) + P + prevR + 8;
+    const size_t need_meta = size_t(11) * T + 2 * size_t(R) + P + prevR + 8;
     if (need_meta > s->meta_cap) return ds_fail(DS_ERR_ARG, "step metadata exceeds capacity");
     const int buf = s->meta_buf;
     s->meta_buf ^= 1;
@@ -584,7 +585,8 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     int32_t* logit_rows = row_poff + T;
     int32_t* logit_slot = logit_rows + R;
     int32_t* prev_slot = logit_slot + R;
-    int32_t* blk = prev_slot + prevR;  // attention query blocks, 3 ints each (<= T blocks)
+    int32_t* rsplit = prev_slot + prevR;  // attention context splits of each row's kind
+    int32_t* blk = rsplit + T;            // attention query blocks, 3 ints each (<= T blocks)
     int32_t* flat = blk + 3 * T;
     {
         int t = 0, r = 0, poff = 0;
@@ -635,6 +637,11 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
             if (rows[i].n_tok == 1) blk[3 * n_blk + n_drow++] = tb;
             tb += rows[i].n_tok;
         }
+        ds::attention_splits(T, m.n_heads, m.d_head, n_blk, n_drow, m.n_kv_heads, max_ctx,
+                             s->attn_ws_floats, &s_prompt, &s_decode);
+        tb = 0;
+        for (int64_t i = 0; i < n_rows; ++i)
+            for (int j = 0; j < rows[i].n_tok; ++j) rsplit[tb++] = rows[i].n_tok == 1 ? s_decode : s_prompt;
     }
     const size_t meta_n = size_t(flat - hm) + P;
     CK(cudaMemcpyAsync(s->d_meta, hm, meta_n * 4, cudaMemcpyHostToDevice, s->stream));
@@ -648,7 +655,8 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     const int32_t* d_lrows = d_poff + T;
     const int32_t* d_lslot = d_lrows + R;
     const int32_t* d_prev = d_lslot + R;
-    const int32_t* d_blk = d_prev + prevR;
+    const int32_t* d_rsplit = d_prev + prevR;
+    const int32_t* d_blk = d_rsplit + T;
     const int32_t* d_flat = d_blk + 3 * T;
 
     // ---- wait for the swap-in this compute depends on
@@ -727,10 +735,10 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
         begin();
         if (!(skip & 4))
             rc |= ds::attention_paged(s->q, T, m.n_heads, d_pos, d_poff, d_flat, d_blk, n_blk,
-                                      d_blk + 3 * n_blk, n_drow, s->kv, li, max_ctx, s->attn,
-                                      s->attn_ws, s->attn_ws_floats, st);
+                                      d_blk + 3 * n_blk, n_drow, d_rsplit, s->kv, li, s_prompt,
+                                      s_decode, s->attn, s->attn_ws, s->attn_ws_floats, st);
         end_other(PK_ATTN, attn_flops, attn_bytes,
-                  ds::attention_launches(n_blk, n_drow, m.n_kv_heads, max_ctx));
+                  ds::attention_launches(n_blk, n_drow, s_prompt, s_decode));
         begin();
         if (!(skip & 16))
             rc |= ds::gemm_bf16(lw.wo, s->attn, T, ds::EPI_RESID, s->x, s->x, nullptr, s->ws,
