@@ -852,9 +852,17 @@ static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) 
     p.m_tiles = N / kBM;
     p.KB = K / kBK;
     p.ks = 1;
-    if (cn == 1 && ((T < kMaxTB ? T : kMaxTB) + 15) / 16 * 16 > 256)
-        cn = (p.m_tiles % 2 == 0) ? 2 : 1;  // TMA box rows <= 256
-    if (!set_block(p, T < kMaxTB ? T : kMaxTB, cn)) { p.T = cn == 1 ? -9 : -4; return p; }
+    // Token block: <= 512 (the TMEM columns); above `tb_max` tokens the blocks shrink to 256
+    // (double-buffered accumulators: the epilogue overlaps the next tile) and run token-block-
+    // fastest so the blocks sharing a weight tile stream it concurrently (L2 serves the re-reads).
+    static const int tb_max = getenv("DS_GEMM_TB_MAX") ? atoi(getenv("DS_GEMM_TB_MAX")) : kMaxTB;
+    int tb0 = T < kMaxTB ? T : kMaxTB;
+    if (T > tb_max) {
+        tb0 = std::min(tb0, 256);
+        p.tb_fast = 1;
+    }
+    if (cn == 1 && (tb0 + 15) / 16 * 16 > 256) cn = (p.m_tiles % 2 == 0) ? 2 : 1;  // TMA box <= 256
+    if (!set_block(p, tb0, cn)) { p.T = cn == 1 ? -9 : -4; return p; }
     int nc = kNumSMs / cn;
     if (max_clusters > 0 && nc > max_clusters) nc = max_clusters;
     const int cl_tiles = p.m_tiles / cn;
@@ -897,6 +905,12 @@ static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) 
     p.dp_rounds = tiles / p.n_clusters;
     p.sk_tiles = tiles - p.dp_rounds * p.n_clusters;
     p.n_sk = std::min(p.n_clusters, p.sk_tiles * p.KB);
+    if (p.dp_rounds == 0 && p.sk_tiles * 2 > p.n_sk) {
+        // more than half a wave of tiles: run them whole (one round), no partial sums
+        p.n_clusters = p.sk_tiles;
+        p.dp_rounds = 1;
+        p.sk_tiles = p.n_sk = 0;
+    }
     if (p.dp_rounds == 0 && p.sk_tiles * 2 <= p.n_sk) {
         // narrow GEMM: every tile split into the same number of k ranges, one piece per cluster
         // (no range straddles two tiles: half the pieces of a free partition, a few idle SMs)
