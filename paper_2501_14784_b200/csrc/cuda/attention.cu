@@ -51,33 +51,42 @@ DS_DEVICE void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// ------------------------------------------------------------------ prompt blocks ----
+// One (prompt query block, KV head, context split) per CTA of 8 warps: warp w owns q rows
+// 16*(w%4).. of the block (<= 64 = positions x G heads) and the tiles of parity w/4, so the two
+// halves of the CTA walk alternate 64-token K/V tiles at the same time (half the serial chain of
+// a long prompt chunk) and merge their softmax states through shared memory at the end. Tile
+// pairs are double-buffered with cp.async.
+constexpr int kPromptWarps = 8;
+
 template <int DH>
-struct AttnSmem {
-    __nv_bfloat16 k[2][kTile][DH + 8];
-    __nv_bfloat16 v[2][kTile][DH + 8];
+struct PromptSmem {
+    __nv_bfloat16 k[2][2][kTile][DH + 8];  // [pair buffer][parity]
+    __nv_bfloat16 v[2][2][kTile][DH + 8];
 };
 
-// blocks: [n_blocks][3] = (first row t0, n positions, decode flag)
+// blocks: [n_blocks][3] = (first row t0, n positions, unused)
 template <int DH>
-__global__ void __launch_bounds__(kAttnWarps * 32)
-attn_tc_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __restrict__ row_pos,
-               const int32_t* __restrict__ row_page_off, const int32_t* __restrict__ flat_pages,
-               const int32_t* __restrict__ blocks, KvLayout kv, int layer, int splits, int stride,
-               __nv_bfloat16* __restrict__ o, float* __restrict__ ws) {
+__global__ void __launch_bounds__(kPromptWarps * 32)
+attn_prompt_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __restrict__ row_pos,
+                   const int32_t* __restrict__ row_page_off, const int32_t* __restrict__ flat_pages,
+                   const int32_t* __restrict__ blocks, KvLayout kv, int layer, int splits, int stride,
+                   __nv_bfloat16* __restrict__ o, float* __restrict__ ws) {
     pdl_launch_dependents();
     pdl_wait();
     extern __shared__ __align__(16) uint8_t attn_smem[];
-    AttnSmem<DH>& sm = *reinterpret_cast<AttnSmem<DH>*>(attn_smem);
+    PromptSmem<DH>& sm = *reinterpret_cast<PromptSmem<DH>*>(attn_smem);
     constexpr int NT = DH / 8;   // output n-tiles
     constexpr int KS = DH / 16;  // k-steps over d_head
+    constexpr int SN = kTile / 8;
     const int n_kv = kv.n_kv;
     const int G = n_h / n_kv;
     const int split = blockIdx.x % splits;
     const int kvh = (blockIdx.x / splits) % n_kv;
     const int bi = blockIdx.x / (splits * n_kv);
     const int t0 = blocks[3 * bi], npos = blocks[3 * bi + 1];
-    const bool decode = blocks[3 * bi + 2] != 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rg = warp & 3, par = warp >> 2;
     const int g = lane >> 2, tq = lane & 3;
     const int rows = npos * G;  // q rows of this block: r = p * G + h
     const int pos0 = row_pos[t0];
@@ -86,8 +95,7 @@ attn_tc_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __re
     const int tile0 = split * n_tiles / splits, tile1 = (split + 1) * n_tiles / splits;
     const int32_t* pages = flat_pages + row_page_off[t0];
 
-    // this warp's 16 q rows (prefill) or all rows (decode, <= 16)
-    const int r_base = decode ? 0 : warp * 16;
+    const int r_base = rg * 16;
     const bool warp_active = r_base < rows;
     // Q fragments, pre-scaled by log2(e)/sqrt(d_head)
     uint32_t qa[KS][4];
@@ -101,14 +109,13 @@ attn_tc_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __re
             float x0 = 0.f, x1 = 0.f;
             if (r < rows) {
                 const int p = r / G, h = r % G;
-                const __nv_bfloat16* src = q + (size_t(t0 + p) * n_h + kvh * G + h) * DH + col;
-                const __nv_bfloat162 v2 = *reinterpret_cast<const __nv_bfloat162*>(src);
+                const __nv_bfloat162 v2 = *reinterpret_cast<const __nv_bfloat162*>(
+                    q + (size_t(t0 + p) * n_h + kvh * G + h) * DH + col);
                 x0 = __bfloat162float(v2.x) * qs;
                 x1 = __bfloat162float(v2.y) * qs;
             }
             qa[kk][i] = pack2(x0, x1);
         }
-    // per-thread row positions (rows g and g+8 of this warp's slice)
     int rpos[2];
 #pragma unroll
     for (int hr = 0; hr < 2; ++hr) {
@@ -124,75 +131,72 @@ attn_tc_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __re
     const size_t head_k = ((size_t(layer) * 2 + 0) * n_kv + kvh) * 256 * DH;
     const size_t head_v = ((size_t(layer) * 2 + 1) * n_kv + kvh) * 256 * DH;
     constexpr int CHUNKS = kTile * DH / 8;  // 16-byte chunks per K (or V) tile
-    auto load_tile = [&](int tile, int buf) {
-        const int tok0 = tile * kTile;
-        const size_t base = size_t(pages[tok0 >> 8]) * kv.page_elems + size_t(tok0 & 255) * DH;
-        const __nv_bfloat16* ks = kv.pool + base + head_k;
-        const __nv_bfloat16* vs = kv.pool + base + head_v;
-        for (int i = threadIdx.x; i < CHUNKS; i += blockDim.x) {
-            const int r = i / (DH / 8), c = (i % (DH / 8)) * 8;
-            cp_async16(&sm.k[buf][r][c], ks + size_t(r) * DH + c);
-            cp_async16(&sm.v[buf][r][c], vs + size_t(r) * DH + c);
+    const int n_pairs = (tile1 - tile0 + 1) / 2;
+    auto load_pair = [&](int pi, int buf) {
+        for (int pp = 0; pp < 2; ++pp) {
+            const int tile = tile0 + 2 * pi + pp;
+            if (tile >= tile1) break;
+            const int tok0 = tile * kTile;
+            const size_t base = size_t(pages[tok0 >> 8]) * kv.page_elems + size_t(tok0 & 255) * DH;
+            const __nv_bfloat16* ks = kv.pool + base + head_k;
+            const __nv_bfloat16* vs = kv.pool + base + head_v;
+            for (int i = threadIdx.x; i < CHUNKS; i += blockDim.x) {
+                const int r = i / (DH / 8), c = (i % (DH / 8)) * 8;
+                cp_async16(&sm.k[buf][pp][r][c], ks + size_t(r) * DH + c);
+                cp_async16(&sm.v[buf][pp][r][c], vs + size_t(r) * DH + c);
+            }
         }
         cp_async_commit();
     };
 
-    if (tile0 < tile1) load_tile(tile0, 0);
-    for (int tile = tile0; tile < tile1; ++tile) {
-        const int buf = (tile - tile0) & 1;
-        if (tile + 1 < tile1) {
-            load_tile(tile + 1, buf ^ 1);
+    if (n_pairs > 0) load_pair(0, 0);
+    for (int pi = 0; pi < n_pairs; ++pi) {
+        const int buf = pi & 1;
+        if (pi + 1 < n_pairs) {
+            load_pair(pi + 1, buf ^ 1);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
         __syncthreads();
-        const int tok0 = tile * kTile;
-        // zero V rows past the last valid token so 0 * garbage cannot produce NaN
-        const int valid = min(kTile, last_pos + 1 - tok0);
-        if (valid < kTile) {
+        // zero V rows past the last valid token (0 * garbage must not produce NaN)
+        for (int pp = 0; pp < 2; ++pp) {
+            const int tile = tile0 + 2 * pi + pp;
+            if (tile >= tile1) break;
+            const int valid = min(kTile, last_pos + 1 - tile * kTile);
             for (int i = threadIdx.x; i < (kTile - valid) * (DH / 8); i += blockDim.x) {
                 const int r = valid + i / (DH / 8), c = (i % (DH / 8)) * 8;
-                *reinterpret_cast<uint4*>(&sm.v[buf][r][c]) = make_uint4(0, 0, 0, 0);
+                *reinterpret_cast<uint4*>(&sm.v[buf][pp][r][c]) = make_uint4(0, 0, 0, 0);
             }
-            __syncthreads();
         }
-        if (warp_active) {
-            // token slice of this warp within the tile
-            const int n0 = decode ? warp * 16 : 0;
-            constexpr int SN_MAX = kTile / 8;
-            const int sn = decode ? 2 : SN_MAX;  // n-tiles of 8 tokens
-            float s[SN_MAX][4];
+        __syncthreads();
+        const int tile = tile0 + 2 * pi + par;
+        if (warp_active && tile < tile1) {
+            const int tok0 = tile * kTile;
+            float s[SN][4];
 #pragma unroll
-            for (int j = 0; j < SN_MAX; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
-            const uint32_t kbase = smem_u32(&sm.k[buf][0][0]);
+            for (int j = 0; j < SN; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+            const uint32_t kbase = smem_u32(&sm.k[buf][par][0][0]);
 #pragma unroll
-            for (int j = 0; j < SN_MAX; ++j) {
-                if (j >= sn) break;
+            for (int j = 0; j < SN; ++j)
 #pragma unroll
                 for (int kk = 0; kk < KS; kk += 2) {
                     const int mi = lane >> 3, rr = lane & 7;
-                    const int tok = n0 + j * 8 + rr;
-                    const int col = kk * 16 + mi * 8;
                     uint32_t b0, b1, b2, b3;
-                    ldsm_x4(kbase + uint32_t((tok * (DH + 8) + col) * 2), b0, b1, b2, b3);
+                    ldsm_x4(kbase + uint32_t(((j * 8 + rr) * (DH + 8) + kk * 16 + mi * 8) * 2), b0, b1, b2, b3);
                     mma16816(s[j], qa[kk], b0, b1);
                     mma16816(s[j], qa[kk + 1], b2, b3);
                 }
-            }
             // causal mask + online softmax (rows g and g+8)
             float mt[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-            for (int j = 0; j < SN_MAX; ++j) {
-                if (j >= sn) break;
+            for (int j = 0; j < SN; ++j)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int hr = e >> 1;
-                    const int tok = tok0 + n0 + j * 8 + 2 * tq + (e & 1);
-                    if (tok > rpos[hr]) s[j][e] = -INFINITY;
+                    if (tok0 + j * 8 + 2 * tq + (e & 1) > rpos[hr]) s[j][e] = -INFINITY;
                     mt[hr] = fmaxf(mt[hr], s[j][e]);
                 }
-            }
             float alpha[2];
 #pragma unroll
             for (int hr = 0; hr < 2; ++hr) {
@@ -203,18 +207,16 @@ attn_tc_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __re
                 m_run[hr] = mn;
             }
             float ls[2] = {0.f, 0.f};
-            uint32_t pa[SN_MAX / 2][4];
+            uint32_t pa[SN / 2][4];
 #pragma unroll
-            for (int j = 0; j < SN_MAX; ++j) {
-                if (j >= sn) break;
+            for (int j = 0; j < SN; ++j)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int hr = e >> 1;
-                    const float p = m_run[hr] == -INFINITY ? 0.f : exp2f(s[j][e] - m_run[hr]);
-                    s[j][e] = p;
-                    ls[hr] += p;
+                    const float pv = m_run[hr] == -INFINITY ? 0.f : exp2f(s[j][e] - m_run[hr]);
+                    s[j][e] = pv;
+                    ls[hr] += pv;
                 }
-            }
 #pragma unroll
             for (int hr = 0; hr < 2; ++hr) l_run[hr] = l_run[hr] * alpha[hr] + ls[hr];  // quad-partial
 #pragma unroll
@@ -225,47 +227,39 @@ attn_tc_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __re
                 acc[j][3] *= alpha[1];
             }
 #pragma unroll
-            for (int kk = 0; kk < SN_MAX / 2; ++kk) {
-                if (2 * kk >= sn) break;
+            for (int kk = 0; kk < SN / 2; ++kk) {
                 pa[kk][0] = pack2(s[2 * kk][0], s[2 * kk][1]);
                 pa[kk][1] = pack2(s[2 * kk][2], s[2 * kk][3]);
                 pa[kk][2] = pack2(s[2 * kk + 1][0], s[2 * kk + 1][1]);
                 pa[kk][3] = pack2(s[2 * kk + 1][2], s[2 * kk + 1][3]);
             }
-            const uint32_t vbase = smem_u32(&sm.v[buf][0][0]);
+            const uint32_t vbase = smem_u32(&sm.v[buf][par][0][0]);
 #pragma unroll
-            for (int kk = 0; kk < SN_MAX / 2; ++kk) {
-                if (2 * kk >= sn) break;
+            for (int kk = 0; kk < SN / 2; ++kk)
 #pragma unroll
                 for (int nt = 0; nt < NT; nt += 2) {
                     const int mi = lane >> 3, rr = lane & 7;
-                    const int tok = n0 + kk * 16 + (mi & 1) * 8 + rr;
-                    const int col = (nt + (mi >> 1)) * 8;
                     uint32_t b0, b1, b2, b3;
-                    ldsm_x4_t(vbase + uint32_t((tok * (DH + 8) + col) * 2), b0, b1, b2, b3);
+                    ldsm_x4_t(vbase + uint32_t(((kk * 16 + (mi & 1) * 8 + rr) * (DH + 8) + (nt + (mi >> 1)) * 8) * 2),
+                              b0, b1, b2, b3);
                     mma16816(acc[nt], pa[kk], b0, b1);
                     mma16816(acc[nt + 1], pa[kk], b2, b3);
                 }
-            }
         }
-        __syncthreads();  // buffer `buf` is overwritten by the prefetch two iterations later
+        __syncthreads();  // pair buffer `buf` is overwritten by the prefetch of pair pi + 2
     }
 
-    // full row sums across the quad
 #pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
+    for (int hr = 0; hr < 2; ++hr) {  // full row sums across the quad
         l_run[hr] += __shfl_xor_sync(0xffffffffu, l_run[hr], 1);
         l_run[hr] += __shfl_xor_sync(0xffffffffu, l_run[hr], 2);
     }
-
-    if (decode) {
-        // merge the 4 warps' partial states through shared memory (reusing the K buffer)
-        float* red = reinterpret_cast<float*>(&sm.k[0][0][0]);  // [4 warps][16 rows][DH + 2]
-        __syncthreads();
+    // merge the odd-tile half into the even-tile half (shared memory of the idle tile buffers)
+    float* red = reinterpret_cast<float*>(&sm.k[0][0][0][0]);  // [4 row groups][16 rows][DH + 2]
+    if (par == 1 && warp_active) {
 #pragma unroll
         for (int hr = 0; hr < 2; ++hr) {
-            const int r = g + 8 * hr;
-            float* dst = red + (warp * 16 + r) * (DH + 2);
+            float* dst = red + (rg * 16 + g + 8 * hr) * (DH + 2);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
                 dst[nt * 8 + 2 * tq] = acc[nt][2 * hr];
@@ -276,59 +270,41 @@ attn_tc_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __re
                 dst[DH + 1] = l_run[hr];
             }
         }
-        __syncthreads();
-        for (int i = threadIdx.x; i < rows * DH; i += blockDim.x) {
-            const int r = i / DH, dd = i % DH;
-            float M = -INFINITY;
-#pragma unroll
-            for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, red[(w * 16 + r) * (DH + 2) + DH]);
-            float num = 0.f, den = 0.f;
-#pragma unroll
-            for (int w = 0; w < kAttnWarps; ++w) {
-                const float* src = red + (w * 16 + r) * (DH + 2);
-                const float wt = src[DH] == -INFINITY ? 0.f : exp2f(src[DH] - M);
-                num += src[dd] * wt;
-                den += src[DH + 1] * wt;
-            }
-            const int p = r / G, h = r % G;
-            const size_t row_head = size_t(t0 + p) * n_h + kvh * G + h;
-            if (splits == 1) {
-                o[row_head * DH + dd] = f2bf(num / den);
-            } else {
-                float* dst = ws + (row_head * stride + split) * (DH + 2);
-                dst[dd] = num;
-                if (dd == 0) {
-                    dst[DH] = M;
-                    dst[DH + 1] = den;
-                }
-            }
-        }
-        return;
     }
-    if (!warp_active) return;
+    __syncthreads();
+    if (par == 1 || !warp_active) return;
 #pragma unroll
     for (int hr = 0; hr < 2; ++hr) {
         const int r = r_base + g + 8 * hr;
+        const float* oth = red + (rg * 16 + g + 8 * hr) * (DH + 2);
+        const float m1 = oth[DH], l1 = oth[DH + 1];
+        const float M = fmaxf(m_run[hr], m1);
+        const float w0 = m_run[hr] == -INFINITY ? 0.f : exp2f(m_run[hr] - M);
+        const float w1 = m1 == -INFINITY ? 0.f : exp2f(m1 - M);
+        const float L = l_run[hr] * w0 + l1 * w1;
         if (r >= rows) continue;
         const int p = r / G, h = r % G;
         const size_t row_head = size_t(t0 + p) * n_h + kvh * G + h;
         if (splits == 1) {
-            const float inv = 1.0f / l_run[hr];
+            const float inv = 1.0f / L;
             __nv_bfloat16* dst = o + row_head * DH;
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-                *reinterpret_cast<uint32_t*>(dst + nt * 8 + 2 * tq) =
-                    pack2(acc[nt][2 * hr] * inv, acc[nt][2 * hr + 1] * inv);
+            for (int nt = 0; nt < NT; ++nt) {
+                const int c = nt * 8 + 2 * tq;
+                *reinterpret_cast<uint32_t*>(dst + c) =
+                    pack2((acc[nt][2 * hr] * w0 + oth[c] * w1) * inv, (acc[nt][2 * hr + 1] * w0 + oth[c + 1] * w1) * inv);
+            }
         } else {
             float* dst = ws + (row_head * stride + split) * (DH + 2);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
-                dst[nt * 8 + 2 * tq] = acc[nt][2 * hr];
-                dst[nt * 8 + 2 * tq + 1] = acc[nt][2 * hr + 1];
+                const int c = nt * 8 + 2 * tq;
+                dst[c] = acc[nt][2 * hr] * w0 + oth[c] * w1;
+                dst[c + 1] = acc[nt][2 * hr + 1] * w0 + oth[c + 1] * w1;
             }
             if (tq == 0) {
-                dst[DH] = m_run[hr];
-                dst[DH + 1] = l_run[hr];
+                dst[DH] = M;
+                dst[DH + 1] = L;
             }
         }
     }
@@ -641,9 +617,9 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
     if (skip & 2) n_drows = 0;
     const int stride = std::max(sp, sd);
     if (n_blocks > 0)
-        launch_pdl(attn_tc_kernel<DH>, dim3(n_blocks * kv.n_kv * sp), dim3(kAttnWarps * 32),
-                   sizeof(AttnSmem<DH>), stream, q, n_h, row_pos, row_page_off, flat_pages, blocks, kv,
-                   layer, sp, stride, o, ws);
+        launch_pdl(attn_prompt_kernel<DH>, dim3(n_blocks * kv.n_kv * sp), dim3(kPromptWarps * 32),
+                   sizeof(PromptSmem<DH>), stream, q, n_h, row_pos, row_page_off, flat_pages, blocks,
+                   kv, layer, sp, stride, o, ws);
     if (n_drows > 0) {
         const dim3 grid(n_drows * kv.n_kv * sd), block(kAttnWarps * 32);
         switch (decode_stages()) {
@@ -698,14 +674,14 @@ static void preload_decode() {
 
 void preload_attention() {
     cudaFuncAttributes a;
-    cudaFuncGetAttributes(&a, attn_tc_kernel<128>);
-    cudaFuncGetAttributes(&a, attn_tc_kernel<64>);
+    cudaFuncGetAttributes(&a, attn_prompt_kernel<128>);
+    cudaFuncGetAttributes(&a, attn_prompt_kernel<64>);
     cudaFuncGetAttributes(&a, attn_combine_kernel<128>);
     cudaFuncGetAttributes(&a, attn_combine_kernel<64>);
-    cudaFuncSetAttribute(attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(sizeof(AttnSmem<128>)));
-    cudaFuncSetAttribute(attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(sizeof(AttnSmem<64>)));
+    cudaFuncSetAttribute(attn_prompt_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(PromptSmem<128>)));
+    cudaFuncSetAttribute(attn_prompt_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(PromptSmem<64>)));
     preload_decode<128, 2>();
     preload_decode<128, 3>();
     preload_decode<128, 4>();
