@@ -10,6 +10,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("dump")
 ap.add_argument("out")
 ap.add_argument("--layers", type=int, default=32, help="layers of the measured stage")
+ap.add_argument("--model", default="Llama-3-8B")
 a = ap.parse_args()
 d = json.load(open(a.dump))
 steps = []
@@ -27,7 +28,7 @@ for b, ms in rows:
     last = max(last, ms)
     out.append((b, last))
 with open(a.out, "w") as f:
-    f.write(f"# measured on B200: Llama-3-8B stage of {a.layers} layers, median ms per stage step by "
+    f.write(f"# measured on B200: {a.model} stage of {a.layers} layers, median ms per stage step by "
             f"row bucket (tools/make_calibration.py from bench.py --dump)\n")
     f.write("batch_size,total_time_ms\n")
     for b, ms in out:
