@@ -871,11 +871,13 @@ static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) 
     static const int ksplit_env = getenv("DS_GEMM_KSPLIT") ? atoi(getenv("DS_GEMM_KSPLIT")) : 1;
     static const int ts_min = getenv("DS_GEMM_TS_MIN") ? atoi(getenv("DS_GEMM_TS_MIN")) : 257;
     const int tiles1 = p.t_blocks * p.m_tiles;
-    if (ksplit_env && max_clusters <= 0 && p.tb_pad <= 256 && p.KB >= 8 && kNumSMs / tiles1 >= 4 &&
+    static const int ks2_env = getenv("DS_GEMM_KS2") ? atoi(getenv("DS_GEMM_KS2")) : 0;
+    const int ks_pick = kNumSMs / tiles1 >= 4 ? 4 : (ks2_env && kNumSMs / tiles1 >= 2 ? 2 : 1);
+    if (ksplit_env && max_clusters <= 0 && p.tb_pad <= 256 && p.KB >= 8 && ks_pick > 1 &&
         T < ts_min) {
         GemmParams q = p;
         if (set_block(q, p.tb, 1) && size_t(q.stages) * (kBM * kBK * 2 + q.b_bytes) >= size_t(q.tb_pad) * kBM * 4) {
-            q.ks = 4;
+            q.ks = ks_pick;
             q.n_clusters = tiles1;
             *cn_out = 1;
             return q;

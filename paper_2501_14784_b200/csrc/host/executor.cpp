@@ -386,7 +386,11 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     for (const auto& r : circ.rows) any_decode |= (r.is_decode && r.pos > 0);
                     has_input = any_decode;
                 }
-                if (has_input) {
+                // single stage: the input is this stream's own previous step (ids loop back on the
+                // device, no link, no injected delay: reference sim.cpp:434-437), so stream order
+                // is the dependency and the host runs ahead instead of draining the GPU per circuit
+                const bool wait_input = has_input && !(NS == 1 && !S->nccl);
+                if (wait_input) {
                     Mailbox& mbx = *w.in[mb];
                     int64_t t_done;
                     {
@@ -463,6 +467,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     else
                         XK(cudaMemcpyPeerAsync(next->recv[mb], next->device, src, w.device, size_t(bytes), w.stream));
                 }
+                if (NS == 1) continue;  // nobody waits on the self loop (stream order)
                 Mailbox& out = *next->in[mb];
                 XK(cudaEventRecord(out.ev, w.stream));
                 XK(cudaLaunchHostFunc(w.stream, post_cb, new PostCtx{&out, c}));
@@ -556,6 +561,11 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
             if (cudaEventElapsedTime(&ms, w.timing[i].a, w.timing[i].b) == cudaSuccess) {
                 st.busy_ms += ms;
                 st.steps.push_back({w.timing[i].rows, double(ms)});
+                float gap = 0;
+                if (i > 0 && cudaEventElapsedTime(&gap, w.timing[i - 1].b, w.timing[i].a) == cudaSuccess)
+                    st.gaps.push_back(gap);
+                else
+                    st.gaps.push_back(0.0);
             }
         }
         std::vector<char> buf(1 << 14);
@@ -606,7 +616,8 @@ std::string GpuRunResult::to_json() const {
            << ",\"swap_out_bytes\":" << s.swap_out_bytes << ",\"kernels\":"
            << (s.kernel_stats.empty() ? "{}" : s.kernel_stats) << ",\"steps\":[";
         for (size_t k = 0; k < s.steps.size(); ++k)
-            os << (k ? "," : "") << "[" << s.steps[k].first << "," << s.steps[k].second << "]";
+            os << (k ? "," : "") << "[" << s.steps[k].first << "," << s.steps[k].second << ","
+               << (k < s.gaps.size() ? s.gaps[k] : 0.0) << "]";
         os << "]}";
     }
     os << "],\"tokens\":[";

@@ -26,6 +26,7 @@ struct StageRunStats {
     int64_t swap_plan_bytes = 0, swap_in_bytes = 0, swap_out_bytes = 0;
     double busy_ms = 0, device_ms = 0;
     std::vector<std::pair<int64_t, double>> steps;  // (rows, ms) per stage step
+    std::vector<double> gaps;  // ms between the end of the previous step and this one's start
     std::string kernel_stats;                       // ds_stage_kernel_stats JSON
 };
 

@@ -20,7 +20,7 @@ for r in d["runs"]:
 buckets = [1, 2, 4, 8, 16, 32, 64, 96, 128, 192, 256, 320, 384, 448, 512]
 rows = []
 for lo, hi in zip([0] + buckets[:-1], buckets):
-    ms = [m for t, m in steps if lo < t <= hi]
+    ms = [st[1] for st in steps if lo < st[0] <= hi]
     if len(ms) >= 3:
         rows.append((hi, statistics.median(ms)))
 out, last = [], 0.0
