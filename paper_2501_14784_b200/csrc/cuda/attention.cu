@@ -622,7 +622,14 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
                    kv, layer, sp, stride, o, ws);
     if (n_drows > 0) {
         const dim3 grid(n_drows * kv.n_kv * sd), block(kAttnWarps * 32);
-        switch (decode_stages()) {
+        // ring depth by occupancy: a grid of <= 1 (2) CTA per SM keeps the same 12 chunks in
+        // flight per SM with 4- (3-) deep rings that 3 resident CTAs get with 2-deep ones
+        int st = decode_stages();
+        if (st == kDecStages && getenv("DS_ATTN_STAGES") == nullptr) {
+            const int ctas = int(grid.x);
+            st = ctas <= kNumSMs ? 4 : (ctas <= 2 * kNumSMs ? 3 : 2);
+        }
+        switch (st) {
             case 3:
                 launch_pdl(attn_decode_kernel<DH, 3>, grid, block, sizeof(DecSmem<DH, 3>), stream, q,
                            n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws);
