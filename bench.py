@@ -95,6 +95,28 @@ def load_peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+NCU_FULL = {"gemm_gate_up": "r01_ncu_full_gemm_gate_up.csv", "attention": "r01_ncu_full_attn_decode.csv"}
+
+
+def ncu_traffic(kind):
+    """dram__bytes_read + dram__bytes_write of one launch of this kernel kind from the committed
+    `ncu --set full` capture under profiles/ (a mid-schedule launch; compare with
+    algorithmic_bytes_per_launch, which averages every launch of the step)."""
+    name = NCU_FULL.get(kind)
+    path = os.path.join(ROOT, "profiles", name) if name else None
+    if not path or not os.path.exists(path):
+        return None, None
+    import csv
+    rows = list(csv.reader(open(path)))
+    hdr, unit, val = rows[0], rows[1], rows[2]
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = 0.0
+    for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        i = hdr.index(key)
+        tot += float(val[i].replace(",", "")) * scale.get(unit[i], 1.0)
+    return tot, f"bytes per launch, profiles/{name} (one mid-schedule launch of {val[0]})"
+
+
 def roofline(kernels):
     """Dominant launch group of the profiled run: algorithmic work / its summed CUDA-event time."""
     hbm, tf_burst, tf_sus, src = load_peaks()
@@ -109,8 +131,10 @@ def roofline(kernels):
     else:
         ach, peak, unit, bound = v["bytes"] / sec / 1e9, hbm, "GB/s", "hbm"
     total_ms = sum(x["ms"] for x in kinds.values())
+    traffic, traffic_note = ncu_traffic(dom)
     return {"kernel": dom, "bound": bound, "achieved": round(ach, 2), "peak": peak, "unit": unit,
-            "frac": round(ach / peak, 4), "traffic": None, "peak_source": src,
+            "frac": round(ach / peak, 4), "traffic": traffic, "traffic_note": traffic_note,
+            "peak_source": src,
             "share_of_step": round(v["ms"] / total_ms, 4), "launches": v["n"],
             "algorithmic_flops_per_launch": v["flops"] / v["n"],
             "algorithmic_bytes_per_launch": v["bytes"] / v["n"],

@@ -41,12 +41,13 @@ def full(path):
             "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
             "lts__t_sector_hit_rate.pct"]
     idx = [(w, h.index(w)) for w in want if w in h]
-    lines = [",".join(w for w, _ in idx)]
-    units = [rd[1][i] for _, i in idx]
-    lines.append(",".join(units))
+    out = io.StringIO()
+    wr = csv.writer(out, lineterminator="\n")
+    wr.writerow([w for w, _ in idx])
+    wr.writerow([rd[1][i] for _, i in idx])
     for r in rd[2:]:
-        lines.append(",".join(r[i].split("(")[0] for _, i in idx))
-    return "\n".join(lines)
+        wr.writerow([r[i].split("(")[0] for _, i in idx])
+    return out.getvalue().rstrip("\n")
 
 
 if __name__ == "__main__":
