@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __restrict__ row_pos,
                    const int32_t* __restrict__ row_page_off, const int32_t* __restrict__ flat_pages,
                    const int32_t* __restrict__ drows, KvLayout kv, int layer, int splits, int stride,
-                   __nv_bfloat16* __restrict__ o, float* __restrict__ ws) {
+                   __nv_bfloat16* __restrict__ o, float* __restrict__ ws, int* __restrict__ counters) {
     pdl_launch_dependents();
     pdl_wait();
     extern __shared__ __align__(16) uint8_t dec_smem[];
@@ -542,12 +542,43 @@ attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
             o[row_head * DH + dd] = f2bf(num / den);
         } else {
             float* dst = ws + (row_head * stride + split) * (DH + 2);
-            dst[dd] = num;
+            __stcg(dst + dd, num);
             if (dd == 0) {
-                dst[DH] = M;
-                dst[DH + 1] = den;
+                __stcg(dst + DH, M);
+                __stcg(dst + DH + 1, den);
             }
         }
+    }
+    if (splits == 1) return;
+    // context splits: the last CTA of this (row, KV head) to finish merges every split's partial
+    // in split order (deterministic) -- no separate combine launch
+    __threadfence();
+    __syncthreads();
+    __shared__ int last_cta;
+    if (threadIdx.x == 0) {
+        int* cnt = counters + size_t(t) * n_kv + kvh;
+        const int old = atomicAdd(cnt, 1);
+        last_cta = old == splits - 1;
+        if (last_cta) *cnt = 0;  // ready for the next launch
+    }
+    __syncthreads();
+    if (!last_cta) return;
+    __threadfence();
+    for (int i = threadIdx.x; i < G * DH; i += blockDim.x) {
+        const int r = i / DH, dd = i % DH;
+        const size_t row_head = size_t(t) * n_h + kvh * G + r;
+        const float* base = ws + row_head * stride * (DH + 2);
+        float M = -INFINITY;
+        for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, __ldcg(base + sp * (DH + 2) + DH));
+        float num = 0.f, den = 0.f;
+        for (int sp = 0; sp < splits; ++sp) {
+            const float ms = __ldcg(base + sp * (DH + 2) + DH);
+            if (ms == -INFINITY) continue;
+            const float w = exp2f(ms - M);
+            num += __ldcg(base + sp * (DH + 2) + dd) * w;
+            den += __ldcg(base + sp * (DH + 2) + DH + 1) * w;
+        }
+        o[row_head * DH + dd] = f2bf(num / den);
     }
 }
 
@@ -586,8 +617,8 @@ void attention_splits(int T, int n_h, int d_head, int n_blocks, int n_drows, int
 
 int attention_launches(int n_blocks, int n_drows, int s_prompt, int s_decode) {
     if (n_blocks + n_drows <= 0) return 0;
-    return (n_blocks > 0) + (n_drows > 0) +
-           (((n_blocks > 0 && s_prompt > 1) || (n_drows > 0 && s_decode > 1)) ? 1 : 0);
+    (void)s_decode;
+    return (n_blocks > 0) + (n_drows > 0) + ((n_blocks > 0 && s_prompt > 1) ? 1 : 0);
 }
 
 size_t attention_workspace_floats(int T, int n_h, int d_head, int splits) {
@@ -609,7 +640,7 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
                    const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
                    int n_blocks, const int32_t* drows, int n_drows, const int32_t* row_splits,
                    const KvLayout& kv, int layer, int sp, int sd, __nv_bfloat16* o, float* ws,
-                   cudaStream_t stream) {
+                   int* counters, cudaStream_t stream) {
     // timing experiments only (results invalid): DS_ATTN_SKIP bit 0 prompt blocks, 1 decode rows,
     // 2 combine
     static const int skip = getenv("DS_ATTN_SKIP") ? atoi(getenv("DS_ATTN_SKIP")) : 0;
@@ -632,18 +663,21 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
         switch (st) {
             case 3:
                 launch_pdl(attn_decode_kernel<DH, 3>, grid, block, sizeof(DecSmem<DH, 3>), stream, q,
-                           n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws);
+                           n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws,
+                           counters);
                 break;
             case 4:
                 launch_pdl(attn_decode_kernel<DH, 4>, grid, block, sizeof(DecSmem<DH, 4>), stream, q,
-                           n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws);
+                           n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws,
+                           counters);
                 break;
             default:
                 launch_pdl(attn_decode_kernel<DH, 2>, grid, block, sizeof(DecSmem<DH, 2>), stream, q,
-                           n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws);
+                           n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws,
+                           counters);
         }
     }
-    if (((n_blocks > 0 && sp > 1) || (n_drows > 0 && sd > 1)) && !(skip & 4))
+    if (n_blocks > 0 && sp > 1 && !(skip & 4))  // decode rows merge their splits in-kernel
         launch_pdl(attn_combine_kernel<DH>, dim3(T * n_h), dim3(DH), 0, stream, (const float*)ws,
                    stride, n_h, row_splits, o);
 }
@@ -652,7 +686,7 @@ int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_p
                     const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
                     int n_blocks, const int32_t* drows, int n_drows, const int32_t* row_splits,
                     const KvLayout& kv, int layer, int s_prompt, int s_decode, __nv_bfloat16* o,
-                    float* ws, size_t ws_floats, cudaStream_t stream) {
+                    float* ws, size_t ws_floats, int* counters, cudaStream_t stream) {
     if (T <= 0 || n_blocks + n_drows <= 0) return 0;
     if (n_h % kv.n_kv != 0 || n_h / kv.n_kv > 16) return -1;
     if (attention_workspace_floats(T, n_h, kv.d_head, std::max(s_prompt, s_decode)) > ws_floats &&
@@ -660,10 +694,10 @@ int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_p
         return -4;
     if (kv.d_head == 128)
         launch<128>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, drows, n_drows,
-                    row_splits, kv, layer, s_prompt, s_decode, o, ws, stream);
+                    row_splits, kv, layer, s_prompt, s_decode, o, ws, counters, stream);
     else if (kv.d_head == 64)
         launch<64>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, drows, n_drows,
-                   row_splits, kv, layer, s_prompt, s_decode, o, ws, stream);
+                   row_splits, kv, layer, s_prompt, s_decode, o, ws, counters, stream);
     else
         return -2;
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -3;

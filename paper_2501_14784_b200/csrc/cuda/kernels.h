@@ -87,7 +87,9 @@ void rope_kv_append(const __nv_bfloat16* qkv, int T, int n_h, int n_kv, int d_he
 // (<= attention_block_positions() rows of one request), [3*i+2] = 0. Decode rows (one query
 // position each) are listed separately in drows[] and go to the decode kernel.
 // Context splits: s_prompt for the prompt blocks, s_decode for the decode rows; row_splits[t]
-// (device) = the split count of row t's kind, read by the combine kernel.
+// (device) = the split count of a prompt row (1 for decode rows), read by the combine kernel.
+// Decode rows merge their splits in-kernel (last CTA per row and KV head; `counters`: zeroed
+// ints, >= rows x n_kv, self-resetting).
 int attention_block_positions(int n_h, int n_kv);
 void attention_splits(int T, int n_h, int d_head, int n_blocks, int n_drows, int n_kv, int max_ctx,
                       size_t ws_floats, int* s_prompt, int* s_decode);
@@ -97,7 +99,7 @@ int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_p
                     const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
                     int n_blocks, const int32_t* drows, int n_drows, const int32_t* row_splits,
                     const KvLayout& kv, int layer, int s_prompt, int s_decode, __nv_bfloat16* o,
-                    float* ws, size_t ws_floats, cudaStream_t stream);
+                    float* ws, size_t ws_floats, int* counters, cudaStream_t stream);
 
 // ids[r] = argmax_v logits[r, v] (lowest index wins ties).
 void argmax_rows(const float* logits, int R, int V, int32_t* ids, cudaStream_t stream);

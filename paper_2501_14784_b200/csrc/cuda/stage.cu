@@ -82,6 +82,7 @@ struct ds_stage {
     size_t ws_floats = 0;
     float* attn_ws = nullptr;
     size_t attn_ws_floats = 0;
+    int* attn_cnt = nullptr;  // decode context-split arrival counters [max_rows][n_kv]
 
     // step metadata: pinned host staging (double-buffered) + device copy
     int32_t* h_meta[2] = {nullptr, nullptr};
@@ -293,6 +294,8 @@ ds_status ds_stage_create(int32_t device, const ds_model_desc* md, int64_t layer
         // context-split partials: up to 4 per row (prompt chunks split up to 8 ways when short)
         s->attn_ws_floats = (4 * R + 1184) * m.n_heads * size_t(m.d_head + 2);
         if ((st = A((void**)&s->attn_ws, s->attn_ws_floats * 4))) { delete s; return st; }
+        if ((st = A((void**)&s->attn_cnt, R * m.n_kv_heads * 4))) { delete s; return st; }
+        CK(cudaMemset(s->attn_cnt, 0, R * m.n_kv_heads * 4));
     }
     s->meta_cap = 16 * R + size_t(max_slots) * 64 + R * size_t((m.max_seq_len + 255) / 256) + 64;
     for (int i = 0; i < 2; ++i) {
@@ -311,7 +314,7 @@ ds_status ds_stage_destroy(ds_stage* s) {
     cudaDeviceSynchronize();
     for (void* p : {(void*)s->wbuf, (void*)s->rope_cos, (void*)s->rope_sin, (void*)s->x, (void*)s->xn,
                     (void*)s->qkv, (void*)s->q, (void*)s->attn, (void*)s->h,
-                    (void*)s->logits, (void*)s->ids, (void*)s->ws, (void*)s->attn_ws,
+                    (void*)s->logits, (void*)s->ids, (void*)s->ws, (void*)s->attn_ws, (void*)s->attn_cnt,
                     (void*)s->d_meta, (void*)s->kv.pool, (void*)s->last_token,
                     (void*)s->pending_ids})
         if (p) cudaFree(p);
@@ -641,7 +644,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
                              s->attn_ws_floats, &s_prompt, &s_decode);
         tb = 0;
         for (int64_t i = 0; i < n_rows; ++i)
-            for (int j = 0; j < rows[i].n_tok; ++j) rsplit[tb++] = rows[i].n_tok == 1 ? s_decode : s_prompt;
+            for (int j = 0; j < rows[i].n_tok; ++j) rsplit[tb++] = rows[i].n_tok == 1 ? 1 : s_prompt;
     }
     const size_t meta_n = size_t(flat - hm) + P;
     CK(cudaMemcpyAsync(s->d_meta, hm, meta_n * 4, cudaMemcpyHostToDevice, s->stream));
@@ -736,7 +739,8 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
         if (!(skip & 4))
             rc |= ds::attention_paged(s->q, T, m.n_heads, d_pos, d_poff, d_flat, d_blk, n_blk,
                                       d_blk + 3 * n_blk, n_drow, d_rsplit, s->kv, li, s_prompt,
-                                      s_decode, s->attn, s->attn_ws, s->attn_ws_floats, st);
+                                      s_decode, s->attn, s->attn_ws, s->attn_ws_floats, s->attn_cnt,
+                                      st);
         end_other(PK_ATTN, attn_flops, attn_bytes,
                   ds::attention_launches(n_blk, n_drow, s_prompt, s_decode));
         begin();
