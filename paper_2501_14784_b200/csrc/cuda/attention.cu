@@ -71,8 +71,9 @@ __global__ void __launch_bounds__(kPromptWarps * 32)
 attn_prompt_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __restrict__ row_pos,
                    const int32_t* __restrict__ row_page_off, const int32_t* __restrict__ flat_pages,
                    const int32_t* __restrict__ blocks, KvLayout kv, int layer, int splits, int stride,
-                   __nv_bfloat16* __restrict__ o, float* __restrict__ ws) {
+                   __nv_bfloat16* __restrict__ o, float* __restrict__ ws, L2Prefetch pf) {
     pdl_launch_dependents();
+    l2_prefetch_slice(pf);
     pdl_wait();
     extern __shared__ __align__(16) uint8_t attn_smem[];
     PromptSmem<DH>& sm = *reinterpret_cast<PromptSmem<DH>*>(attn_smem);
@@ -358,8 +359,10 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __restrict__ row_pos,
                    const int32_t* __restrict__ row_page_off, const int32_t* __restrict__ flat_pages,
                    const int32_t* __restrict__ drows, KvLayout kv, int layer, int splits, int stride,
-                   __nv_bfloat16* __restrict__ o, float* __restrict__ ws, int* __restrict__ counters) {
+                   __nv_bfloat16* __restrict__ o, float* __restrict__ ws, int* __restrict__ counters,
+                   L2Prefetch pf) {
     pdl_launch_dependents();
+    l2_prefetch_slice(pf);
     pdl_wait();
     extern __shared__ __align__(16) uint8_t dec_smem[];
     DecSmem<DH, ST>& sm = *reinterpret_cast<DecSmem<DH, ST>*>(dec_smem);
@@ -640,7 +643,8 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
                    const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
                    int n_blocks, const int32_t* drows, int n_drows, const int32_t* row_splits,
                    const KvLayout& kv, int layer, int sp, int sd, __nv_bfloat16* o, float* ws,
-                   int* counters, cudaStream_t stream) {
+                   int* counters, const L2Prefetch& pf, cudaStream_t stream) {
+    const L2Prefetch pf_dec = pf;  // the decode launch (or the prompt one when alone) prefetches
     // timing experiments only (results invalid): DS_ATTN_SKIP bit 0 prompt blocks, 1 decode rows,
     // 2 combine
     static const int skip = getenv("DS_ATTN_SKIP") ? atoi(getenv("DS_ATTN_SKIP")) : 0;
@@ -650,7 +654,7 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
     if (n_blocks > 0)
         launch_pdl(attn_prompt_kernel<DH>, dim3(n_blocks * kv.n_kv * sp), dim3(kPromptWarps * 32),
                    sizeof(PromptSmem<DH>), stream, q, n_h, row_pos, row_page_off, flat_pages, blocks,
-                   kv, layer, sp, stride, o, ws);
+                   kv, layer, sp, stride, o, ws, n_drows > 0 ? L2Prefetch{} : pf);
     if (n_drows > 0) {
         const dim3 grid(n_drows * kv.n_kv * sd), block(kAttnWarps * 32);
         // ring depth by occupancy: a grid of <= 1 (2) CTA per SM keeps the same 12 chunks in
@@ -664,17 +668,17 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
             case 3:
                 launch_pdl(attn_decode_kernel<DH, 3>, grid, block, sizeof(DecSmem<DH, 3>), stream, q,
                            n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws,
-                           counters);
+                           counters, pf_dec);
                 break;
             case 4:
                 launch_pdl(attn_decode_kernel<DH, 4>, grid, block, sizeof(DecSmem<DH, 4>), stream, q,
                            n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws,
-                           counters);
+                           counters, pf_dec);
                 break;
             default:
                 launch_pdl(attn_decode_kernel<DH, 2>, grid, block, sizeof(DecSmem<DH, 2>), stream, q,
                            n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws,
-                           counters);
+                           counters, pf_dec);
         }
     }
     if (n_blocks > 0 && sp > 1 && !(skip & 4))  // decode rows merge their splits in-kernel
@@ -686,7 +690,8 @@ int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_p
                     const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
                     int n_blocks, const int32_t* drows, int n_drows, const int32_t* row_splits,
                     const KvLayout& kv, int layer, int s_prompt, int s_decode, __nv_bfloat16* o,
-                    float* ws, size_t ws_floats, int* counters, cudaStream_t stream) {
+                    float* ws, size_t ws_floats, int* counters, const L2Prefetch& pf,
+                    cudaStream_t stream) {
     if (T <= 0 || n_blocks + n_drows <= 0) return 0;
     if (n_h % kv.n_kv != 0 || n_h / kv.n_kv > 16) return -1;
     if (attention_workspace_floats(T, n_h, kv.d_head, std::max(s_prompt, s_decode)) > ws_floats &&
@@ -694,10 +699,10 @@ int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_p
         return -4;
     if (kv.d_head == 128)
         launch<128>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, drows, n_drows,
-                    row_splits, kv, layer, s_prompt, s_decode, o, ws, counters, stream);
+                    row_splits, kv, layer, s_prompt, s_decode, o, ws, counters, pf, stream);
     else if (kv.d_head == 64)
         launch<64>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, drows, n_drows,
-                   row_splits, kv, layer, s_prompt, s_decode, o, ws, counters, stream);
+                   row_splits, kv, layer, s_prompt, s_decode, o, ws, counters, pf, stream);
     else
         return -2;
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -3;

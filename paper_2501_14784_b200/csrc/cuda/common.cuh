@@ -113,6 +113,32 @@ DS_DEVICE uint64_t policy_evict_last() {
     return p;
 }
 
+// L2 prefetch hint of a byte range (e.g. the next GEMM's weights) spread over a grid: thread 0 of
+// each CTA issues bulk prefetches of <= 64 KB for its slice, evict_last so the lines survive the
+// streaming traffic of the kernel in between. Independent of the previous kernel's results, so
+// it is issued before griddepcontrol.wait.
+struct L2Prefetch {
+    const void* p = nullptr;
+    size_t bytes = 0;
+};
+DS_DEVICE void l2_prefetch_slice(const L2Prefetch& pf) {
+    if (pf.p == nullptr || threadIdx.x != 0) return;
+    const size_t per = ((pf.bytes + gridDim.x - 1) / gridDim.x + 255) & ~size_t(255);
+    const size_t beg = per * blockIdx.x;
+    if (beg >= pf.bytes) return;
+    const size_t end = beg + per < pf.bytes ? beg + per : pf.bytes;
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    for (size_t o = beg; o < end; o += 65536) {
+        const uint32_t n = uint32_t((end - o < 65536 ? end - o : 65536) & ~size_t(15));
+        if (n == 0) break;
+        asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(
+                         reinterpret_cast<const char*>(pf.p) + o),
+                     "r"(n), "l"(pol)
+                     : "memory");
+    }
+}
+
 // -------------------------------------------------------------- tcgen05 ----
 DS_DEVICE void tmem_alloc(uint32_t* smem_slot, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(

@@ -6,6 +6,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include "common.cuh"
+
 namespace ds {
 
 enum GemmEpilogue : int {
@@ -99,7 +101,8 @@ int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_p
                     const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
                     int n_blocks, const int32_t* drows, int n_drows, const int32_t* row_splits,
                     const KvLayout& kv, int layer, int s_prompt, int s_decode, __nv_bfloat16* o,
-                    float* ws, size_t ws_floats, int* counters, cudaStream_t stream);
+                    float* ws, size_t ws_floats, int* counters, const L2Prefetch& pf,
+                    cudaStream_t stream);
 
 // ids[r] = argmax_v logits[r, v] (lowest index wins ties).
 void argmax_rows(const float* logits, int R, int V, int32_t* ids, cudaStream_t stream);
