@@ -148,6 +148,11 @@ ds_status ds_stage_profile(ds_stage* stage, int32_t enable);
 ds_status ds_stage_kernel_stats(ds_stage* stage, char* out, size_t cap, int64_t* launches);
 /* 1 if every KV page of mb is device-resident (compute-requires-resident, sim.cpp:629-639). */
 ds_status ds_kv_resident(ds_stage* stage, int32_t mb, int32_t* resident);
+/* 1 if mb is resident AND the pages this step's rows append fit its free local pages (plus its
+ * global slot's free pages when it holds one); 0 means the caller must swap mb in first -- the
+ * on-demand swap-in of reference try_start (sim.cpp:355-382) for growth the plan's byte-level
+ * prefetch did not cover (local capacity is whole pages). */
+ds_status ds_kv_ready(ds_stage* stage, int32_t mb, const ds_row* rows, int64_t n_rows, int32_t* ready);
 
 /* H2D prefetch of mb's global pages into global slot `slot` after evicting the occupant (D2H),
  * on the stage's copy streams (reference issue_swap_in, sim.cpp:328-353). plan_bytes is the

@@ -93,6 +93,7 @@ def _load() -> C.CDLL:
         "ds_stage_stream": (I32, [P, P]),
         "ds_stage_logits": (I32, [P, P, I64, P]),
         "ds_kv_resident": (I32, [P, I32, P]),
+        "ds_kv_ready": (I32, [P, I32, P, I64, P]),
         "ds_kv_reset": (I32, [P]),
         "ds_session_create": (I32, [S, S, S, I64, I64, P, P, P]),
         "ds_session_run": (I32, [P, I32, I32, P, C.c_size_t, P]),

@@ -286,13 +286,15 @@ ds_status ds_stage_create(int32_t device, const ds_model_desc* md, int64_t layer
         delete s;
         return st;
     }
-    if (s->last && (st = A((void**)&s->logits, R * size_t(m.vocab) * 4))) { delete s; return st; }
+    // logits: one row per sampled request (<= the microbatch's slots), not per step row
+    const size_t logit_rows = std::min<size_t>(R, size_t(std::max(1, max_slots)));
+    if (s->last && (st = A((void**)&s->logits, logit_rows * size_t(m.vocab) * 4))) { delete s; return st; }
     {
         s->ws_floats = ds::gemm_workspace_floats();
         if ((st = A((void**)&s->ws, s->ws_floats * 4))) { delete s; return st; }
         CK(cudaMemset(s->ws, 0, s->ws_floats * 4));
-        // context-split partials: up to 4 per row (prompt chunks split up to 8 ways when short)
-        s->attn_ws_floats = (4 * R + 1184) * m.n_heads * size_t(m.d_head + 2);
+        // context-split partials (splits shrink to fit: many splits only occur for few rows)
+        s->attn_ws_floats = (R + 4096) * m.n_heads * size_t(m.d_head + 2);
         if ((st = A((void**)&s->attn_ws, s->attn_ws_floats * 4))) { delete s; return st; }
         if ((st = A((void**)&s->attn_cnt, R * m.n_kv_heads * 4))) { delete s; return st; }
         CK(cudaMemset(s->attn_cnt, 0, R * m.n_kv_heads * 4));
@@ -452,6 +454,26 @@ ds_status ds_kv_resident(ds_stage* s, int32_t mb, int32_t* resident) {
     return DS_OK;
 }
 
+ds_status ds_kv_ready(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_rows, int32_t* ready) {
+    if (!s || mb < 0 || mb >= s->n_mb || !ready || (n_rows > 0 && !rows)) return ds_fail(DS_ERR_ARG, "bad mb");
+    if (s->mbs.empty()) return ds_fail(DS_ERR_ARG, "ds_kv_create not called");
+    int32_t res = 1;
+    ds_status st = ds_kv_resident(s, mb, &res);
+    if (st) return st;
+    const MbKv& k = s->mbs[mb];
+    int64_t need = 0;
+    for (int64_t i = 0; i < n_rows; ++i) {
+        const ds_row& r = rows[i];
+        if (r.slot < 0 || r.slot >= s->max_slots) return ds_fail(DS_ERR_ARG, "bad row descriptor");
+        const int64_t have = k.slot_req[r.slot] == r.req_id ? int64_t(k.pages[r.slot].size()) : 0;
+        need += std::max<int64_t>(0, page_count_for(r.pos + r.n_tok) - have);
+    }
+    int64_t avail = int64_t(k.local_free.size());
+    if (k.resident_slot >= 0) avail += int64_t(s->gslot[k.resident_slot].free.size());
+    *ready = (res && need <= avail) ? 1 : 0;
+    return DS_OK;
+}
+
 ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, int64_t* moved_in,
                      int64_t* moved_out) {
     (void)plan_bytes;
@@ -566,6 +588,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
         max_ctx = std::max(max_ctx, r.pos + r.n_tok);
     }
     if (T > s->max_rows) return ds_fail(DS_ERR_ARG, "circuit has more rows than max_rows");
+    if (R > std::max(1, s->max_slots)) return ds_fail(DS_ERR_ARG, "more sampled rows than slots");
     // residency check (compute-requires-resident, reference replay_check sim.cpp:629-639)
     for (int64_t i = 0; i < n_rows; ++i)
         for (int32_t hnd : k.pages[rows[i].slot])

@@ -119,8 +119,11 @@ struct Session {
     const NcclApi* api = nullptr;
     RingLinks links;
     cudaStream_t s_send = nullptr, s_recv = nullptr;
-    std::vector<void*> send_buf;        // per mb: staged output for the send
-    std::vector<cudaEvent_t> ev_copy;   // per mb: output staged (send stream waits on it)
+    std::vector<void*> send_buf;        // ring of staged outputs for the sends
+    std::vector<cudaEvent_t> ev_sent;   // per ring slot: its last send retired (slot reusable)
+    int64_t send_seq = 0;
+    static constexpr int kSendRing = 4;
+    std::vector<cudaEvent_t> ev_copy;   // per ring slot: output staged (send stream waits on it)
     std::vector<cudaEvent_t> ev_recv;   // per circuit: the receive of that circuit landed
     // receives in flight are bounded: a receive posted far ahead spins on the GPU and, once
     // NCCL's work queue fills, blocks the host inside ncclRecv while the peer waits on us
@@ -244,12 +247,16 @@ Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, con
         XK(cudaSetDevice(w.device));
         XK(cudaStreamCreateWithFlags(&S->s_send, cudaStreamNonBlocking));
         XK(cudaStreamCreateWithFlags(&S->s_recv, cudaStreamNonBlocking));
-        S->send_buf.assign(NB, nullptr);
-        S->ev_copy.assign(NB, nullptr);
+        // a small ring of staging buffers (not one per microbatch: with 16 K-row prefill chunks
+        // those would take gigabytes the planner budgeted for KV)
+        S->send_buf.assign(Session::kSendRing, nullptr);
+        S->ev_copy.assign(Session::kSendRing, nullptr);
+        S->ev_sent.assign(Session::kSendRing, nullptr);
         const size_t sb = rank == NS - 1 ? size_t(S->max_rows) * 4 : size_t(S->max_rows) * md.d_model * 2;
-        for (int64_t m = 0; m < NB; ++m) {
-            XK(cudaMalloc(&S->send_buf[m], sb));
-            XK(cudaEventCreateWithFlags(&S->ev_copy[m], cudaEventDisableTiming));
+        for (int k = 0; k < Session::kSendRing; ++k) {
+            XK(cudaMalloc(&S->send_buf[k], sb));
+            XK(cudaEventCreateWithFlags(&S->ev_copy[k], cudaEventDisableTiming));
+            XK(cudaEventCreateWithFlags(&S->ev_sent[k], cudaEventDisableTiming));
         }
         S->ev_recv.assign(S->n_circ, nullptr);
         for (auto& e : S->ev_recv) XK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -300,6 +307,7 @@ void session_destroy(Session* S) {
     if (S->nccl) {
         for (void* p : S->send_buf) cudaFree(p);
         for (auto e : S->ev_copy) cudaEventDestroy(e);
+        for (auto e : S->ev_sent) cudaEventDestroy(e);
         for (auto e : S->ev_recv) cudaEventDestroy(e);
         if (S->s_send) cudaStreamDestroy(S->s_send);
         if (S->s_recv) cudaStreamDestroy(S->s_recv);
@@ -406,9 +414,14 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     if (wait > 0) std::this_thread::sleep_for(std::chrono::microseconds(wait));
                     XK(cudaStreamWaitEvent(w.stream, S->nccl ? S->ev_recv[need] : mbx.ev, 0));
                 }
-                // ---- residency top-up: the plan's prefetch may be stale
+                // ---- residency top-up: the plan's prefetch may be stale, or the
+                // step's growth may exceed the whole local pages before the plan's byte figure
+                // shows a global portion
+                rows.clear();
+                for (const auto& r : circ.rows)
+                    rows.push_back({r.slot, r.pos, r.n_tok, r.need_logits, r.is_decode, 0, r.req});
                 int32_t resident = 1;
-                DK(ds_kv_resident(w.st, mb, &resident));
+                DK(ds_kv_ready(w.st, mb, rows.data(), int64_t(rows.size()), &resident));
                 if (!resident) {
                     int64_t mi = 0, mo = 0;
                     DK(ds_swap_in(w.st, mb, int32_t(w.served % 2), 0, &mi, &mo));
@@ -417,9 +430,6 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     w.topups++;
                 }
                 // ---- the stage step
-                rows.clear();
-                for (const auto& r : circ.rows)
-                    rows.push_back({r.slot, r.pos, r.n_tok, r.need_logits, r.is_decode, 0, r.req});
                 StepTiming* tm = nullptr;
                 if (opt.step_timing) {
                     if (w.timing_used == w.timing.size()) {
@@ -449,14 +459,17 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 if (S->nccl) {
                     // stage the output per microbatch, then ncclSend on the send stream
                     if (bytes > 0) {
-                        XK(cudaMemcpyAsync(S->send_buf[mb], src, size_t(bytes), cudaMemcpyDeviceToDevice,
+                        const int k = int(S->send_seq++ % Session::kSendRing);
+                        XK(cudaStreamWaitEvent(w.stream, S->ev_sent[k], 0));  // slot's last send done
+                        XK(cudaMemcpyAsync(S->send_buf[k], src, size_t(bytes), cudaMemcpyDeviceToDevice,
                                            w.stream));
-                        XK(cudaEventRecord(S->ev_copy[mb], w.stream));
-                        XK(cudaStreamWaitEvent(S->s_send, S->ev_copy[mb], 0));
-                        const ncclResult_t nr = S->api->Send(S->send_buf[mb], size_t(bytes), ncclUint8, 1,
+                        XK(cudaEventRecord(S->ev_copy[k], w.stream));
+                        XK(cudaStreamWaitEvent(S->s_send, S->ev_copy[k], 0));
+                        const ncclResult_t nr = S->api->Send(S->send_buf[k], size_t(bytes), ncclUint8, 1,
                                                              S->links.send, S->s_send);
                         if (nr != ncclSuccess)
                             throw SimError(std::string("ncclSend: ") + S->api->GetErrorString(nr));
+                        XK(cudaEventRecord(S->ev_sent[k], S->s_send));
                         if (g_trace) fprintf(stderr, "[ds r%lld] send enqueued c=%lld mb=%d bytes=%lld\n", (long long)s, (long long)c, mb, (long long)bytes);
                     }
                     continue;
@@ -519,10 +532,44 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
             for (auto& m : w.in) m->cv.notify_all();
         }
     };
+    // NCCL mode watchdog: a local failure, or no landing and no step for DS_NCCL_TIMEOUT_S
+    // (default 600 s; the injected hop delays are at most seconds), aborts both link
+    // communicators so blocked sends / receives return and the run fails instead of hanging
+    std::atomic<bool> done{false};
+    std::thread watchdog;
+    if (S->nccl) {
+        watchdog = std::thread([&]() {
+            const char* e = getenv("DS_NCCL_TIMEOUT_S");
+            const int64_t limit_us = int64_t(e ? atof(e) : 600.0) * 1000000;
+            int64_t last = -1, t_last = now_us();
+            while (!done.load()) {
+                std::this_thread::sleep_for(std::chrono::milliseconds(200));
+                int64_t prog = S->landed;
+                for (auto& w : S->W) prog += w.computes;
+                if (prog != last) {
+                    last = prog;
+                    t_last = now_us();
+                }
+                const bool stalled = now_us() - t_last > limit_us;
+                if (failed.load() || stalled) {
+                    if (stalled && S->W[0].error.empty())
+                        S->W[0].error = "NCCL hop made no progress for DS_NCCL_TIMEOUT_S: aborted";
+                    failed = true;
+                    S->links.abort(*S->api);
+                    S->land_cv.notify_all();
+                    for (auto& w : S->W)
+                        for (auto& m : w.in) m->cv.notify_all();
+                    return;
+                }
+            }
+        });
+    }
     std::vector<std::thread> th;
     if (S->nccl) th.emplace_back(receiver);
     for (auto& w : S->W) th.emplace_back(body, std::ref(w));
     for (auto& t : th) t.join();
+    done = true;
+    if (watchdog.joinable()) watchdog.join();
     if (S->nccl) {
         cudaSetDevice(S->W[0].device);
         cudaStreamSynchronize(S->s_send);

@@ -23,6 +23,7 @@ const NcclApi* nccl_api(std::string* why) {
         api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
         api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
         api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+        api.CommAbort = reinterpret_cast<decltype(api.CommAbort)>(sym("ncclCommAbort"));
         api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
         api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
         api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
@@ -71,6 +72,14 @@ void RingLinks::destroy(const NcclApi& api) {
     ncclComm_t second = send_link < recv_link ? recv : send;
     if (first) api.CommDestroy(first);
     if (second) api.CommDestroy(second);
+    send = recv = nullptr;
+}
+
+void RingLinks::abort(const NcclApi& api) {
+    if (api.CommAbort) {
+        if (send) api.CommAbort(send);
+        if (recv) api.CommAbort(recv);
+    }
     send = recv = nullptr;
 }
 

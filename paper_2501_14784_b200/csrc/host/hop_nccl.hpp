@@ -16,6 +16,7 @@ struct NcclApi {
     ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
@@ -37,6 +38,9 @@ struct RingLinks {
     // p2p connections on every rank at once
     void warmup(const NcclApi& api, void* send_buf, void* recv_buf, cudaStream_t stream);
     void destroy(const NcclApi& api);
+    // failure path: abort both communicators (pending sends / receives return, no finalize
+    // handshake with a peer that may be gone)
+    void abort(const NcclApi& api);
     int rank_ = 0, world_ = 1;
 };
 

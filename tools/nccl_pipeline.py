@@ -43,7 +43,11 @@ out = C.create_string_buffer(1 << 24)
 st = lib.ds_session_run(h, 0, 1, out, 1 << 24, None)
 r = json.loads(out.value.decode() or "{}")
 print(f"rank {rank} status {st} err={lib.ds_last_error().decode()[:200]} circuits={r.get('circuits')} "
-      f"tokens={r.get('decode_tokens')} wall_us={r.get('wall_us')}", flush=True)
+      f"tokens={r.get('decode_tokens')} wall_us={r.get('wall_us')} "
+      f"swap={[(x.get('swap_plan_bytes'), x.get('swap_in_bytes'), x.get('topups')) for x in r.get('stages', [])]}",
+      flush=True)
+if st != 0:  # exit now: torchrun then stops the peers (a barrier would wait on them forever)
+    os._exit(1)
 if rank == world - 1 and r.get("tokens"):
     json.dump(r["tokens"], open(os.path.join(ROOT, "gpurun_out", f"nccl_tokens_{world}.json"), "w"))
 dist.barrier()
