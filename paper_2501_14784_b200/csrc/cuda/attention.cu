@@ -482,12 +482,15 @@ attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
         ls[1] = s[0][2] + s[0][3] + s[1][2] + s[1][3];
         l_run[0] = l_run[0] * alpha[0] + ls[0];
         l_run[1] = l_run[1] * alpha[1] + ls[1];
+        // the running max rarely moves after the first chunks: skip the 64-FMUL rescale then
+        if (__any_sync(0xffffffffu, alpha[0] != 1.f || alpha[1] != 1.f)) {
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-            acc[nt][0] *= alpha[0];
-            acc[nt][1] *= alpha[0];
-            acc[nt][2] *= alpha[1];
-            acc[nt][3] *= alpha[1];
+            for (int nt = 0; nt < NT; ++nt) {
+                acc[nt][0] *= alpha[0];
+                acc[nt][1] *= alpha[0];
+                acc[nt][2] *= alpha[1];
+                acc[nt][3] *= alpha[1];
+            }
         }
         uint32_t pa[4] = {pack2(s[0][0], s[0][1]), pack2(s[0][2], s[0][3]), pack2(s[1][0], s[1][1]),
                           pack2(s[1][2], s[1][3])};
