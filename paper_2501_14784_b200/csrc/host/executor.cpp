@@ -122,7 +122,8 @@ struct Session {
     std::vector<void*> send_buf;        // ring of staged outputs for the sends
     std::vector<cudaEvent_t> ev_sent;   // per ring slot: its last send retired (slot reusable)
     int64_t send_seq = 0;
-    static constexpr int kSendRing = 4;
+    int send_ring = 4;  // staging buffers: one per microbatch while they fit 1.5 GB (a slot
+                        // reused while its send waits on the peer's receive couples the stages)
     std::vector<cudaEvent_t> ev_copy;   // per ring slot: output staged (send stream waits on it)
     std::vector<cudaEvent_t> ev_recv;   // per circuit: the receive of that circuit landed
     // receives in flight are bounded: a receive posted far ahead spins on the GPU and, once
@@ -247,13 +248,14 @@ Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, con
         XK(cudaSetDevice(w.device));
         XK(cudaStreamCreateWithFlags(&S->s_send, cudaStreamNonBlocking));
         XK(cudaStreamCreateWithFlags(&S->s_recv, cudaStreamNonBlocking));
-        // a small ring of staging buffers (not one per microbatch: with 16 K-row prefill chunks
-        // those would take gigabytes the planner budgeted for KV)
-        S->send_buf.assign(Session::kSendRing, nullptr);
-        S->ev_copy.assign(Session::kSendRing, nullptr);
-        S->ev_sent.assign(Session::kSendRing, nullptr);
+        // a ring of staging buffers (one per microbatch unless 16 K-row prefill chunks would make
+        // that gigabytes the planner budgeted for KV)
         const size_t sb = rank == NS - 1 ? size_t(S->max_rows) * 4 : size_t(S->max_rows) * md.d_model * 2;
-        for (int k = 0; k < Session::kSendRing; ++k) {
+        S->send_ring = int(std::max<int64_t>(4, std::min<int64_t>(NB, int64_t((size_t(3) << 29) / sb))));
+        S->send_buf.assign(S->send_ring, nullptr);
+        S->ev_copy.assign(S->send_ring, nullptr);
+        S->ev_sent.assign(S->send_ring, nullptr);
+        for (int k = 0; k < S->send_ring; ++k) {
             XK(cudaMalloc(&S->send_buf[k], sb));
             XK(cudaEventCreateWithFlags(&S->ev_copy[k], cudaEventDisableTiming));
             XK(cudaEventCreateWithFlags(&S->ev_sent[k], cudaEventDisableTiming));
@@ -459,7 +461,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 if (S->nccl) {
                     // stage the output per microbatch, then ncclSend on the send stream
                     if (bytes > 0) {
-                        const int k = int(S->send_seq++ % Session::kSendRing);
+                        const int k = int(S->send_seq++ % S->send_ring);
                         XK(cudaStreamWaitEvent(w.stream, S->ev_sent[k], 0));  // slot's last send done
                         XK(cudaMemcpyAsync(S->send_buf[k], src, size_t(bytes), cudaMemcpyDeviceToDevice,
                                            w.stream));
