@@ -71,7 +71,8 @@ __global__ void __launch_bounds__(kPromptWarps * 32)
 attn_prompt_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __restrict__ row_pos,
                    const int32_t* __restrict__ row_page_off, const int32_t* __restrict__ flat_pages,
                    const int32_t* __restrict__ blocks, KvLayout kv, int layer, int splits, int stride,
-                   __nv_bfloat16* __restrict__ o, float* __restrict__ ws, L2Prefetch pf) {
+                   __nv_bfloat16* __restrict__ o, float* __restrict__ ws, int* __restrict__ counters,
+                   L2Prefetch pf) {
     pdl_launch_dependents();
     l2_prefetch_slice(pf);
     pdl_wait();
@@ -273,7 +274,7 @@ attn_prompt_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
         }
     }
     __syncthreads();
-    if (par == 1 || !warp_active) return;
+    if (par == 0 && warp_active) {
 #pragma unroll
     for (int hr = 0; hr < 2; ++hr) {
         const int r = r_base + g + 8 * hr;
@@ -300,14 +301,45 @@ attn_prompt_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
                 const int c = nt * 8 + 2 * tq;
-                dst[c] = acc[nt][2 * hr] * w0 + oth[c] * w1;
-                dst[c + 1] = acc[nt][2 * hr + 1] * w0 + oth[c + 1] * w1;
+                __stcg(dst + c, acc[nt][2 * hr] * w0 + oth[c] * w1);
+                __stcg(dst + c + 1, acc[nt][2 * hr + 1] * w0 + oth[c + 1] * w1);
             }
             if (tq == 0) {
-                dst[DH] = M;
-                dst[DH + 1] = L;
+                __stcg(dst + DH, M);
+                __stcg(dst + DH + 1, L);
             }
         }
+    }
+    }
+    if (splits == 1) return;
+    // context splits: the last CTA of this (block, KV head) merges all splits in split order
+    __threadfence();
+    __syncthreads();
+    __shared__ int last_cta;
+    if (threadIdx.x == 0) {
+        int* cnt = counters + size_t(bi) * n_kv + kvh;
+        const int old = atomicAdd(cnt, 1);
+        last_cta = old == splits - 1;
+        if (last_cta) *cnt = 0;  // ready for the next launch
+    }
+    __syncthreads();
+    if (!last_cta) return;
+    __threadfence();
+    for (int i = threadIdx.x; i < rows * DH; i += blockDim.x) {
+        const int r = i / DH, dd = i % DH;
+        const size_t row_head = size_t(t0 + r / G) * n_h + kvh * G + r % G;
+        const float* base = ws + row_head * stride * (DH + 2);
+        float M = -INFINITY;
+        for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, __ldcg(base + sp * (DH + 2) + DH));
+        float num = 0.f, den = 0.f;
+        for (int sp = 0; sp < splits; ++sp) {
+            const float ms = __ldcg(base + sp * (DH + 2) + DH);
+            if (ms == -INFINITY) continue;
+            const float w = exp2f(ms - M);
+            num += __ldcg(base + sp * (DH + 2) + dd) * w;
+            den += __ldcg(base + sp * (DH + 2) + DH + 1) * w;
+        }
+        o[row_head * DH + dd] = f2bf(num / den);
     }
 }
 
@@ -609,9 +641,12 @@ int attention_pick_splits(int n_blocks, int n_kv, int max_ctx) {
 // walks more than 2 tiles (128 tokens) of the longest context (their mma.sync work, not HBM,
 // bounds a long prompt chunk). Both shrink until T x max(splits) partials fit the workspace.
 void attention_splits(int T, int n_h, int d_head, int n_blocks, int n_drows, int n_kv, int max_ctx,
-                      size_t ws_floats, int* s_prompt, int* s_decode) {
+                      int max_prompt_ctx, size_t ws_floats, int* s_prompt, int* s_decode) {
     int sd = n_drows > 0 ? attention_pick_splits(n_blocks + n_drows, n_kv, max_ctx) : 1;
-    const int tiles = (max_ctx + kTile - 1) / kTile;
+    const int tiles = (max_prompt_ctx + kTile - 1) / kTile;
+    // prompt blocks: unsplit by default. DS_ATTN_PROMPT_TILES=n caps a CTA at n tiles; measured
+    // 0.5-0.8 s slower per config-2 step at n = 2..4: the last CTA's merge of 64 rows x d_head
+    // over the splits costs more than the shorter tile chain saves
     static const int sp_tiles = getenv("DS_ATTN_PROMPT_TILES") ? atoi(getenv("DS_ATTN_PROMPT_TILES")) : 0;
     int sp = (n_blocks > 0 && sp_tiles > 0) ? std::min(8, std::max(1, (tiles + sp_tiles - 1) / sp_tiles)) : 1;
     while (std::max(sp, sd) > 1 && attention_workspace_floats(T, n_h, d_head, std::max(sp, sd)) > ws_floats) {
@@ -623,8 +658,9 @@ void attention_splits(int T, int n_h, int d_head, int n_blocks, int n_drows, int
 
 int attention_launches(int n_blocks, int n_drows, int s_prompt, int s_decode) {
     if (n_blocks + n_drows <= 0) return 0;
+    (void)s_prompt;
     (void)s_decode;
-    return (n_blocks > 0) + (n_drows > 0) + ((n_blocks > 0 && s_prompt > 1) ? 1 : 0);
+    return (n_blocks > 0) + (n_drows > 0);
 }
 
 size_t attention_workspace_floats(int T, int n_h, int d_head, int splits) {
@@ -657,7 +693,8 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
     if (n_blocks > 0)
         launch_pdl(attn_prompt_kernel<DH>, dim3(n_blocks * kv.n_kv * sp), dim3(kPromptWarps * 32),
                    sizeof(PromptSmem<DH>), stream, q, n_h, row_pos, row_page_off, flat_pages, blocks,
-                   kv, layer, sp, stride, o, ws, n_drows > 0 ? L2Prefetch{} : pf);
+                   kv, layer, sp, stride, o, ws, counters + size_t(T) * kv.n_kv,
+                   n_drows > 0 ? L2Prefetch{} : pf);
     if (n_drows > 0) {
         const dim3 grid(n_drows * kv.n_kv * sd), block(kAttnWarps * 32);
         // ring depth by occupancy: a grid of <= 1 (2) CTA per SM keeps the same 12 chunks in
@@ -684,9 +721,7 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
                            counters, pf_dec);
         }
     }
-    if (n_blocks > 0 && sp > 1 && !(skip & 4))  // decode rows merge their splits in-kernel
-        launch_pdl(attn_combine_kernel<DH>, dim3(T * n_h), dim3(DH), 0, stream, (const float*)ws,
-                   stride, n_h, row_splits, o);
+    (void)row_splits;  // both kernels merge their context splits in-kernel
 }
 
 int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,

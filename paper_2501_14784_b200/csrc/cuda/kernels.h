@@ -94,7 +94,7 @@ void rope_kv_append(const __nv_bfloat16* qkv, int T, int n_h, int n_kv, int d_he
 // ints, >= rows x n_kv, self-resetting).
 int attention_block_positions(int n_h, int n_kv);
 void attention_splits(int T, int n_h, int d_head, int n_blocks, int n_drows, int n_kv, int max_ctx,
-                      size_t ws_floats, int* s_prompt, int* s_decode);
+                      int max_prompt_ctx, size_t ws_floats, int* s_prompt, int* s_decode);
 int attention_launches(int n_blocks, int n_drows, int s_prompt, int s_decode);
 size_t attention_workspace_floats(int T, int n_h, int d_head, int splits);
 int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,

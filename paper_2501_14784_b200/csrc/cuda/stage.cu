@@ -296,8 +296,9 @@ ds_status ds_stage_create(int32_t device, const ds_model_desc* md, int64_t layer
         // context-split partials (splits shrink to fit: many splits only occur for few rows)
         s->attn_ws_floats = (R + 4096) * m.n_heads * size_t(m.d_head + 2);
         if ((st = A((void**)&s->attn_ws, s->attn_ws_floats * 4))) { delete s; return st; }
-        if ((st = A((void**)&s->attn_cnt, R * m.n_kv_heads * 4))) { delete s; return st; }
-        CK(cudaMemset(s->attn_cnt, 0, R * m.n_kv_heads * 4));
+        // [decode rows x n_kv | prompt blocks x n_kv] (the prompt half starts at T * n_kv)
+        if ((st = A((void**)&s->attn_cnt, 2 * R * m.n_kv_heads * 4))) { delete s; return st; }
+        CK(cudaMemset(s->attn_cnt, 0, 2 * R * m.n_kv_heads * 4));
     }
     s->meta_cap = 16 * R + size_t(max_slots) * 64 + R * size_t((m.max_seq_len + 255) / 256) + 64;
     for (int i = 0; i < 2; ++i) {
@@ -663,8 +664,11 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
             if (rows[i].n_tok == 1) blk[3 * n_blk + n_drow++] = tb;
             tb += rows[i].n_tok;
         }
+        int max_prompt_ctx = 1;
+        for (int64_t i = 0; i < n_rows; ++i)
+            if (rows[i].n_tok > 1) max_prompt_ctx = std::max(max_prompt_ctx, rows[i].pos + rows[i].n_tok);
         ds::attention_splits(T, m.n_heads, m.d_head, n_blk, n_drow, m.n_kv_heads, max_ctx,
-                             s->attn_ws_floats, &s_prompt, &s_decode);
+                             max_prompt_ctx, s->attn_ws_floats, &s_prompt, &s_decode);
         tb = 0;
         for (int64_t i = 0; i < n_rows; ++i)
             for (int j = 0; j < rows[i].n_tok; ++j) rsplit[tb++] = rows[i].n_tok == 1 ? 1 : s_prompt;
