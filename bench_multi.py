@@ -29,6 +29,30 @@ def pipeline_config(n_stages, latency_us=100_000, nb=32):
     return cfg
 
 
+def steady_window(cfg_txt, n_circ, world, runs_steps):
+    """Reference metric semantics (SimReport.output_throughput, sim.cpp:510; windowed_stats,
+    workload.cpp:82-116): decode tokens counted at the last stage's compute ends inside the
+    measurement window / window length. The window starts after the first third of the last
+    stage's computes (the prefill transient from empty KV pools: warm-up), on the GPU event clock
+    of the last stage."""
+    from paper_2501_14784_b200 import pipeline as pl
+    sched = pl.schedule_config(cfg_txt, CONFIGS, max_circuits=n_circ)
+    order = [op[3] for op in sched["ops"][world - 1] if op[0] == 0 and 0 <= op[3] < n_circ]
+    n_dec = [c["n_decode"] for c in sched["circuits"]]
+    rates = []
+    for steps in runs_steps:
+        n = min(len(steps), len(order))
+        k0 = n // 3
+        toks = sum(n_dec[order[k]] for k in range(k0, n))
+        ms = steps[n - 1][3] - steps[k0 - 1][3]
+        rates.append(toks / (ms / 1e3))
+    return {"tokens_per_s": sum(rates) / len(rates),
+            "desc": "steady state: decode tokens of the last stage's computes after the first third "
+                    "(warm-up from empty KV pools excluded, as the reference's windowed metric) over "
+                    "that window on the last stage's GPU event clock; step_tokens_per_s counts the "
+                    "whole step"}
+
+
 def run_multi(args):
     import torch.distributed as dist
 
@@ -88,8 +112,11 @@ def run_multi(args):
         lib.ds_session_destroy(h)
     dev = [r["device_us"] for r in runs]
     wall = [r["wall_us"] for r in runs]
+    window = None
+    if rank == world - 1:
+        window = steady_window(txt, nb * rounds, world, [r["stages"][0]["steps"] for r in runs])
     gathered = [None] * world
-    dist.all_gather_object(gathered, {"dev": dev, "wall": wall, "clk": clk.summary(),
+    dist.all_gather_object(gathered, {"dev": dev, "wall": wall, "clk": clk.summary(), "window": window,
                                       "kernels": prof["stages"][0]["kernels"],
                                       "launches": sum(r["launches"] for r in runs),
                                       "stage": prof["stages"][0]})
@@ -104,8 +131,12 @@ def run_multi(args):
     clocks["reasons"] = sorted({r for g in gathered for r in g["clk"]["reasons"]})
     rf = roofline(gathered[0]["kernels"])
     rf["rank"] = 0
+    win = gathered[world - 1]["window"]
+    step_tps = toks * args.steps / (sum(dev_max) / 1e6)
     return {
-        "metric": METRIC, "value": round(toks * args.steps / (sum(dev_max) / 1e6), 2),
+        "metric": METRIC, "value": round(win["tokens_per_s"], 2),
+        "step_tokens_per_s": round(step_tps, 2),
+        "window": win["desc"],
         "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(statistics.mean(dev_max) / 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",

@@ -615,6 +615,8 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     st.gaps.push_back(gap);
                 else
                     st.gaps.push_back(0.0);
+                float end = 0;
+                st.ends.push_back(cudaEventElapsedTime(&end, w.t_begin, w.timing[i].b) == cudaSuccess ? end : 0.0);
             }
         }
         std::vector<char> buf(1 << 14);
@@ -666,7 +668,8 @@ std::string GpuRunResult::to_json() const {
            << (s.kernel_stats.empty() ? "{}" : s.kernel_stats) << ",\"steps\":[";
         for (size_t k = 0; k < s.steps.size(); ++k)
             os << (k ? "," : "") << "[" << s.steps[k].first << "," << s.steps[k].second << ","
-               << (k < s.gaps.size() ? s.gaps[k] : 0.0) << "]";
+               << (k < s.gaps.size() ? s.gaps[k] : 0.0) << "," << (k < s.ends.size() ? s.ends[k] : 0.0)
+               << "]";
         os << "]}";
     }
     os << "],\"tokens\":[";

@@ -27,6 +27,7 @@ struct StageRunStats {
     double busy_ms = 0, device_ms = 0;
     std::vector<std::pair<int64_t, double>> steps;  // (rows, ms) per stage step
     std::vector<double> gaps;  // ms between the end of the previous step and this one's start
+    std::vector<double> ends;  // ms from the run's start to the end of each step (GPU events)
     std::string kernel_stats;                       // ds_stage_kernel_stats JSON
 };
 
