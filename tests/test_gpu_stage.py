@@ -102,3 +102,30 @@ def test_llama8b_dims_last_stage_logits():
         _check_logits(o)
     finally:
         p.close()
+
+
+def test_llama70b_dims_first_and_last_stage():
+    # Llama-3-70B dims (d 8192, GQA 64:8 -> 8 query heads per KV head, ffn 28672): one layer as a
+    # first stage and the last layer + LM head as a last stage (BASELINE configs[3] shapes)
+    a = Pair("llama3-70b-bf16", 0, 1, True, False, n_mb=1, max_slots=4, pages_per_mb=8)
+    try:
+        rows = [(0, 0, 40, 1, 0, 1), (1, 0, 1, 1, 1, 2), (2, 0, 270, 1, 0, 3)]
+        o = a.step(0, rows)
+        err = np.abs(o["gpu_act"] - o["cpu_act"]).max(axis=1)
+        assert np.all(err <= 0.03 * np.abs(o["cpu_act"]).max(axis=1)), err
+        rows = [(0, 40, 1, 1, 1, 1), (1, 1, 1, 1, 1, 2), (2, 270, 1, 1, 1, 3)]
+        for slot, tok in enumerate((5, 6, 7)):  # the previous circuit's samples, in row order
+            a.last_tok[(0, slot)] = tok
+        o = a.step(0, rows, ids_in=np.array([5, 6, 7], dtype=np.int32))
+        err = np.abs(o["gpu_act"] - o["cpu_act"]).max(axis=1)
+        assert np.all(err <= 0.03 * np.abs(o["cpu_act"]).max(axis=1)), err
+    finally:
+        a.close()
+    b = Pair("llama3-70b-bf16", 79, 80, False, True, n_mb=1, max_slots=4, pages_per_mb=8)
+    try:
+        rows = [(0, 0, 17, 1, 0, 1), (1, 0, 1, 1, 1, 2), (2, 0, 300, 1, 0, 3)]
+        _check_logits(b.step(0, rows, act_in=random_act(318, 8192, 9)))
+        rows = [(0, 17, 1, 1, 1, 1), (1, 1, 1, 1, 1, 2), (2, 300, 1, 1, 1, 3)]
+        _check_logits(b.step(0, rows, act_in=random_act(3, 8192, 10)))
+    finally:
+        b.close()
