@@ -620,6 +620,234 @@ attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
     }
 }
 
+DS_DEVICE uint32_t movmatrix_t(uint32_t a) {
+    uint32_t d;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+    return d;
+}
+
+// Operand-swapped decode rows (G <= 8 query heads per KV head): S^T = K . Q^T with the 16 chunk
+// tokens as the MMA M rows and the heads as N (8 columns, G real) and O^T += V^T . P^T with
+// 16 head dims as M -- half the mma.sync and softmax work of the Q-as-M form (where only G of
+// the 16 M rows are real), fewer accumulator registers. P^T moves from the accumulator layout
+// into the B-operand layout with movmatrix. Same ring / split / merge structure as
+// attn_decode_kernel.
+template <int DH, int ST = kDecStages>
+__global__ void __launch_bounds__(kAttnWarps * 32)
+attn_decode_t_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* __restrict__ row_pos,
+                     const int32_t* __restrict__ row_page_off, const int32_t* __restrict__ flat_pages,
+                     const int32_t* __restrict__ drows, KvLayout kv, int layer, int splits, int stride,
+                     __nv_bfloat16* __restrict__ o, float* __restrict__ ws, int* __restrict__ counters,
+                     L2Prefetch pf) {
+    pdl_launch_dependents();
+    l2_prefetch_slice(pf);
+    pdl_wait();
+    extern __shared__ __align__(16) uint8_t dec_smem[];
+    DecSmem<DH, ST>& sm = *reinterpret_cast<DecSmem<DH, ST>*>(dec_smem);
+    constexpr int KS = DH / 16;  // k-steps of S^T and M tiles of O^T
+    const int n_kv = kv.n_kv;
+    const int G = n_h / n_kv;
+    const int split = blockIdx.x % splits;
+    const int kvh = (blockIdx.x / splits) % n_kv;
+    const int t = drows[blockIdx.x / (splits * n_kv)];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, tq = lane & 3;
+    const int ctx = row_pos[t] + 1;
+    const int n_chunks = (ctx + kDecChunk - 1) / kDecChunk;
+    const int ch0 = split * n_chunks / splits, ch1 = (split + 1) * n_chunks / splits;
+    const int32_t* pages = flat_pages + row_page_off[t];
+
+    // Q^T as the B operand (k = head dim, n = head g): b0 = dims 2tq..+1, b1 = dims 2tq+8..+9
+    uint32_t qb[KS][2];
+    const float qs = rsqrtf(float(DH)) * 1.4426950408889634f;
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            float x0 = 0.f, x1 = 0.f;
+            if (g < G) {
+                const __nv_bfloat162 v2 = *reinterpret_cast<const __nv_bfloat162*>(
+                    q + (size_t(t) * n_h + kvh * G + g) * DH + kk * 16 + 2 * tq + 8 * i);
+                x0 = __bfloat162float(v2.x) * qs;
+                x1 = __bfloat162float(v2.y) * qs;
+            }
+            qb[kk][i] = pack2(x0, x1);
+        }
+    // per head column (2tq, 2tq+1): running max and this thread's partial row sum
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+    float acc[KS][4];  // O^T tile mt: dims mt*16 + g (+8), heads 2tq, 2tq+1
+#pragma unroll
+    for (int j = 0; j < KS; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+
+    const size_t head_k = ((size_t(layer) * 2 + 0) * n_kv + kvh) * 256 * DH;
+    const size_t head_v = ((size_t(layer) * 2 + 1) * n_kv + kvh) * 256 * DH;
+    const int my_n = ch1 - ch0 > warp ? (ch1 - ch0 - warp + kAttnWarps - 1) / kAttnWarps : 0;
+    auto load = [&](int j, int buf) {
+        const int tok0 = (ch0 + warp + j * kAttnWarps) * kDecChunk;
+        const size_t base = size_t(pages[tok0 >> 8]) * kv.page_elems + size_t(tok0 & 255) * DH;
+        const __nv_bfloat16* ksrc = kv.pool + base + head_k;
+        const __nv_bfloat16* vsrc = kv.pool + base + head_v;
+#pragma unroll
+        for (int i = lane; i < kDecChunk * DH / 8; i += 32) {
+            const int r = i / (DH / 8), c = (i % (DH / 8)) * 8;
+            cp_async16(&sm.k[warp][buf][r][c], ksrc + size_t(r) * DH + c);
+            cp_async16(&sm.v[warp][buf][r][c], vsrc + size_t(r) * DH + c);
+        }
+    };
+#pragma unroll
+    for (int j = 0; j < ST - 1; ++j) {
+        if (j < my_n) load(j, j);
+        cp_async_commit();
+    }
+    for (int j = 0; j < my_n; ++j) {
+        const int buf = j % ST;
+        if (j + ST - 1 < my_n) load(j + ST - 1, (j + ST - 1) % ST);
+        cp_async_commit();
+        cp_async_wait<ST - 1>();
+        __syncwarp();
+        const int tok0 = (ch0 + warp + j * kAttnWarps) * kDecChunk;
+        const int valid = min(kDecChunk, ctx - tok0);
+        if (valid < kDecChunk) {  // no 0 * garbage = NaN from rows past the context
+            for (int i = lane; i < (kDecChunk - valid) * (DH / 8); i += 32) {
+                const int r = valid + i / (DH / 8), c = (i % (DH / 8)) * 8;
+                *reinterpret_cast<uint4*>(&sm.v[warp][buf][r][c]) = make_uint4(0, 0, 0, 0);
+            }
+            __syncwarp();
+        }
+        // S^T[16 tokens][8 heads]
+        float s[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint32_t kbase = smem_u32(&sm.k[warp][buf][0][0]);
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+            uint32_t a[4];
+            // A = K rows (tokens) x 16 dims: lanes 0-15 rows 0-15 at col kk*16, lanes 16-31 at +8
+            ldsm_x4(kbase + uint32_t(((lane & 15) * (DH + 8) + kk * 16 + (lane >> 4) * 8) * 2), a[0], a[1],
+                    a[2], a[3]);
+            mma16816(s, a, qb[kk][0], qb[kk][1]);
+        }
+        // s[0], s[1]: token g, heads 2tq, 2tq+1; s[2], s[3]: token g + 8
+        if (tok0 + g >= ctx) s[0] = s[1] = -INFINITY;
+        if (tok0 + g + 8 >= ctx) s[2] = s[3] = -INFINITY;
+        float mt[2] = {fmaxf(s[0], s[2]), fmaxf(s[1], s[3])};
+        float alpha[2];
+#pragma unroll
+        for (int hc = 0; hc < 2; ++hc) {
+            mt[hc] = fmaxf(mt[hc], __shfl_xor_sync(0xffffffffu, mt[hc], 4));
+            mt[hc] = fmaxf(mt[hc], __shfl_xor_sync(0xffffffffu, mt[hc], 8));
+            mt[hc] = fmaxf(mt[hc], __shfl_xor_sync(0xffffffffu, mt[hc], 16));
+            const float mn = fmaxf(m_run[hc], mt[hc]);
+            alpha[hc] = mn == -INFINITY ? 1.f : exp2f(m_run[hc] - mn);
+            m_run[hc] = mn;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s[e] = m_run[e & 1] == -INFINITY ? 0.f : exp2f(s[e] - m_run[e & 1]);
+        l_run[0] = l_run[0] * alpha[0] + s[0] + s[2];
+        l_run[1] = l_run[1] * alpha[1] + s[1] + s[3];
+        if (__any_sync(0xffffffffu, alpha[0] != 1.f || alpha[1] != 1.f)) {
+#pragma unroll
+            for (int mt2 = 0; mt2 < KS; ++mt2) {
+                acc[mt2][0] *= alpha[0];
+                acc[mt2][1] *= alpha[1];
+                acc[mt2][2] *= alpha[0];
+                acc[mt2][3] *= alpha[1];
+            }
+        }
+        // P^T (k = token, n = head) as the B operand: transpose the two 8x8 token halves
+        const uint32_t pb0 = movmatrix_t(pack2(s[0], s[1]));
+        const uint32_t pb1 = movmatrix_t(pack2(s[2], s[3]));
+        const uint32_t vbase = smem_u32(&sm.v[warp][buf][0][0]);
+#pragma unroll
+        for (int mt2 = 0; mt2 < KS; ++mt2) {
+            uint32_t a[4];
+            // A = V^T (dims x tokens) from V [token][dim] with the transposing ldmatrix
+            ldsm_x4_t(vbase + uint32_t((((lane & 7) + ((lane >> 4) & 1) * 8) * (DH + 8) + mt2 * 16 +
+                                        ((lane >> 3) & 1) * 8) * 2),
+                      a[0], a[1], a[2], a[3]);
+            mma16816(acc[mt2], a, pb0, pb1);
+        }
+        __syncwarp();
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int hc = 0; hc < 2; ++hc) {  // row sums: over the tokens held by the 8 g-lanes
+        l_run[hc] += __shfl_xor_sync(0xffffffffu, l_run[hc], 4);
+        l_run[hc] += __shfl_xor_sync(0xffffffffu, l_run[hc], 8);
+        l_run[hc] += __shfl_xor_sync(0xffffffffu, l_run[hc], 16);
+    }
+    // merge the 4 warps' states through shared memory: red[warp][head 8][DH + 2]
+    __syncthreads();
+    float* red = reinterpret_cast<float*>(&sm.k[0][0][0][0]);
+#pragma unroll
+    for (int mt2 = 0; mt2 < KS; ++mt2)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int h = 2 * tq + (e & 1), dd = mt2 * 16 + g + ((e & 2) ? 8 : 0);
+            red[(warp * 8 + h) * (DH + 2) + dd] = acc[mt2][e];
+        }
+    if (g == 0) {
+#pragma unroll
+        for (int hc = 0; hc < 2; ++hc) {
+            red[(warp * 8 + 2 * tq + hc) * (DH + 2) + DH] = m_run[hc];
+            red[(warp * 8 + 2 * tq + hc) * (DH + 2) + DH + 1] = l_run[hc];
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < G * DH; i += blockDim.x) {
+        const int r = i / DH, dd = i % DH;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, red[(w * 8 + r) * (DH + 2) + DH]);
+        float num = 0.f, den = 0.f;
+#pragma unroll
+        for (int w = 0; w < kAttnWarps; ++w) {
+            const float* src = red + (w * 8 + r) * (DH + 2);
+            const float wt = src[DH] == -INFINITY ? 0.f : exp2f(src[DH] - M);
+            num += src[dd] * wt;
+            den += src[DH + 1] * wt;
+        }
+        const size_t row_head = size_t(t) * n_h + kvh * G + r;
+        if (splits == 1) {
+            o[row_head * DH + dd] = f2bf(num / den);
+        } else {
+            float* dst = ws + (row_head * stride + split) * (DH + 2);
+            __stcg(dst + dd, num);
+            if (dd == 0) {
+                __stcg(dst + DH, M);
+                __stcg(dst + DH + 1, den);
+            }
+        }
+    }
+    if (splits == 1) return;
+    __threadfence();
+    __syncthreads();
+    __shared__ int last_cta;
+    if (threadIdx.x == 0) {
+        int* cnt = counters + size_t(t) * n_kv + kvh;
+        const int old = atomicAdd(cnt, 1);
+        last_cta = old == splits - 1;
+        if (last_cta) *cnt = 0;
+    }
+    __syncthreads();
+    if (!last_cta) return;
+    __threadfence();
+    for (int i = threadIdx.x; i < G * DH; i += blockDim.x) {
+        const int r = i / DH, dd = i % DH;
+        const size_t row_head = size_t(t) * n_h + kvh * G + r;
+        const float* base = ws + row_head * stride * (DH + 2);
+        float M = -INFINITY;
+        for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, __ldcg(base + sp * (DH + 2) + DH));
+        float num = 0.f, den = 0.f;
+        for (int sp = 0; sp < splits; ++sp) {
+            const float ms = __ldcg(base + sp * (DH + 2) + DH);
+            if (ms == -INFINITY) continue;
+            const float w = exp2f(ms - M);
+            num += __ldcg(base + sp * (DH + 2) + dd) * w;
+            den += __ldcg(base + sp * (DH + 2) + DH + 1) * w;
+        }
+        o[row_head * DH + dd] = f2bf(num / den);
+    }
+}
+
 int attention_block_positions(int n_h, int n_kv) { return (kAttnWarps * 16) / (n_h / n_kv); }
 
 // Context splits (flash-decoding): at least kSplitTarget CTAs per SM when the (block, kv head)
@@ -704,6 +932,28 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
             const int ctas = int(grid.x);
             st = ctas <= kNumSMs ? 4 : (ctas <= 2 * kNumSMs ? 3 : 2);
         }
+        // operand-swapped kernel for G <= 8 (measured 5% less attention time on config 2);
+        // DS_ATTN_DECODE=1 selects the Q-as-M kernel
+        static const int dec_env = getenv("DS_ATTN_DECODE") ? atoi(getenv("DS_ATTN_DECODE")) : 2;
+        if (dec_env == 2 && n_h / kv.n_kv <= 8) {
+            switch (st) {
+                case 3:
+                    launch_pdl(attn_decode_t_kernel<DH, 3>, grid, block, sizeof(DecSmem<DH, 3>), stream, q,
+                               n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws,
+                               counters, pf_dec);
+                    break;
+                case 4:
+                    launch_pdl(attn_decode_t_kernel<DH, 4>, grid, block, sizeof(DecSmem<DH, 4>), stream, q,
+                               n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws,
+                               counters, pf_dec);
+                    break;
+                default:
+                    launch_pdl(attn_decode_t_kernel<DH, 2>, grid, block, sizeof(DecSmem<DH, 2>), stream, q,
+                               n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd, stride, o, ws,
+                               counters, pf_dec);
+            }
+            return;
+        }
         switch (st) {
             case 3:
                 launch_pdl(attn_decode_kernel<DH, 3>, grid, block, sizeof(DecSmem<DH, 3>), stream, q,
@@ -753,6 +1003,9 @@ static void preload_decode() {
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, attn_decode_kernel<DH, ST>);
     cudaFuncSetAttribute(attn_decode_kernel<DH, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(DecSmem<DH, ST>)));
+    cudaFuncGetAttributes(&a, attn_decode_t_kernel<DH, ST>);
+    cudaFuncSetAttribute(attn_decode_t_kernel<DH, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(sizeof(DecSmem<DH, ST>)));
 }
 
