@@ -13,7 +13,7 @@ if [[ $what == launches || $what == all ]]; then
       --csv --log-file "$OUT/launches.csv" $DRV > "$OUT/ncu_launches.log" 2>&1 || true
 fi
 if [[ $what == full || $what == all ]]; then
-  ncu --set full --clock-control none --import-source on -k regex:attn_decode_kernel \
+  ncu --set full --clock-control none --import-source on -k regex:attn_decode \
       --launch-skip 9000 --launch-count 1 -o "$OUT/attn_decode" -f $DRV > "$OUT/ncu_attn.log" 2>&1 || true
   ncu --set full --clock-control none --import-source on -k regex:gemm_tc_kernel \
       --launch-skip 35842 --launch-count 1 -o "$OUT/gemm_gu" -f $DRV > "$OUT/ncu_gemm.log" 2>&1 || true
