@@ -63,6 +63,7 @@ template <int DH>
 struct PromptSmem {
     __nv_bfloat16 k[2][2][kTile][DH + 8];  // [pair buffer][parity]
     __nv_bfloat16 v[2][2][kTile][DH + 8];
+    __nv_bfloat16 q[64][DH + 8];           // the block's query rows (r = position * G + head)
 };
 
 // blocks: [n_blocks][3] = (first row t0, n positions, unused)
@@ -99,25 +100,15 @@ attn_prompt_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
 
     const int r_base = rg * 16;
     const bool warp_active = r_base < rows;
-    // Q fragments, pre-scaled by log2(e)/sqrt(d_head)
+    // Q rows stream into shared memory with the first K/V tiles (cp.async, 16 B per request, the
+    // G heads of a position contiguous); fragments via ldmatrix once they land. S is scaled by
+    // log2(e)/sqrt(d_head) after the MMA.
     uint32_t qa[KS][4];
     const float qs = rsqrtf(float(DH)) * 1.4426950408889634f;
-#pragma unroll
-    for (int kk = 0; kk < KS; ++kk)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int r = r_base + g + ((i & 1) ? 8 : 0);
-            const int col = kk * 16 + 2 * tq + ((i & 2) ? 8 : 0);
-            float x0 = 0.f, x1 = 0.f;
-            if (r < rows) {
-                const int p = r / G, h = r % G;
-                const __nv_bfloat162 v2 = *reinterpret_cast<const __nv_bfloat162*>(
-                    q + (size_t(t0 + p) * n_h + kvh * G + h) * DH + col);
-                x0 = __bfloat162float(v2.x) * qs;
-                x1 = __bfloat162float(v2.y) * qs;
-            }
-            qa[kk][i] = pack2(x0, x1);
-        }
+    for (int i = threadIdx.x; i < rows * (DH / 8); i += blockDim.x) {
+        const int r = i / (DH / 8), c = (i % (DH / 8)) * 8;
+        cp_async16(&sm.q[r][c], q + (size_t(t0 + r / G) * n_h + kvh * G + r % G) * DH + c);
+    }
     int rpos[2];
 #pragma unroll
     for (int hr = 0; hr < 2; ++hr) {
@@ -151,7 +142,12 @@ attn_prompt_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
         cp_async_commit();
     };
 
-    if (n_pairs > 0) load_pair(0, 0);
+    if (n_pairs > 0) {
+        load_pair(0, 0);  // commits the Q rows with the first tile pair
+    } else {
+        cp_async_commit();
+        cp_async_wait<0>();
+    }
     for (int pi = 0; pi < n_pairs; ++pi) {
         const int buf = pi & 1;
         if (pi + 1 < n_pairs) {
@@ -161,6 +157,12 @@ attn_prompt_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
             cp_async_wait<0>();
         }
         __syncthreads();
+        if (pi == 0 && warp_active) {  // the Q rows landed with the first pair
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk)
+                ldsm_x4(smem_u32(&sm.q[r_base + (lane & 15)][kk * 16 + (lane >> 4) * 8]), qa[kk][0],
+                        qa[kk][1], qa[kk][2], qa[kk][3]);
+        }
         // zero V rows past the last valid token (0 * garbage must not produce NaN)
         for (int pp = 0; pp < 2; ++pp) {
             const int tile = tile0 + 2 * pi + pp;
@@ -189,14 +191,14 @@ attn_prompt_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
                     mma16816(s[j], qa[kk], b0, b1);
                     mma16816(s[j], qa[kk + 1], b2, b3);
                 }
-            // causal mask + online softmax (rows g and g+8)
+            // scale, causal mask + online softmax (rows g and g+8)
             float mt[2] = {-INFINITY, -INFINITY};
 #pragma unroll
             for (int j = 0; j < SN; ++j)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int hr = e >> 1;
-                    if (tok0 + j * 8 + 2 * tq + (e & 1) > rpos[hr]) s[j][e] = -INFINITY;
+                    s[j][e] = tok0 + j * 8 + 2 * tq + (e & 1) > rpos[hr] ? -INFINITY : s[j][e] * qs;
                     mt[hr] = fmaxf(mt[hr], s[j][e]);
                 }
             float alpha[2];
