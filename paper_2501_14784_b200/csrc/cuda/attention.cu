@@ -1,18 +1,18 @@
 // Paged causal GQA attention over the stage's KV pages on tensor cores (mma.sync m16n8k16 bf16,
 // fp32 accumulate), FlashAttention-2 style with an online softmax in the log2 domain.
 //
-// Work item = (query block, kv head, context split). A query block is either one decode row or
-// up to QP consecutive prompt positions of one request (chunked prefill, reference
-// begin_circuit sim.cpp:386-407); its G = n_h / n_kv query heads share every staged K/V tile
-// (GQA reuse), so the Q tile has QP*G rows. K/V tiles of 64 tokens (never straddling a 256-token
-// page) are double-buffered in shared memory with cp.async. Prefill blocks give each of the 4
-// warps 16 query rows over the whole tile; decode blocks (G <= 16 rows) give each warp a 16-token
-// slice of the tile and merge the 4 partial softmax states at the end. Context splits
-// (flash-decoding) keep >= 2 CTAs per SM when the block count is small; a combine kernel merges
-// the (o, m, l) partials.
+// Two kernels per layer:
+//  * prompt blocks (attn_prompt_kernel): up to QP = 64/G consecutive prompt positions of one
+//    request (chunked prefill, reference begin_circuit sim.cpp:386-407); the G = n_h / n_kv query
+//    heads of a KV head share every staged 64-token K/V tile (a 256-token page never straddled),
+//    so the request's KV is read once per block; 8 warps = 4 row groups x 2 tile parities.
+//  * decode rows (attn_decode_t_kernel, attn_decode_kernel for G > 8): one row x KV head per CTA,
+//    per-warp cp.async rings over 16-token chunks, operand-swapped GQA MMAs.
+// Context splits (flash-decoding) when rows are few; the last CTA of each (row / block, KV head)
+// merges the (o, m, l) partials in split order.
 //
-// HBM roofline: each (block, kv head) reads its request's KV once: ctx * d_head * 2 (K,V) * 2 B
-// per kv head.
+// HBM roofline: each (row or block, kv head) reads its request's KV once: ctx * d_head * 2 (K,V)
+// * 2 B per kv head.
 #include <stdlib.h>
 
 #include <algorithm>
@@ -345,32 +345,6 @@ attn_prompt_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
     }
 }
 
-// Merges the (o, m, l) context-split partials of every row-head with row_splits[row] > 1
-// (partials at ws[(row_head * stride + split) * (DH + 2)]).
-template <int DH>
-__global__ void attn_combine_kernel(const float* __restrict__ ws, int stride, int n_h,
-                                    const int32_t* __restrict__ row_splits,
-                                    __nv_bfloat16* __restrict__ o) {
-    pdl_launch_dependents();
-    pdl_wait();
-    const int rh = blockIdx.x;
-    const int splits = row_splits[rh / n_h];
-    if (splits <= 1) return;  // written directly by the attention kernel
-    const float* base = ws + size_t(rh) * stride * (DH + 2);
-    float M = -INFINITY;
-    for (int s = 0; s < splits; ++s) M = fmaxf(M, base[s * (DH + 2) + DH]);
-    for (int dd = threadIdx.x; dd < DH; dd += blockDim.x) {
-        float num = 0.f, den = 0.f;
-        for (int s = 0; s < splits; ++s) {
-            const float ms = base[s * (DH + 2) + DH];
-            if (ms == -INFINITY) continue;
-            const float w = exp2f(ms - M);
-            num += base[s * (DH + 2) + dd] * w;
-            den += base[s * (DH + 2) + DH + 1] * w;
-        }
-        o[size_t(rh) * DH + dd] = f2bf(num / den);
-    }
-}
 
 // ------------------------------------------------------------------ decode rows ----
 // One decode row x one KV head x one context split per CTA. The split's context is cut into
@@ -910,12 +884,11 @@ static int decode_stages() {
 template <int DH>
 static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,
                    const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
-                   int n_blocks, const int32_t* drows, int n_drows, const int32_t* row_splits,
+                   int n_blocks, const int32_t* drows, int n_drows,
                    const KvLayout& kv, int layer, int sp, int sd, __nv_bfloat16* o, float* ws,
                    int* counters, const L2Prefetch& pf, cudaStream_t stream) {
     const L2Prefetch pf_dec = pf;  // the decode launch (or the prompt one when alone) prefetches
-    // timing experiments only (results invalid): DS_ATTN_SKIP bit 0 prompt blocks, 1 decode rows,
-    // 2 combine
+    // timing experiments only (results invalid): DS_ATTN_SKIP bit 0 prompt blocks, 1 decode rows
     static const int skip = getenv("DS_ATTN_SKIP") ? atoi(getenv("DS_ATTN_SKIP")) : 0;
     if (skip & 1) n_blocks = 0;
     if (skip & 2) n_drows = 0;
@@ -973,12 +946,11 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
                            counters, pf_dec);
         }
     }
-    (void)row_splits;  // both kernels merge their context splits in-kernel
 }
 
 int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,
                     const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
-                    int n_blocks, const int32_t* drows, int n_drows, const int32_t* row_splits,
+                    int n_blocks, const int32_t* drows, int n_drows,
                     const KvLayout& kv, int layer, int s_prompt, int s_decode, __nv_bfloat16* o,
                     float* ws, size_t ws_floats, int* counters, const L2Prefetch& pf,
                     cudaStream_t stream) {
@@ -989,10 +961,10 @@ int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_p
         return -4;
     if (kv.d_head == 128)
         launch<128>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, drows, n_drows,
-                    row_splits, kv, layer, s_prompt, s_decode, o, ws, counters, pf, stream);
+                    kv, layer, s_prompt, s_decode, o, ws, counters, pf, stream);
     else if (kv.d_head == 64)
         launch<64>(q, T, n_h, row_pos, row_page_off, flat_pages, blocks, n_blocks, drows, n_drows,
-                   row_splits, kv, layer, s_prompt, s_decode, o, ws, counters, pf, stream);
+                   kv, layer, s_prompt, s_decode, o, ws, counters, pf, stream);
     else
         return -2;
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -3;
@@ -1015,8 +987,6 @@ void preload_attention() {
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, attn_prompt_kernel<128>);
     cudaFuncGetAttributes(&a, attn_prompt_kernel<64>);
-    cudaFuncGetAttributes(&a, attn_combine_kernel<128>);
-    cudaFuncGetAttributes(&a, attn_combine_kernel<64>);
     cudaFuncSetAttribute(attn_prompt_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(sizeof(PromptSmem<128>)));
     cudaFuncSetAttribute(attn_prompt_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,

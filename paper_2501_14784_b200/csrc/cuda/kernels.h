@@ -88,10 +88,9 @@ void rope_kv_append(const __nv_bfloat16* qkv, int T, int n_h, int n_kv, int d_he
 // Prompt query blocks: blocks[3*i] = first row, [3*i+1] = consecutive positions
 // (<= attention_block_positions() rows of one request), [3*i+2] = 0. Decode rows (one query
 // position each) are listed separately in drows[] and go to the decode kernel.
-// Context splits: s_prompt for the prompt blocks, s_decode for the decode rows; row_splits[t]
-// (device) = the split count of a prompt row (1 for decode rows), read by the combine kernel.
-// Decode rows merge their splits in-kernel (last CTA per row and KV head; `counters`: zeroed
-// ints, >= rows x n_kv, self-resetting).
+// Context splits: s_prompt for the prompt blocks, s_decode for the decode rows; each kernel's
+// last CTA of a (row or block, KV head) merges the split partials (`counters`: zeroed ints,
+// >= 2 x rows x n_kv, self-resetting; ws: rows x n_h x max(splits) x (d_head + 2) floats).
 int attention_block_positions(int n_h, int n_kv);
 void attention_splits(int T, int n_h, int d_head, int n_blocks, int n_drows, int n_kv, int max_ctx,
                       int max_prompt_ctx, size_t ws_floats, int* s_prompt, int* s_decode);
@@ -99,7 +98,7 @@ int attention_launches(int n_blocks, int n_drows, int s_prompt, int s_decode);
 size_t attention_workspace_floats(int T, int n_h, int d_head, int splits);
 int attention_paged(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_pos,
                     const int32_t* row_page_off, const int32_t* flat_pages, const int32_t* blocks,
-                    int n_blocks, const int32_t* drows, int n_drows, const int32_t* row_splits,
+                    int n_blocks, const int32_t* drows, int n_drows,
                     const KvLayout& kv, int layer, int s_prompt, int s_decode, __nv_bfloat16* o,
                     float* ws, size_t ws_floats, int* counters, const L2Prefetch& pf,
                     cudaStream_t stream);

@@ -598,7 +598,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
                                                    std::to_string(mb) + " has non-resident pages");
 
     const int prevR = int(k.prev_logit_slots.size());
-    const size_t need_meta = size_t(11) * T + 2 * size_t(R) + P + prevR + 8;
+    const size_t need_meta = size_t(10) * T + 2 * size_t(R) + P + prevR + 8;
     if (need_meta > s->meta_cap) return ds_fail(DS_ERR_ARG, "step metadata exceeds capacity");
     const int buf = s->meta_buf;
     s->meta_buf ^= 1;
@@ -612,8 +612,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     int32_t* logit_rows = row_poff + T;
     int32_t* logit_slot = logit_rows + R;
     int32_t* prev_slot = logit_slot + R;
-    int32_t* rsplit = prev_slot + prevR;  // attention context splits of each row's kind
-    int32_t* blk = rsplit + T;            // attention query blocks, 3 ints each (<= T blocks)
+    int32_t* blk = prev_slot + prevR;  // attention query blocks, 3 ints each (<= T blocks)
     int32_t* flat = blk + 3 * T;
     {
         int t = 0, r = 0, poff = 0;
@@ -669,9 +668,6 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
             if (rows[i].n_tok > 1) max_prompt_ctx = std::max(max_prompt_ctx, rows[i].pos + rows[i].n_tok);
         ds::attention_splits(T, m.n_heads, m.d_head, n_blk, n_drow, m.n_kv_heads, max_ctx,
                              max_prompt_ctx, s->attn_ws_floats, &s_prompt, &s_decode);
-        tb = 0;
-        for (int64_t i = 0; i < n_rows; ++i)
-            for (int j = 0; j < rows[i].n_tok; ++j) rsplit[tb++] = rows[i].n_tok == 1 ? 1 : s_prompt;
     }
     const size_t meta_n = size_t(flat - hm) + P;
     CK(cudaMemcpyAsync(s->d_meta, hm, meta_n * 4, cudaMemcpyHostToDevice, s->stream));
@@ -685,8 +681,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     const int32_t* d_lrows = d_poff + T;
     const int32_t* d_lslot = d_lrows + R;
     const int32_t* d_prev = d_lslot + R;
-    const int32_t* d_rsplit = d_prev + prevR;
-    const int32_t* d_blk = d_rsplit + T;
+    const int32_t* d_blk = d_prev + prevR;
     const int32_t* d_flat = d_blk + 3 * T;
 
     // ---- wait for the swap-in this compute depends on
@@ -771,7 +766,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
         if (pf_env) pf_o = {lw.wo.data, size_t(d) * qdim * 2};
         if (!(skip & 4))
             rc |= ds::attention_paged(s->q, T, m.n_heads, d_pos, d_poff, d_flat, d_blk, n_blk,
-                                      d_blk + 3 * n_blk, n_drow, d_rsplit, s->kv, li, s_prompt,
+                                      d_blk + 3 * n_blk, n_drow, s->kv, li, s_prompt,
                                       s_decode, s->attn, s->attn_ws, s->attn_ws_floats, s->attn_cnt,
                                       pf_o, st);
         end_other(PK_ATTN, attn_flops, attn_bytes,
