@@ -88,3 +88,27 @@ def test_gemm_silu_epilogue(T, clusters):
     got = from_bf16(out).astype(np.float64)
     assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max() + 1e-3
 
+
+
+@pytest.mark.parametrize("T", [600, 1100])
+def test_gemm_wide_multi_token_blocks(T):
+    # wide GEMM (>= one wave of 256-row pair tiles) above 512 tokens: 256-token blocks, tile
+    # order token-block-fastest, data-parallel rounds + remainder
+    got, ref = _run(T, 19456, 256, epi=1, seed=T)
+    assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max() + 1e-3
+
+
+@pytest.mark.parametrize("T", [700])
+def test_gemm_wide_silu_multi_token_blocks(T):
+    from paper_2501_14784_b200 import _native as nat
+    from paper_2501_14784_b200.bf16 import from_bf16, to_bf16
+    N, K = 19456, 256
+    rng = np.random.default_rng(T)
+    x = to_bf16(rng.standard_normal((T, K)).astype(np.float32))
+    w = to_bf16((rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32))
+    acc = from_bf16(x).astype(np.float64) @ from_bf16(w).astype(np.float64).T
+    ref = _silu_ref(acc)
+    out = np.zeros((T, N // 2), dtype=np.uint16)
+    nat.check(nat.lib.ds_dbg_gemm(x.ctypes.data, w.ctypes.data, T, N, K, 3, None, 0, out.ctypes.data))
+    got = from_bf16(out).astype(np.float64)
+    assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max() + 1e-3

@@ -129,3 +129,16 @@ def test_llama70b_dims_first_and_last_stage():
         _check_logits(b.step(0, rows, act_in=random_act(3, 8192, 10)))
     finally:
         b.close()
+
+
+def test_llama8b_dims_long_prefill_chunk():
+    # a 700-row prefill circuit (prefill_chunk > 512): 256-token GEMM blocks in token-block-
+    # fastest order, token-split q/k/v and o, prompt attention over three KV pages
+    p = Pair("llama3-8b", 0, 2, True, False, max_rows=768, n_mb=1, max_slots=4, pages_per_mb=8)
+    try:
+        rows = [(0, 0, 600, 1, 0, 1), (1, 0, 100, 1, 0, 2)]
+        o = p.step(0, rows)
+        err = np.abs(o["gpu_act"] - o["cpu_act"]).max(axis=1)
+        assert np.all(err <= 0.03 * np.abs(o["cpu_act"]).max(axis=1)), (err / np.abs(o["cpu_act"]).max(axis=1)).max()
+    finally:
+        p.close()
