@@ -98,6 +98,17 @@ struct Worker {
     int64_t moved_in = 0, moved_out = 0, plan_in = 0;
     int64_t computes = 0;
     std::string error;
+    // per mb: the last circuit whose step (reading recv[mb]) is enqueued, and an event after it.
+    // A producer may overwrite recv[mb] with the mb's next input only after that step: a circuit
+    // without decode rows starts on stage 0 without waiting for its predecessor, so inputs of
+    // one microbatch can otherwise overtake its unconsumed previous input.
+    struct Sync {
+        std::mutex mu;
+        std::condition_variable cv;
+    };
+    std::unique_ptr<Sync> cs{new Sync()};
+    std::vector<int64_t> consumed_c;
+    std::vector<cudaEvent_t> consumed_ev;
 };
 
 }  // namespace
@@ -227,6 +238,10 @@ Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, con
         XK(cudaEventCreate(&w.t_end));
         w.in.resize(NB);
         w.recv.assign(NB, nullptr);
+        w.consumed_c.assign(NB, -1);
+        w.consumed_ev.assign(NB, nullptr);
+        for (int64_t m = 0; m < NB; ++m)
+            XK(cudaEventCreateWithFlags(&w.consumed_ev[m], cudaEventDisableTiming));
         for (int64_t m = 0; m < NB; ++m) {
             w.in[m].reset(new Mailbox());
             const size_t bytes = s == 0 ? size_t(S->max_rows) * 4 : size_t(S->max_rows) * md.d_model * 2;
@@ -297,6 +312,7 @@ void session_destroy(Session* S) {
         cudaSetDevice(w.device);
         cudaDeviceSynchronize();
         for (auto& m : w.in) cudaEventDestroy(m->ev);
+        for (auto e : w.consumed_ev) cudaEventDestroy(e);
         for (void* p : w.recv) cudaFree(p);
         for (auto& t : w.timing) {
             cudaEventDestroy(t.a);
@@ -331,6 +347,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
         for (auto& m : w.in) m->posted = -1;
         S->landed = 0;
         w.served = w.topups = w.moved_in = w.moved_out = w.plan_in = w.computes = 0;
+        std::fill(w.consumed_c.begin(), w.consumed_c.end(), int64_t(-1));
         w.timing_used = 0;
         w.error.clear();
     }
@@ -447,6 +464,12 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 const void* act_in = s == 0 ? (has_input ? w.recv[mb] : nullptr) : w.recv[mb];
                 void* act_out = (last && NS == 1) ? w.recv[mb] : nullptr;  // ids loop back
                 DK(ds_stage_step(w.st, mb, rows.data(), int64_t(rows.size()), act_in, act_out));
+                XK(cudaEventRecord(w.consumed_ev[mb], w.stream));  // recv[mb] read by this step
+                {
+                    std::lock_guard<std::mutex> lk(w.cs->mu);
+                    w.consumed_c[mb] = c;
+                }
+                w.cs->cv.notify_all();
                 if (g_trace) fprintf(stderr, "[ds r%lld] step c=%lld mb=%d rows=%lld need=%lld\n", (long long)s, (long long)c, mb, (long long)circ.eff_batch, (long long)need);
                 if (tm) XK(cudaEventRecord(tm->b, w.stream));
                 w.computes++;
@@ -477,6 +500,16 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     continue;
                 }
                 if (NS > 1 && bytes > 0) {
+                    // forward hop: the consumer must have read the mb's previous input
+                    const int64_t pc = S->prev[c];
+                    if (!last && pc >= 0) {
+                        {
+                            std::unique_lock<std::mutex> lk(next->cs->mu);
+                            next->cs->cv.wait(lk, [&] { return next->consumed_c[mb] >= pc || failed.load(); });
+                        }
+                        if (failed) return;
+                        XK(cudaStreamWaitEvent(w.stream, next->consumed_ev[mb], 0));
+                    }
                     if (next->device == w.device)
                         XK(cudaMemcpyAsync(next->recv[mb], src, size_t(bytes), cudaMemcpyDeviceToDevice, w.stream));
                     else
@@ -492,8 +525,10 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
         } catch (const std::exception& e) {
             w.error = e.what();
             failed = true;
-            for (auto& ww : S->W)
+            for (auto& ww : S->W) {
                 for (auto& m : ww.in) m->cv.notify_all();
+                ww.cs->cv.notify_all();
+            }
             S->land_cv.notify_all();
         }
     };
@@ -518,6 +553,15 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     S->land_cv.wait(lk, [&] { return posted_n - S->landed < Session::kRecvAhead || failed.load(); });
                 }
                 if (failed) return;
+                if (w.idx > 0 && S->prev[c] >= 0) {  // the mb's previous input must be read first
+                    const int64_t pc = S->prev[c];
+                    {
+                        std::unique_lock<std::mutex> lk(w.cs->mu);
+                        w.cs->cv.wait(lk, [&] { return w.consumed_c[mb] >= pc || failed.load(); });
+                    }
+                    if (failed) return;
+                    XK(cudaStreamWaitEvent(S->s_recv, w.consumed_ev[mb], 0));
+                }
                 const ncclResult_t nr =
                     S->api->Recv(w.recv[mb], bytes, ncclUint8, 0, S->links.recv, S->s_recv);
                 ++posted_n;
@@ -532,6 +576,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
             if (w.error.empty()) w.error = std::string("receiver: ") + e.what();
             failed = true;
             for (auto& m : w.in) m->cv.notify_all();
+            w.cs->cv.notify_all();
         }
     };
     // NCCL mode watchdog: a local failure, or no landing and no step for DS_NCCL_TIMEOUT_S
@@ -559,8 +604,10 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     failed = true;
                     S->links.abort(*S->api);
                     S->land_cv.notify_all();
-                    for (auto& w : S->W)
+                    for (auto& w : S->W) {
                         for (auto& m : w.in) m->cv.notify_all();
+                        w.cs->cv.notify_all();
+                    }
                     return;
                 }
             }
