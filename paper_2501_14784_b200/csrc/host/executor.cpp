@@ -143,6 +143,14 @@ struct Session {
     std::mutex land_mu;
     std::condition_variable land_cv;
     int64_t landed = 0;
+    // NCCL mode, stage > 0: activation receives land in a ring of slots instead of one buffer
+    // per microbatch (hundreds of microbatches with the opt policy at high latency). Slot k is
+    // refilled once the step that read its previous occupant was enqueued (ev_consumed).
+    bool ring_mode = false;
+    std::vector<void*> recv_ring;
+    std::vector<int32_t> recv_slot;        // per circuit
+    std::vector<cudaEvent_t> ev_consumed;  // per slot
+    std::vector<int64_t> consumed_n;       // per slot: consumptions enqueued (under land_mu)
 };
 
 namespace {
@@ -242,11 +250,50 @@ Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, con
         w.consumed_ev.assign(NB, nullptr);
         for (int64_t m = 0; m < NB; ++m)
             XK(cudaEventCreateWithFlags(&w.consumed_ev[m], cudaEventDisableTiming));
+        // ring for activation receives when one buffer per microbatch would pass 1.5 GB
+        const size_t slot_bytes = size_t(S->max_rows) * md.d_model * 2;
+        // DS_RECV_RING=0 disables, =2 forces the ring (tests)
+        const int ring_env = getenv("DS_RECV_RING") ? atoi(getenv("DS_RECV_RING")) : 1;
+        const bool ring = S->nccl && s > 0 && ring_env != 0 &&
+                          (ring_env == 2 || size_t(NB) * slot_bytes > (size_t(3) << 29));
         for (int64_t m = 0; m < NB; ++m) {
             w.in[m].reset(new Mailbox());
-            const size_t bytes = s == 0 ? size_t(S->max_rows) * 4 : size_t(S->max_rows) * md.d_model * 2;
+            if (ring) continue;
+            const size_t bytes = s == 0 ? size_t(S->max_rows) * 4 : slot_bytes;
             XK(cudaMalloc(&w.recv[m], bytes));
             XK(cudaMemset(w.recv[m], 0, bytes));
+        }
+        if (ring) {
+            // size: when this stage's compute needs receive j, all receives below the first
+            // unconsumed index f are consumed, and posting j needs slot j % R free: R > j - f
+            std::vector<int64_t> ridx(S->n_circ, -1);
+            int64_t n_recv = 0;
+            for (const StageOp& op : S->sched.ops[s - 1])
+                if (op.kind == OpKind::Compute && op.circuit >= 0 && op.circuit < S->n_circ)
+                    ridx[op.circuit] = n_recv++;
+            std::vector<char> used(n_recv, 0);
+            int64_t first = 0, need = 1;
+            for (const StageOp& op : S->sched.ops[s])
+                if (op.kind == OpKind::Compute && op.circuit >= 0 && op.circuit < S->n_circ &&
+                    ridx[op.circuit] >= 0) {
+                    const int64_t j = ridx[op.circuit];
+                    need = std::max(need, j - first + 1);
+                    used[j] = 1;
+                    while (first < n_recv && used[first]) ++first;
+                }
+            const int64_t fit = int64_t((size_t(3) << 29) / slot_bytes);
+            const int R = int(std::min<int64_t>(NB, std::max<int64_t>(need + Session::kRecvAhead + 1, fit)));
+            S->ring_mode = true;
+            S->recv_ring.assign(R, nullptr);
+            S->ev_consumed.assign(R, nullptr);
+            S->consumed_n.assign(R, 0);
+            S->recv_slot.assign(S->n_circ, -1);
+            for (int k = 0; k < R; ++k) {
+                XK(cudaMalloc(&S->recv_ring[k], slot_bytes));
+                XK(cudaMemset(S->recv_ring[k], 0, slot_bytes));
+                XK(cudaEventCreateWithFlags(&S->ev_consumed[k], cudaEventDisableTiming));
+            }
+            w.recv[0] = S->recv_ring[0];  // warm-up target
         }
     }
     // a mailbox event is recorded on the PRODUCER's stream, so it must belong to that device
@@ -313,7 +360,12 @@ void session_destroy(Session* S) {
         cudaDeviceSynchronize();
         for (auto& m : w.in) cudaEventDestroy(m->ev);
         for (auto e : w.consumed_ev) cudaEventDestroy(e);
-        for (void* p : w.recv) cudaFree(p);
+        if (!S->ring_mode)
+            for (void* p : w.recv) cudaFree(p);
+        for (void* p : S->recv_ring) cudaFree(p);
+        for (auto e : S->ev_consumed) cudaEventDestroy(e);
+        S->recv_ring.clear();
+        S->ev_consumed.clear();
         for (auto& t : w.timing) {
             cudaEventDestroy(t.a);
             cudaEventDestroy(t.b);
@@ -348,6 +400,8 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
         S->landed = 0;
         w.served = w.topups = w.moved_in = w.moved_out = w.plan_in = w.computes = 0;
         std::fill(w.consumed_c.begin(), w.consumed_c.end(), int64_t(-1));
+        std::fill(S->consumed_n.begin(), S->consumed_n.end(), 0);
+        std::fill(S->recv_slot.begin(), S->recv_slot.end(), -1);
         w.timing_used = 0;
         w.error.clear();
     }
@@ -461,10 +515,21 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     tm->rows = circ.eff_batch;
                     XK(cudaEventRecord(tm->a, w.stream));
                 }
-                const void* act_in = s == 0 ? (has_input ? w.recv[mb] : nullptr) : w.recv[mb];
+                int32_t ring_slot = -1;
+                if (S->ring_mode && s > 0) ring_slot = S->recv_slot[c];
+                const void* act_in = s == 0 ? (has_input ? w.recv[mb] : nullptr)
+                                            : (ring_slot >= 0 ? S->recv_ring[ring_slot] : w.recv[mb]);
                 void* act_out = (last && NS == 1) ? w.recv[mb] : nullptr;  // ids loop back
                 DK(ds_stage_step(w.st, mb, rows.data(), int64_t(rows.size()), act_in, act_out));
                 XK(cudaEventRecord(w.consumed_ev[mb], w.stream));  // recv[mb] read by this step
+                if (ring_slot >= 0) {  // the ring slot may be refilled once this step has read it
+                    XK(cudaEventRecord(S->ev_consumed[ring_slot], w.stream));
+                    {
+                        std::lock_guard<std::mutex> lk(S->land_mu);
+                        S->consumed_n[ring_slot]++;
+                    }
+                    S->land_cv.notify_all();
+                }
                 {
                     std::lock_guard<std::mutex> lk(w.cs->mu);
                     w.consumed_c[mb] = c;
@@ -553,7 +618,20 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     S->land_cv.wait(lk, [&] { return posted_n - S->landed < Session::kRecvAhead || failed.load(); });
                 }
                 if (failed) return;
-                if (w.idx > 0 && S->prev[c] >= 0) {  // the mb's previous input must be read first
+                void* dst = w.recv[mb];
+                if (S->ring_mode) {  // slot k: its previous occupant's step must be enqueued
+                    const int R = int(S->recv_ring.size());
+                    const int k = int(posted_n % R);
+                    const int64_t uses = posted_n / R;
+                    {
+                        std::unique_lock<std::mutex> lk(S->land_mu);
+                        S->land_cv.wait(lk, [&] { return S->consumed_n[k] >= uses || failed.load(); });
+                    }
+                    if (failed) return;
+                    if (uses > 0) XK(cudaStreamWaitEvent(S->s_recv, S->ev_consumed[k], 0));
+                    S->recv_slot[c] = k;
+                    dst = S->recv_ring[k];
+                } else if (w.idx > 0 && S->prev[c] >= 0) {  // the mb's previous input must be read first
                     const int64_t pc = S->prev[c];
                     {
                         std::unique_lock<std::mutex> lk(w.cs->mu);
@@ -562,8 +640,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     if (failed) return;
                     XK(cudaStreamWaitEvent(S->s_recv, w.consumed_ev[mb], 0));
                 }
-                const ncclResult_t nr =
-                    S->api->Recv(w.recv[mb], bytes, ncclUint8, 0, S->links.recv, S->s_recv);
+                const ncclResult_t nr = S->api->Recv(dst, bytes, ncclUint8, 0, S->links.recv, S->s_recv);
                 ++posted_n;
                 if (nr != ncclSuccess) throw SimError(std::string("ncclRecv: ") + S->api->GetErrorString(nr));
                 XK(cudaEventRecord(S->ev_recv[c], S->s_recv));
