@@ -829,7 +829,9 @@ int attention_block_positions(int n_h, int n_kv) { return (kAttnWarps * 16) / (n
 // Context splits (flash-decoding): at least kSplitTarget CTAs per SM when the (block, kv head)
 // count alone is short of that, each split keeping >= 2 tiles (128 tokens) of the longest context.
 static int split_target() {
-    static const int v = getenv("DS_ATTN_TARGET") ? atoi(getenv("DS_ATTN_TARGET")) : 2;
+    // 1 CTA per SM of (row, KV head) work before splitting (measured on config 2: targets 0 / 1 /
+    // 2 / 3 -> 4786 / 4796 / 4953 / 4988 ms per step with the operand-swapped decode kernel)
+    static const int v = getenv("DS_ATTN_TARGET") ? atoi(getenv("DS_ATTN_TARGET")) : 1;
     return v;
 }
 int attention_pick_splits(int n_blocks, int n_kv, int max_ctx) {
