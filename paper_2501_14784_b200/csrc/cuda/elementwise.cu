@@ -94,11 +94,19 @@ __global__ void __launch_bounds__(512) rmsnorm_kernel(const __nv_bfloat16* __res
                                int d, const __nv_bfloat16* __restrict__ g, float eps,
                                __nv_bfloat16* __restrict__ y, Planes pl) {
     pdl_launch_dependents();
+    const int nv = d / 8;
+    uint4 gq[VPT];  // gains: weights written at init, so loaded before the dependency wait
+    if (y != nullptr) {
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            const int idx = threadIdx.x + k * blockDim.x;
+            if (idx < nv) gq[k] = reinterpret_cast<const uint4*>(g)[idx];
+        }
+    }
     pdl_wait();
     const int i = blockIdx.x;
     const int src_row = rows ? rows[i] : i;
     const uint4* xr = reinterpret_cast<const uint4*>(x + size_t(src_row) * d);
-    const int nv = d / 8;
     float v[VPT][8];
     float ss = 0.f;
 #pragma unroll
@@ -129,14 +137,13 @@ __global__ void __launch_bounds__(512) rmsnorm_kernel(const __nv_bfloat16* __res
     }
     __syncthreads();
     const float r = 1.0f / sqrtf(red[0] / float(d) + eps);
-    const uint4* gr = reinterpret_cast<const uint4*>(g);
     uint4* yr = reinterpret_cast<uint4*>(y + size_t(i) * d);
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
         const int idx = threadIdx.x + k * blockDim.x;
         if (idx < nv) {
             float gv[8], o[8];
-            unpack8(gr[idx], gv);
+            unpack8(gq[k], gv);
 #pragma unroll
             for (int j = 0; j < 8; ++j) o[j] = gv[j] * round_bf(v[k][j] * r);
             yr[idx] = pack8(o);
@@ -176,9 +183,26 @@ __global__ void __launch_bounds__(512) rope_kv_kernel(const __nv_bfloat16* __res
     const float* s = rs + size_t(pos) * half;
     const size_t page_base = size_t(row_page[t]) * kv.page_elems;
     const int slot = pos & 255;
-    // rotated q and k: each thread handles 8 consecutive rotary pairs (16-byte accesses)
+    // rotated q and k: 8 consecutive rotary pairs per work item (16-byte accesses); then the v
+    // vectors, 16 B per item. One flat index space so all of a row's loads are in flight together.
     const int n_rot = (n_h + n_kv) * (half / 8);
-    for (int w = threadIdx.x; w < n_rot; w += blockDim.x) {
+    const int nv = n_kv * dh / 8;
+    for (int w = threadIdx.x; w < n_rot + nv; w += blockDim.x) {
+        if (w >= n_rot) {
+            const int kh = ((w - n_rot) * 8) / dh, i = ((w - n_rot) * 8) % dh;
+            uint4 val;
+            if (pl.n > 0) {
+                float a[8];
+                sum_planes8(pl, size_t(t) * width + (n_h + n_kv) * dh + kh * dh + i, a);
+                val = pack8(a);
+            } else {
+                val = *reinterpret_cast<const uint4*>(src + (n_h + n_kv) * dh + kh * dh + i);
+            }
+            __nv_bfloat16* dv = kv.pool + page_base + ((size_t(layer) * 2 + 1) * n_kv + kh) * 256 * dh +
+                                size_t(slot) * dh + i;
+            *reinterpret_cast<uint4*>(dv) = val;
+            continue;
+        }
         const int head = w / (half / 8), i = (w % (half / 8)) * 8;
         float x1[8], x2[8], o1[8], o2[8];
         if (pl.n > 0) {  // deferred GEMM epilogue: bf16(sum of planes)
@@ -213,30 +237,14 @@ __global__ void __launch_bounds__(512) rope_kv_kernel(const __nv_bfloat16* __res
         *reinterpret_cast<uint4*>(dst + i) = pack8(o1);
         *reinterpret_cast<uint4*>(dst + i + half) = pack8(o2);
     }
-    // v: plain copy, 16 B per thread-iteration
-    const int nv = n_kv * dh / 8;
-    for (int w = threadIdx.x; w < nv; w += blockDim.x) {
-        const int kh = (w * 8) / dh, i = (w * 8) % dh;
-        uint4 val;
-        if (pl.n > 0) {
-            float a[8];
-            sum_planes8(pl, size_t(t) * width + (n_h + n_kv) * dh + kh * dh + i, a);
-            val = pack8(a);
-        } else {
-            val = *reinterpret_cast<const uint4*>(src + (n_h + n_kv) * dh + kh * dh + i);
-        }
-        __nv_bfloat16* dv = kv.pool + page_base + ((size_t(layer) * 2 + 1) * n_kv + kh) * 256 * dh +
-                            size_t(slot) * dh + i;
-        *reinterpret_cast<uint4*>(dv) = val;
-    }
 }
 
 void rope_kv_append(const __nv_bfloat16* qkv, int T, int n_h, int n_kv, int d_head,
                     const int32_t* row_pos, const int32_t* row_page, const float* rope_cos,
                     const float* rope_sin, const KvLayout& kv, int layer, __nv_bfloat16* q_out,
                     cudaStream_t stream, const Planes& planes) {
-    // one rotary 8-pair group (and one v vector) per thread: all loads of the row in flight
-    const int work = std::max((n_h + n_kv) * (d_head / 16), n_kv * d_head / 8);
+    // one rotary 8-pair group or one v vector per thread: all loads of the row in flight
+    const int work = (n_h + n_kv) * (d_head / 16) + n_kv * d_head / 8;
     const int threads = std::min(512, (work + 31) / 32 * 32);
     if (T > 0)
         launch_pdl(rope_kv_kernel, dim3(T), dim3(threads), 0, stream, qkv, n_h, n_kv, d_head, row_pos,
