@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../host/capi_util.hpp"
@@ -45,6 +46,7 @@ struct MbKv {
     int resident_slot = -1;
     cudaEvent_t last_compute = nullptr;
     bool computed = false;
+    cudaEvent_t evicted = nullptr;  // end of this microbatch's last eviction (its host pages written)
     // previous circuit's sampled rows (first+last stage loopback)
     std::vector<int32_t> prev_logit_slots;
 };
@@ -66,6 +68,9 @@ struct ds_stage {
     int max_rows = 0, max_slots = 0;
     cudaStream_t stream = nullptr, h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_h2d = nullptr, ev_d2h = nullptr;
+    // per-page D2H completion events of one ds_swap_in call: an H2D into a slot page waits only
+    // for the eviction of that page (and of the host page it reads), so both directions overlap
+    std::vector<cudaEvent_t> swap_ev;
 
     bf16* wbuf = nullptr;
     std::vector<LayerW> layers;
@@ -328,8 +333,11 @@ ds_status ds_stage_destroy(ds_stage* s) {
     if (s->host_backing) cudaFreeHost(s->host_backing);
     for (auto& mb : s->mbs)
         if (mb.last_compute) cudaEventDestroy(mb.last_compute);
+    for (auto& mb : s->mbs)
+        if (mb.evicted) cudaEventDestroy(mb.evicted);
     if (s->ev_h2d) cudaEventDestroy(s->ev_h2d);
     if (s->ev_d2h) cudaEventDestroy(s->ev_d2h);
+    for (cudaEvent_t e : s->swap_ev) cudaEventDestroy(e);
     if (s->stream) cudaStreamDestroy(s->stream);
     if (s->h2d) cudaStreamDestroy(s->h2d);
     if (s->d2h) cudaStreamDestroy(s->d2h);
@@ -483,22 +491,51 @@ ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, 
     int64_t in = 0, outb = 0;
     MbKv& k = s->mbs[mb];
     GlobalSlot& gs = s->gslot[slot];
-    // 1. evict the slot occupant (and mb itself if it sits in the other slot)
+    // host pages of mb written by an eviction in an earlier call (this call's: host_done below);
+    // captured before this call re-records the event
+    if (k.evicted) CK(cudaStreamWaitEvent(s->h2d, k.evicted, 0));
+    // 1. evict the slot occupant (and mb itself if it sits in the other slot). Every page copy
+    //    records an event: dev_done[device page] / host_done[host page of mb] -> event index.
+    size_t n_ev = 0;
+    std::unordered_map<int, size_t> dev_done, host_done;
+    auto next_event = [&]() -> cudaEvent_t {
+        if (n_ev == s->swap_ev.size()) {
+            cudaEvent_t e;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+            s->swap_ev.push_back(e);
+        }
+        return s->swap_ev[n_ev++];
+    };
     auto evict = [&](int owner, int g) -> ds_status {
         MbKv& o = s->mbs[owner];
         if (o.computed) CK(cudaStreamWaitEvent(s->d2h, o.last_compute, 0));
+        CK(cudaStreamWaitEvent(s->d2h, s->ev_h2d, 0));  // a prefetch not yet computed on
         for (int h = 0; h < s->host_pages; ++h) {
             if (o.host_dev[h] < 0) continue;
             CK(cudaMemcpyAsync(host_page_ptr(s, owner, h), dev_page_ptr(s, o.host_dev[h]),
                                s->page_bytes, cudaMemcpyDeviceToHost, s->d2h));
+            cudaEvent_t e = next_event();
+            if (!e) return ds_fail(DS_ERR_RUNTIME, "swap event creation failed");
+            CK(cudaEventRecord(e, s->d2h));
+            dev_done[o.host_dev[h]] = n_ev - 1;
+            if (owner == mb) host_done[h] = n_ev - 1;
             o.host_dev[h] = -1;
             outb += s->page_bytes;
         }
+        if (!o.evicted) CK(cudaEventCreateWithFlags(&o.evicted, cudaEventDisableTiming));
+        CK(cudaEventRecord(o.evicted, s->d2h));
         o.resident_slot = -1;
         s->gslot[g].owner = -1;
         s->gslot[g].free.clear();
         for (int p = int(s->gslot[g].dev_pages.size()) - 1; p >= 0; --p)
             s->gslot[g].free.push_back(s->gslot[g].dev_pages[p]);
+        return DS_OK;
+    };
+    auto wait_for = [&](int p, int h) -> ds_status {
+        auto a = dev_done.find(p);
+        if (a != dev_done.end()) CK(cudaStreamWaitEvent(s->h2d, s->swap_ev[a->second], 0));
+        auto b = host_done.find(h);
+        if (b != host_done.end()) CK(cudaStreamWaitEvent(s->h2d, s->swap_ev[b->second], 0));
         return DS_OK;
     };
     ds_status st;
@@ -510,7 +547,8 @@ ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, 
         for (int p = int(gs.dev_pages.size()) - 1; p >= 0; --p) gs.free.push_back(gs.dev_pages[p]);
     }
     CK(cudaEventRecord(s->ev_d2h, s->d2h));
-    CK(cudaStreamWaitEvent(s->h2d, s->ev_d2h, 0));
+    static const bool serial = getenv("DS_SWAP_SERIAL") && atoi(getenv("DS_SWAP_SERIAL"));
+    if (serial) CK(cudaStreamWaitEvent(s->h2d, s->ev_d2h, 0));
     if (k.computed) CK(cudaStreamWaitEvent(s->h2d, k.last_compute, 0));
     // 2. bring mb's host pages in: migrate into free local pages first, then the slot
     for (int sl = 0; sl < s->max_slots; ++sl)
@@ -521,6 +559,7 @@ ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, 
             if (!k.local_free.empty()) {
                 const int p = k.local_free.back();
                 k.local_free.pop_back();
+                if ((st = wait_for(p, h))) return st;
                 CK(cudaMemcpyAsync(dev_page_ptr(s, p), host_page_ptr(s, mb, h), s->page_bytes,
                                    cudaMemcpyHostToDevice, s->h2d));
                 k.host_free.push_back(h);
@@ -529,6 +568,7 @@ ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, 
                 if (gs.free.empty()) return ds_fail(DS_ERR_RUNTIME, "global slot overflow");
                 const int p = gs.free.back();
                 gs.free.pop_back();
+                if ((st = wait_for(p, h))) return st;
                 CK(cudaMemcpyAsync(dev_page_ptr(s, p), host_page_ptr(s, mb, h), s->page_bytes,
                                    cudaMemcpyHostToDevice, s->h2d));
                 k.host_dev[h] = p;
@@ -537,6 +577,9 @@ ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, 
         }
     gs.owner = mb;
     k.resident_slot = slot;
+    // ev_h2d (what the compute waits for) also covers the evictions: the slot pages they read
+    // are handed to this microbatch's appends. Enqueued after the copies, so they still overlap.
+    CK(cudaStreamWaitEvent(s->h2d, s->ev_d2h, 0));
     CK(cudaEventRecord(s->ev_h2d, s->h2d));
     s->moved_in_total += in;
     s->moved_out_total += outb;
