@@ -120,7 +120,8 @@ def ncu_traffic(kind):
 def roofline(kernels):
     """Dominant launch group of the profiled run: algorithmic work / its summed CUDA-event time."""
     hbm, tf_burst, tf_sus, src = load_peaks()
-    kinds = {k: v for k, v in kernels.items() if isinstance(v, dict) and v.get("n")}
+    kinds = {k: v for k, v in kernels.items()
+             if isinstance(v, dict) and v.get("n") and k != "swap_wait"}  # swap_wait: not a kernel
     dom = max(kinds, key=lambda k: kinds[k]["ms"])
     v = kinds[dom]
     sec = v["ms"] / 1e3

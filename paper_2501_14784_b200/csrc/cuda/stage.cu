@@ -143,9 +143,10 @@ uint8_t* host_page_ptr(ds_stage* s, int mb, int h) {
 }
 bf16* dev_page_ptr(ds_stage* s, int p) { return s->kv.pool + size_t(p) * s->kv.page_elems; }
 
-enum ProfKind { PK_QKV, PK_ATTN, PK_O, PK_GU, PK_DOWN, PK_LMHEAD, PK_ELEM, PK_COUNT };
+// PK_SWAPW: time the compute stream waits for the KV swap-in of its microbatch (not a kernel)
+enum ProfKind { PK_QKV, PK_ATTN, PK_O, PK_GU, PK_DOWN, PK_LMHEAD, PK_ELEM, PK_SWAPW, PK_COUNT };
 const char* kPkName[PK_COUNT] = {"gemm_qkv", "attention", "gemm_o", "gemm_gate_up", "gemm_down",
-                                 "gemm_lm_head", "elementwise"};
+                                 "gemm_lm_head", "elementwise", "swap_wait"};
 
 size_t prof_mark(ds_stage* s) {
     if (s->ev_used == s->ev_pool.size()) {
@@ -728,7 +729,11 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     const int32_t* d_flat = d_blk + 3 * T;
 
     // ---- wait for the swap-in this compute depends on
-    if (k.resident_slot >= 0) CK(cudaStreamWaitEvent(s->stream, s->ev_h2d, 0));
+    if (k.resident_slot >= 0) {
+        const size_t w0 = s->prof ? prof_mark(s) : 0;
+        CK(cudaStreamWaitEvent(s->stream, s->ev_h2d, 0));
+        if (s->prof) s->recs.push_back({PK_SWAPW, T, 0.0, 0.0, w0, prof_mark(s)});
+    }
 
     cudaStream_t st = s->stream;
     const int d = m.d_model;

@@ -13,6 +13,7 @@ from paper_2501_14784_b200._native import GpuOpts, check, lib  # noqa: E402
 
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "tiny_2stage.json"
 n_circ = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+profile = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # 1: CUDA events per launch group + swap waits
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 dist.init_process_group("gloo")
 ids = [None]
@@ -40,12 +41,19 @@ check(lib.ds_session_create_rank(txt.encode(), cdir.encode(), b"", -1, -1, C.byr
                                  rank, world, idb, C.byref(h)))
 print(f"rank {rank} session ready", flush=True)
 out = C.create_string_buffer(1 << 24)
-st = lib.ds_session_run(h, 0, 1, out, 1 << 24, None)
+st = lib.ds_session_run(h, profile, 1, out, 1 << 24, None)
 r = json.loads(out.value.decode() or "{}")
 print(f"rank {rank} status {st} err={lib.ds_last_error().decode()[:200]} circuits={r.get('circuits')} "
       f"tokens={r.get('decode_tokens')} wall_us={r.get('wall_us')} "
       f"swap={[(x.get('swap_plan_bytes'), x.get('swap_in_bytes'), x.get('topups')) for x in r.get('stages', [])]}",
       flush=True)
+if profile:
+    for x in r.get("stages", []):
+        kern = x.get("kernels", {})
+        busy = sum(v["ms"] for k, v in kern.items() if isinstance(v, dict) and k != "swap_wait")
+        sw = kern.get("swap_wait", {})
+        print(f"rank {rank} kernels_ms={busy:.1f} swap_wait_ms={sw.get('ms', 0):.2f} "
+              f"swap_waits={sw.get('n', 0)}", flush=True)
 if st != 0:  # exit now: torchrun then stops the peers (a barrier would wait on them forever)
     os._exit(1)
 if rank == world - 1 and r.get("tokens"):
