@@ -156,7 +156,9 @@ ds_status ds_kv_ready(ds_stage* stage, int32_t mb, const ds_row* rows, int64_t n
 
 /* H2D prefetch of mb's global pages into global slot `slot` after evicting the occupant (D2H),
  * on the stage's copy streams (reference issue_swap_in, sim.cpp:328-353). plan_bytes is the
- * reference's integer contract (logged); the copy moves whole pages. moved_in/out may be NULL. */
+ * reference's integer contract (logged); the copy moves whole pages. The refill of a slot page
+ * waits only for that page's eviction, so both directions run at once; the microbatch's next
+ * ds_stage_step waits for both. moved_in/out may be NULL. */
 ds_status ds_swap_in(ds_stage* stage, int32_t mb, int32_t slot, int64_t plan_bytes,
                      int64_t* moved_in, int64_t* moved_out);
 
