@@ -62,8 +62,8 @@ def host_link(nbytes=1 << 30, reps=5):
             "bidir_gbs": 2 * nbytes / tb / 1e9}
 
 
-def swap(n_layers=8, tokens_per_mb=24 * 1024, rounds=6):
-    dims = dict(pl.MODEL_DIMS["llama3-8b"])
+def swap(model="llama3-8b", n_layers=8, tokens_per_mb=24 * 1024, rounds=6):
+    dims = dict(pl.MODEL_DIMS[model])
     md = pl.model_desc(dims)
     st = C.c_void_p()
     max_rows = 4096
@@ -95,7 +95,7 @@ def swap(n_layers=8, tokens_per_mb=24 * 1024, rounds=6):
     nat.lib.ds_stage_destroy(st)
     moved = sum(a + b for a, b, _ in res)
     t = sum(x for _, _, x in res)
-    return {"page_bytes": page, "pages_per_mb": pages, "calls": len(res),
+    return {"model": model, "layers": n_layers, "page_bytes": page, "pages_per_mb": pages, "calls": len(res),
             "in_bytes_per_call": res[0][0], "out_bytes_per_call": res[0][1],
             "ms_per_call": 1e3 * t / len(res), "gbs": moved / t / 1e9}
 
@@ -103,7 +103,8 @@ def swap(n_layers=8, tokens_per_mb=24 * 1024, rounds=6):
 def main():
     torch.cuda.init()
     link = host_link()
-    sw = swap()
+    # argv: model layers (default the 8B 4-stage page; "llama3-70b-bf16 10" = the 70B 8-stage page)
+    sw = swap(sys.argv[1], int(sys.argv[2])) if len(sys.argv) > 2 else swap()
     # eviction and refill overlap page by page: the bound is both directions at once
     bound_s = (sw["out_bytes_per_call"] + sw["in_bytes_per_call"]) / (link["bidir_gbs"] * 1e9)
     sw["bound_ms_per_call"] = 1e3 * bound_s
