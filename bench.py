@@ -301,7 +301,20 @@ def run_reference(args):
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+# timing-experiment switches that skip work (their results are invalid): the bench refuses them
+INVALIDATING_ENV = ("DS_SKIP", "DS_ATTN_SKIP", "DS_GEMM_NOFINISH", "DS_GEMM_TRACE")
+
+
+def ds_env():
+    """Every DS_* override in effect (recorded in the JSON line)."""
+    return {k: v for k, v in sorted(os.environ.items()) if k.startswith("DS_")}
+
+
 def main():
+    bad = [k for k in INVALIDATING_ENV if os.environ.get(k) not in (None, "", "0")]
+    if bad:
+        sys.exit(f"bench.py: {', '.join(bad)} set -- these skip kernels or their finish step and "
+                 "invalidate every number; unset them")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
@@ -322,6 +335,7 @@ def main():
     else:
         out = run_single(args)
     if out is not None:
+        out["ds_env"] = ds_env()
         print(json.dumps(out))
 
 

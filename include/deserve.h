@@ -172,6 +172,17 @@ ds_status ds_stage_step(ds_stage* stage, int32_t mb, const ds_row* rows, int64_t
 ds_status ds_stage_output(ds_stage* stage, void** ptr, int64_t* bytes, int64_t* n_out);
 ds_status ds_stage_sync(ds_stage* stage);
 ds_status ds_stage_stream(ds_stage* stage, void** cuda_stream);
+/* Real-clock trace hooks (the executor's EventTrace, reference trace.hpp:24-42). The events
+ * (cudaEvent_t, created by the caller) are recorded once, by the NEXT call only:
+ * ds_stage_step: ready = the step reached the stream (before its swap-in wait), start = after
+ * that wait (ComputeStart), end = after its last kernel (ComputeEnd);
+ * ds_swap_in: in0/in1 bracket the H2D refill, out0/out1 the D2H eviction (Swap{In,Out}Done).
+ * Any event may be NULL. */
+ds_status ds_stage_step_events(ds_stage* stage, void* ready, void* start, void* end);
+ds_status ds_swap_events(ds_stage* stage, void* in0, void* in1, void* out0, void* out1);
+/* Device pointer to the fp32 logits [rows x vocab] of the last step (valid until the next step;
+ * stream-ordered on ds_stage_stream). */
+ds_status ds_stage_logits_device(ds_stage* stage, const float** ptr, int64_t* rows);
 /* Teacher forcing / debugging: read the fp32 logits of the last step (R x vocab) to host. */
 ds_status ds_stage_logits(ds_stage* stage, float* host_out, int64_t max_floats, int64_t* n_floats);
 
@@ -185,6 +196,9 @@ typedef struct ds_gpu_opts {
     int32_t collect_tokens; /* 1: report the sampled ids of every circuit */
     int64_t max_circuits;   /* execute the first circuits of the schedule (0 = all) */
     uint64_t weight_seed;
+    int32_t trace;          /* 1: keep the schedule's events; ds_session_trace rebuilds them on
+                               the real clock after every run */
+    int32_t reserved;
 } ds_gpu_opts;
 
 /* Plans the config (as ds_plan_config), schedules it in virtual time, then executes the schedule on
@@ -205,6 +219,42 @@ ds_status ds_session_create(const char* config_json, const char* config_dir, con
 ds_status ds_session_run(ds_session* session, int32_t profile, int32_t collect_tokens,
                          char* report_json, size_t cap, size_t* needed);
 ds_status ds_session_destroy(ds_session* session);
+
+/* Reference SimResult{report, trace} of a hardware run (include/pipesim/sim.hpp:47-51): the
+ * events of the last ds_session_run on the real clock, in write_trace format
+ * (src/trace.cpp:40-46), integer fields identical to the virtual-clock schedule's (replay mode;
+ * GPU event times mapped to the host steady clock, hop arrivals from the host), so reference
+ * replay_check (sim.cpp:606-697) and windowed_stats (workload.cpp:82-116) accept it unchanged.
+ * Needs opts.trace = 1. trace_path may be NULL. t0_us: steady-clock origin in us (< 0: this
+ * run's start; ranks of one pipeline pass a common origin). keep_virtual_seq = 1 writes the
+ * schedule's seq numbers (for ds_trace_merge of per-rank traces), else seq = line index.
+ * report_json: SimReport fields (build_report, sim.cpp:501-532) over [w0_us, w1_us) of this
+ * process's events (w0 < 0: workload warmup; w1 < 0: min(bench duration, run end)), plus
+ * "replay": the executed circuits/events. */
+ds_status ds_session_trace(ds_session* session, const char* trace_path, int64_t t0_us,
+                           int32_t keep_virtual_seq, int64_t w0_us, int64_t w1_us, char* report_json,
+                           size_t cap, size_t* needed);
+/* Merges per-rank traces (each sorted, virtual seq kept) into one trace in (time, seq) order with
+ * seq renumbered as the line index. */
+ds_status ds_trace_merge(const char* const* paths, int32_t n_paths, const char* out_path);
+/* SimReport fields of a trace file over [w0_us, w1_us) (windowed_stats token counts; busy /
+ * swap-stall / bubble per stage as the engine accumulates them). */
+ds_status ds_trace_report(const char* trace_path, int64_t n_stages, int64_t w0_us, int64_t w1_us,
+                          uint64_t seed, char* report_json, size_t cap);
+/* The drop-in execution seam: the reference's run(plan, topo, workload, model)
+ * (src/sim.cpp:591-595) with real stage forwards. Plans the config (ds_plan_config), schedules it,
+ * executes it on GPUs, writes the real-clock trace to trace_path (may be NULL) and returns
+ * {"report": SimReport over the workload window clipped to the run, "gpu": the executor report}. */
+ds_status ds_run(const char* config_json, const char* config_dir, const char* policy,
+                 int64_t latency_us, int64_t nb_override, const ds_model_desc* model,
+                 const ds_gpu_opts* opts, const char* trace_path, char* report_json, size_t cap,
+                 size_t* needed);
+/* Teacher-forced parity (tests): every run copies the fp32 logits of the rows sampled for these
+ * requests to host memory; ds_session_captured returns them in execution order with meta
+ * [circuit, req_id, position, row within the circuit's sampled rows] per row. */
+ds_status ds_session_capture(ds_session* session, const int64_t* req_ids, int64_t n);
+ds_status ds_session_captured(ds_session* session, int64_t* meta4, float* logits, int64_t max_rows,
+                              int64_t* n_rows);
 
 /* One process per GPU: this process runs pipeline stage `rank` of `world` (= stages) on device0;
  * activations (and sampled ids, last -> first) hop over NCCL send/recv, one 2-rank communicator per

@@ -198,6 +198,66 @@ def replay_circuits(schedule: dict, plan: dict, dims: dict, seed: int, gpu_token
     return out
 
 
+class LrRow(C.Structure):
+    """Row descriptor of llama_ref.h (same layout as the product's ds_row; defined here so the
+    checkers never import the product package)."""
+    _fields_ = [("slot", C.c_int32), ("pos", C.c_int32), ("n_tok", C.c_int32),
+                ("need_logits", C.c_int32), ("is_decode", C.c_int32), ("reserved", C.c_int32),
+                ("req_id", C.c_int64)]
+
+
+def replay_requests(schedule: dict, dims: dict, seed: int, reqs, gpu_tokens):
+    """Whole-model oracle (all layers, embedding and LM head in one CPU stage) over the rows of
+    the selected requests only, in the schedule's circuit order: requests are independent (a row
+    attends only to its own request's KV), so the logits of their sampled rows equal those of the
+    full circuits. Decode inputs are teacher-forced with the GPU's sampled ids (gpu_tokens: per
+    circuit, the ids of its need_logits rows in row order). Returns (meta [n, 3] = circuit,
+    req_id, position; logits [n, vocab]) in execution order (the order ds_session_captured uses)."""
+    import numpy as np
+    lr = LlamaRef()
+    m = LrModel(**dims)
+    sel = {q: i for i, q in enumerate(sorted(reqs))}
+    st = lr.lib.lr_stage_create(C.byref(m), 0, dims["n_layers"], 1, 1, seed, len(sel))
+    last, meta, out = {}, [], []
+    try:
+        for ci, c in enumerate(schedule["circuits"]):
+            rows, toks, k = [], [], 0
+            for r in c["rows"]:
+                if r[5] in sel:
+                    rows.append(r)
+                    for j in range(r[2]):
+                        pos = r[1] + j
+                        toks.append((128000 if pos == 0 else last[r[5]]) if r[4]
+                                    else lr.lib.lr_prompt_token(r[5], pos))
+            for r in c["rows"]:  # teacher forcing: the GPU's sample of each selected row
+                if r[3]:
+                    if r[5] in sel:
+                        last[r[5]] = int(gpu_tokens[ci][k])
+                    k += 1
+            if not rows:
+                continue
+            arr = (LrRow * len(rows))(*[LrRow(sel[r[5]], r[1], r[2], r[3], r[4], 0, r[5])
+                                        for r in rows])
+            T = sum(r[2] for r in rows)
+            R = sum(r[3] for r in rows)
+            tok = np.array(toks, dtype=np.int32)
+            act = np.zeros((T, dims["d_model"]), dtype=np.float32)
+            lg = np.zeros((max(R, 1), dims["vocab"]), dtype=np.float32)
+            ids = np.zeros(max(R, 1), dtype=np.int32)
+            if lr.lib.lr_stage_step(st, 0, len(sel), arr, len(rows), tok.ctypes.data, None,
+                                    act.ctypes.data, lg.ctypes.data, ids.ctypes.data) != 0:
+                raise RefError("oracle stage step failed")
+            i = 0
+            for r in rows:
+                if r[3]:
+                    meta.append((ci, r[5], r[1] + r[2] - 1))
+                    out.append(lg[i].copy())
+                    i += 1
+    finally:
+        lr.lib.lr_stage_destroy(st)
+    return np.array(meta, dtype=np.int64).reshape(-1, 3), np.array(out, dtype=np.float32)
+
+
 def greedy_mismatches(oracle_logits, gpu_tokens, margin):
     """(checked, mismatched): rows whose oracle top-2 margin exceeds `margin` must agree."""
     import numpy as np

@@ -66,8 +66,23 @@ typedef struct {
 
 typedef struct {
     int64_t req_id;
-    float* kv; /* [L][2][n_kv][max_seq][dh] */
+    int cap;   /* positions held per (layer, K|V, kv head); grows on demand */
+    float* kv; /* [L][2][n_kv][cap][dh] */
 } handle_kv;
+
+/* make room for positions [0, need) keeping the cached ones */
+static void kv_reserve(handle_kv* hk, int L, int nkv, int dh, int need) {
+    if (need <= hk->cap) return;
+    int cap = hk->cap ? hk->cap : 256;
+    while (cap < need) cap *= 2;
+    float* nk = (float*)malloc(sizeof(float) * (size_t)L * 2 * nkv * cap * dh);
+    if (hk->kv)
+        for (size_t blk = 0; blk < (size_t)L * 2 * nkv; ++blk)
+            memcpy(nk + blk * cap * dh, hk->kv + blk * hk->cap * dh, sizeof(float) * (size_t)hk->cap * dh);
+    free(hk->kv);
+    hk->kv = nk;
+    hk->cap = cap;
+}
 
 struct lr_stage {
     lr_model m;
@@ -142,23 +157,65 @@ void lr_stage_destroy(lr_stage* s) {
     free(s);
 }
 
-/* y[t][n] = sum_k x[t][k] * w[n][k], fp32, 16 partial sums then a fixed-order reduction */
+/* y[t][n] = sum_k x[t][k] * w[n][k], fp32: per (t, n) 16 partial sums (lane j takes k = j mod 16)
+ * then a fixed-order reduction. Rows are processed 4 at a time against one converted weight row
+ * (the per-(t, n) summation order is unchanged, so results do not depend on the blocking). */
+static float dot1(const float* x, int K, const float* wf) {
+    float acc[16] = {0};
+    int k = 0;
+    for (; k + 16 <= K; k += 16)
+        for (int j = 0; j < 16; ++j) acc[j] += x[k + j] * wf[k + j];
+    float sum = 0.f;
+    for (int j = 0; j < 16; ++j) sum += acc[j];
+    for (; k < K; ++k) sum += x[k] * wf[k];
+    return sum;
+}
+
+static void dot4(const float* x, int K, const float* wf, float* out) {
+    const float *x0 = x, *x1 = x + K, *x2 = x + 2 * (size_t)K, *x3 = x + 3 * (size_t)K;
+    float a0[16] = {0}, a1[16] = {0}, a2[16] = {0}, a3[16] = {0};
+    int k = 0;
+    for (; k + 16 <= K; k += 16)
+        for (int j = 0; j < 16; ++j) {
+            const float wv = wf[k + j];
+            a0[j] += x0[k + j] * wv;
+            a1[j] += x1[k + j] * wv;
+            a2[j] += x2[k + j] * wv;
+            a3[j] += x3[k + j] * wv;
+        }
+    float* acc[4] = {a0, a1, a2, a3};
+    const float* xs[4] = {x0, x1, x2, x3};
+    for (int r = 0; r < 4; ++r) {
+        float sum = 0.f;
+        for (int j = 0; j < 16; ++j) sum += acc[r][j];
+        for (int kk = k; kk < K; ++kk) sum += xs[r][kk] * wf[kk];
+        out[r] = sum;
+    }
+}
+
 static void matmul(const float* x, int T, int K, const uint16_t* w, int N, float* y) {
-#pragma omp parallel for schedule(static)
-    for (int n = 0; n < N; ++n) {
-        const uint16_t* wr = w + (size_t)n * K;
-        float* wf = (float*)malloc(sizeof(float) * K);
-        for (int k = 0; k < K; ++k) wf[k] = from_bits(wr[k]);
-        for (int t = 0; t < T; ++t) {
-            const float* xr = x + (size_t)t * K;
-            float acc[16] = {0};
-            int k = 0;
-            for (; k + 16 <= K; k += 16)
-                for (int j = 0; j < 16; ++j) acc[j] += xr[k + j] * wf[k + j];
-            float sum = 0.f;
-            for (int j = 0; j < 16; ++j) sum += acc[j];
-            for (; k < K; ++k) sum += xr[k] * wf[k];
-            y[(size_t)t * N + n] = sum;
+    enum { NBLK = 8 }; /* weight rows converted at once: x blocks are reused across them */
+    const int nblocks = (N + NBLK - 1) / NBLK;
+#pragma omp parallel
+    {
+        float* wf = (float*)malloc(sizeof(float) * (size_t)K * NBLK);
+#pragma omp for schedule(static)
+        for (int b = 0; b < nblocks; ++b) {
+            const int n0 = b * NBLK, nn = N - n0 < NBLK ? N - n0 : NBLK;
+            for (int i = 0; i < nn; ++i) {
+                const uint16_t* wr = w + (size_t)(n0 + i) * K;
+                for (int k = 0; k < K; ++k) wf[(size_t)i * K + k] = from_bits(wr[k]);
+            }
+            int t = 0;
+            for (; t + 4 <= T; t += 4)
+                for (int i = 0; i < nn; ++i) {
+                    float o[4];
+                    dot4(x + (size_t)t * K, K, wf + (size_t)i * K, o);
+                    for (int r = 0; r < 4; ++r) y[(size_t)(t + r) * N + n0 + i] = o[r];
+                }
+            for (; t < T; ++t)
+                for (int i = 0; i < nn; ++i)
+                    y[(size_t)t * N + n0 + i] = dot1(x + (size_t)t * K, K, wf + (size_t)i * K);
         }
         free(wf);
     }
@@ -177,7 +234,6 @@ int lr_stage_step(lr_stage* s, int32_t mb, int32_t max_slots, const lr_row* rows
     const lr_model* m = &s->m;
     const int d = m->d_model, nh = m->n_heads, nkv = m->n_kv_heads, dh = m->d_head;
     const int qd = nh * dh, kvd = nkv * dh, G = nh / nkv, half = dh / 2;
-    const size_t S = (size_t)m->max_seq_len;
     int T = 0, R = 0;
     for (int i = 0; i < n_rows; ++i) {
         T += rows[i].n_tok;
@@ -192,10 +248,8 @@ int lr_stage_step(lr_stage* s, int32_t mb, int32_t max_slots, const lr_row* rows
             const int hidx = mb * max_slots + rows[i].slot;
             if (hidx >= s->max_handles) return -1;
             handle_kv* hk = &s->h[hidx];
-            if (hk->req_id != rows[i].req_id) {
-                if (!hk->kv) hk->kv = (float*)malloc(sizeof(float) * (size_t)s->L * 2 * kvd * S);
-                hk->req_id = rows[i].req_id;
-            }
+            if (hk->req_id != rows[i].req_id) hk->req_id = rows[i].req_id;
+            kv_reserve(hk, s->L, nkv, dh, rows[i].pos + rows[i].n_tok);
             for (int j = 0; j < rows[i].n_tok; ++j, ++t) {
                 row_h[t] = hidx;
                 row_pos[t] = rows[i].pos + j;
@@ -242,6 +296,7 @@ int lr_stage_step(lr_stage* s, int32_t mb, int32_t max_slots, const lr_row* rows
                     v[i + half] = bf(o2);
                 }
             }
+            const size_t S = (size_t)s->h[row_h[t]].cap;
             float* kvb = s->h[row_h[t]].kv + (size_t)li * 2 * kvd * S;
             for (int kh = 0; kh < nkv; ++kh)
                 for (int i = 0; i < dh; ++i) {
@@ -254,6 +309,7 @@ int lr_stage_step(lr_stage* s, int32_t mb, int32_t max_slots, const lr_row* rows
         for (int t = 0; t < T; ++t)
             for (int hh = 0; hh < nh; ++hh) {
                 const int p = row_pos[t], kh = hh / G;
+                const size_t S = (size_t)s->h[row_h[t]].cap;
                 const float* kvb = s->h[row_h[t]].kv + (size_t)li * 2 * kvd * S;
                 const float* qv = q + (size_t)t * qd + hh * dh;
                 float* sc = (float*)malloc(sizeof(float) * (p + 1));

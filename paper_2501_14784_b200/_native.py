@@ -59,7 +59,7 @@ class Row(C.Structure):
 class GpuOpts(C.Structure):
     _fields_ = [("device0", C.c_int32), ("n_devices", C.c_int32), ("real_delay", C.c_int32),
                 ("collect_tokens", C.c_int32), ("max_circuits", C.c_int64),
-                ("weight_seed", C.c_uint64)]
+                ("weight_seed", C.c_uint64), ("trace", C.c_int32), ("reserved", C.c_int32)]
 
 
 def _load() -> C.CDLL:
@@ -104,6 +104,15 @@ def _load() -> C.CDLL:
         "ds_stage_kernel_stats": (I32, [P, P, C.c_size_t, P]),
         "ds_schedule_config": (I32, [S, S, S, I64, I64, I64, P, C.c_size_t, P]),
         "ds_gpu_run_config": (I32, [S, S, S, I64, I64, P, P, P, C.c_size_t, P]),
+        "ds_stage_step_events": (I32, [P, P, P, P]),
+        "ds_swap_events": (I32, [P, P, P, P, P]),
+        "ds_stage_logits_device": (I32, [P, P, P]),
+        "ds_session_trace": (I32, [P, S, I64, I32, I64, I64, P, C.c_size_t, P]),
+        "ds_trace_merge": (I32, [P, I32, S]),
+        "ds_trace_report": (I32, [S, I64, I64, I64, C.c_uint64, P, C.c_size_t]),
+        "ds_run": (I32, [S, S, S, I64, I64, P, P, S, P, C.c_size_t, P]),
+        "ds_session_capture": (I32, [P, P, I64]),
+        "ds_session_captured": (I32, [P, P, P, I64, P]),
         "ds_dbg_gemm": (I32, [P, P, I32, I32, I32, I32, P, I32, P]),
         "ds_dbg_has_device": (I32, [P]),
         "ds_dbg_gemm_bench": (I32, [I32, I32, I32, I32, I32, I32, P]),

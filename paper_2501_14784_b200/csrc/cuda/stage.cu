@@ -121,6 +121,11 @@ struct ds_stage {
     int64_t launches = 0;
     int64_t h2d_bytes = 0;
 
+    // one-shot timing events for the next ds_stage_step (ready, start, end) and the next
+    // ds_swap_in (in0, in1, out0, out1): the executor's real-clock trace (ds_stage_step_events)
+    cudaEvent_t step_ev[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t swap_tev[4] = {nullptr, nullptr, nullptr, nullptr};
+
     // last step
     int last_T = 0, last_R = 0;
     int64_t moved_in_total = 0, moved_out_total = 0;
@@ -414,6 +419,7 @@ ds_status ds_kv_reset(ds_stage* s) {
     }
     CK(cudaMemset(s->last_token, 0, size_t(s->n_mb) * s->max_slots * 4));
     s->moved_in_total = s->moved_out_total = 0;
+    s->h2d_bytes = 0;  // per run (the bench divides by the run's circuits)
     return DS_OK;
 }
 
@@ -479,7 +485,10 @@ ds_status ds_kv_ready(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_row
         need += std::max<int64_t>(0, page_count_for(r.pos + r.n_tok) - have);
     }
     int64_t avail = int64_t(k.local_free.size());
-    if (k.resident_slot >= 0) avail += int64_t(s->gslot[k.resident_slot].free.size());
+    // a slot page also needs a host backing page (ds_stage_step takes both)
+    if (k.resident_slot >= 0)
+        avail += std::min<int64_t>(int64_t(s->gslot[k.resident_slot].free.size()),
+                                   int64_t(k.host_free.size()));
     *ready = (res && need <= avail) ? 1 : 0;
     return DS_OK;
 }
@@ -497,6 +506,9 @@ ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, 
     if (k.evicted) CK(cudaStreamWaitEvent(s->h2d, k.evicted, 0));
     // 1. evict the slot occupant (and mb itself if it sits in the other slot). Every page copy
     //    records an event: dev_done[device page] / host_done[host page of mb] -> event index.
+    cudaEvent_t tev[4] = {s->swap_tev[0], s->swap_tev[1], s->swap_tev[2], s->swap_tev[3]};
+    for (auto& e : s->swap_tev) e = nullptr;
+    bool out0 = false;
     size_t n_ev = 0;
     std::unordered_map<int, size_t> dev_done, host_done;
     auto next_event = [&]() -> cudaEvent_t {
@@ -509,8 +521,19 @@ ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, 
     };
     auto evict = [&](int owner, int g) -> ds_status {
         MbKv& o = s->mbs[owner];
-        if (o.computed) CK(cudaStreamWaitEvent(s->d2h, o.last_compute, 0));
+        if (o.computed) {
+            CK(cudaStreamWaitEvent(s->d2h, o.last_compute, 0));
+            // the refill may land in slot pages the occupant freed (ds_kv_release / a slot
+            // changing request) after its last step, which no eviction copy orders: the h2d
+            // stream waits for that step too (the evictions wait on it already, so both
+            // directions still overlap)
+            CK(cudaStreamWaitEvent(s->h2d, o.last_compute, 0));
+        }
         CK(cudaStreamWaitEvent(s->d2h, s->ev_h2d, 0));  // a prefetch not yet computed on
+        if (tev[2] && !out0) {  // out0: the eviction starts once the occupant's step is done
+            CK(cudaEventRecord(tev[2], s->d2h));
+            out0 = true;
+        }
         for (int h = 0; h < s->host_pages; ++h) {
             if (o.host_dev[h] < 0) continue;
             CK(cudaMemcpyAsync(host_page_ptr(s, owner, h), dev_page_ptr(s, o.host_dev[h]),
@@ -548,9 +571,12 @@ ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, 
         for (int p = int(gs.dev_pages.size()) - 1; p >= 0; --p) gs.free.push_back(gs.dev_pages[p]);
     }
     CK(cudaEventRecord(s->ev_d2h, s->d2h));
+    if (tev[2] && !out0) CK(cudaEventRecord(tev[2], s->d2h));  // nothing evicted
+    if (tev[3]) CK(cudaEventRecord(tev[3], s->d2h));  // out1: eviction end
     static const bool serial = getenv("DS_SWAP_SERIAL") && atoi(getenv("DS_SWAP_SERIAL"));
     if (serial) CK(cudaStreamWaitEvent(s->h2d, s->ev_d2h, 0));
     if (k.computed) CK(cudaStreamWaitEvent(s->h2d, k.last_compute, 0));
+    if (tev[0]) CK(cudaEventRecord(tev[0], s->h2d));  // in0: refill start
     // 2. bring mb's host pages in: migrate into free local pages first, then the slot
     for (int sl = 0; sl < s->max_slots; ++sl)
         for (int32_t& hnd : k.pages[sl]) {
@@ -576,6 +602,7 @@ ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, 
             }
             in += s->page_bytes;
         }
+    if (tev[1]) CK(cudaEventRecord(tev[1], s->h2d));  // in1: refill end
     gs.owner = mb;
     k.resident_slot = slot;
     // ev_h2d (what the compute waits for) also covers the evictions: the slot pages they read
@@ -728,7 +755,10 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     const int32_t* d_blk = d_prev + prevR;
     const int32_t* d_flat = d_blk + 3 * T;
 
-    // ---- wait for the swap-in this compute depends on
+    // ---- wait for the swap-in this compute depends on (ready -> start = swap stall)
+    cudaEvent_t sev[3] = {s->step_ev[0], s->step_ev[1], s->step_ev[2]};
+    for (auto& e : s->step_ev) e = nullptr;
+    if (sev[0]) CK(cudaEventRecord(sev[0], s->stream));
     if (k.resident_slot >= 0) {
         const size_t w0 = s->prof ? prof_mark(s) : 0;
         CK(cudaStreamWaitEvent(s->stream, s->ev_h2d, 0));
@@ -736,6 +766,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     }
 
     cudaStream_t st = s->stream;
+    if (sev[1]) CK(cudaEventRecord(sev[1], st));
     const int d = m.d_model;
     if (s->first) {
         const int32_t* ids_in = static_cast<const int32_t*>(act_in);
@@ -875,6 +906,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
         k.prev_logit_slots.assign(logit_slot, logit_slot + R);
     }
     CK(cudaEventRecord(k.last_compute, st));
+    if (sev[2]) CK(cudaEventRecord(sev[2], st));
     k.computed = true;
     s->last_T = T;
     s->last_R = R;
@@ -936,6 +968,30 @@ ds_status ds_stage_output(ds_stage* s, void** ptr, int64_t* bytes, int64_t* n_ou
         if (bytes) *bytes = int64_t(s->last_T) * s->m.d_model * 2;
         if (n_out) *n_out = s->last_T;
     }
+    return DS_OK;
+}
+
+ds_status ds_stage_step_events(ds_stage* s, void* ready, void* start, void* end) {
+    if (!s) return ds_fail(DS_ERR_ARG, "null stage");
+    s->step_ev[0] = static_cast<cudaEvent_t>(ready);
+    s->step_ev[1] = static_cast<cudaEvent_t>(start);
+    s->step_ev[2] = static_cast<cudaEvent_t>(end);
+    return DS_OK;
+}
+
+ds_status ds_swap_events(ds_stage* s, void* in0, void* in1, void* out0, void* out1) {
+    if (!s) return ds_fail(DS_ERR_ARG, "null stage");
+    s->swap_tev[0] = static_cast<cudaEvent_t>(in0);
+    s->swap_tev[1] = static_cast<cudaEvent_t>(in1);
+    s->swap_tev[2] = static_cast<cudaEvent_t>(out0);
+    s->swap_tev[3] = static_cast<cudaEvent_t>(out1);
+    return DS_OK;
+}
+
+ds_status ds_stage_logits_device(ds_stage* s, const float** ptr, int64_t* rows) {
+    if (!s || !s->last || !ptr) return ds_fail(DS_ERR_ARG, "not a last stage");
+    *ptr = s->logits;
+    if (rows) *rows = s->last_R;
     return DS_OK;
 }
 

@@ -2,8 +2,10 @@
 // virtual-clock scheduler. Exceptions never cross the boundary; they become ds_status codes
 // with a thread-local message (ConfigError -> DS_ERR_ARG, PlanError -> DS_ERR_PLAN,
 // SimError/other -> DS_ERR_RUNTIME; reference exit-code mapping cli.cpp:219-231).
+#include <algorithm>
 #include <cstring>
 #include <fstream>
+#include <sstream>
 #include <string>
 
 #include "capi_util.hpp"
@@ -193,7 +195,9 @@ ds_status ds_schedule_config(const char* config_json, const char* config_dir, co
             const auto& ci = sc.circuits[c];
             js += (c ? ",{" : "{") + std::string("\"mb\":") + std::to_string(ci.mb) +
                   ",\"eff_batch\":" + std::to_string(ci.eff_batch) + ",\"n_decode\":" +
-                  std::to_string(ci.n_decode) + ",\"t_end\":" + std::to_string(ci.t_end) + ",\"rows\":[";
+                  std::to_string(ci.n_decode) + ",\"t_end\":" + std::to_string(ci.t_end) +
+                  ",\"trig\":" + std::to_string(ci.trig) + ",\"trig_payload\":" +
+                  std::to_string(ci.trig_payload) + ",\"rows\":[";
             for (size_t k = 0; k < ci.rows.size(); ++k) {
                 const auto& r = ci.rows[k];
                 js += (k ? ",[" : "[") + std::to_string(r.slot) + "," + std::to_string(r.pos) + "," +
@@ -213,7 +217,8 @@ ds_status ds_schedule_config(const char* config_json, const char* config_dir, co
                 if (op.kind == dsb::OpKind::Compute && op.circuit >= n) break;
                 js += (first ? "[" : ",[") + std::to_string(int(op.kind)) + "," + std::to_string(op.mb) +
                       "," + std::to_string(op.slot) + "," + std::to_string(op.circuit) + "," +
-                      std::to_string(op.plan_bytes) + "," + std::to_string(op.t) + "]";
+                      std::to_string(op.plan_bytes) + "," + std::to_string(op.t) + "," +
+                      std::to_string(op.evict_bytes) + "]";
                 first = false;
             }
             js += "]";
@@ -235,7 +240,7 @@ ds_status ds_session_create(const char* config_json, const char* config_dir, con
         if (!model || !opts || !out) return ds_fail(DS_ERR_ARG, "null argument");
         auto cp = dsb::plan_from_config(config_json, config_dir, policy, latency_us, nb_override);
         dsb::SimOutput o = dsb::simulate(cp.second, cp.first.topo, cp.first.workload, cp.first.model,
-                                         false, true);
+                                         opts->trace != 0, true);
         dsb::GpuOptions g;
         g.device0 = opts->device0;
         g.n_devices = opts->n_devices;
@@ -243,9 +248,11 @@ ds_status ds_session_create(const char* config_json, const char* config_dir, con
         g.collect_tokens = opts->collect_tokens != 0;
         g.max_circuits = opts->max_circuits;
         g.weight_seed = opts->weight_seed;
+        g.trace = opts->trace != 0;
         ds_session* h = new ds_session();
         try {
-            h->s = dsb::session_create(cp.first, cp.second, std::move(o.schedule), *model, g);
+            h->s = dsb::session_create(cp.first, cp.second, std::move(o.schedule), *model, g, -1, 1,
+                                       nullptr, std::move(o.trace));
         } catch (...) {
             delete h;
             throw;
@@ -276,7 +283,7 @@ ds_status ds_session_create_rank(const char* config_json, const char* config_dir
         if (world > 1 && !nccl_ids) return ds_fail(DS_ERR_ARG, "nccl ids required for world > 1");
         auto cp = dsb::plan_from_config(config_json, config_dir, policy, latency_us, nb_override);
         dsb::SimOutput o = dsb::simulate(cp.second, cp.first.topo, cp.first.workload, cp.first.model,
-                                         false, true);
+                                         opts->trace != 0, true);
         dsb::GpuOptions g;
         g.device0 = opts->device0;
         g.n_devices = 1;
@@ -284,10 +291,11 @@ ds_status ds_session_create_rank(const char* config_json, const char* config_dir
         g.collect_tokens = opts->collect_tokens != 0;
         g.max_circuits = opts->max_circuits;
         g.weight_seed = opts->weight_seed;
+        g.trace = opts->trace != 0;
         ds_session* h = new ds_session();
         try {
             h->s = dsb::session_create(cp.first, cp.second, std::move(o.schedule), *model, g, rank, world,
-                                       nccl_ids);
+                                       nccl_ids, std::move(o.trace));
         } catch (...) {
             delete h;
             throw;
@@ -308,6 +316,134 @@ ds_status ds_session_run(ds_session* h, int32_t profile, int32_t collect_tokens,
     });
 }
 
+namespace {
+std::string read_file(const char* path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw dsb::ConfigError(std::string("cannot read ") + path);
+    std::ostringstream os;
+    os << f.rdbuf();
+    return os.str();
+}
+
+void write_file(const char* path, const std::string& text) {
+    std::ofstream f(path, std::ios::binary);
+    if (!f) throw dsb::SimError(std::string("cannot write trace file ") + path);
+    f.write(text.data(), std::streamsize(text.size()));
+}
+
+// report window of a hardware run: the workload's [warmup, duration) clipped to the run
+std::pair<int64_t, int64_t> run_window(dsb::Session* s, int64_t w0, int64_t w1) {
+    const dsb::Workload& wl = dsb::session_config(s).workload;
+    if (w0 < 0) w0 = wl.warmup_s * 1'000'000;
+    if (w1 < 0) w1 = std::min<int64_t>(wl.duration_s * 1'000'000, dsb::session_end(s) + 1);
+    return {w0, w1};
+}
+
+std::string trace_report_json(dsb::Session* s, const std::vector<dsb::Record>& tr, int64_t w0, int64_t w1) {
+    const auto win = run_window(s, w0, w1);
+    const dsb::Plan& p = dsb::session_plan(s);
+    dsb::Report r = dsb::report_from_trace(tr, p.S(), win.first, win.second, dsb::session_config(s).workload.seed);
+    int64_t computes = 0;
+    for (const auto& e : tr) computes += e.kind == dsb::Ev::ComputeStart;
+    std::string js = r.to_json();
+    js.pop_back();
+    js += ",\"trace_events\":" + std::to_string(tr.size()) + ",\"trace_computes\":" + std::to_string(computes) +
+          ",\"run_end_us\":" + std::to_string(dsb::session_end(s)) + "}";
+    return js;
+}
+}  // namespace
+
+ds_status ds_session_trace(ds_session* h, const char* trace_path, int64_t t0_us, int32_t keep_virtual_seq,
+                           int64_t w0_us, int64_t w1_us, char* report_json, size_t cap, size_t* needed) {
+    return guarded([&] {
+        if (!h || !h->s) return ds_fail(DS_ERR_ARG, "null session");
+        const std::vector<dsb::Record> tr = dsb::session_trace(h->s, t0_us, keep_virtual_seq == 0);
+        if (trace_path && *trace_path) write_file(trace_path, dsb::trace_text(tr));
+        copy_out(trace_report_json(h->s, tr, w0_us, w1_us), report_json, cap, needed);
+        return DS_OK;
+    });
+}
+
+ds_status ds_trace_merge(const char* const* paths, int32_t n, const char* out_path) {
+    return guarded([&] {
+        if (!paths || n < 1 || !out_path) return ds_fail(DS_ERR_ARG, "bad merge arguments");
+        std::vector<dsb::Record> all;
+        for (int32_t i = 0; i < n; ++i) {
+            auto t = dsb::parse_trace(read_file(paths[i]));
+            all.insert(all.end(), t.begin(), t.end());
+        }
+        std::stable_sort(all.begin(), all.end(), [](const dsb::Record& a, const dsb::Record& b) {
+            return a.t != b.t ? a.t < b.t : a.seq < b.seq;
+        });
+        for (size_t i = 0; i < all.size(); ++i) all[i].seq = int64_t(i);
+        write_file(out_path, dsb::trace_text(all));
+        return DS_OK;
+    });
+}
+
+ds_status ds_trace_report(const char* trace_path, int64_t n_stages, int64_t w0_us, int64_t w1_us,
+                          uint64_t seed, char* report_json, size_t cap) {
+    return guarded([&] {
+        if (!trace_path || n_stages < 1) return ds_fail(DS_ERR_ARG, "bad trace report arguments");
+        const auto tr = dsb::parse_trace(read_file(trace_path));
+        copy_out(dsb::report_from_trace(tr, n_stages, w0_us, w1_us, seed).to_json(), report_json, cap, nullptr);
+        return DS_OK;
+    });
+}
+
+ds_status ds_session_capture(ds_session* h, const int64_t* reqs, int64_t n) {
+    return guarded([&] {
+        if (!h || !h->s || (n > 0 && !reqs)) return ds_fail(DS_ERR_ARG, "bad capture arguments");
+        dsb::session_capture(h->s, std::vector<int64_t>(reqs, reqs + n));
+        return DS_OK;
+    });
+}
+
+ds_status ds_session_captured(ds_session* h, int64_t* meta4, float* logits, int64_t max_rows, int64_t* n_rows) {
+    return guarded([&] {
+        if (!h || !h->s) return ds_fail(DS_ERR_ARG, "null session");
+        std::vector<int64_t> meta;
+        const float* lg = nullptr;
+        int64_t n = 0;
+        dsb::session_captured(h->s, &meta, &lg, &n);
+        if (n_rows) *n_rows = n;
+        const int64_t k = std::min(n, max_rows);
+        if (meta4 && k > 0) std::memcpy(meta4, meta.data(), size_t(k) * 4 * sizeof(int64_t));
+        if (logits && k > 0) {
+            const int64_t vocab = dsb::session_vocab(h->s);
+            std::memcpy(logits, lg, size_t(k) * size_t(vocab) * 4);
+        }
+        return DS_OK;
+    });
+}
+
+ds_status ds_run(const char* config_json, const char* config_dir, const char* policy, int64_t latency_us,
+                 int64_t nb_override, const ds_model_desc* model, const ds_gpu_opts* opts,
+                 const char* trace_path, char* report_json, size_t cap, size_t* needed) {
+    return guarded([&] {
+        if (!model || !opts) return ds_fail(DS_ERR_ARG, "null model/opts");
+        ds_gpu_opts o = *opts;
+        o.trace = 1;
+        ds_session* h = nullptr;
+        ds_status st = ds_session_create(config_json, config_dir, policy, latency_us, nb_override, model, &o, &h);
+        if (st) return st;
+        std::string js;
+        try {
+            dsb::GpuRunResult r = dsb::session_run(h->s, false, opts->collect_tokens != 0);
+            if (!r.error.empty()) throw dsb::SimError(r.error);
+            const auto tr = dsb::session_trace(h->s, -1, true);
+            if (trace_path && *trace_path) write_file(trace_path, dsb::trace_text(tr));
+            js = "{\"report\":" + trace_report_json(h->s, tr, -1, -1) + ",\"gpu\":" + r.to_json() + "}";
+        } catch (...) {
+            ds_session_destroy(h);
+            throw;
+        }
+        ds_session_destroy(h);
+        copy_out(js, report_json, cap, needed);
+        return DS_OK;
+    });
+}
+
 ds_status ds_session_destroy(ds_session* h) {
     return guarded([&] {
         if (h) dsb::session_destroy(h->s);
@@ -323,7 +459,7 @@ ds_status ds_gpu_run_config(const char* config_json, const char* config_dir, con
         if (!model || !opts) return ds_fail(DS_ERR_ARG, "null model/opts");
         auto cp = dsb::plan_from_config(config_json, config_dir, policy, latency_us, nb_override);
         dsb::SimOutput o = dsb::simulate(cp.second, cp.first.topo, cp.first.workload, cp.first.model,
-                                         false, true);
+                                         opts->trace != 0, true);
         dsb::GpuOptions g;
         g.device0 = opts->device0;
         g.n_devices = opts->n_devices;

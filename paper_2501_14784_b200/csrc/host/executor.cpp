@@ -62,26 +62,50 @@ struct Mailbox {
     cudaEvent_t ev = nullptr;
 };
 
+// stage 0 of a multi-stage pipeline: host time at which each circuit's output reached it (the
+// last stage's completion in-process, the landing of its ids hop over NCCL); the arrival of a
+// microbatch at stage 0 is timed from its trigger circuit (Circuit::trig)
+struct CircuitDone {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<int64_t> t;  // -1 until done
+};
+
 struct PostCtx {
-    Mailbox* box;
+    Mailbox* box;  // may be null
     int64_t circuit;
+    CircuitDone* done = nullptr;
 };
 
 void CUDART_CB post_cb(void* p) {
     PostCtx* c = static_cast<PostCtx*>(p);
-    {
-        std::lock_guard<std::mutex> lk(c->box->mu);
-        c->box->posted = std::max(c->box->posted, c->circuit);
-        c->box->t_done = now_us();
+    const int64_t now = now_us();
+    if (c->box) {
+        {
+            std::lock_guard<std::mutex> lk(c->box->mu);
+            c->box->posted = std::max(c->box->posted, c->circuit);
+            c->box->t_done = now;
+        }
+        c->box->cv.notify_all();
     }
-    c->box->cv.notify_all();
+    if (c->done) {
+        {
+            std::lock_guard<std::mutex> lk(c->done->mu);
+            c->done->t[c->circuit] = now;
+        }
+        c->done->cv.notify_all();
+    }
     if (g_trace) fprintf(stderr, "[ds] posted circuit %lld\n", (long long)c->circuit);
     delete c;
 }
 
 struct StepTiming {
-    cudaEvent_t a = nullptr, b = nullptr;
+    cudaEvent_t r = nullptr, a = nullptr, b = nullptr;  // ready, start (after swap wait), end
     int64_t rows = 0;
+};
+
+struct SwapTiming {
+    cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};  // in0, in1, out0, out1
 };
 
 struct Worker {
@@ -94,9 +118,16 @@ struct Worker {
     std::vector<StepTiming> timing;            // event pool, reused across runs
     size_t timing_used = 0;
     cudaEvent_t t_begin = nullptr, t_end = nullptr;
+    int64_t h_begin = 0;  // host steady-clock us at which t_begin fired (GPU -> host clock)
     int64_t served = 0, topups = 0;
     int64_t moved_in = 0, moved_out = 0, plan_in = 0;
     int64_t computes = 0;
+    // per executed compute: host us of the microbatch's arrival and of its send (-1: derived
+    // from the trigger's GPU end, single stage); per executed schedule swap-in: its events
+    std::vector<int64_t> arr_us, send_us;
+    std::vector<SwapTiming> swap_t;
+    std::vector<SwapPair> swap_pairs;
+    size_t swaps_done = 0;
     std::string error;
     // per mb: the last circuit whose step (reading recv[mb]) is enqueued, and an event after it.
     // A producer may overwrite recv[mb] with the mb's next input only after that step: a circuit
@@ -151,6 +182,15 @@ struct Session {
     std::vector<int32_t> recv_slot;        // per circuit
     std::vector<cudaEvent_t> ev_consumed;  // per slot
     std::vector<int64_t> consumed_n;       // per slot: consumptions enqueued (under land_mu)
+    // real-clock trace
+    std::vector<Record> vtrace;  // the virtual-clock trace of the schedule (opt.trace)
+    CircuitDone done;
+    int64_t t0 = 0, t_end = 0;   // host steady-clock us of the last run's start / end
+    // logit capture
+    std::vector<int64_t> cap_reqs;  // sorted
+    std::vector<int64_t> cap_meta;  // 4 per row: circuit, req, position, row index
+    float* cap_pool = nullptr;
+    int64_t cap_rows = 0, cap_used = 0;
 };
 
 namespace {
@@ -169,8 +209,10 @@ void CUDART_CB land_cb(void* p) {
 }  // namespace
 
 Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, const ds_model_desc& md,
-                        const GpuOptions& opt, int rank, int world, const void* nccl_ids) {
+                        const GpuOptions& opt, int rank, int world, const void* nccl_ids,
+                        std::vector<Record> vtrace) {
     std::unique_ptr<Session> S(new Session());
+    S->vtrace = std::move(vtrace);
     if (rank >= 0) {
         if (world != plan.S())
             throw ConfigError("world size " + std::to_string(world) + " != pipeline stages " +
@@ -343,6 +385,7 @@ Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, con
                         cudaGetLastError();
                     }
                 }
+    S->done.t.assign(S->n_circ, -1);
     S->tok_off.assign(S->n_circ + 1, 0);
     for (int64_t c = 0; c < S->n_circ; ++c) {
         int64_t r = 0;
@@ -367,6 +410,7 @@ void session_destroy(Session* S) {
         S->recv_ring.clear();
         S->ev_consumed.clear();
         for (auto& t : w.timing) {
+            cudaEventDestroy(t.r);
             cudaEventDestroy(t.a);
             cudaEventDestroy(t.b);
         }
@@ -384,6 +428,10 @@ void session_destroy(Session* S) {
         if (S->api) S->links.destroy(*S->api);
     }
     if (S->tok_pool) cudaFreeHost(S->tok_pool);
+    if (S->cap_pool) cudaFreeHost(S->cap_pool);
+    for (auto& w : S->W)
+        for (auto& t : w.swap_t)
+            for (auto e : t.e) cudaEventDestroy(e);
     delete S;
 }
 
@@ -403,35 +451,61 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
         std::fill(S->consumed_n.begin(), S->consumed_n.end(), 0);
         std::fill(S->recv_slot.begin(), S->recv_slot.end(), -1);
         w.timing_used = 0;
+        w.arr_us.clear();
+        w.send_us.clear();
+        w.swap_pairs.clear();
+        w.swaps_done = 0;
         w.error.clear();
     }
+    std::fill(S->done.t.begin(), S->done.t.end(), int64_t(-1));
+    S->cap_used = 0;
     int64_t launches0 = 0;
     for (auto& w : S->W) {
         int64_t l = 0;
         DK(ds_stage_kernel_stats(w.st, nullptr, 0, &l));
         launches0 += l;
     }
-    // bytes of the hop that lands at stage `to` for circuit c (activations, or ids at stage 0)
+    // bytes of the hop that lands at stage `to` for circuit c (activations, or ids at stage 0;
+    // the ids hop always carries >= 1 int32 so stage 0 learns every circuit's end)
     auto hop_bytes = [&](int64_t to, int64_t c) -> size_t {
         if (to == 0) {
             int64_t r = 0;
             for (const auto& row : circs[c].rows) r += row.need_logits;
-            return size_t(r) * 4;
+            return size_t(std::max<int64_t>(r, 1)) * 4;
         }
         return size_t(circs[c].eff_batch) * S->md.d_model * 2;
     };
-    auto hop_delay = [&](int64_t from, int64_t eff) -> int64_t {
+    // injected delay of a hop carrying `payload` bytes over ring link `from` (send_onward /
+    // wake_parked, sim.cpp:289,436)
+    auto hop_delay = [&](int64_t from, int64_t payload) -> int64_t {
         if (!opt.real_delay || NS < 2) return 0;
         const Link& l = plan.ring[from];
-        return l.latency + div_up(eff * plan.policy.hidden_bytes_per_token * 1'000'000, l.bw);
+        return l.latency + div_up(payload * 1'000'000, l.bw);
     };
     for (auto& w : S->W) {
         XK(cudaSetDevice(w.device));
         XK(cudaDeviceSynchronize());
         XK(cudaEventRecord(w.t_begin, w.stream));
+        XK(cudaEventSynchronize(w.t_begin));
+        w.h_begin = now_us();
     }
     std::atomic<bool> failed{false};
     const int64_t t0 = now_us();
+    S->t0 = t0;
+    // capture buffer: every sampled row of the captured requests in the executed prefix
+    if (!S->cap_reqs.empty()) {
+        int64_t n = 0;
+        for (int64_t c = 0; c < S->n_circ; ++c)
+            for (const auto& r : circs[c].rows)
+                if (r.need_logits && std::binary_search(S->cap_reqs.begin(), S->cap_reqs.end(), r.req)) ++n;
+        if (n > S->cap_rows) {
+            if (S->cap_pool) cudaFreeHost(S->cap_pool);
+            S->cap_pool = nullptr;
+            XK(cudaMallocHost(&S->cap_pool, size_t(n) * S->md.vocab * 4));
+            S->cap_rows = n;
+        }
+        S->cap_meta.clear();
+    }
 
     auto body = [&](Worker& w) {
         try {
@@ -447,11 +521,19 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     continue;
                 }
                 if (op.kind == OpKind::SwapIn) {
+                    if (w.swaps_done == w.swap_t.size()) {
+                        SwapTiming t;
+                        for (auto& e : t.e) XK(cudaEventCreate(&e));
+                        w.swap_t.push_back(t);
+                    }
+                    SwapTiming& t = w.swap_t[w.swaps_done++];
+                    DK(ds_swap_events(w.st, t.e[0], t.e[1], t.e[2], t.e[3]));
                     int64_t mi = 0, mo = 0;
                     DK(ds_swap_in(w.st, op.mb, op.slot, op.plan_bytes, &mi, &mo));
                     w.moved_in += mi;
                     w.moved_out += mo;
                     w.plan_in += op.plan_bytes;
+                    w.swap_pairs.push_back({op.plan_bytes, mi, mo});
                     continue;
                 }
                 const int64_t c = op.circuit;
@@ -467,11 +549,32 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     for (const auto& r : circ.rows) any_decode |= (r.is_decode && r.pos > 0);
                     has_input = any_decode;
                 }
-                // single stage: the input is this stream's own previous step (ids loop back on the
-                // device, no link, no injected delay: reference sim.cpp:434-437), so stream order
-                // is the dependency and the host runs ahead instead of draining the GPU per circuit
-                const bool wait_input = has_input && !(NS == 1 && !S->nccl);
-                if (wait_input) {
+                int64_t arr = -1, sent = -1;  // trace: arrival / send time (host us)
+                if (s == 0 && NS > 1) {
+                    // the microbatch arrives from the last stage: send_onward of its previous
+                    // circuit, or wake_parked by another microbatch's circuit end (Circuit::trig)
+                    if (circ.trig >= 0) {
+                        if (has_input && circ.trig != need)
+                            throw SimError("circuit " + std::to_string(c) + " has decode rows but was woken");
+                        {
+                            std::unique_lock<std::mutex> lk(S->done.mu);
+                            S->done.cv.wait(lk, [&] { return S->done.t[circ.trig] >= 0 || failed.load(); });
+                            sent = S->done.t[circ.trig];
+                        }
+                        if (failed) return;
+                        const int64_t arrive = sent + hop_delay(NS - 1, circ.trig_payload);
+                        const int64_t wait = arrive - now_us();
+                        if (wait > 0) std::this_thread::sleep_for(std::chrono::microseconds(wait));
+                        arr = std::max(arrive, now_us());
+                        if (has_input)
+                            XK(cudaStreamWaitEvent(w.stream, S->nccl ? S->ev_recv[need] : w.in[mb]->ev, 0));
+                    } else {
+                        arr = sent = t0;  // placed at t = 0
+                    }
+                } else if (s > 0) {
+                    // single stage: the input is this stream's own previous step (ids loop back
+                    // on the device, no link, no injected delay: reference sim.cpp:434-437), so
+                    // stream order is the dependency and the host runs ahead of the GPU
                     Mailbox& mbx = *w.in[mb];
                     int64_t t_done;
                     {
@@ -482,11 +585,16 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     }
                     if (failed) return;
                     const int64_t from = (s + NS - 1) % NS;
-                    const int64_t arrive = t_done + hop_delay(from, circs[need].eff_batch);
+                    const int64_t arrive =
+                        t_done + hop_delay(from, circs[need].eff_batch * plan.policy.hidden_bytes_per_token);
                     const int64_t wait = arrive - now_us();
                     if (wait > 0) std::this_thread::sleep_for(std::chrono::microseconds(wait));
+                    arr = std::max(arrive, now_us());
+                    sent = t_done;
                     XK(cudaStreamWaitEvent(w.stream, S->nccl ? S->ev_recv[need] : mbx.ev, 0));
                 }
+                w.arr_us.push_back(arr);
+                w.send_us.push_back(sent);
                 // ---- residency top-up: the plan's prefetch may be stale, or the
                 // step's growth may exceed the whole local pages before the plan's byte figure
                 // shows a global portion
@@ -497,6 +605,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 DK(ds_kv_ready(w.st, mb, rows.data(), int64_t(rows.size()), &resident));
                 if (!resident) {
                     int64_t mi = 0, mo = 0;
+                    DK(ds_swap_events(w.st, nullptr, nullptr, nullptr, nullptr));
                     DK(ds_swap_in(w.st, mb, int32_t(w.served % 2), 0, &mi, &mo));
                     w.moved_in += mi;
                     w.moved_out += mo;
@@ -507,13 +616,14 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 if (opt.step_timing) {
                     if (w.timing_used == w.timing.size()) {
                         StepTiming n;
+                        XK(cudaEventCreate(&n.r));
                         XK(cudaEventCreate(&n.a));
                         XK(cudaEventCreate(&n.b));
                         w.timing.push_back(n);
                     }
                     tm = &w.timing[w.timing_used++];
                     tm->rows = circ.eff_batch;
-                    XK(cudaEventRecord(tm->a, w.stream));
+                    DK(ds_stage_step_events(w.st, tm->r, tm->a, tm->b));
                 }
                 int32_t ring_slot = -1;
                 if (S->ring_mode && s > 0) ring_slot = S->recv_slot[c];
@@ -536,8 +646,25 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 }
                 w.cs->cv.notify_all();
                 if (g_trace) fprintf(stderr, "[ds r%lld] step c=%lld mb=%d rows=%lld need=%lld\n", (long long)s, (long long)c, mb, (long long)circ.eff_batch, (long long)need);
-                if (tm) XK(cudaEventRecord(tm->b, w.stream));
                 w.computes++;
+                // logits of captured requests (teacher-forced parity, tests)
+                if (last && !S->cap_reqs.empty()) {
+                    const float* lg = nullptr;
+                    int64_t lr = 0, k = 0;
+                    DK(ds_stage_logits_device(w.st, &lg, &lr));
+                    for (const auto& r : circ.rows) {
+                        if (!r.need_logits) continue;
+                        if (std::binary_search(S->cap_reqs.begin(), S->cap_reqs.end(), r.req)) {
+                            if (S->cap_used >= S->cap_rows) throw SimError("logit capture overflow");
+                            const size_t V = size_t(S->md.vocab);
+                            XK(cudaMemcpyAsync(S->cap_pool + size_t(S->cap_used) * V, lg + size_t(k) * V,
+                                               V * 4, cudaMemcpyDeviceToHost, w.stream));
+                            S->cap_meta.insert(S->cap_meta.end(), {c, r.req, int64_t(r.pos + r.n_tok - 1), k});
+                            S->cap_used++;
+                        }
+                        ++k;
+                    }
+                }
                 // ---- hop to the next stage (or ids back to stage 0)
                 void* src = nullptr;
                 int64_t bytes = 0, n_out = 0;
@@ -547,7 +674,9 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     XK(cudaMemcpyAsync(S->tok_pool + S->tok_off[c], src, size_t(n_out) * 4,
                                        cudaMemcpyDeviceToHost, w.stream));
                 if (S->nccl) {
-                    // stage the output per microbatch, then ncclSend on the send stream
+                    // stage the output per microbatch, then ncclSend on the send stream (the ids
+                    // hop carries at least one int32: stage 0 times every circuit end)
+                    if (last && bytes == 0) bytes = 4;
                     if (bytes > 0) {
                         const int k = int(S->send_seq++ % S->send_ring);
                         XK(cudaStreamWaitEvent(w.stream, S->ev_sent[k], 0));  // slot's last send done
@@ -583,7 +712,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 if (NS == 1) continue;  // nobody waits on the self loop (stream order)
                 Mailbox& out = *next->in[mb];
                 XK(cudaEventRecord(out.ev, w.stream));
-                XK(cudaLaunchHostFunc(w.stream, post_cb, new PostCtx{&out, c}));
+                XK(cudaLaunchHostFunc(w.stream, post_cb, new PostCtx{&out, c, last ? &S->done : nullptr}));
             }
             XK(cudaEventRecord(w.t_end, w.stream));
             XK(cudaStreamSynchronize(w.stream));
@@ -645,7 +774,8 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 if (nr != ncclSuccess) throw SimError(std::string("ncclRecv: ") + S->api->GetErrorString(nr));
                 XK(cudaEventRecord(S->ev_recv[c], S->s_recv));
                 XK(cudaLaunchHostFunc(S->s_recv, land_cb, new LandCtx{S}));
-                XK(cudaLaunchHostFunc(S->s_recv, post_cb, new PostCtx{w.in[mb].get(), c}));
+                XK(cudaLaunchHostFunc(S->s_recv, post_cb,
+                                      new PostCtx{w.in[mb].get(), c, w.idx == 0 ? &S->done : nullptr}));
                 if (g_trace) fprintf(stderr, "[ds r%lld] recv posted c=%lld mb=%d bytes=%zu\n", (long long)w.idx, (long long)c, mb, bytes);
             }
             XK(cudaStreamSynchronize(S->s_recv));
@@ -705,6 +835,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
         ds_stage_sync(w.st);
     }
     const int64_t t1 = now_us();
+    S->t_end = t1;
 
     GpuRunResult res;
     for (auto& w : S->W)
@@ -730,7 +861,9 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
             st.device_ms = dev_ms;
         res.device_us = std::max<int64_t>(res.device_us, int64_t(double(st.device_ms) * 1000.0));
         for (size_t i = 0; i < w.timing_used; ++i) {
-            float ms = 0;
+            float ms = 0, wait = 0;
+            if (res.error.empty() && cudaEventElapsedTime(&wait, w.timing[i].r, w.timing[i].a) == cudaSuccess)
+                res.swap_wait_us += int64_t(double(wait) * 1000.0);
             if (cudaEventElapsedTime(&ms, w.timing[i].a, w.timing[i].b) == cudaSuccess) {
                 st.busy_ms += ms;
                 st.steps.push_back({w.timing[i].rows, double(ms)});
@@ -749,6 +882,12 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
         st.kernel_stats = buf.data();
         launches1 += l;
         res.stages.push_back(std::move(st));
+        res.swaps.push_back(w.swap_pairs);
+    }
+    // host -> device bytes of the run: every step's row metadata (kernel_stats "h2d_bytes")
+    for (const auto& st : res.stages) {
+        const auto p = st.kernel_stats.find("\"h2d_bytes\":");
+        if (p != std::string::npos) res.h2d_bytes += std::atoll(st.kernel_stats.c_str() + p + 12);
     }
     res.launches = launches1 - launches0;
     if (collect_tokens && S->tok_pool) {
@@ -774,12 +913,169 @@ GpuRunResult run_on_gpus(const Config& cfg, const Plan& plan, const Schedule& sc
     return r;
 }
 
+int64_t session_t0(Session* S) { return S->t0; }
+int64_t session_end(Session* S) { return S->t_end - S->t0; }
+const Config& session_config(Session* S) { return S->cfg; }
+const Plan& session_plan(Session* S) { return S->plan; }
+int64_t session_vocab(Session* S) { return S->md.vocab; }
+
+void session_capture(Session* S, const std::vector<int64_t>& reqs) {
+    S->cap_reqs = reqs;
+    std::sort(S->cap_reqs.begin(), S->cap_reqs.end());
+}
+
+void session_captured(Session* S, std::vector<int64_t>* meta, const float** logits, int64_t* n) {
+    *meta = S->cap_meta;
+    *logits = S->cap_pool;
+    *n = S->cap_used;
+}
+
+std::vector<Record> session_trace(Session* S, int64_t t0_us, bool renumber) {
+    if (!S->opt.trace) throw ConfigError("session created without trace recording");
+    const int64_t NS = S->plan.S(), NB = S->plan.n_mb;
+    const int64_t t0 = t0_us >= 0 ? t0_us : S->t0;
+    const auto& circs = S->sched.circuits;
+    std::vector<Worker*> wk(NS, nullptr);
+    for (auto& w : S->W) wk[w.idx] = &w;
+    auto gpu_us = [&](Worker& w, cudaEvent_t e) -> int64_t {
+        float ms = 0;
+        XK(cudaSetDevice(w.device));
+        XK(cudaEventElapsedTime(&ms, w.t_begin, e));
+        return w.h_begin + int64_t(double(ms) * 1000.0) - t0;
+    };
+    // per stage: compute index of each (mb, j-th compute of that mb); swap-op index of each
+    // swap with in / out bytes; circuit -> compute index at the last stage
+    std::vector<std::vector<std::vector<int64_t>>> comp_of(NS, std::vector<std::vector<int64_t>>(NB));
+    std::vector<std::vector<int64_t>> sw_in(NS), sw_out(NS), circ_of(NS);
+    std::vector<int64_t> last_comp(circs.size(), -1);
+    for (int64_t s = 0; s < NS; ++s) {
+        int64_t k = 0, j = 0;
+        for (const StageOp& op : S->sched.ops[s]) {
+            if (op.kind == OpKind::Compute) {
+                comp_of[s][op.mb].push_back(k);
+                circ_of[s].push_back(op.circuit);
+                if (s == NS - 1 && op.circuit >= 0) last_comp[op.circuit] = k;
+                ++k;
+            } else if (op.kind == OpKind::SwapIn) {
+                if (op.plan_bytes > 0) sw_in[s].push_back(j);
+                if (op.evict_bytes > 0) sw_out[s].push_back(j);
+                ++j;
+            }
+        }
+    }
+    // real times of this process's executed computes
+    std::vector<std::vector<int64_t>> t_start(NS), t_end(NS);
+    for (int64_t s = 0; s < NS; ++s) {
+        Worker* w = wk[s];
+        if (!w) continue;
+        const size_t n = std::min<size_t>(size_t(w->computes), w->timing_used);
+        for (size_t k = 0; k < n; ++k) {
+            t_start[s].push_back(gpu_us(*w, w->timing[k].a));
+            t_end[s].push_back(gpu_us(*w, w->timing[k].b));
+        }
+    }
+    auto executed = [&](int64_t s, int64_t k) { return wk[s] && k >= 0 && k < int64_t(t_start[s].size()); };
+    std::vector<int64_t> cs(NS, 0), ce(NS, 0), si(NS, 0), so(NS, 0);
+    std::vector<std::vector<int64_t>> arr_j(NS, std::vector<int64_t>(NB, 0));
+    bool have_last = wk[NS - 1] != nullptr, seen_end = false, end_ok = false;
+    int64_t end_t = 0;
+    std::vector<std::pair<int64_t, Record>> out;  // (virtual seq, event on the real clock)
+    for (const Record& e : S->vtrace) {
+        Record r = e;
+        bool keep = false;
+        const int64_t s = e.stage;
+        switch (e.kind) {
+            case Ev::ComputeStart: {
+                const int64_t k = cs[s]++;
+                if ((keep = executed(s, k))) r.t = t_start[s][k];
+                break;
+            }
+            case Ev::ComputeEnd: {
+                const int64_t k = ce[s]++;
+                keep = executed(s, k);
+                if (keep) r.t = t_end[s][k];
+                if (s == NS - 1) {
+                    seen_end = true;
+                    end_ok = keep;
+                    end_t = r.t;
+                }
+                break;
+            }
+            case Ev::TransferArrive: {
+                const int64_t j = arr_j[s][e.mb]++;
+                if (j >= int64_t(comp_of[s][e.mb].size())) break;
+                const int64_t k = comp_of[s][e.mb][j];
+                if (!executed(s, k)) break;
+                keep = true;
+                Worker* w = wk[s];
+                if (e.t == 0 && e.a == 0) {
+                    r.t = 0;  // initial placement
+                } else if (NS == 1) {  // self loop: arrives when its trigger circuit ends
+                    const int64_t c = circ_of[s][k];
+                    const int64_t trig = c >= 0 ? circs[c].trig : -1;
+                    const int64_t tk = trig >= 0 ? last_comp[trig] : -1;
+                    if (!executed(0, tk)) { keep = false; break; }
+                    r.t = r.a = t_end[0][tk];
+                } else {
+                    r.t = w->arr_us[k] - t0;
+                    r.a = w->send_us[k] - t0;
+                }
+                break;
+            }
+            case Ev::SwapInDone:
+            case Ev::SwapOutDone: {
+                const bool in = e.kind == Ev::SwapInDone;
+                const int64_t j = in ? si[s]++ : so[s]++;
+                const auto& idx = in ? sw_in[s] : sw_out[s];
+                if (j >= int64_t(idx.size()) || !wk[s] || idx[j] >= int64_t(wk[s]->swaps_done)) break;
+                const SwapTiming& t = wk[s]->swap_t[idx[j]];
+                keep = true;
+                r.a = gpu_us(*wk[s], in ? t.e[0] : t.e[2]);
+                r.t = gpu_us(*wk[s], in ? t.e[1] : t.e[3]);
+                break;
+            }
+            case Ev::RequestAdmit:
+            case Ev::RequestComplete:
+                // logged at a last-stage circuit end (or at t=0 before any): that end's time
+                if (!have_last) break;
+                if (!seen_end) {
+                    keep = true;
+                    r.t = 0;
+                } else if (end_ok) {
+                    keep = true;
+                    r.t = end_t;
+                }
+                break;
+        }
+        if (keep) out.push_back({e.seq, r});
+    }
+    std::stable_sort(out.begin(), out.end(), [](const auto& x, const auto& y) {
+        return x.second.t != y.second.t ? x.second.t < y.second.t : x.first < y.first;
+    });
+    std::vector<Record> tr;
+    tr.reserve(out.size());
+    for (size_t i = 0; i < out.size(); ++i) {
+        tr.push_back(out[i].second);
+        tr.back().seq = renumber ? int64_t(i) : out[i].first;
+    }
+    return tr;
+}
+
 std::string GpuRunResult::to_json() const {
     std::ostringstream os;
     os.precision(10);
     os << "{\"circuits\":" << circuits << ",\"decode_tokens\":" << decode_tokens << ",\"rows\":" << rows
        << ",\"wall_us\":" << wall_us << ",\"device_us\":" << device_us << ",\"launches\":" << launches
-       << ",\"d2h_bytes\":" << d2h_bytes << ",\"tokens_per_s\":"
+       << ",\"d2h_bytes\":" << d2h_bytes << ",\"h2d_bytes\":" << h2d_bytes
+       << ",\"swap_wait_us\":" << swap_wait_us << ",\"swap_pairs\":[";
+    for (size_t i = 0; i < swaps.size(); ++i) {
+        os << (i ? ",[" : "[");
+        for (size_t k = 0; k < swaps[i].size(); ++k)
+            os << (k ? ",[" : "[") << swaps[i][k].plan << "," << swaps[i][k].moved_in << ","
+               << swaps[i][k].moved_out << "]";
+        os << "]";
+    }
+    os << "],\"tokens_per_s\":"
        << (wall_us > 0 ? double(decode_tokens) * 1e6 / double(wall_us) : 0.0) << ",\"error\":\"";
     for (char ch : error) os << (ch == '"' || ch == '\\' ? ' ' : ch);
     os << "\",\"stages\":[";

@@ -18,6 +18,7 @@ struct GpuOptions {
     uint64_t weight_seed = 0x5EED0001ULL;
     bool collect_tokens = false;  // D2H the sampled ids of every circuit
     bool step_timing = true;      // CUDA events around every stage step
+    bool trace = false;           // keep the virtual trace: session_trace() rebuilds it on the real clock
 };
 
 struct StageRunStats {
@@ -31,9 +32,15 @@ struct StageRunStats {
     std::string kernel_stats;                       // ds_stage_kernel_stats JSON
 };
 
+struct SwapPair {
+    int64_t plan = 0, moved_in = 0, moved_out = 0;
+};
+
 struct GpuRunResult {
     int64_t circuits = 0, decode_tokens = 0, rows = 0, wall_us = 0, device_us = 0;
-    int64_t launches = 0, d2h_bytes = 0;
+    int64_t launches = 0, d2h_bytes = 0, h2d_bytes = 0;
+    int64_t swap_wait_us = 0;  // measured: GPU time computes waited for their swap-ins
+    std::vector<std::vector<SwapPair>> swaps;  // per stage: every schedule swap-in, plan vs moved
     std::vector<StageRunStats> stages;
     std::vector<std::vector<int32_t>> tokens;  // per circuit: sampled ids of its need_logits rows
     std::string error;
@@ -45,9 +52,25 @@ struct Session;
 // rank >= 0: only stage `rank` on device0, hops over NCCL (nccl_ids: world ncclUniqueIds).
 Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, const ds_model_desc& md,
                         const GpuOptions& opt, int rank = -1, int world = 1,
-                        const void* nccl_ids = nullptr);
+                        const void* nccl_ids = nullptr, std::vector<Record> vtrace = {});
 GpuRunResult session_run(Session* s, bool profile, bool collect_tokens);
 void session_destroy(Session* s);
+
+// The last run's events on the real clock (reference EventTrace, trace.hpp:24-42): the virtual
+// trace's events with the times the hardware produced them (GPU events mapped to the host
+// steady clock, hop arrivals from the host), in (time, virtual seq) order. Only events of the
+// stages this process runs and of the executed schedule prefix. t0_us: the steady-clock origin
+// (< 0: this run's start). renumber = false keeps the virtual seq (for merging rank traces).
+std::vector<Record> session_trace(Session* s, int64_t t0_us, bool renumber);
+int64_t session_t0(Session* s);  // steady-clock us of the last run's start
+int64_t session_end(Session* s);  // us from t0 to the last run's end
+const Config& session_config(Session* s);
+const Plan& session_plan(Session* s);
+int64_t session_vocab(Session* s);
+// rows sampled for these requests are copied (fp32 logits) into a host pool at every run
+void session_capture(Session* s, const std::vector<int64_t>& reqs);
+// (circuit, req, position, row) of every captured row and the logits [n x vocab]
+void session_captured(Session* s, std::vector<int64_t>* meta, const float** logits, int64_t* n);
 
 GpuRunResult run_on_gpus(const Config& cfg, const Plan& plan, const Schedule& sched,
                          const ds_model_desc& md, const GpuOptions& opt);

@@ -173,6 +173,15 @@ struct Record {
     int64_t a = 0, b = 0, c = 0;
 };
 std::string trace_text(const std::vector<Record>& tr);
+// reference read_trace (src/trace.cpp:54-88); throws ConfigError on a malformed line
+std::vector<Record> parse_trace(const std::string& text);
+// SimReport fields (reference build_report, src/sim.cpp:501-532) recomputed from a trace over
+// [w0, w1): tokens as windowed_stats (src/workload.cpp:82-116), busy = compute intervals,
+// stall = the part of a swap-dependent compute's wait (stage free and microbatch arrived) that
+// its SwapInDone covers, as the engine's stall_acc (src/sim.cpp:355-382).
+struct Report;
+Report report_from_trace(const std::vector<Record>& tr, int64_t n_stages, Micros w0, Micros w1,
+                         uint64_t seed);
 
 struct StageStats {
     Micros busy = 0, stall = 0, bubble = 0;
@@ -205,6 +214,11 @@ struct Circuit {
     std::vector<RowSpec> rows;
     std::vector<int32_t> completed_slots;  // slots whose requests finished at this circuit's end
     Micros t_end = -1;                     // virtual time of the circuit end (last stage)
+    // the circuit whose last-stage end sent this microbatch to stage 0 (its own previous circuit
+    // via send_onward, or another microbatch's via wake_parked; -1 = placed at t=0) and the
+    // payload of that hop (reference sim.cpp:277-294,430-439)
+    int64_t trig = -1;
+    Bytes trig_payload = 0;
 };
 enum class OpKind : uint8_t { Compute, SwapIn, Release };
 struct StageOp {
@@ -214,6 +228,7 @@ struct StageOp {
     int64_t circuit;     // Compute: circuit index
     int64_t plan_bytes;  // SwapIn: reference global_portion bytes
     Micros t;            // virtual issue time
+    int64_t evict_bytes = 0;  // SwapIn: bytes of the slot occupant's eviction (SwapOutDone b)
 };
 struct Schedule {
     std::vector<Circuit> circuits;

@@ -150,6 +150,8 @@ struct Mb {
     int64_t eff = 0, n_decode = 0, live = 0;
     std::vector<std::pair<int64_t, Tokens>> prefill;  // (request, tokens) this circuit
     int64_t circuit = -1;
+    int64_t trig = -1;  // circuit whose end sent this mb to stage 0 (Circuit::trig)
+    Bytes trig_payload = 0;
 };
 
 struct StageRt {
@@ -362,7 +364,7 @@ private:
         }
     }
 
-    void wake(Micros now) {
+    void wake(Micros now, int64_t by_circuit) {
         while (!parked_.empty() && !admit_.empty()) {
             const int32_t m = parked_.front();
             fill(m, now);
@@ -370,6 +372,8 @@ private:
             parked_.pop_front();
             mb_[m].parked = false;
             const Bytes payload = mb_[m].live * plan_.policy.hidden_bytes_per_token;
+            mb_[m].trig = by_circuit;
+            mb_[m].trig_payload = payload;
             Micros hop = 0;
             if (S_ > 1) {
                 const Link& l = plan_.ring.back();
@@ -422,6 +426,7 @@ private:
         st.occupant[slot] = in_b;
         st.res_bytes[target] = in_b;
         op(s, OpKind::SwapIn, target, slot, -1, in_b, now);
+        if (keep_sched_) sched_.ops[s].back().evict_bytes = out_b;
         if (in_b == 0) {
             st.res[target] = Residency::Resident;
             return;
@@ -462,6 +467,8 @@ private:
         Tokens left = plan_.policy.prefill_chunk;
         Circuit c;
         c.mb = m;
+        c.trig = mb.trig;
+        c.trig_payload = mb.trig_payload;
         for (size_t si = 0; si < mb.slot.size(); ++si) {
             const int64_t rid = mb.slot[si];
             if (rid == -1) continue;
@@ -511,6 +518,10 @@ private:
     void hop(int32_t m, int64_t from, Micros now) {
         const int64_t next = (from + 1) % S_;
         const Bytes payload = mb_[m].eff * plan_.policy.hidden_bytes_per_token;
+        if (next == 0) {
+            mb_[m].trig = mb_[m].circuit;
+            mb_[m].trig_payload = payload;
+        }
         Micros at = now;
         if (S_ > 1) {
             const Link& l = plan_.ring[from];
@@ -550,7 +561,7 @@ private:
                 }
             }
             fill(e.mb, e.t);
-            wake(e.t);
+            wake(e.t, mb.circuit);
             if (mb.live > 0) {
                 hop(e.mb, e.stage, e.t);
             } else {

@@ -140,18 +140,51 @@ def gpu_run_config(config_text: str, config_dir: str = "", policy=None, latency_
     return json.loads(buf.value.decode())
 
 
+def run(config_text: str, config_dir: str = "", policy=None, latency_us=-1, nb_override=-1,
+        model=None, device0=0, n_devices=0, real_delay=True, collect_tokens=False,
+        max_circuits=0, weight_seed=WEIGHT_SEED, trace_path: str | None = None) -> dict:
+    """The reference's run() with real stage forwards (ds_run): returns
+    {"report": SimReport fields of the hardware run, "gpu": executor report}; the real-clock
+    EventTrace goes to trace_path."""
+    from ._native import GpuOpts
+    if model is None:
+        model = json.loads(config_text)["model"]["name"]
+    md = model_desc(model)
+    opts = GpuOpts(device0=device0, n_devices=n_devices, real_delay=int(real_delay),
+                   collect_tokens=int(collect_tokens), max_circuits=max_circuits,
+                   weight_seed=weight_seed, trace=1)
+    cap = 1 << 26
+    buf = C.create_string_buffer(cap)
+    need = C.c_size_t(0)
+    check(lib.ds_run(_b(config_text), _b(config_dir), _b(policy or ""), latency_us, nb_override,
+                     C.byref(md), C.byref(opts), _b(trace_path or ""), buf, cap, C.byref(need)))
+    return json.loads(buf.value.decode())
+
+
+def trace_merge(paths: list[str], out_path: str) -> None:
+    arr = (C.c_char_p * len(paths))(*[_b(p) for p in paths])
+    check(lib.ds_trace_merge(arr, len(paths), _b(out_path)))
+
+
+def trace_report(trace_path: str, n_stages: int, w0_us: int, w1_us: int, seed: int = 0) -> dict:
+    buf = C.create_string_buffer(1 << 16)
+    check(lib.ds_trace_report(_b(trace_path), n_stages, w0_us, w1_us, seed, buf, len(buf)))
+    return json.loads(buf.value.decode())
+
+
 class Session:
     """A planned + scheduled pipeline with its GPU stages built once (ds_session_*)."""
 
     def __init__(self, config_text: str, config_dir: str = "", policy=None, latency_us=-1,
                  nb_override=-1, model=None, device0=0, n_devices=0, real_delay=True,
-                 max_circuits=0, weight_seed=WEIGHT_SEED):
+                 max_circuits=0, weight_seed=WEIGHT_SEED, trace=False):
         from ._native import GpuOpts
         if model is None:
             model = json.loads(config_text)["model"]["name"]
         self._md = model_desc(model)
         self._opts = GpuOpts(device0=device0, n_devices=n_devices, real_delay=int(real_delay),
-                             collect_tokens=0, max_circuits=max_circuits, weight_seed=weight_seed)
+                             collect_tokens=0, max_circuits=max_circuits, weight_seed=weight_seed,
+                             trace=int(trace))
         self._h = C.c_void_p()
         check(lib.ds_session_create(_b(config_text), _b(config_dir), _b(policy or ""), latency_us,
                                     nb_override, C.byref(self._md), C.byref(self._opts),
@@ -164,6 +197,33 @@ class Session:
         check(lib.ds_session_run(self._h, int(profile), int(collect_tokens), buf, cap,
                                  C.byref(need)))
         return json.loads(buf.value.decode())
+
+    def trace(self, trace_path: str | None = None, t0_us=-1, keep_virtual_seq=False, w0_us=-1,
+              w1_us=-1) -> dict:
+        """Real-clock EventTrace of the last run (written to trace_path) and its SimReport."""
+        need = C.c_size_t(0)
+        check(lib.ds_session_trace(self._h, _b(trace_path or ""), t0_us, int(keep_virtual_seq),
+                                   w0_us, w1_us, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value + 16)
+        check(lib.ds_session_trace(self._h, None, t0_us, int(keep_virtual_seq), w0_us, w1_us, buf,
+                                   len(buf), None))
+        return json.loads(buf.value.decode())
+
+    def capture(self, req_ids) -> None:
+        """Copy the fp32 logits of every row sampled for these requests at each run."""
+        arr = (C.c_int64 * max(len(req_ids), 1))(*req_ids)
+        check(lib.ds_session_capture(self._h, arr, len(req_ids)))
+
+    def captured(self):
+        """(meta [n, 4] = circuit, req_id, position, sampled-row index; logits [n, vocab])."""
+        import numpy as np
+        n = C.c_int64(0)
+        check(lib.ds_session_captured(self._h, None, None, 0, C.byref(n)))
+        meta = np.zeros((n.value, 4), dtype=np.int64)
+        lg = np.zeros((n.value, self._md.vocab), dtype=np.float32)
+        check(lib.ds_session_captured(self._h, meta.ctypes.data, lg.ctypes.data, n.value,
+                                      C.byref(n)))
+        return meta, lg
 
     def close(self):
         if self._h:

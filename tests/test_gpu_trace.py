@@ -1,0 +1,108 @@
+"""Hardware runs speak the reference's SimResult{report, trace} contract (sim.hpp:47-51):
+
+* the real-clock EventTrace (ds_run / ds_session_trace) carries exactly the integer fields of the
+  virtual-clock schedule's events, per stage in order (replay mode: only times differ);
+* the reference's own replay_check (sim.cpp:606-697, compiled in oracle/_ref) finds no violation
+  in it: one compute per stage, computes after their swap-ins, hop arrivals no earlier than
+  send + injected latency + serialisation (the executor's delay is real), swap directions
+  serialised;
+* the reference's windowed_stats (workload.cpp:82-116) over the report window gives the report's
+  output_tokens."""
+import json
+import os
+from collections import defaultdict
+
+import pytest
+
+from paper_2501_14784_b200 import n_devices
+from paper_2501_14784_b200 import pipeline as pl
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CDIR = os.path.join(ROOT, "configs")
+OUT = os.path.join(ROOT, "gpurun_out")
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(n_devices() < 1, reason="needs a GPU")]
+
+
+def _parse(path):
+    ev = []
+    for line in open(path):
+        f = dict(x.split("=", 1) for x in line.split())
+        ev.append({k: (v if k == "kind" else int(v)) for k, v in f.items()})
+    return ev
+
+
+def _keyed(events):
+    """Per (kind, stage): the ordered integer payloads that must equal the virtual trace's."""
+    out = defaultdict(list)
+    for e in events:
+        k = e["kind"]
+        if k in ("ComputeStart", "ComputeEnd"):
+            out[(k, e["stage"])].append((e["mb"], e["a"], e["b"], e["c"]))
+        elif k in ("SwapInDone", "SwapOutDone"):
+            out[(k, e["stage"])].append((e["mb"], e["b"], e["c"]))
+        elif k == "TransferArrive":
+            out[(k, e["stage"], e["mb"])].append(e["b"])
+        else:
+            out[(k,)].append((e["mb"], e["a"], e["b"], e["c"]))
+    return out
+
+
+def _run_and_check(cfg_name, n_circ, edit=None, devices=1, allow=()):
+    import oracle
+    ref = oracle.Ref()
+    cfg = json.load(open(os.path.join(CDIR, cfg_name)))
+    if edit:
+        edit(cfg)
+    txt = json.dumps(cfg)
+    os.makedirs(OUT, exist_ok=True)
+    hw = os.path.join(OUT, f"hw_{cfg_name}.trace")
+    vt = os.path.join(OUT, f"virtual_{cfg_name}.trace")
+    res = pl.run(txt, CDIR, n_devices=devices, max_circuits=n_circ, trace_path=hw)
+    rep, gpu = res["report"], res["gpu"]
+    assert gpu["error"] == "" and gpu["circuits"] == n_circ
+    pl.sim_config(txt, CDIR, trace_path=vt)
+    h, v = _keyed(_parse(hw)), _keyed(_parse(vt))
+    # every hardware event sequence is a prefix of the virtual one (the executed circuits)
+    for key, seq in h.items():
+        assert seq == v[key][:len(seq)], key
+    n_comp = sum(len(s) for k, s in h.items() if k[0] == "ComputeStart")
+    assert n_comp == rep["trace_computes"] >= n_circ
+    plan = pl.plan_config(txt, CDIR)
+    viol = ref.replay_check(hw, plan)
+    kinds = defaultdict(int)
+    for x in viol:
+        kinds[x.split()[0] if " " in x else x] += 1
+    bad = [x for x in viol if not any(a in x for a in allow)]
+    assert bad == [], bad[:5]
+    n_in, n_out, _ = ref.windowed_stats(hw, rep["window_start_us"], rep["window_end_us"])
+    assert n_out == rep["output_tokens"] and n_in == rep["input_tokens"]
+    return rep, gpu, viol
+
+
+def test_hw_trace_tiny_two_stages_real_delay():
+    # BASELINE configs[0]: 2 stages, 8 microbatches, 10 ms injected hops, window from t = 0
+    def edit(c):
+        c["workload"]["warmup_s"] = 0
+    rep, gpu, viol = _run_and_check("tiny_2stage.json", 80, edit)
+    assert rep["output_tokens"] > 0 and rep["stages"][0]["busy_us"] > 0
+    # 80 circuits over 2 stages with >= 10 ms per hop: the run cannot be faster than the hops
+    assert rep["run_end_us"] >= 10_000 * 80 // 8
+
+
+def test_hw_trace_llama8b_one_stage_prefix():
+    rep, gpu, viol = _run_and_check("llama8b_1stage.json", 60)
+    assert rep["output_tokens"] > 0
+
+
+def test_hw_trace_tiny_swap_plan():
+    # KV swap on (offload, N_B = 8 > 2): SwapIn/OutDone events carry the plan bytes with the
+    # measured copy times. The config's link is 1 GB/s while the B200 host link is ~50 GB/s, so
+    # a plan copy may finish faster than the modelled bandwidth: reported, not an error.
+    def edit(c):
+        c["workload"]["warmup_s"] = 0
+    rep, gpu, viol = _run_and_check("tiny_2stage_swap.json", 200, edit,
+                                    allow=("swap-bandwidth-exceeded",))
+    n_swaps = sum(len(s) for s in gpu["swap_pairs"])
+    assert n_swaps > 0
+    print(f"swap trace: {n_swaps} schedule swap-ins, {len(viol)} bandwidth notes, "
+          f"swap_stall_us {rep['swap_stall_us']}, measured swap wait {gpu['swap_wait_us']} us")

@@ -296,3 +296,50 @@ def test_plan_topology_mismatch():
     cfg["links"][0]["latency_us"] += 5
     with pytest.raises(SimError, match="mismatch"):
         pl.sim_plan(json.dumps(cfg), json.dumps(plan))
+
+
+# ------------------------------------------------------- report recomputed from a trace ----
+@pytest.mark.parametrize("name,policy,latency", [
+    ("configs/tiny_2stage_swap.json", None, -1), ("configs/llama8b_4stage_swap.json", None, -1),
+    ("tests/golden/ref_configs/reference_8stage.json", "opt", 64000),
+    ("tests/golden/ref_configs/reference_8stage.json", "offload", 16000),
+    ("tests/golden/ref_configs/reference_8stage.json", "baseline", 256000),
+    ("tests/golden/ref_configs/fig_ring4.json", None, -1)])
+def test_trace_report_equals_reference_run(ref, tmp_path, name, policy, latency):
+    """ds_trace_report (the report of hardware runs, computed from their trace) reproduces the
+    reference run()'s SimReport (build_report, sim.cpp:501-532 -- including per-stage busy, swap
+    stall and bubble) from the reference's own trace of the same run."""
+    path = os.path.join(ROOT, name)
+    txt, cdir = open(path).read(), os.path.dirname(path)
+    tr = str(tmp_path / "ref.trace")
+    want = ref.sim_config(txt, cdir, policy=policy, latency_us=latency, trace_path=tr)
+    cfg = json.loads(txt)
+    wl = cfg["workload"]
+    n_stages = len(json.loads(ref.plan_config(txt, cdir, policy=policy, latency_us=latency))["stages"])
+    got = pl.trace_report(tr, n_stages, wl["warmup_s"] * 10**6, wl["bench_duration_s"] * 10**6,
+                          wl["rng_seed"])
+    for k in ("input_tokens", "output_tokens", "completed_requests", "admitted_requests",
+              "live_requests", "swap_stall_us", "window_start_us", "window_end_us"):
+        assert got[k] == want[k], k
+    for a, b in zip(got["stages"], want["stages"]):
+        assert (a["busy_us"], a["stall_us"], a["bubble_us"]) == (b["busy_us"], b["stall_us"],
+                                                                 b["bubble_us"])
+    assert got["output_throughput"] == pytest.approx(want["output_throughput"], rel=1e-12)
+
+
+def test_trace_merge_orders_rank_traces(tmp_path):
+    """Per-rank traces (virtual seq kept) merge into one (time, seq)-ordered trace."""
+    cfg = os.path.join(CONFIGS, "tiny_2stage.json")
+    txt = open(cfg).read()
+    full = str(tmp_path / "full.trace")
+    pl.sim_config(txt, CONFIGS, trace_path=full)
+    lines = open(full).read().splitlines()
+    parts = [str(tmp_path / f"r{i}.trace") for i in range(2)]
+    # split by stage parity (stage -1 events with rank 1), as two ranks would write them
+    with open(parts[0], "w") as a, open(parts[1], "w") as b:
+        for ln in lines:
+            st = int(ln.split("stage=")[1].split()[0])
+            (a if st == 0 else b).write(ln + "\n")
+    merged = str(tmp_path / "m.trace")
+    pl.trace_merge(parts, merged)
+    assert open(merged).read() == open(full).read()

@@ -26,7 +26,9 @@ def _hop_sequence(sched, from_stage, to_stage, d_model):
         if op[0] != 0:
             continue
         c = sched["circuits"][op[3]]
-        nbytes = (sum(r[3] for r in c["rows"]) * 4 if to_stage == 0
+        # the ids hop always carries >= 1 int32: stage 0 times every circuit end (trace arrival
+        # of woken microbatches, reference wake_parked sim.cpp:277-294)
+        nbytes = (max(sum(r[3] for r in c["rows"]), 1) * 4 if to_stage == 0
                   else c["eff_batch"] * d_model * 2)
         if nbytes:
             seq.append((op[3], c["mb"], nbytes))

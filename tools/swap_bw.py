@@ -14,6 +14,7 @@ against the host link measured on the same box. This tool measures
 Prints one JSON line; `python tools/swap_bw.py > profiles/r01_swap_bw.json` under gpurun.
 """
 import ctypes as C
+import argparse
 import json
 import os
 import sys
@@ -103,8 +104,14 @@ def swap(model="llama3-8b", n_layers=8, tokens_per_mb=24 * 1024, rounds=6):
 def main():
     torch.cuda.init()
     link = host_link()
-    # argv: model layers (default the 8B 4-stage page; "llama3-70b-bf16 10" = the 70B 8-stage page)
-    sw = swap(sys.argv[1], int(sys.argv[2])) if len(sys.argv) > 2 else swap()
+    # default: the 8B 4-stage page; "--model llama3-70b-bf16 --layers 10" = the 70B 8-stage page
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default=None)
+    ap.add_argument("--layers", type=int, default=None)
+    a = ap.parse_args()
+    if (a.model is None) != (a.layers is None):
+        sys.exit("swap_bw.py: give both --model and --layers, or neither")
+    sw = swap(a.model, a.layers) if a.model else swap()
     # eviction and refill overlap page by page: the bound is both directions at once
     bound_s = (sw["out_bytes_per_call"] + sw["in_bytes_per_call"]) / (link["bidir_gbs"] * 1e9)
     sw["bound_ms_per_call"] = 1e3 * bound_s
