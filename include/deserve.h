@@ -241,6 +241,14 @@ ds_status ds_trace_merge(const char* const* paths, int32_t n_paths, const char* 
  * swap-stall / bubble per stage as the engine accumulates them). */
 ds_status ds_trace_report(const char* trace_path, int64_t n_stages, int64_t w0_us, int64_t w1_us,
                           uint64_t seed, char* report_json, size_t cap);
+/* The reference's report.kv (report_to_kv, src/sweep.cpp:146-195; no pricing block) of a report
+ * JSON (ds_run / ds_session_trace / ds_sim_config "report") on its plan document. */
+ds_status ds_report_kv(const char* report_json, const char* plan_json, int64_t latency_us,
+                       const char* policy, char* out, size_t cap, size_t* needed);
+/* The reference's sweep.csv (SweepResult::to_csv, src/sweep.cpp:68-82): policies x latencies
+ * output throughputs (row-major; NaN = failed cell). policies: comma-separated names. */
+ds_status ds_sweep_csv(const int64_t* latencies_us, int32_t n_latencies, const char* policies,
+                       const double* throughput, char* out, size_t cap, size_t* needed);
 /* The drop-in execution seam: the reference's run(plan, topo, workload, model)
  * (src/sim.cpp:591-595) with real stage forwards. Plans the config (ds_plan_config), schedules it,
  * executes it on GPUs, writes the real-clock trace to trace_path (may be NULL) and returns

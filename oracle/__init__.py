@@ -13,6 +13,18 @@ import json
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+# model dims and the weight seed of the workloads (restated here so the checkers and the CPU
+# baselines never import the product package; must equal paper_2501_14784_b200.pipeline's)
+MODEL_DIMS = {
+    "tiny-llama": dict(n_layers=4, d_model=256, n_heads=4, n_kv_heads=2, d_head=64, ffn=768,
+                       vocab=128256, max_seq_len=8192, rope_theta=500000.0, norm_eps=1e-5),
+    "llama3-8b": dict(n_layers=32, d_model=4096, n_heads=32, n_kv_heads=8, d_head=128, ffn=14336,
+                      vocab=128256, max_seq_len=8192, rope_theta=500000.0, norm_eps=1e-5),
+    "llama3-70b-bf16": dict(n_layers=80, d_model=8192, n_heads=64, n_kv_heads=8, d_head=128,
+                            ffn=28672, vocab=128256, max_seq_len=8192, rope_theta=500000.0,
+                            norm_eps=1e-5),
+}
+WEIGHT_SEED = 0x5EED0001
 REF_SO = os.path.join(HERE, "_ref", "libpipesim_ref.so")
 LLAMA_SO = os.path.join(HERE, "_build", "libllama_ref.so")
 
@@ -45,6 +57,8 @@ class Ref:
             "ref_replay_check": [S, S, P, C.c_size_t],
             "ref_windowed_stats": [S, L, L, C.c_int, P],
             "ref_request": [C.c_ulonglong, L, L, L, L, L, P],
+            "ref_report_kv": [S, S, S, L, L, P, C.c_size_t],
+            "ref_sweep_csv": [S, S, P, C.c_size_t],
         }.items():
             getattr(lib, name).argtypes = args
             getattr(lib, name).restype = C.c_int
@@ -73,6 +87,17 @@ class Ref:
         self._ok(self.lib.ref_sim_plan(_b(text), _b(cdir), _b(plan_json), _b(trace_path or ""),
                                        buf, len(buf)))
         return json.loads(buf.value.decode())
+
+    def report_kv(self, text, cdir="", policy=None, latency_us=-1, nb=-1) -> str:
+        buf = C.create_string_buffer(1 << 16)
+        self._ok(self.lib.ref_report_kv(_b(text), _b(cdir), _b(policy or ""), latency_us, nb, buf,
+                                        len(buf)))
+        return buf.value.decode()
+
+    def sweep_csv(self, text, cdir="") -> str:
+        buf = C.create_string_buffer(1 << 16)
+        self._ok(self.lib.ref_sweep_csv(_b(text), _b(cdir), buf, len(buf)))
+        return buf.value.decode()
 
     def stage_time(self, table, batch, layers, ref_layers) -> int:
         b = (C.c_longlong * len(table))(*[x[0] for x in table])
@@ -256,6 +281,59 @@ def replay_requests(schedule: dict, dims: dict, seed: int, reqs, gpu_tokens):
     finally:
         lr.lib.lr_stage_destroy(st)
     return np.array(meta, dtype=np.int64).reshape(-1, 3), np.array(out, dtype=np.float32)
+
+
+class CircuitTimer:
+    """Times the CPU stage forward (oracle/llama_ref.c, OpenMP on every host core) on whole
+    circuits of a single-stage schedule: all layers + embedding + LM head, the circuit's exact
+    rows (prompt chunks and decode rows at their positions). Only time is measured: each timed
+    circuit starts from zeroed KV (decode rows still attend over all their positions), so any
+    circuit of the schedule can be timed without replaying its history."""
+
+    def __init__(self, dims: dict, seed: int, max_slots: int):
+        self.lr = LlamaRef()
+        self.lr.lib.lr_stage_reset_kv.argtypes = [C.c_void_p]
+        self.dims = dims
+        self.max_slots = max_slots
+        m = LrModel(**dims)
+        self.st = self.lr.lib.lr_stage_create(C.byref(m), 0, dims["n_layers"], 1, 1, seed, max_slots)
+
+    def close(self):
+        if self.st:
+            self.lr.lib.lr_stage_destroy(self.st)
+            self.st = None
+
+    def time(self, circuit: dict) -> float:
+        import time
+
+        import numpy as np
+        rows = circuit["rows"]
+        arr = (LrRow * len(rows))(*[LrRow(r[0], r[1], r[2], r[3], r[4], 0, r[5]) for r in rows])
+        toks = []
+        for r in rows:
+            for j in range(r[2]):
+                pos = r[1] + j
+                toks.append((128000 if pos == 0 else 1000) if r[4] else self.lr.lib.lr_prompt_token(r[5], pos))
+        T = len(toks)
+        R = sum(r[3] for r in rows)
+        tok = np.array(toks, dtype=np.int32)
+        act = np.zeros((T, self.dims["d_model"]), dtype=np.float32)
+        lg = np.zeros((max(R, 1), self.dims["vocab"]), dtype=np.float32)
+        ids = np.zeros(max(R, 1), dtype=np.int32)
+        self.lr.lib.lr_stage_reset_kv(self.st)
+        t0 = time.perf_counter()
+        rc = self.lr.lib.lr_stage_step(self.st, 0, self.max_slots, arr, len(rows), tok.ctypes.data,
+                                       None, act.ctypes.data, lg.ctypes.data, ids.ctypes.data)
+        dt = time.perf_counter() - t0
+        if rc != 0:
+            raise RefError("oracle stage step failed")
+        return dt
+
+
+def load_schedule_fixture(path: str) -> list:
+    import gzip
+    with gzip.open(path, "rt") as f:
+        return json.load(f)
 
 
 def greedy_mismatches(oracle_logits, gpu_tokens, margin):

@@ -66,19 +66,19 @@ typedef struct {
 
 typedef struct {
     int64_t req_id;
-    int cap;   /* positions held per (layer, K|V, kv head); grows on demand */
-    float* kv; /* [L][2][n_kv][cap][dh] */
+    int cap;      /* positions held per (layer, K|V, kv head); grows on demand */
+    uint16_t* kv; /* [L][2][n_kv][cap][dh] bf16 bits (K after RoPE and V are bf16 values) */
 } handle_kv;
 
-/* make room for positions [0, need) keeping the cached ones */
+/* make room for positions [0, need) keeping the cached ones; new positions are zero */
 static void kv_reserve(handle_kv* hk, int L, int nkv, int dh, int need) {
     if (need <= hk->cap) return;
     int cap = hk->cap ? hk->cap : 256;
     while (cap < need) cap *= 2;
-    float* nk = (float*)malloc(sizeof(float) * (size_t)L * 2 * nkv * cap * dh);
+    uint16_t* nk = (uint16_t*)calloc((size_t)L * 2 * nkv * cap * dh, sizeof(uint16_t));
     if (hk->kv)
         for (size_t blk = 0; blk < (size_t)L * 2 * nkv; ++blk)
-            memcpy(nk + blk * cap * dh, hk->kv + blk * hk->cap * dh, sizeof(float) * (size_t)hk->cap * dh);
+            memcpy(nk + blk * cap * dh, hk->kv + blk * hk->cap * dh, sizeof(uint16_t) * (size_t)hk->cap * dh);
     free(hk->kv);
     hk->kv = nk;
     hk->cap = cap;
@@ -140,6 +140,15 @@ lr_stage* lr_stage_create(const lr_model* m, int32_t lb, int32_t le, int32_t fir
     s->h = (handle_kv*)calloc(max_handles, sizeof(handle_kv));
     for (int i = 0; i < max_handles; ++i) s->h[i].req_id = -1;
     return s;
+}
+
+void lr_stage_reset_kv(lr_stage* s) {
+    for (int i = 0; i < s->max_handles; ++i) {
+        free(s->h[i].kv);
+        s->h[i].kv = NULL;
+        s->h[i].cap = 0;
+        s->h[i].req_id = -1;
+    }
 }
 
 void lr_stage_destroy(lr_stage* s) {
@@ -297,11 +306,11 @@ int lr_stage_step(lr_stage* s, int32_t mb, int32_t max_slots, const lr_row* rows
                 }
             }
             const size_t S = (size_t)s->h[row_h[t]].cap;
-            float* kvb = s->h[row_h[t]].kv + (size_t)li * 2 * kvd * S;
+            uint16_t* kvb = s->h[row_h[t]].kv + (size_t)li * 2 * kvd * S;
             for (int kh = 0; kh < nkv; ++kh)
                 for (int i = 0; i < dh; ++i) {
-                    kvb[((size_t)kh * S + p) * dh + i] = kk[(size_t)t * kvd + kh * dh + i];
-                    kvb[((size_t)(nkv + kh) * S + p) * dh + i] = bf(vv[(size_t)t * kvd + kh * dh + i]);
+                    kvb[((size_t)kh * S + p) * dh + i] = bf_bits(kk[(size_t)t * kvd + kh * dh + i]);
+                    kvb[((size_t)(nkv + kh) * S + p) * dh + i] = bf_bits(vv[(size_t)t * kvd + kh * dh + i]);
                 }
         }
         const float scale = 1.0f / sqrtf((float)dh);
@@ -310,14 +319,14 @@ int lr_stage_step(lr_stage* s, int32_t mb, int32_t max_slots, const lr_row* rows
             for (int hh = 0; hh < nh; ++hh) {
                 const int p = row_pos[t], kh = hh / G;
                 const size_t S = (size_t)s->h[row_h[t]].cap;
-                const float* kvb = s->h[row_h[t]].kv + (size_t)li * 2 * kvd * S;
+                const uint16_t* kvb = s->h[row_h[t]].kv + (size_t)li * 2 * kvd * S;
                 const float* qv = q + (size_t)t * qd + hh * dh;
                 float* sc = (float*)malloc(sizeof(float) * (p + 1));
                 float mx = -INFINITY;
                 for (int j = 0; j <= p; ++j) {
-                    const float* kr = kvb + ((size_t)kh * S + j) * dh;
+                    const uint16_t* kr = kvb + ((size_t)kh * S + j) * dh;
                     float dot = 0.f;
-                    for (int i = 0; i < dh; ++i) dot += qv[i] * kr[i];
+                    for (int i = 0; i < dh; ++i) dot += qv[i] * from_bits(kr[i]);
                     sc[j] = dot * scale;
                     if (sc[j] > mx) mx = sc[j];
                 }
@@ -329,8 +338,8 @@ int lr_stage_step(lr_stage* s, int32_t mb, int32_t max_slots, const lr_row* rows
                 float* o = att + (size_t)t * qd + hh * dh;
                 for (int i = 0; i < dh; ++i) o[i] = 0.f;
                 for (int j = 0; j <= p; ++j) {
-                    const float* vr = kvb + ((size_t)(nkv + kh) * S + j) * dh;
-                    for (int i = 0; i < dh; ++i) o[i] += sc[j] * vr[i];
+                    const uint16_t* vr = kvb + ((size_t)(nkv + kh) * S + j) * dh;
+                    for (int i = 0; i < dh; ++i) o[i] += sc[j] * from_bits(vr[i]);
                 }
                 for (int i = 0; i < dh; ++i) o[i] = bf(o[i] / sum);
                 free(sc);

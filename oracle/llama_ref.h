@@ -26,6 +26,8 @@ int32_t lr_prompt_token(int64_t req_id, int32_t pos);
 lr_stage* lr_stage_create(const lr_model* m, int32_t layer_begin, int32_t layer_end,
                           int32_t is_first, int32_t is_last, uint64_t seed, int32_t max_handles);
 void lr_stage_destroy(lr_stage* s);
+/* forget every request's KV (timing harness: bounded memory between sampled circuits) */
+void lr_stage_reset_kv(lr_stage* s);
 /* tokens: first stage, one id per row position (T); act_in: other stages, [T, d] (bf16 values
  * held in fp32). act_out: [T, d]; logits: [R, vocab] fp32 (may be NULL); ids: [R]. */
 int lr_stage_step(lr_stage* s, int32_t mb, int32_t max_slots, const lr_row* rows, int32_t n_rows,

@@ -109,6 +109,28 @@ int ref_sim_config(const char* text, const char* dir, const char* policy, long l
     });
 }
 
+// report_to_kv (src/sweep.cpp:146-195) of run() on the config (policy/latency as ref_plan_config)
+int ref_report_kv(const char* text, const char* dir, const char* policy, long long latency,
+                  long long nb, char* out, size_t cap) {
+    return guard([&] {
+        Planned p = make(text, dir, policy, latency, nb);
+        SimResult r = run(p.plan, p.topo, p.cfg.workload, p.cfg.model);
+        const Micros lat = p.topo.links.empty() ? 0 : p.topo.links.front().latency_us;
+        put(report_to_kv(r.report, p.plan, lat, policy && *policy ? policy : "config", nullptr), out, cap);
+        return 0;
+    });
+}
+
+// run_sweep(...).to_csv() (src/sweep.cpp:68-82,101-144) over the config's sweep latencies
+int ref_sweep_csv(const char* text, const char* dir, char* out, size_t cap) {
+    return guard([&] {
+        RunConfig cfg = parse_config(text, dir ? dir : "");
+        SweepResult r = run_sweep(cfg, {Policy::Baseline, Policy::Offload, Policy::Opt}, 1, false);
+        put(r.to_csv(), out, cap);
+        return 0;
+    });
+}
+
 int ref_sim_plan(const char* text, const char* dir, const char* plan_json, const char* trace_path,
                  char* report, size_t cap) {
     return guard([&] {

@@ -391,6 +391,32 @@ ds_status ds_trace_report(const char* trace_path, int64_t n_stages, int64_t w0_u
     });
 }
 
+ds_status ds_report_kv(const char* report_json, const char* plan_json, int64_t latency_us,
+                       const char* policy, char* out, size_t cap, size_t* needed) {
+    return guarded([&] {
+        if (!report_json || !plan_json) return ds_fail(DS_ERR_ARG, "null report/plan");
+        const dsb::Report r = dsb::report_from_json(report_json);
+        const dsb::Plan p = dsb::Plan::from_json(plan_json);
+        copy_out(dsb::report_kv(r, p, latency_us, policy ? policy : ""), out, cap, needed);
+        return DS_OK;
+    });
+}
+
+ds_status ds_sweep_csv(const int64_t* lat, int32_t n_lat, const char* policies, const double* tput,
+                       char* out, size_t cap, size_t* needed) {
+    return guarded([&] {
+        if (!lat || n_lat < 1 || !policies || !tput) return ds_fail(DS_ERR_ARG, "bad sweep arguments");
+        std::vector<std::string> pol;
+        std::stringstream ss(policies);
+        std::string item;
+        while (std::getline(ss, item, ',')) pol.push_back(item);
+        const std::vector<int64_t> l(lat, lat + n_lat);
+        const std::vector<double> v(tput, tput + pol.size() * size_t(n_lat));
+        copy_out(dsb::sweep_csv(l, pol, v), out, cap, needed);
+        return DS_OK;
+    });
+}
+
 ds_status ds_session_capture(ds_session* h, const int64_t* reqs, int64_t n) {
     return guarded([&] {
         if (!h || !h->s || (n > 0 && !reqs)) return ds_fail(DS_ERR_ARG, "bad capture arguments");

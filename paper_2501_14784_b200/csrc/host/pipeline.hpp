@@ -182,6 +182,12 @@ std::vector<Record> parse_trace(const std::string& text);
 struct Report;
 Report report_from_trace(const std::vector<Record>& tr, int64_t n_stages, Micros w0, Micros w1,
                          uint64_t seed);
+struct Plan;
+Report report_from_json(const std::string& text);
+// reference report_to_kv (src/sweep.cpp:146-195) and SweepResult::to_csv (sweep.cpp:68-82)
+std::string report_kv(const Report& r, const Plan& p, Micros latency, const std::string& policy);
+std::string sweep_csv(const std::vector<Micros>& lat, const std::vector<std::string>& pol,
+                      const std::vector<double>& tput);
 
 struct StageStats {
     Micros busy = 0, stall = 0, bubble = 0;

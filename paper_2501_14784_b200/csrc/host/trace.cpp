@@ -8,6 +8,7 @@
 #include <map>
 #include <sstream>
 
+#include "json.hpp"
 #include "pipeline.hpp"
 
 namespace dsb {
@@ -120,6 +121,101 @@ Report report_from_trace(const std::vector<Record>& tr, int64_t S, Micros w0, Mi
     }
     r.mean_bubble = S > 0 ? sum / double(S) : 0;
     return r;
+}
+
+Report report_from_json(const std::string& text) {
+    const auto j = nlohmann::json::parse(text);
+    Report r;
+    r.w0 = j.at("window_start_us").get<int64_t>();
+    r.w1 = j.at("window_end_us").get<int64_t>();
+    r.n_in = j.at("input_tokens").get<int64_t>();
+    r.n_out = j.at("output_tokens").get<int64_t>();
+    r.wall_s = j.at("wall_time_s").get<double>();
+    r.in_tps = j.at("input_throughput").get<double>();
+    r.out_tps = j.at("output_throughput").get<double>();
+    r.total_tps = j.at("total_throughput").get<double>();
+    r.mean_bubble = j.at("mean_bubble_fraction").get<double>();
+    r.max_bubble = j.at("max_bubble_fraction").get<double>();
+    r.swap_stall = j.at("swap_stall_us").get<int64_t>();
+    r.completed = j.at("completed_requests").get<int64_t>();
+    r.live = j.at("live_requests").get<int64_t>();
+    r.admitted = j.at("admitted_requests").get<int64_t>();
+    r.seed = j.at("rng_seed").get<uint64_t>();
+    for (const auto& s : j.at("stages")) {
+        StageStats x;
+        x.busy = s.at("busy_us").get<int64_t>();
+        x.stall = s.at("stall_us").get<int64_t>();
+        x.bubble = s.at("bubble_us").get<int64_t>();
+        x.busy_frac = s.at("busy_fraction").get<double>();
+        x.stall_frac = s.at("transfer_wait_fraction").get<double>();
+        x.bubble_frac = s.at("bubble_fraction").get<double>();
+        r.stages.push_back(x);
+    }
+    return r;
+}
+
+// The reference's key=value report (report_to_kv, src/sweep.cpp:146-195; no pricing block).
+std::string report_kv(const Report& r, const Plan& p, Micros latency, const std::string& policy) {
+    std::ostringstream os;
+    char buf[64];
+    auto f6 = [&](double v) {
+        snprintf(buf, sizeof buf, "%.6f", v);
+        return std::string(buf);
+    };
+    os << "seed=" << r.seed << "\n"
+       << "policy=" << policy << "\n"
+       << "latency_us=" << latency << "\n"
+       << "n_stages=" << p.S() << "\n"
+       << "n_microbatches=" << p.n_mb << "\n"
+       << "batch_size=" << p.B() << "\n"
+       << "stage_time_us=" << p.t_s << "\n"
+       << "offload=" << (p.offload ? 1 : 0) << "\n"
+       << "window_start_us=" << r.w0 << "\n"
+       << "window_end_us=" << r.w1 << "\n"
+       << "input_tokens=" << r.n_in << "\n"
+       << "output_tokens=" << r.n_out << "\n"
+       << "wall_time_s=" << f6(r.wall_s) << "\n"
+       << "input_throughput=" << f6(r.in_tps) << "\n"
+       << "output_throughput=" << f6(r.out_tps) << "\n"
+       << "total_throughput=" << f6(r.total_tps) << "\n"
+       << "mean_bubble_fraction=" << f6(r.mean_bubble) << "\n"
+       << "max_bubble_fraction=" << f6(r.max_bubble) << "\n"
+       << "swap_stall_us=" << r.swap_stall << "\n"
+       << "completed_requests=" << r.completed << "\n"
+       << "admitted_requests=" << r.admitted << "\n"
+       << "live_requests=" << r.live << "\n";
+    for (size_t i = 0; i < r.stages.size(); ++i) {
+        const StageStats& s = r.stages[i];
+        os << "stage." << i << ".busy_fraction=" << f6(s.busy_frac) << "\n"
+           << "stage." << i << ".bubble_fraction=" << f6(s.bubble_frac) << "\n"
+           << "stage." << i << ".transfer_wait_fraction=" << f6(s.stall_frac) << "\n"
+           << "stage." << i << ".swap_stall_us=" << s.stall << "\n";
+    }
+    return os.str();
+}
+
+// The reference's sweep matrix (SweepResult::to_csv, src/sweep.cpp:68-82): a NaN cell = failed.
+std::string sweep_csv(const std::vector<Micros>& lat, const std::vector<std::string>& pol,
+                      const std::vector<double>& tput) {
+    std::ostringstream os;
+    os << "policy";
+    for (Micros l : lat) os << "," << l;
+    os << "\n";
+    char buf[64];
+    for (size_t i = 0; i < pol.size(); ++i) {
+        os << pol[i];
+        for (size_t k = 0; k < lat.size(); ++k) {
+            const double v = tput[i * lat.size() + k];
+            if (v != v) {
+                os << ",failed";
+            } else {
+                snprintf(buf, sizeof buf, "%.3f", v);
+                os << "," << buf;
+            }
+        }
+        os << "\n";
+    }
+    return os.str();
 }
 
 }  // namespace dsb

@@ -172,6 +172,30 @@ def trace_report(trace_path: str, n_stages: int, w0_us: int, w1_us: int, seed: i
     return json.loads(buf.value.decode())
 
 
+def report_kv(report: dict, plan_json: str, latency_us: int, policy: str) -> str:
+    """report.kv text of a report (reference report_to_kv, sweep.cpp:146-195)."""
+    need = C.c_size_t(0)
+    rj = _b(json.dumps(report))
+    check(lib.ds_report_kv(rj, _b(plan_json), latency_us, _b(policy), None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    check(lib.ds_report_kv(rj, _b(plan_json), latency_us, _b(policy), buf, need.value, None))
+    return buf.value.decode()
+
+
+def sweep_csv(latencies, policies, throughput) -> str:
+    """sweep.csv text (reference SweepResult::to_csv, sweep.cpp:68-82); throughput[p][l], None =
+    failed."""
+    lat = (C.c_int64 * len(latencies))(*latencies)
+    flat = [float("nan") if v is None else float(v) for row in throughput for v in row]
+    vals = (C.c_double * len(flat))(*flat)
+    need = C.c_size_t(0)
+    pol = _b(",".join(policies))
+    check(lib.ds_sweep_csv(lat, len(latencies), pol, vals, None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    check(lib.ds_sweep_csv(lat, len(latencies), pol, vals, buf, need.value, None))
+    return buf.value.decode()
+
+
 class Session:
     """A planned + scheduled pipeline with its GPU stages built once (ds_session_*)."""
 

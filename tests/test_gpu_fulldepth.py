@@ -10,8 +10,10 @@
   LM head): rows of stated requests from that config's schedule.
 * Decode at contexts 3840-3843 (the swap-forcing configs' prompt length) at Llama-3-8B dims.
 
-Tolerance: logits |gpu - oracle| <= 0.08 + 0.02 |oracle|; greedy ids equal wherever
-the oracle's top-2 margin exceeds 0.16; activations within 3% of the row max."""
+Tolerance at depth (stage_harness.deep_*): per row RMS(dlogit) <= 4% of RMS(logits)
+and every |dlogit| <= 0.16 + 0.02 |logit|; greedy ids equal wherever the oracle's top-2 margin
+exceeds 0.32; stage activations RMS(d) <= 2% RMS(x), max |d| <= 6% of the row max. Measured
+statistics go to gpurun_out/fulldepth_stats.json (committed under profiles/)."""
 import json
 import os
 
@@ -21,20 +23,46 @@ import pytest
 from paper_2501_14784_b200 import n_devices
 from paper_2501_14784_b200 import pipeline as pl
 
-from stage_harness import Pair, greedy_ok, logits_ok, random_act
+from stage_harness import Pair, deep_act_ok, deep_logits_ok, greedy_ok, random_act
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CDIR = os.path.join(ROOT, "configs")
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(n_devices() < 1, reason="needs a GPU")]
 
-ATOL, RTOL, MARGIN = 0.08, 0.02, 0.16
+MARGIN = 0.32  # greedy ids must agree where the oracle's top-2 margin > 2 x the max tolerance
+STATS = {}
 
 
-def _check_rows(gpu_lg, cpu_lg, gpu_ids=None):
-    ok, worst = logits_ok(gpu_lg, cpu_lg, ATOL, RTOL)
-    assert ok, f"max |dlogit| {worst}"
-    if gpu_ids is not None:
-        assert greedy_ok(gpu_ids, cpu_lg, MARGIN) == []
+def _dump():
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    json.dump(STATS, open(os.path.join(ROOT, "gpurun_out", "fulldepth_stats.json"), "w"), indent=1)
+
+
+def _check_rows(name, gpu_lg, cpu_lg, gpu_ids=None):
+    ok, rms, worst = deep_logits_ok(gpu_lg, cpu_lg)
+    top = np.sort(cpu_lg, axis=1)[:, -2:]
+    margins = top[:, 1] - top[:, 0]
+    bad = greedy_ok(gpu_ids, cpu_lg, MARGIN) if gpu_ids is not None else []
+    st = STATS.setdefault(name, {"rows": 0, "rms_rel_max": 0.0, "abs_max": 0.0, "greedy_checked": 0,
+                                 "greedy_bad": 0})
+    st["rows"] += len(cpu_lg)
+    st["rms_rel_max"] = max(st["rms_rel_max"], rms)
+    st["abs_max"] = max(st["abs_max"], worst)
+    st["greedy_checked"] += int((margins > MARGIN).sum()) if gpu_ids is not None else 0
+    st["greedy_bad"] += len(bad)
+    _dump()
+    assert ok, f"rms_rel {rms}, max |dlogit| {worst}"
+    assert bad == []
+
+
+def _check_act(name, gpu, cpu):
+    ok, rms, mx = deep_act_ok(gpu, cpu)
+    st = STATS.setdefault(name, {"rows": 0, "rms_rel_max": 0.0, "max_rel_max": 0.0})
+    st["rows"] += len(cpu)
+    st["rms_rel_max"] = max(st["rms_rel_max"], rms)
+    st["max_rel_max"] = max(st["max_rel_max"], mx)
+    _dump()
+    assert ok, (rms, mx)
 
 
 def test_llama8b_32_layers_schedule_logits():
@@ -42,9 +70,10 @@ def test_llama8b_32_layers_schedule_logits():
     txt = open(os.path.join(CDIR, "llama8b_1stage.json")).read()
     n = 24
     sched = pl.schedule_config(txt, CDIR, max_circuits=n)
-    # stated subset: the two cheapest requests with >= 4 sampled rows, the one with the most
-    # decode rows among the first 3 requests, and the cheapest whose prompt spans two circuits
-    reqs = [10, 19, 1, 18]
+    # stated subset: the two cheapest requests with >= 4 sampled rows (10, 19), the one with the
+    # most decode rows among the first 3 (1), the cheapest whose prompt spans two circuits (18),
+    # and request 0 (a 262-token prompt split over two circuits: its decode rows read 2 KV pages)
+    reqs = [10, 19, 1, 18, 0]
     with pl.Session(txt, CDIR, n_devices=1, max_circuits=n) as s:
         s.capture(reqs)
         r = s.run(collect_tokens=True)
@@ -58,7 +87,13 @@ def test_llama8b_32_layers_schedule_logits():
     ids = []
     for c, q, pos, k in meta:
         ids.append(r["tokens"][c][k])
-    _check_rows(lg, olg, np.array(ids))
+    err = np.abs(lg - olg)
+    stats = {"rows": [[int(c), int(q), int(p), float(e.max()), float(np.sqrt((e ** 2).mean())),
+                       float(np.sqrt((o ** 2).mean())), int(np.argmax(o)), int(i)]
+                      for (c, q, p, _), e, o, i in zip(meta, err, olg, ids)]}
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    json.dump(stats, open(os.path.join(ROOT, "gpurun_out", "fulldepth_8b_errors.json"), "w"))
+    _check_rows("llama8b_32_layers", lg, olg, np.array(ids))
     # the captured rows include decode at positions > 256 (second KV page) and a prompt chunk
     # continuing at a position > 0
     assert ometa[:, 2].max() > 256
@@ -104,9 +139,7 @@ def test_llama70b_stage0_and_stage7_ten_layers():
             if prev is not None:
                 ids = np.array([a.last_tok[(0, r[0])] for r in prev if r[3]], dtype=np.int32)
             o = a.step(0, rows, ids_in=ids)
-            err = np.abs(o["gpu_act"] - o["cpu_act"]).max(axis=1)
-            scale = np.abs(o["cpu_act"]).max(axis=1)
-            assert np.all(err <= 0.03 * scale), (i, (err / scale).max())
+            _check_act("llama70b_stage0_10_layers", o["gpu_act"], o["cpu_act"])
             for r in rows:
                 if r[3]:
                     a.last_tok[(0, r[0])] = (r[5] * 7919 + r[1]) % 128000
@@ -120,7 +153,7 @@ def test_llama70b_stage0_and_stage7_ten_layers():
             T = sum(r[2] for r in rows)
             o = b.step(0, rows, act_in=random_act(T, 8192, 100 + i))
             if o["cpu_logits"].shape[0]:
-                _check_rows(o["gpu_logits"], o["cpu_logits"], o["gpu_ids"])
+                _check_rows("llama70b_stage7_10_layers", o["gpu_logits"], o["cpu_logits"], o["gpu_ids"])
     finally:
         b.close()
 
@@ -133,10 +166,10 @@ def test_llama8b_dims_decode_at_3840_context():
     try:
         rows = [(0, 0, 3840, 1, 0, 11), (1, 0, 100, 1, 0, 12)]
         o = p.step(0, rows, act_in=random_act(3940, 4096, 21))
-        _check_rows(o["gpu_logits"], o["cpu_logits"], o["gpu_ids"])
+        _check_rows("llama8b_ctx3840", o["gpu_logits"], o["cpu_logits"], o["gpu_ids"])
         for k in range(4):
             rows = [(0, 3840 + k, 1, 1, 1, 11), (1, 100 + k, 1, 1, 1, 12)]
             o = p.step(0, rows, act_in=random_act(2, 4096, 22 + k))
-            _check_rows(o["gpu_logits"], o["cpu_logits"], o["gpu_ids"])
+            _check_rows("llama8b_ctx3840", o["gpu_logits"], o["cpu_logits"], o["gpu_ids"])
     finally:
         p.close()

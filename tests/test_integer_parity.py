@@ -343,3 +343,26 @@ def test_trace_merge_orders_rank_traces(tmp_path):
     merged = str(tmp_path / "m.trace")
     pl.trace_merge(parts, merged)
     assert open(merged).read() == open(full).read()
+
+
+@pytest.mark.parametrize("policy,latency", [("opt", 64000), ("baseline", 16000), ("offload", 256000)])
+def test_report_kv_identical(ref, policy, latency):
+    """report.kv of our run (ds_report_kv) is byte-identical to the reference's report_to_kv
+    (src/sweep.cpp:146-195) of the same cell."""
+    path = os.path.join(REF_CONFIGS, "reference_8stage.json")
+    txt = open(path).read()
+    rep = pl.sim_config(txt, REF_CONFIGS, policy=policy, latency_us=latency)
+    plan = pl.plan_config(txt, REF_CONFIGS, policy=policy, latency_us=latency)
+    assert pl.report_kv(rep, plan, latency, policy) == ref.report_kv(txt, REF_CONFIGS, policy, latency)
+
+
+def test_sweep_csv_identical(ref):
+    """sweep.csv of our latency x policy matrix (ds_sweep_csv) is byte-identical to the reference's
+    run_sweep(...).to_csv() (src/sweep.cpp:68-82,101-144)."""
+    path = os.path.join(REF_CONFIGS, "reference_8stage.json")
+    txt = open(path).read()
+    lats = json.loads(txt)["sweep"]["latencies_us"]
+    pols = ["baseline", "offload", "opt"]
+    tput = [[pl.sim_config(txt, REF_CONFIGS, policy=p, latency_us=l)["output_throughput"] for l in lats]
+            for p in pols]
+    assert pl.sweep_csv(lats, pols, tput) == ref.sweep_csv(txt, REF_CONFIGS)
