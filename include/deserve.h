@@ -162,6 +162,11 @@ ds_status ds_kv_ready(ds_stage* stage, int32_t mb, const ds_row* rows, int64_t n
 ds_status ds_swap_in(ds_stage* stage, int32_t mb, int32_t slot, int64_t plan_bytes,
                      int64_t* moved_in, int64_t* moved_out);
 
+/* Bytes of the last ds_swap_in: out4 = {refill into the global slot (compare with plan_bytes;
+ * <= plan + 1 page), migration into local pages freed by completions, eviction, page copies}.
+ * Copies move only the occupied tokens of a partial page (one 2D copy per page). */
+ds_status ds_swap_stats(ds_stage* stage, int64_t* out4);
+
 /* One stage step of microbatch mb over `rows`. act_in: first stage = device int32 ids sampled by
  * the previous circuit of this mb (NULL on its first circuit); other stages = device bf16
  * [T, d_model]. act_out: last stage = device int32 ids [R] (R = rows with need_logits); other

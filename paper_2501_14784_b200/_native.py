@@ -105,6 +105,7 @@ def _load() -> C.CDLL:
         "ds_schedule_config": (I32, [S, S, S, I64, I64, I64, P, C.c_size_t, P]),
         "ds_gpu_run_config": (I32, [S, S, S, I64, I64, P, P, P, C.c_size_t, P]),
         "ds_stage_step_events": (I32, [P, P, P, P]),
+        "ds_swap_stats": (I32, [P, P]),
         "ds_swap_events": (I32, [P, P, P, P, P]),
         "ds_stage_logits_device": (I32, [P, P, P]),
         "ds_session_trace": (I32, [P, S, I64, I32, I64, I64, P, C.c_size_t, P]),

@@ -43,6 +43,8 @@ struct MbKv {
     std::vector<int64_t> slot_req;
     std::vector<int32_t> host_free;
     std::vector<int32_t> host_dev;  // host page -> device page while resident, -1 otherwise
+    std::vector<int32_t> slot_tokens;  // per slot: KV positions written (steps enqueued so far)
+    std::vector<int32_t> host_slot, host_idx;  // host page -> (slot, page index in that slot)
     int resident_slot = -1;
     cudaEvent_t last_compute = nullptr;
     bool computed = false;
@@ -129,6 +131,7 @@ struct ds_stage {
     // last step
     int last_T = 0, last_R = 0;
     int64_t moved_in_total = 0, moved_out_total = 0;
+    int64_t last_swap[4] = {0, 0, 0, 0};  // last ds_swap_in: slot refill, migration, eviction bytes, copies
 };
 
 namespace {
@@ -405,6 +408,9 @@ ds_status ds_kv_reset(ds_stage* s) {
         k.host_free.clear();
         for (int h = s->host_pages - 1; h >= 0; --h) k.host_free.push_back(h);
         k.host_dev.assign(s->host_pages, -1);
+        k.slot_tokens.assign(s->max_slots, 0);
+        k.host_slot.assign(s->host_pages, -1);
+        k.host_idx.assign(s->host_pages, -1);
         k.resident_slot = -1;
         k.computed = false;
         k.prev_logit_slots.clear();
@@ -432,11 +438,32 @@ static void release_slot(ds_stage* s, MbKv& k, int slot) {
             if (k.host_dev[h] >= 0 && k.resident_slot >= 0)
                 s->gslot[k.resident_slot].free.push_back(k.host_dev[h]);
             k.host_dev[h] = -1;
+            k.host_slot[h] = k.host_idx[h] = -1;
             k.host_free.push_back(h);
         }
     }
     k.pages[slot].clear();
     k.slot_req[slot] = -1;
+    k.slot_tokens[slot] = 0;
+}
+
+// Occupied tokens of page j of a slot holding `tokens` KV positions.
+static int page_occupancy(int32_t tokens, int j) { return std::max(0, std::min(256, tokens - 256 * j)); }
+
+// Copies the occupied prefix (occ tokens) of every [layer][K|V][kv head] run of one page: a whole
+// page is one contiguous copy; a partial page is one 2D copy of L*2*n_kv rows of occ*d_head
+// elements (pitch 256 tokens) instead of the whole 256-token page.
+static cudaError_t copy_page(ds_stage* s, void* dst, const void* src, int occ, cudaMemcpyKind kind,
+                             cudaStream_t st, int64_t* bytes) {
+    const size_t run = size_t(256) * s->m.d_head * 2;
+    if (occ >= 256 || occ <= 0) {
+        *bytes += s->page_bytes;
+        return cudaMemcpyAsync(dst, src, size_t(s->page_bytes), kind, st);
+    }
+    const size_t rows = size_t(s->L) * 2 * s->m.n_kv_heads;
+    const size_t w = size_t(occ) * s->m.d_head * 2;
+    *bytes += int64_t(w * rows);
+    return cudaMemcpy2DAsync(dst, run, src, run, w, rows, kind, st);
 }
 
 ds_status ds_kv_release(ds_stage* s, int32_t mb, int32_t slot) {
@@ -498,7 +525,7 @@ ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, 
     (void)plan_bytes;
     if (!s || mb < 0 || mb >= s->n_mb || slot < 0 || slot > 1) return ds_fail(DS_ERR_ARG, "bad swap");
     CK(cudaSetDevice(s->device));
-    int64_t in = 0, outb = 0;
+    int64_t in = 0, outb = 0, migrated = 0, n_copies = 0;
     MbKv& k = s->mbs[mb];
     GlobalSlot& gs = s->gslot[slot];
     // host pages of mb written by an eviction in an earlier call (this call's: host_done below);
@@ -536,15 +563,16 @@ ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, 
         }
         for (int h = 0; h < s->host_pages; ++h) {
             if (o.host_dev[h] < 0) continue;
-            CK(cudaMemcpyAsync(host_page_ptr(s, owner, h), dev_page_ptr(s, o.host_dev[h]),
-                               s->page_bytes, cudaMemcpyDeviceToHost, s->d2h));
+            const int occ = o.host_slot[h] >= 0 ? page_occupancy(o.slot_tokens[o.host_slot[h]], o.host_idx[h]) : 256;
+            CK(copy_page(s, host_page_ptr(s, owner, h), dev_page_ptr(s, o.host_dev[h]), occ,
+                         cudaMemcpyDeviceToHost, s->d2h, &outb));
+            ++n_copies;
             cudaEvent_t e = next_event();
             if (!e) return ds_fail(DS_ERR_RUNTIME, "swap event creation failed");
             CK(cudaEventRecord(e, s->d2h));
             dev_done[o.host_dev[h]] = n_ev - 1;
             if (owner == mb) host_done[h] = n_ev - 1;
             o.host_dev[h] = -1;
-            outb += s->page_bytes;
         }
         if (!o.evicted) CK(cudaEventCreateWithFlags(&o.evicted, cudaEventDisableTiming));
         CK(cudaEventRecord(o.evicted, s->d2h));
@@ -579,28 +607,32 @@ ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, 
     if (tev[0]) CK(cudaEventRecord(tev[0], s->h2d));  // in0: refill start
     // 2. bring mb's host pages in: migrate into free local pages first, then the slot
     for (int sl = 0; sl < s->max_slots; ++sl)
-        for (int32_t& hnd : k.pages[sl]) {
+        for (size_t j = 0; j < k.pages[sl].size(); ++j) {
+            int32_t& hnd = k.pages[sl][j];
             if (hnd >= 0) continue;
             const int h = -hnd - 1;
             if (k.host_dev[h] >= 0) continue;  // already resident here
+            const int occ = page_occupancy(k.slot_tokens[sl], int(j));
             if (!k.local_free.empty()) {
+                // a local page freed by a completion: the page migrates back for good
                 const int p = k.local_free.back();
                 k.local_free.pop_back();
                 if ((st = wait_for(p, h))) return st;
-                CK(cudaMemcpyAsync(dev_page_ptr(s, p), host_page_ptr(s, mb, h), s->page_bytes,
-                                   cudaMemcpyHostToDevice, s->h2d));
+                CK(copy_page(s, dev_page_ptr(s, p), host_page_ptr(s, mb, h), occ, cudaMemcpyHostToDevice,
+                             s->h2d, &migrated));
                 k.host_free.push_back(h);
+                k.host_slot[h] = k.host_idx[h] = -1;
                 hnd = p;
             } else {
                 if (gs.free.empty()) return ds_fail(DS_ERR_RUNTIME, "global slot overflow");
                 const int p = gs.free.back();
                 gs.free.pop_back();
                 if ((st = wait_for(p, h))) return st;
-                CK(cudaMemcpyAsync(dev_page_ptr(s, p), host_page_ptr(s, mb, h), s->page_bytes,
-                                   cudaMemcpyHostToDevice, s->h2d));
+                CK(copy_page(s, dev_page_ptr(s, p), host_page_ptr(s, mb, h), occ, cudaMemcpyHostToDevice,
+                             s->h2d, &in));
                 k.host_dev[h] = p;
             }
-            in += s->page_bytes;
+            ++n_copies;
         }
     if (tev[1]) CK(cudaEventRecord(tev[1], s->h2d));  // in1: refill end
     gs.owner = mb;
@@ -609,9 +641,13 @@ ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, 
     // are handed to this microbatch's appends. Enqueued after the copies, so they still overlap.
     CK(cudaStreamWaitEvent(s->h2d, s->ev_d2h, 0));
     CK(cudaEventRecord(s->ev_h2d, s->h2d));
-    s->moved_in_total += in;
+    s->moved_in_total += in + migrated;
     s->moved_out_total += outb;
-    if (moved_in) *moved_in = in;
+    s->last_swap[0] = in;
+    s->last_swap[1] = migrated;
+    s->last_swap[2] = outb;
+    s->last_swap[3] = n_copies;
+    if (moved_in) *moved_in = in + migrated;
     if (moved_out) *moved_out = outb;
     return DS_OK;
 }
@@ -638,6 +674,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
         }
         auto& pg = k.pages[r.slot];
         const int64_t need = page_count_for(r.pos + r.n_tok);
+        k.slot_tokens[r.slot] = std::max(k.slot_tokens[r.slot], r.pos + r.n_tok);
         while (int64_t(pg.size()) < need) {
             if (!k.local_free.empty()) {
                 pg.push_back(k.local_free.back());
@@ -649,6 +686,8 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
                 const int p = s->gslot[k.resident_slot].free.back();
                 s->gslot[k.resident_slot].free.pop_back();
                 k.host_dev[h] = p;
+                k.host_slot[h] = r.slot;
+                k.host_idx[h] = int32_t(pg.size());
                 pg.push_back(-(h + 1));
             } else {
                 return ds_fail(DS_ERR_PLAN, "KV pool exhausted for microbatch " + std::to_string(mb));
@@ -968,6 +1007,12 @@ ds_status ds_stage_output(ds_stage* s, void** ptr, int64_t* bytes, int64_t* n_ou
         if (bytes) *bytes = int64_t(s->last_T) * s->m.d_model * 2;
         if (n_out) *n_out = s->last_T;
     }
+    return DS_OK;
+}
+
+ds_status ds_swap_stats(ds_stage* s, int64_t* out4) {
+    if (!s || !out4) return ds_fail(DS_ERR_ARG, "null argument");
+    for (int i = 0; i < 4; ++i) out4[i] = s->last_swap[i];
     return DS_OK;
 }
 

@@ -533,7 +533,9 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     w.moved_in += mi;
                     w.moved_out += mo;
                     w.plan_in += op.plan_bytes;
-                    w.swap_pairs.push_back({op.plan_bytes, mi, mo});
+                    int64_t sw[4] = {0, 0, 0, 0};
+                    DK(ds_swap_stats(w.st, sw));
+                    w.swap_pairs.push_back({op.plan_bytes, sw[0], sw[1], sw[2]});
                     continue;
                 }
                 const int64_t c = op.circuit;
@@ -883,6 +885,8 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
         launches1 += l;
         res.stages.push_back(std::move(st));
         res.swaps.push_back(w.swap_pairs);
+        const StagePlanD& sp = S->plan.stages[w.idx];
+        res.page_bytes.push_back(page_size(S->cfg.model, sp.layer_end - sp.layer_begin, S->cfg.model.num_layers));
     }
     // host -> device bytes of the run: every step's row metadata (kernel_stats "h2d_bytes")
     for (const auto& st : res.stages) {
@@ -1067,12 +1071,14 @@ std::string GpuRunResult::to_json() const {
     os << "{\"circuits\":" << circuits << ",\"decode_tokens\":" << decode_tokens << ",\"rows\":" << rows
        << ",\"wall_us\":" << wall_us << ",\"device_us\":" << device_us << ",\"launches\":" << launches
        << ",\"d2h_bytes\":" << d2h_bytes << ",\"h2d_bytes\":" << h2d_bytes
-       << ",\"swap_wait_us\":" << swap_wait_us << ",\"swap_pairs\":[";
+       << ",\"swap_wait_us\":" << swap_wait_us << ",\"page_bytes\":[";
+    for (size_t i = 0; i < page_bytes.size(); ++i) os << (i ? "," : "") << page_bytes[i];
+    os << "],\"swap_pairs\":[";  // per stage: [plan, slot refill, migration, eviction] per swap-in
     for (size_t i = 0; i < swaps.size(); ++i) {
         os << (i ? ",[" : "[");
         for (size_t k = 0; k < swaps[i].size(); ++k)
-            os << (k ? ",[" : "[") << swaps[i][k].plan << "," << swaps[i][k].moved_in << ","
-               << swaps[i][k].moved_out << "]";
+            os << (k ? ",[" : "[") << swaps[i][k].plan << "," << swaps[i][k].slot_in << ","
+               << swaps[i][k].migrated << "," << swaps[i][k].moved_out << "]";
         os << "]";
     }
     os << "],\"tokens_per_s\":"

@@ -32,8 +32,8 @@ struct StageRunStats {
     std::string kernel_stats;                       // ds_stage_kernel_stats JSON
 };
 
-struct SwapPair {
-    int64_t plan = 0, moved_in = 0, moved_out = 0;
+struct SwapPair {  // one schedule swap-in: plan bytes vs what moved (ds_swap_stats)
+    int64_t plan = 0, slot_in = 0, migrated = 0, moved_out = 0;
 };
 
 struct GpuRunResult {
@@ -41,6 +41,7 @@ struct GpuRunResult {
     int64_t launches = 0, d2h_bytes = 0, h2d_bytes = 0;
     int64_t swap_wait_us = 0;  // measured: GPU time computes waited for their swap-ins
     std::vector<std::vector<SwapPair>> swaps;  // per stage: every schedule swap-in, plan vs moved
+    std::vector<int64_t> page_bytes;           // per stage
     std::vector<StageRunStats> stages;
     std::vector<std::vector<int32_t>> tokens;  // per circuit: sampled ids of its need_logits rows
     std::string error;

@@ -83,3 +83,39 @@ def test_swap_round_trips_bit_exact(cycles):
     for a, b in zip(ref, got):
         assert torch.isfinite(a.float()).all()
         assert torch.equal(a, b)
+
+
+def test_refill_after_release_waits_for_the_occupants_step():
+    """the occupant of a global slot runs a step, then releases a slot-backed request
+    (its pages go back to the slot's free list without an eviction copy), and another
+    microbatch is swapped into that slot before anything syncs: the refill must wait for the
+    occupant's step, so the refilled microbatch computes exactly as without swapping."""
+    torch.cuda.init()
+    ref, _ = _run(False)
+    md = pl.model_desc(DIMS)
+    st = C.c_void_p()
+    nat.check(nat.lib.ds_stage_create(0, C.byref(md), 0, LAYERS, 1, 0, 11, 2048, 4, C.byref(st)))
+    try:
+        nat.check(nat.lib.ds_kv_create(st, PAGE, 2, PAGE, 12 * PAGE, 12 * PAGE))
+        mi, mo = C.c_int64(), C.c_int64()
+        for mb in (1, 0):  # mb 1 filled first and evicted when mb 0 takes slot 0
+            nat.check(nat.lib.ds_swap_in(st, mb, 0, 0, C.byref(mi), C.byref(mo)))
+            spec = [(s, 0, n, r + mb) for s, n, r in FILL]
+            nat.check(nat.lib.ds_stage_step(st, mb, _rows(spec), len(spec), None, None))
+        # mb 0: one more step, then its slot-backed request in slot 0 completes
+        spec = [(0, 600, 8, 0)]
+        nat.check(nat.lib.ds_stage_step(st, 0, _rows(spec), 1, None, None))
+        nat.check(nat.lib.ds_kv_release(st, 0, 0))
+        # mb 1 back into slot 0 (freed pages of mb 0 are refilled) with no sync in between
+        nat.check(nat.lib.ds_swap_in(st, 1, 0, 0, C.byref(mi), C.byref(mo)))
+        spec = [(s, n, 8, r + 1) for s, n, r in FILL]
+        T = sum(x[2] for x in spec)
+        out = torch.empty(T, DIMS["d_model"], dtype=torch.bfloat16, device="cuda")
+        nat.check(nat.lib.ds_stage_step(st, 1, _rows(spec), len(spec), None, C.c_void_p(out.data_ptr())))
+        nat.check(nat.lib.ds_stage_sync(st))
+        assert torch.equal(out, ref[0])
+        stats = (C.c_int64 * 4)()
+        nat.check(nat.lib.ds_swap_stats(st, stats))
+        assert stats[0] > 0  # mb 1's host pages came back through the slot
+    finally:
+        nat.lib.ds_stage_destroy(st)

@@ -113,6 +113,12 @@ def main():
                  "moved_out_bytes": sum(s["swap_out_bytes"] for s in gpu["stages"]),
                  "topups": sum(s["topups"] for s in gpu["stages"]),
                  "schedule_swap_ins": sum(len(x) for x in gpu["swap_pairs"]),
+                 # per schedule swap-in: slot refill vs the plan's bytes (H4: <= plan + 1 page)
+                 "refill_over_plan_plus_page": sum(1 for st, pg in zip(gpu["swap_pairs"], gpu["page_bytes"])
+                                                   for x in st if x[1] > x[0] + pg),
+                 "refill_bytes": sum(x[1] for st in gpu["swap_pairs"] for x in st),
+                 "migrated_bytes": sum(x[2] for st in gpu["swap_pairs"] for x in st),
+                 "evicted_bytes": sum(x[3] for st in gpu["swap_pairs"] for x in st),
                  "measured_swap_wait_us": gpu["swap_wait_us"]},
         "per_stage": [{"device": s["device"], "computes": s["computes"], "busy_ms": round(s["busy_ms"], 1),
                        "swap_plan_bytes": s["swap_plan_bytes"], "swap_in_bytes": s["swap_in_bytes"],
