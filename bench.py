@@ -236,7 +236,7 @@ def run_single(args):
     from paper_2501_14784_b200 import pipeline as pl
     cfg_path = os.path.join(CONFIGS, "llama8b_1stage.json")
     txt = open(cfg_path).read()
-    sess = pl.Session(txt, CONFIGS, n_devices=1, real_delay=True)
+    sess = pl.Session(txt, CONFIGS, n_devices=1, real_delay=True, trace=True)
     try:
         for _ in range(args.warmup):
             sess.run()
@@ -244,6 +244,9 @@ def run_single(args):
         with ClockSampler([0]) as clk:
             for _ in range(args.steps):
                 runs.append(sess.run(collect_tokens=True))
+        # the last timed run as the reference's SimResult: real-clock trace + SimReport
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        hw_report = sess.trace(os.path.join(ROOT, "gpurun_out", "bench_n1.trace"))
         prof = sess.run(profile=True)
     finally:
         sess.close()
@@ -267,6 +270,11 @@ def run_single(args):
                 "h2d_bytes_per_step": int(h2d / max(len(runs), 1)) if h2d else None,
                 "d2h_bytes_per_step": runs[0]["d2h_bytes"]},
         "gpu_launches": sum(r["launches"] for r in runs),
+        "report": {"desc": "SimReport of the last timed run from its real-clock EventTrace "
+                           "(ds_session_trace; window = [0, run end): the offline batch's makespan)",
+                   **{k: hw_report[k] for k in ("output_tokens", "output_throughput", "window_end_us",
+                                                 "mean_bubble_fraction", "completed_requests",
+                                                 "trace_events")}},
         "roofline": rf,
         "clocks": clk.summary(),
     }

@@ -1,56 +1,41 @@
-"""N>1 leg of bench.py: one process per GPU (torchrun), stage r on GPU r, NCCL hops.
+"""N>1 leg of bench.py: one process per GPU (torchrun), pipeline stage r on GPU r, NCCL hops.
 
-Workload: Llama-3-8B cut into N pipeline stages (32/N layers each, reference partition_layers),
-100 ms injected latency per hop, 32 microbatches with KV swap enabled (BASELINE configs[2] at
-N=4), §5 prompts [0,512] x [0,512], 4096-token prefill chunk. A step replays the first `rounds` circuits of every
-microbatch of the reference schedule from empty KV pools. value = generated tokens / max over
-ranks of the step's CUDA-event time on the stage stream (idle waits for delayed hops included);
-e2e = same on the host clock around the C-ABI call.
+Workload: BASELINE configs[2] as written -- configs/llama8b_4stage_swap.json (Llama-3-8B, 4
+stages of 8 layers, 100 ms injected latency per hop, 32 microbatches, KV swap on with the
+swap-forcing prompts: 3840-token prompts, 256 generated tokens, prefill_chunk 16384). At N = 2 / 8
+the same document with N nodes (same per-node memory, calibration, link and scheduler settings;
+the reference planner re-partitions the 32 layers). No field is rewritten and no circuit cap is
+applied: the timed run executes every circuit the reference schedule starts before the workload's
+bench_duration_s.
+
+Metric = the reference's own (SimReport.output_throughput, sim.cpp:510; windowed_stats,
+workload.cpp:82-116): decode tokens at last-stage circuit ends inside [warmup_s, duration) of the
+hardware run's real-clock EventTrace (every rank writes its stage's events on the shared host
+steady clock; rank 0 merges them, ds_trace_merge) / window length. `steps` = K equal sub-windows
+of that window (ms_per_step = window / K); warm-up = W runs of a short schedule prefix (two
+circuits per microbatch) from empty KV pools before the measured run. e2e = all decode tokens of
+the measured run / host wall time of its ds_session_run call (prefill transient from empty pools
+included, sampled ids copied to host every circuit).
 """
+import ctypes as C
 import json
 import os
-import statistics
 
 CONFIGS = os.path.join(os.path.dirname(os.path.abspath(__file__)), "configs")
 METRIC = "generated tokens/sec (whole pipeline) at injected inter-stage latency; roofline fraction"
+BASE_CONFIG = "llama8b_4stage_swap.json"
 
 
-def pipeline_config(n_stages, latency_us=100_000, nb=32):
-    cfg = json.load(open(os.path.join(CONFIGS, "llama8b_4stage.json")))
+def pipeline_config(n_stages, name=BASE_CONFIG, latency_us=None):
+    """The config document with n_stages nodes (identical node/link/scheduler fields)."""
+    cfg = json.load(open(os.path.join(CONFIGS, name)))
     node = cfg["nodes"][0]
     cfg["nodes"] = [dict(node, node_id=f"g{i}") for i in range(n_stages)]
     link = cfg["links"][0]
-    cfg["links"] = [dict(link, src=f"g{i}", dst=f"g{(i + 1) % n_stages}", latency_us=latency_us)
+    cfg["links"] = [dict(link, src=f"g{i}", dst=f"g{(i + 1) % n_stages}",
+                         latency_us=link["latency_us"] if latency_us is None else latency_us)
                     for i in range(n_stages)]
-    cfg["scheduler"]["nb_override"] = nb
-    # a 4096-token prefill chunk per circuit: with the reference default (256) the 32 x B requests
-    # admitted at t=0 need ~B circuits of prefill per microbatch before decode dominates
-    cfg["scheduler"]["prefill_chunk"] = 4096
     return cfg
-
-
-def steady_window(cfg_txt, n_circ, world, runs_steps):
-    """Reference metric semantics (SimReport.output_throughput, sim.cpp:510; windowed_stats,
-    workload.cpp:82-116): decode tokens counted at the last stage's compute ends inside the
-    measurement window / window length. The window starts after the first third of the last
-    stage's computes (the prefill transient from empty KV pools: warm-up), on the GPU event clock
-    of the last stage."""
-    from paper_2501_14784_b200 import pipeline as pl
-    sched = pl.schedule_config(cfg_txt, CONFIGS, max_circuits=n_circ)
-    order = [op[3] for op in sched["ops"][world - 1] if op[0] == 0 and 0 <= op[3] < n_circ]
-    n_dec = [c["n_decode"] for c in sched["circuits"]]
-    rates = []
-    for steps in runs_steps:
-        n = min(len(steps), len(order))
-        k0 = n // 3
-        toks = sum(n_dec[order[k]] for k in range(k0, n))
-        ms = steps[n - 1][3] - steps[k0 - 1][3]
-        rates.append(toks / (ms / 1e3))
-    return {"tokens_per_s": sum(rates) / len(rates),
-            "desc": "steady state: decode tokens of the last stage's computes after the first third "
-                    "(warm-up from empty KV pools excluded, as the reference's windowed metric) over "
-                    "that window on the last stage's GPU event clock; step_tokens_per_s counts the "
-                    "whole step"}
 
 
 def run_multi(args):
@@ -58,7 +43,6 @@ def run_multi(args):
 
     from bench import ClockSampler, roofline
     from paper_2501_14784_b200 import pipeline as pl
-    import ctypes as C
     from paper_2501_14784_b200._native import GpuOpts, check, lib
 
     rank = int(os.environ.get("RANK", "0"))
@@ -80,80 +64,110 @@ def run_multi(args):
 
     cfg = pipeline_config(world)
     txt = json.dumps(cfg)
-    plan = json.loads(pl.plan_config(txt, CONFIGS))
+    plan_txt = pl.plan_config(txt, CONFIGS)
+    plan = json.loads(plan_txt)
     nb = plan["n_microbatches"]
-    rounds = 30
     md = pl.model_desc("llama3-8b")
-    opts = GpuOpts(device0=local, n_devices=1, real_delay=1, collect_tokens=0,
-                   max_circuits=nb * rounds, weight_seed=pl.WEIGHT_SEED)
+    opts = GpuOpts(device0=local, n_devices=1, real_delay=1, collect_tokens=0, max_circuits=0,
+                   weight_seed=pl.WEIGHT_SEED, trace=1)
     h = C.c_void_p()
     check(lib.ds_session_create_rank(txt.encode(), CONFIGS.encode(), b"", -1, -1, C.byref(md),
                                      C.byref(opts), rank, world, id_buf, C.byref(h)))
+    out_dir = os.path.join(os.path.dirname(CONFIGS), "gpurun_out", f"bench_n{world}")
+    os.makedirs(out_dir, exist_ok=True)
 
-    def run(profile=False):
-        cap = 1 << 24
+    def run(profile=False, collect=False):
+        cap = 1 << 26
         out = C.create_string_buffer(cap)
-        check(lib.ds_session_run(h, int(profile), 0, out, cap, None))
+        check(lib.ds_session_run(h, int(profile), int(collect), out, cap, None))
         return json.loads(out.value.decode())
 
+    t0 = C.c_int64(0)
     try:
+        check(lib.ds_session_limit(h, 2 * nb, None))
         for _ in range(args.warmup):
             dist.barrier()
             run()
-        runs = []
-        with ClockSampler([local]) as clk:
-            for _ in range(args.steps):
-                dist.barrier()
-                runs.append(run())
+        check(lib.ds_session_limit(h, 0, None))
         dist.barrier()
+        with ClockSampler([local]) as clk:
+            r = run(collect=True)
+        check(lib.ds_session_limit(h, 0, C.byref(t0)))
+        starts = [None] * world
+        dist.all_gather_object(starts, t0.value)
+        origin = min(starts)
+        trace = os.path.join(out_dir, f"rank{rank}.trace")
+        need = C.c_size_t(0)
+        check(lib.ds_session_trace(h, trace.encode(), origin, 1, 0, 1, None, 0, C.byref(need)))
+        dist.barrier()
+        check(lib.ds_session_limit(h, 2 * nb, None))
         prof = run(profile=True)
     finally:
         dist.barrier()
         lib.ds_session_destroy(h)
-    dev = [r["device_us"] for r in runs]
-    wall = [r["wall_us"] for r in runs]
-    window = None
-    if rank == world - 1:
-        window = steady_window(txt, nb * rounds, world, [r["stages"][0]["steps"] for r in runs])
     gathered = [None] * world
-    dist.all_gather_object(gathered, {"dev": dev, "wall": wall, "clk": clk.summary(), "window": window,
+    dist.all_gather_object(gathered, {"wall_us": r["wall_us"], "clk": clk.summary(),
                                       "kernels": prof["stages"][0]["kernels"],
-                                      "launches": sum(r["launches"] for r in runs),
-                                      "stage": prof["stages"][0]})
+                                      "launches": r["launches"], "stage": r["stages"][0],
+                                      "d2h": r["d2h_bytes"], "h2d": r["h2d_bytes"],
+                                      "swap_wait_us": r["swap_wait_us"],
+                                      "tokens": r["decode_tokens"], "circuits": r["circuits"],
+                                      "rows": r["rows"]})
     dist.destroy_process_group()
     if rank != 0:
         return None
-    dev_max = [max(g["dev"][i] for g in gathered) for i in range(args.steps)]
-    wall_max = [max(g["wall"][i] for g in gathered) for i in range(args.steps)]
-    toks = runs[0]["decode_tokens"]
+    merged = os.path.join(out_dir, "hw.trace")
+    pl.trace_merge([os.path.join(out_dir, f"rank{i}.trace") for i in range(world)], merged)
+    wl = cfg["workload"]
+    end_us = 0
+    for line in open(merged):
+        end_us = max(end_us, int(line.split()[0][2:]))
+    w0, w1 = wl["warmup_s"] * 10**6, min(wl["bench_duration_s"] * 10**6, end_us + 1)
+    rep = pl.trace_report(merged, world, w0, w1, wl["rng_seed"])
+    subs = []
+    for k in range(args.steps):  # K equal sub-windows of the measurement window
+        a = w0 + (w1 - w0) * k // args.steps
+        b = w0 + (w1 - w0) * (k + 1) // args.steps
+        subs.append(pl.trace_report(merged, world, a, b, wl["rng_seed"])["output_throughput"])
+    open(os.path.join(out_dir, "report.kv"), "w").write(
+        pl.report_kv(rep, plan_txt, cfg["links"][0]["latency_us"], "config"))
+    sim = pl.sim_config(txt, CONFIGS)
     clocks = gathered[0]["clk"]
     clocks["per_rank_sm_mhz"] = [g["clk"]["sm_mhz"] for g in gathered]
-    clocks["reasons"] = sorted({r for g in gathered for r in g["clk"]["reasons"]})
+    clocks["reasons"] = sorted({x for g in gathered for x in g["clk"]["reasons"]})
     rf = roofline(gathered[0]["kernels"])
     rf["rank"] = 0
-    win = gathered[world - 1]["window"]
-    step_tps = toks * args.steps / (sum(dev_max) / 1e6)
+    wall_max = max(g["wall_us"] for g in gathered)
+    last = gathered[world - 1]
     return {
-        "metric": METRIC, "value": round(win["tokens_per_s"], 2),
-        "step_tokens_per_s": round(step_tps, 2),
-        "window": win["desc"],
+        "metric": METRIC, "value": round(rep["output_throughput"], 2),
         "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(statistics.mean(dev_max) / 1e3, 3), "higher_is_better": True,
+        "ms_per_step": round((w1 - w0) / 1e3 / args.steps, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights, counter-RNG prompts; lengths from the reference "
                 "generator seed 42)",
         "config": {"workload": f"Llama-3-8B {world}-stage pipeline on {world}xB200, 100 ms injected "
-                               f"latency per hop, {nb} microbatches, KV swap enabled, first {rounds} "
-                               "circuits of every microbatch",
-                   "parallelism": f"pp{world}", "tokens_per_step": toks,
-                   "circuits_per_step": runs[0]["circuits"],
-                   "analytic_bound_tokens_per_s": pl.steady_state_throughput(json.dumps(plan)),
+                               f"latency per hop, {nb} microbatches, KV swap on (configs/{BASE_CONFIG} "
+                               f"with {world} nodes, as written)",
+                   "parallelism": f"pp{world}",
+                   "window_us": [w0, w1], "circuits": last["circuits"], "rows": last["rows"],
                    "hops": "NCCL send/recv over NVLink, one 2-rank communicator per ring link"},
-        "e2e": {"value": round(toks * args.steps / (sum(wall_max) / 1e6), 2), "unit": "tokens/s",
-                "h2d_bytes_per_step": None, "d2h_bytes_per_step": 0},
+        "window": "reference windowed_stats over [warmup_s, min(bench_duration_s, run end)) of the "
+                  "real-clock EventTrace (merged over ranks); steps = equal sub-windows",
+        "sub_window_tokens_per_s": [round(x, 1) for x in subs],
+        "report": {k: rep[k] for k in ("output_tokens", "output_throughput", "mean_bubble_fraction",
+                                        "swap_stall_us", "completed_requests")},
+        "reference_sim_tokens_per_s": sim["output_throughput"],
+        "analytic_bound_tokens_per_s": pl.steady_state_throughput(plan_txt),
+        "e2e": {"value": round(last["tokens"] / (wall_max / 1e6), 2), "unit": "tokens/s",
+                "h2d_bytes_per_step": sum(g["h2d"] for g in gathered),
+                "d2h_bytes_per_step": last["d2h"],
+                "desc": "all decode tokens of the measured run / host wall time of ds_session_run "
+                        "(max over ranks; prefill transient included)"},
         "gpu_launches": sum(g["launches"] for g in gathered),
         "roofline": rf, "clocks": clocks,
         "per_rank": [{"device_ms": g["stage"]["device_ms"], "busy_ms": g["stage"]["busy_ms"],
-                      "swap_in_bytes": g["stage"]["swap_in_bytes"], "topups": g["stage"]["topups"]}
-                     for g in gathered],
+                      "swap_plan_bytes": g["stage"]["swap_plan_bytes"],
+                      "swap_in_bytes": g["stage"]["swap_in_bytes"], "topups": g["stage"]["topups"],
+                      "swap_wait_us": g["swap_wait_us"]} for g in gathered],
     }

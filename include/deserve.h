@@ -239,6 +239,10 @@ ds_status ds_session_destroy(ds_session* session);
 ds_status ds_session_trace(ds_session* session, const char* trace_path, int64_t t0_us,
                            int32_t keep_virtual_seq, int64_t w0_us, int64_t w1_us, char* report_json,
                            size_t cap, size_t* needed);
+/* Later runs execute only the first max_circuits circuits of the prefix prepared at creation
+ * (0 = all of it: warm-up runs on a short prefix, then the measured run). *t0_us (may be NULL)
+ * receives the host steady-clock start of the last run (ranks agree on a common trace origin). */
+ds_status ds_session_limit(ds_session* session, int64_t max_circuits, int64_t* t0_us);
 /* Merges per-rank traces (each sorted, virtual seq kept) into one trace in (time, seq) order with
  * seq renumbered as the line index. */
 ds_status ds_trace_merge(const char* const* paths, int32_t n_paths, const char* out_path);

@@ -140,6 +140,27 @@ class Ref:
         return out[0], out[1]
 
 
+BINDING_SO = os.path.join(HERE, "_ref", "libb200_binding.so")
+
+
+def binding_run_and_check(config_text: str, config_dir: str, plan_json: str, model_desc, gpu_opts,
+                          trace_path: str) -> dict:
+    """integration/run_on_b200.cpp -- the reference-side binding compiled against the reference
+    headers -- runs the config on the GPU (ds_run) into a pipesim::SimResult and applies the
+    reference's replay_check / windowed_stats to it in C++. Raises RefError with the binding's
+    message (e.g. the product's "no CUDA device" on a CPU box)."""
+    lib = C.CDLL(BINDING_SO)
+    lib.b200_run_and_check.argtypes = [C.c_char_p] * 3 + [C.c_void_p] * 2 + [C.c_char_p, C.c_void_p,
+                                                                           C.c_size_t]
+    lib.b200_run_and_check.restype = C.c_int
+    buf = C.create_string_buffer(1 << 16)
+    rc = lib.b200_run_and_check(_b(config_text), _b(config_dir), _b(plan_json), C.byref(model_desc),
+                                C.byref(gpu_opts), _b(trace_path), buf, len(buf))
+    if rc != 0:
+        raise RefError(buf.value.decode())
+    return json.loads(buf.value.decode())
+
+
 class LrModel(C.Structure):
     _fields_ = [("n_layers", C.c_int32), ("d_model", C.c_int32), ("n_heads", C.c_int32),
                 ("n_kv_heads", C.c_int32), ("d_head", C.c_int32), ("ffn", C.c_int32),

@@ -113,6 +113,7 @@ def _load() -> C.CDLL:
         "ds_trace_report": (I32, [S, I64, I64, I64, C.c_uint64, P, C.c_size_t]),
         "ds_run": (I32, [S, S, S, I64, I64, P, P, S, P, C.c_size_t, P]),
         "ds_session_capture": (I32, [P, P, I64]),
+        "ds_session_limit": (I32, [P, I64, P]),
         "ds_report_kv": (I32, [S, S, I64, S, P, C.c_size_t, P]),
         "ds_sweep_csv": (I32, [P, I32, S, P, P, C.c_size_t, P]),
         "ds_session_captured": (I32, [P, P, P, I64, P]),

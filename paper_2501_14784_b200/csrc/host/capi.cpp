@@ -417,6 +417,15 @@ ds_status ds_sweep_csv(const int64_t* lat, int32_t n_lat, const char* policies, 
     });
 }
 
+ds_status ds_session_limit(ds_session* h, int64_t max_circuits, int64_t* t0_us) {
+    return guarded([&] {
+        if (!h || !h->s) return ds_fail(DS_ERR_ARG, "null session");
+        dsb::session_limit(h->s, max_circuits);
+        if (t0_us) *t0_us = dsb::session_t0(h->s);
+        return DS_OK;
+    });
+}
+
 ds_status ds_session_capture(ds_session* h, const int64_t* reqs, int64_t n) {
     return guarded([&] {
         if (!h || !h->s || (n > 0 && !reqs)) return ds_fail(DS_ERR_ARG, "bad capture arguments");

@@ -151,6 +151,7 @@ struct Session {
     ds_model_desc md{};
     GpuOptions opt;
     int64_t n_circ = 0, max_rows = 16, B = 1;
+    int64_t n_circ_all = 0;  // circuits prepared at creation; runs execute the first n_circ
     std::vector<int64_t> prev;
     std::vector<Worker> W;
     int32_t* tok_pool = nullptr;
@@ -247,6 +248,7 @@ Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, con
         for (const auto& r : circs[c].rows) max_slot = std::max<int64_t>(max_slot, r.slot + 1);
     }
     S->max_rows = (S->max_rows + 15) / 16 * 16;
+    S->n_circ_all = S->n_circ;
     S->B = std::min<int64_t>(plan.B(), max_slot);
     S->prev.assign(S->n_circ, -1);
     {
@@ -917,6 +919,9 @@ GpuRunResult run_on_gpus(const Config& cfg, const Plan& plan, const Schedule& sc
     return r;
 }
 
+void session_limit(Session* S, int64_t max_circuits) {
+    S->n_circ = max_circuits > 0 ? std::min(max_circuits, S->n_circ_all) : S->n_circ_all;
+}
 int64_t session_t0(Session* S) { return S->t0; }
 int64_t session_end(Session* S) { return S->t_end - S->t0; }
 const Config& session_config(Session* S) { return S->cfg; }

@@ -63,6 +63,8 @@ void session_destroy(Session* s);
 // stages this process runs and of the executed schedule prefix. t0_us: the steady-clock origin
 // (< 0: this run's start). renumber = false keeps the virtual seq (for merging rank traces).
 std::vector<Record> session_trace(Session* s, int64_t t0_us, bool renumber);
+// later runs execute only the first max_circuits of the prepared prefix (0 = all of it)
+void session_limit(Session* s, int64_t max_circuits);
 int64_t session_t0(Session* s);  // steady-clock us of the last run's start
 int64_t session_end(Session* s);  // us from t0 to the last run's end
 const Config& session_config(Session* s);

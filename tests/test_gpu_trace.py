@@ -106,3 +106,20 @@ def test_hw_trace_tiny_swap_plan():
     assert n_swaps > 0
     print(f"swap trace: {n_swaps} schedule swap-ins, {len(viol)} bandwidth notes, "
           f"swap_stall_us {rep['swap_stall_us']}, measured swap wait {gpu['swap_wait_us']} us")
+
+
+def test_reference_binding_checks_hardware_run(tmp_path):
+    """integration/run_on_b200.cpp (the binding INTEGRATION.md shows, compiled against the
+    reference's sim.hpp/trace.hpp) returns a pipesim::SimResult of a GPU run; the reference's
+    replay_check finds nothing and windowed_stats reproduces the report's N_O."""
+    import oracle
+    from paper_2501_14784_b200._native import GpuOpts
+    cfg = json.load(open(os.path.join(CDIR, "tiny_2stage.json")))
+    cfg["workload"]["warmup_s"] = 0
+    txt = json.dumps(cfg)
+    opts = GpuOpts(device0=0, n_devices=1, real_delay=1, collect_tokens=0, max_circuits=40,
+                   weight_seed=pl.WEIGHT_SEED, trace=1)
+    out = oracle.binding_run_and_check(txt, CDIR, pl.plan_config(txt, CDIR), pl.model_desc("tiny-llama"),
+                                       opts, str(tmp_path / "b.trace"))
+    assert out["violations"] == 0 and out["trace_events"] > 0
+    assert out["windowed_output_tokens"] == out["report_output_tokens"] > 0

@@ -366,3 +366,20 @@ def test_sweep_csv_identical(ref):
     tput = [[pl.sim_config(txt, REF_CONFIGS, policy=p, latency_us=l)["output_throughput"] for l in lats]
             for p in pols]
     assert pl.sweep_csv(lats, pols, tput) == ref.sweep_csv(txt, REF_CONFIGS)
+
+
+def test_reference_binding_links_and_maps_errors(tmp_path):
+    """The reference-side binding (integration/run_on_b200.cpp) compiles against the reference
+    headers and links both libraries; without a GPU the product's no-device error reaches the
+    caller as pipesim::SimError text (no CPU fallback)."""
+    import oracle
+    from paper_2501_14784_b200 import n_devices
+    from paper_2501_14784_b200._native import GpuOpts
+    if n_devices() > 0:
+        pytest.skip("GPU present: tests/test_gpu_trace.py runs the binding end to end")
+    txt = open(os.path.join(CONFIGS, "tiny_2stage.json")).read()
+    opts = GpuOpts(device0=0, n_devices=1, real_delay=1, collect_tokens=0, max_circuits=4,
+                   weight_seed=pl.WEIGHT_SEED, trace=1)
+    with pytest.raises(oracle.RefError, match="CUDA device"):
+        oracle.binding_run_and_check(txt, CONFIGS, pl.plan_config(txt, CONFIGS),
+                                     pl.model_desc("tiny-llama"), opts, str(tmp_path / "t.trace"))

@@ -46,56 +46,38 @@ def kernel_kinds(stages):
     return out
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("config")
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--circuits", type=int, default=0, help="executed schedule prefix (0 = all)")
-    ap.add_argument("--policy", default=None)
-    ap.add_argument("--latency-us", type=int, default=-1)
-    ap.add_argument("--no-profile", action="store_true")
-    ap.add_argument("--out", default=None)
-    a = ap.parse_args()
+def run_one(txt, cdir, policy=None, latency_us=-1, gpus=1, circuits=0, profile=True, out=None):
+    """Plan + schedule + execute one config document; returns the summary dict (and writes
+    hw.trace / report.kv / summary.json under `out` when given)."""
     import oracle
     from paper_2501_14784_b200 import pipeline as pl
-    cfg_path = os.path.abspath(a.config)
-    cdir = os.path.dirname(cfg_path)
-    txt = open(cfg_path).read()
-    name = os.path.basename(cfg_path).replace(".json", "")
-    if a.policy:
-        name += f"_{a.policy}"
-    if a.latency_us >= 0:
-        name += f"_{a.latency_us // 1000}ms"
-    out = a.out or os.path.join(ROOT, "gpurun_out", name)
-    os.makedirs(out, exist_ok=True)
-    plan = pl.plan_config(txt, cdir, policy=a.policy, latency_us=a.latency_us)
+    plan = pl.plan_config(txt, cdir, policy=policy, latency_us=latency_us)
     t0 = time.time()
-    sess = pl.Session(txt, cdir, policy=a.policy, latency_us=a.latency_us, n_devices=a.gpus,
-                      max_circuits=a.circuits, trace=True)
+    sess = pl.Session(txt, cdir, policy=policy, latency_us=latency_us, n_devices=gpus,
+                      max_circuits=circuits, trace=True)
     t_build = time.time() - t0
+    trace = os.path.join(out or "/tmp", "hw.trace")
     try:
         t0 = time.time()
         gpu = sess.run()
         wall = time.time() - t0
-        trace = os.path.join(out, "hw.trace")
         rep = sess.trace(trace)
-        prof = None if a.no_profile else sess.run(profile=True)
+        prof = sess.run(profile=True) if profile else None
     finally:
         sess.close()
-    lat = a.latency_us
+    lat = latency_us
     if lat < 0:
         links = json.loads(txt).get("links", [])
         lat = links[0]["latency_us"] if links else 0
-    kv = pl.report_kv(rep, plan, lat, a.policy or "config")
-    open(os.path.join(out, "report.kv"), "w").write(kv)
+    kv = pl.report_kv(rep, plan, lat, policy or "config")
     viol = oracle.Ref().replay_check(trace, plan)
     kinds = {}
     for v in viol:
         kinds[v.split()[0]] = kinds.get(v.split()[0], 0) + 1
     p = json.loads(plan)
     summary = {
-        "config": os.path.relpath(cfg_path, ROOT), "policy": a.policy, "latency_us": lat,
-        "gpus": a.gpus, "stages": len(p["stages"]), "n_microbatches": p["n_microbatches"],
+        "policy": policy, "latency_us": lat,
+        "gpus": gpus, "stages": len(p["stages"]), "n_microbatches": p["n_microbatches"],
         "batch_per_mb": p["stages"][0]["batch_size_per_microbatch"],
         "circuits": gpu["circuits"], "decode_tokens": gpu["decode_tokens"], "rows": gpu["rows"],
         "wall_s": round(wall, 3), "build_s": round(t_build, 1),
@@ -103,8 +85,8 @@ def main():
                                         "output_throughput", "mean_bubble_fraction",
                                         "swap_stall_us", "trace_events", "run_end_us")},
         "analytic_bound_tokens_per_s": pl.steady_state_throughput(plan),
-        "reference_sim": {k: v for k, v in pl.sim_config(txt, cdir, policy=a.policy,
-                                                        latency_us=a.latency_us).items()
+        "reference_sim": {k: v for k, v in pl.sim_config(txt, cdir, policy=policy,
+                                                        latency_us=latency_us).items()
                           if k in ("output_throughput", "output_tokens", "swap_stall_us",
                                    "mean_bubble_fraction")},
         "replay_check": {"violations": len(viol), "by_kind": kinds},
@@ -128,6 +110,33 @@ def main():
         summary["kernels"] = kernel_kinds(prof["stages"])
         summary["kernel_ms_total"] = round(sum(v["ms"] for k, v in summary["kernels"].items()
                                                if k != "swap_wait"), 1)
+    if out:
+        open(os.path.join(out, "report.kv"), "w").write(kv)
+        json.dump(summary, open(os.path.join(out, "summary.json"), "w"), indent=1)
+    return summary
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config")
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--circuits", type=int, default=0, help="executed schedule prefix (0 = all)")
+    ap.add_argument("--policy", default=None)
+    ap.add_argument("--latency-us", type=int, default=-1)
+    ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    cfg_path = os.path.abspath(a.config)
+    name = os.path.basename(cfg_path).replace(".json", "")
+    if a.policy:
+        name += f"_{a.policy}"
+    if a.latency_us >= 0:
+        name += f"_{a.latency_us // 1000}ms"
+    out = a.out or os.path.join(ROOT, "gpurun_out", name)
+    os.makedirs(out, exist_ok=True)
+    summary = run_one(open(cfg_path).read(), os.path.dirname(cfg_path), a.policy, a.latency_us,
+                      a.gpus, a.circuits, not a.no_profile, out)
+    summary["config"] = os.path.relpath(cfg_path, ROOT)
     json.dump(summary, open(os.path.join(out, "summary.json"), "w"), indent=1)
     print(json.dumps(summary))
 
