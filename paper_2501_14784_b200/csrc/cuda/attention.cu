@@ -13,6 +13,7 @@
 //
 // HBM roofline: each (row or block, kv head) reads its request's KV once: ctx * d_head * 2 (K,V)
 // * 2 B per kv head.
+#include <cuda.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -824,6 +825,242 @@ attn_decode_t_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t
     }
 }
 
+// TMA-staged variant of attn_decode_t_kernel (the default for d_head 64 / 128, G <= 8): each
+// warp's ring slots are filled by cp.async.bulk.tensor loads of its 16-token K and V chunks
+// (16 rows x 64 elements per box, 128-byte swizzle: conflict-free ldmatrix without padding)
+// completing on a per-slot mbarrier -- one elected lane issues 2 * DH/64 bulk copies per chunk
+// instead of 32 lanes x 16 cp.async, and the copy engine streams them. Same operand-swapped
+// MMAs, online softmax, warp merge and split merge as attn_decode_t_kernel.
+template <int DH, int ST>
+struct DecTmaSmem {
+    static constexpr int kBox = kDecChunk * 64;  // elements of one 16 x 64 box (2 KB)
+    static constexpr int kChunk = DH / 64 * kBox;
+    alignas(1024) __nv_bfloat16 k[kAttnWarps][ST][kChunk];
+    alignas(1024) __nv_bfloat16 v[kAttnWarps][ST][kChunk];
+    uint64_t bar[kAttnWarps][ST];
+};
+
+// byte offset of (row, 16-byte chunk c over the d_head elements) in a chunk of 64-element boxes
+DS_DEVICE uint32_t swz_off(int row, int c) {
+    return uint32_t((c >> 3) * (kDecChunk * 128) + row * 128 + (((c & 7) ^ (row & 7)) << 4));
+}
+
+DS_DEVICE void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int DH, int ST>
+__global__ void __launch_bounds__(kAttnWarps * 32)
+attn_decode_tma_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __nv_bfloat16* __restrict__ q,
+                       int n_h, const int32_t* __restrict__ row_pos,
+                       const int32_t* __restrict__ row_page_off, const int32_t* __restrict__ flat_pages,
+                       const int32_t* __restrict__ drows, KvLayout kv, int layer, int splits, int stride,
+                       __nv_bfloat16* __restrict__ o, float* __restrict__ ws, int* __restrict__ counters) {
+    pdl_launch_dependents();
+    extern __shared__ __align__(1024) uint8_t dec_smem_raw[];
+    DecTmaSmem<DH, ST>& sm = *reinterpret_cast<DecTmaSmem<DH, ST>*>(
+        (reinterpret_cast<uintptr_t>(dec_smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int KS = DH / 16;
+    constexpr uint32_t kChunkBytes = uint32_t(2 * kDecChunk * DH * 2);  // K + V
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        tma_prefetch_desc(&tmap_kv);
+#pragma unroll
+        for (int b = 0; b < ST; ++b) mbar_init(&sm.bar[warp][b], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    pdl_wait();
+    const int n_kv = kv.n_kv;
+    const int G = n_h / n_kv;
+    const int split = blockIdx.x % splits;
+    const int kvh = (blockIdx.x / splits) % n_kv;
+    const int t = drows[blockIdx.x / (splits * n_kv)];
+    const int g = lane >> 2, tq = lane & 3;
+    const int ctx = row_pos[t] + 1;
+    const int n_chunks = (ctx + kDecChunk - 1) / kDecChunk;
+    const int ch0 = split * n_chunks / splits, ch1 = (split + 1) * n_chunks / splits;
+    const int32_t* pages = flat_pages + row_page_off[t];
+
+    uint32_t qb[KS][2];
+    const float qs = rsqrtf(float(DH)) * 1.4426950408889634f;
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            float x0 = 0.f, x1 = 0.f;
+            if (g < G) {
+                const __nv_bfloat162 v2 = *reinterpret_cast<const __nv_bfloat162*>(
+                    q + (size_t(t) * n_h + kvh * G + g) * DH + kk * 16 + 2 * tq + 8 * i);
+                x0 = __bfloat162float(v2.x) * qs;
+                x1 = __bfloat162float(v2.y) * qs;
+            }
+            qb[kk][i] = pack2(x0, x1);
+        }
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+    float acc[KS][4];
+#pragma unroll
+    for (int j = 0; j < KS; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+
+    // TMA rows of token 0 of this (layer, kv head) K / V block within a page
+    const int row_k = (layer * 2 + 0) * n_kv + kvh;
+    const int row_v = (layer * 2 + 1) * n_kv + kvh;
+    const int rows_per_page = kv.n_layers * 2 * n_kv * 256;
+    const int my_n = ch1 - ch0 > warp ? (ch1 - ch0 - warp + kAttnWarps - 1) / kAttnWarps : 0;
+    auto load = [&](int j, int buf) {  // lane 0 only
+        const int tok0 = (ch0 + warp + j * kAttnWarps) * kDecChunk;
+        const int base = pages[tok0 >> 8] * rows_per_page + (tok0 & 255);
+        uint64_t* bar = &sm.bar[warp][buf];
+        fence_proxy_async_smem();  // generic reads / zero-fill of this slot precede the refill
+        mbar_arrive_expect_tx(bar, kChunkBytes);
+#pragma unroll
+        for (int bx = 0; bx < DH / 64; ++bx) {
+            tma_load_2d(&sm.k[warp][buf][bx * DecTmaSmem<DH, ST>::kBox], &tmap_kv, bar, bx * 64, base + row_k * 256);
+            tma_load_2d(&sm.v[warp][buf][bx * DecTmaSmem<DH, ST>::kBox], &tmap_kv, bar, bx * 64, base + row_v * 256);
+        }
+    };
+    if (lane == 0) {
+#pragma unroll
+        for (int j = 0; j < ST - 1; ++j)
+            if (j < my_n) load(j, j);
+    }
+    for (int j = 0; j < my_n; ++j) {
+        const int buf = j % ST;
+        if (lane == 0 && j + ST - 1 < my_n) load(j + ST - 1, (j + ST - 1) % ST);
+        mbar_wait(&sm.bar[warp][buf], uint32_t((j / ST) & 1));
+        const int tok0 = (ch0 + warp + j * kAttnWarps) * kDecChunk;
+        const int valid = min(kDecChunk, ctx - tok0);
+        const uint32_t kbase = smem_u32(&sm.k[warp][buf][0]);
+        const uint32_t vbase = smem_u32(&sm.v[warp][buf][0]);
+        if (valid < kDecChunk) {  // rows past the context: zero V (no 0 * garbage = NaN)
+            uint8_t* vb = reinterpret_cast<uint8_t*>(&sm.v[warp][buf][0]);
+            for (int i = lane; i < (kDecChunk - valid) * (DH / 8); i += 32) {
+                const int r = valid + i / (DH / 8), c = i % (DH / 8);
+                *reinterpret_cast<uint4*>(vb + swz_off(r, c)) = make_uint4(0, 0, 0, 0);
+            }
+            __syncwarp();
+        }
+        float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+            uint32_t a[4];
+            ldsm_x4(kbase + swz_off(lane & 15, kk * 2 + (lane >> 4)), a[0], a[1], a[2], a[3]);
+            mma16816(s, a, qb[kk][0], qb[kk][1]);
+        }
+        if (tok0 + g >= ctx) s[0] = s[1] = -INFINITY;
+        if (tok0 + g + 8 >= ctx) s[2] = s[3] = -INFINITY;
+        float mt[2] = {fmaxf(s[0], s[2]), fmaxf(s[1], s[3])};
+        float alpha[2];
+#pragma unroll
+        for (int hc = 0; hc < 2; ++hc) {
+            mt[hc] = fmaxf(mt[hc], __shfl_xor_sync(0xffffffffu, mt[hc], 4));
+            mt[hc] = fmaxf(mt[hc], __shfl_xor_sync(0xffffffffu, mt[hc], 8));
+            mt[hc] = fmaxf(mt[hc], __shfl_xor_sync(0xffffffffu, mt[hc], 16));
+            const float mn = fmaxf(m_run[hc], mt[hc]);
+            alpha[hc] = mn == -INFINITY ? 1.f : exp2f(m_run[hc] - mn);
+            m_run[hc] = mn;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s[e] = m_run[e & 1] == -INFINITY ? 0.f : exp2f(s[e] - m_run[e & 1]);
+        l_run[0] = l_run[0] * alpha[0] + s[0] + s[2];
+        l_run[1] = l_run[1] * alpha[1] + s[1] + s[3];
+        if (__any_sync(0xffffffffu, alpha[0] != 1.f || alpha[1] != 1.f)) {
+#pragma unroll
+            for (int mt2 = 0; mt2 < KS; ++mt2) {
+                acc[mt2][0] *= alpha[0];
+                acc[mt2][1] *= alpha[1];
+                acc[mt2][2] *= alpha[0];
+                acc[mt2][3] *= alpha[1];
+            }
+        }
+        const uint32_t pb0 = movmatrix_t(pack2(s[0], s[1]));
+        const uint32_t pb1 = movmatrix_t(pack2(s[2], s[3]));
+#pragma unroll
+        for (int mt2 = 0; mt2 < KS; ++mt2) {
+            uint32_t a[4];
+            ldsm_x4_t(vbase + swz_off((lane & 7) + ((lane >> 4) & 1) * 8, mt2 * 2 + ((lane >> 3) & 1)),
+                      a[0], a[1], a[2], a[3]);
+            mma16816(acc[mt2], a, pb0, pb1);
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int hc = 0; hc < 2; ++hc) {
+        l_run[hc] += __shfl_xor_sync(0xffffffffu, l_run[hc], 4);
+        l_run[hc] += __shfl_xor_sync(0xffffffffu, l_run[hc], 8);
+        l_run[hc] += __shfl_xor_sync(0xffffffffu, l_run[hc], 16);
+    }
+    __syncthreads();  // every warp's bulk copies have landed (waited) before the slots are reused
+    float* red = reinterpret_cast<float*>(&sm.k[0][0][0]);
+#pragma unroll
+    for (int mt2 = 0; mt2 < KS; ++mt2)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int h = 2 * tq + (e & 1), dd = mt2 * 16 + g + ((e & 2) ? 8 : 0);
+            red[(warp * 8 + h) * (DH + 2) + dd] = acc[mt2][e];
+        }
+    if (g == 0) {
+#pragma unroll
+        for (int hc = 0; hc < 2; ++hc) {
+            red[(warp * 8 + 2 * tq + hc) * (DH + 2) + DH] = m_run[hc];
+            red[(warp * 8 + 2 * tq + hc) * (DH + 2) + DH + 1] = l_run[hc];
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < G * DH; i += blockDim.x) {
+        const int r = i / DH, dd = i % DH;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, red[(w * 8 + r) * (DH + 2) + DH]);
+        float num = 0.f, den = 0.f;
+#pragma unroll
+        for (int w = 0; w < kAttnWarps; ++w) {
+            const float* src = red + (w * 8 + r) * (DH + 2);
+            const float wt = src[DH] == -INFINITY ? 0.f : exp2f(src[DH] - M);
+            num += src[dd] * wt;
+            den += src[DH + 1] * wt;
+        }
+        const size_t row_head = size_t(t) * n_h + kvh * G + r;
+        if (splits == 1) {
+            o[row_head * DH + dd] = f2bf(num / den);
+        } else {
+            float* dst = ws + (row_head * stride + split) * (DH + 2);
+            __stcg(dst + dd, num);
+            if (dd == 0) {
+                __stcg(dst + DH, M);
+                __stcg(dst + DH + 1, den);
+            }
+        }
+    }
+    if (splits == 1) return;
+    __threadfence();
+    __syncthreads();
+    __shared__ int last_cta;
+    if (threadIdx.x == 0) {
+        int* cnt = counters + size_t(t) * n_kv + kvh;
+        const int old = atomicAdd(cnt, 1);
+        last_cta = old == splits - 1;
+        if (last_cta) *cnt = 0;
+    }
+    __syncthreads();
+    if (!last_cta) return;
+    __threadfence();
+    for (int i = threadIdx.x; i < G * DH; i += blockDim.x) {
+        const int r = i / DH, dd = i % DH;
+        const size_t row_head = size_t(t) * n_h + kvh * G + r;
+        const float* base = ws + row_head * stride * (DH + 2);
+        float M = -INFINITY;
+        for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, __ldcg(base + sp * (DH + 2) + DH));
+        float num = 0.f, den = 0.f;
+        for (int sp = 0; sp < splits; ++sp) {
+            const float ms = __ldcg(base + sp * (DH + 2) + DH);
+            if (ms == -INFINITY) continue;
+            const float w = exp2f(ms - M);
+            num += __ldcg(base + sp * (DH + 2) + dd) * w;
+            den += __ldcg(base + sp * (DH + 2) + DH + 1) * w;
+        }
+        o[row_head * DH + dd] = f2bf(num / den);
+    }
+}
+
 int attention_block_positions(int n_h, int n_kv) { return (kAttnWarps * 16) / (n_h / n_kv); }
 
 // Context splits (flash-decoding): at least kSplitTarget CTAs per SM when the (block, kv head)
@@ -909,9 +1146,29 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
             const int ctas = int(grid.x);
             st = ctas <= kNumSMs ? 4 : (ctas <= 2 * kNumSMs ? 3 : 2);
         }
-        // operand-swapped kernel for G <= 8 (measured 5% less attention time on config 2);
-        // DS_ATTN_DECODE=1 selects the Q-as-M kernel
-        static const int dec_env = getenv("DS_ATTN_DECODE") ? atoi(getenv("DS_ATTN_DECODE")) : 2;
+        // TMA-staged operand-swapped kernel for G <= 8 (DS_ATTN_DECODE=3, the default when the
+        // pool has a tensor map); 2: the same MMAs staged with cp.async; 1: the Q-as-M kernel
+        static const int dec_env = getenv("DS_ATTN_DECODE") ? atoi(getenv("DS_ATTN_DECODE")) : 3;
+        if (dec_env == 3 && n_h / kv.n_kv <= 8 && kv.tmap) {
+            const CUtensorMap& tm = *static_cast<const CUtensorMap*>(kv.tmap);
+            switch (st) {
+                case 3:
+                    launch_pdl(attn_decode_tma_kernel<DH, 3>, grid, block, sizeof(DecTmaSmem<DH, 3>) + 1024,
+                               stream, tm, q, n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd,
+                               stride, o, ws, counters);
+                    break;
+                case 4:
+                    launch_pdl(attn_decode_tma_kernel<DH, 4>, grid, block, sizeof(DecTmaSmem<DH, 4>) + 1024,
+                               stream, tm, q, n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd,
+                               stride, o, ws, counters);
+                    break;
+                default:
+                    launch_pdl(attn_decode_tma_kernel<DH, 2>, grid, block, sizeof(DecTmaSmem<DH, 2>) + 1024,
+                               stream, tm, q, n_h, row_pos, row_page_off, flat_pages, drows, kv, layer, sd,
+                               stride, o, ws, counters);
+            }
+            return;
+        }
         if (dec_env == 2 && n_h / kv.n_kv <= 8) {
             switch (st) {
                 case 3:
@@ -977,6 +1234,9 @@ namespace ds {
 template <int DH, int ST>
 static void preload_decode() {
     cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, attn_decode_tma_kernel<DH, ST>);
+    cudaFuncSetAttribute(attn_decode_tma_kernel<DH, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(DecTmaSmem<DH, ST>) + 1024));
     cudaFuncGetAttributes(&a, attn_decode_kernel<DH, ST>);
     cudaFuncSetAttribute(attn_decode_kernel<DH, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(sizeof(DecSmem<DH, ST>)));

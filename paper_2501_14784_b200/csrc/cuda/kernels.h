@@ -73,7 +73,14 @@ struct KvLayout {
     __nv_bfloat16* pool = nullptr;  // [n_pages][L_stage][2][n_kv][256][d_head]
     int64_t page_elems = 0;
     int n_layers = 0, n_kv = 0, d_head = 0;
+    // TMA view of the pool (host copy of a CUtensorMap, 128-byte aligned): rows of d_head
+    // elements, row = ((page * L + layer) * 2 + K|V) * n_kv + kv head) * 256 + token; 16-row x
+    // 64-element boxes, 128-byte swizzle. Null: the decode kernel stages with cp.async.
+    const void* tmap = nullptr;
 };
+// 2-D bf16 tensor map (rows x cols, K-major) with box_rows x box_cols boxes, 128-byte swizzle.
+int make_tmap_2d_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t cols,
+                      uint32_t box_rows, uint32_t box_cols);
 
 // Rotary embedding on q and k (rotate-half, table [max_pos][d_head/2] cos / sin) and
 // the paged KV append of k, v for every row at row_pos[t] into page row_page[t].

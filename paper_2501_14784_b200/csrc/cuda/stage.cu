@@ -100,6 +100,7 @@ struct ds_stage {
 
     // KV
     KvLayout kv;
+    alignas(128) CUtensorMap kv_tmap;  // TMA view of the pool (KvLayout::tmap)
     int64_t page_bytes = 0;
     int n_mb = 0;
     int local_pages = 0, slot_pages = 0, host_pages = 0;
@@ -378,6 +379,13 @@ ds_status ds_kv_create(ds_stage* s, int64_t page_bytes, int64_t n_mb, int64_t lo
     s->kv.d_head = m.d_head;
     ds_status st = alloc_dev(reinterpret_cast<void**>(&s->kv.pool), size_t(dev_pages) * page_bytes);
     if (st) return st;
+    {   // rows of d_head elements; int32 TMA coordinates bound the pool at 2^31 rows
+        const uint64_t rows = uint64_t(dev_pages) * (page_bytes / (m.d_head * 2));
+        s->kv.tmap = nullptr;
+        if (rows > 0 && rows < (uint64_t(1) << 31) &&
+            ds::make_tmap_2d_bf16(&s->kv_tmap, s->kv.pool, rows, uint64_t(m.d_head), 16, 64) == 0)
+            s->kv.tmap = &s->kv_tmap;
+    }
     if (s->host_pages > 0) {
         cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&s->host_backing),
                                        size_t(s->n_mb) * s->host_pages * page_bytes);
