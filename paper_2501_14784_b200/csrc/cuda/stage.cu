@@ -123,6 +123,7 @@ struct ds_stage {
     std::vector<ProfRec> recs;
     int64_t launches = 0;
     int64_t h2d_bytes = 0;
+    int64_t not_ready_resident = 0, not_ready_growth = 0;  // ds_kv_ready refusals by reason
 
     // one-shot timing events for the next ds_stage_step (ready, start, end) and the next
     // ds_swap_in (in0, in1, out0, out1): the executor's real-clock trace (ds_stage_step_events)
@@ -434,6 +435,7 @@ ds_status ds_kv_reset(ds_stage* s) {
     CK(cudaMemset(s->last_token, 0, size_t(s->n_mb) * s->max_slots * 4));
     s->moved_in_total = s->moved_out_total = 0;
     s->h2d_bytes = 0;  // per run (the bench divides by the run's circuits)
+    s->not_ready_resident = s->not_ready_growth = 0;
     return DS_OK;
 }
 
@@ -525,6 +527,8 @@ ds_status ds_kv_ready(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_row
         avail += std::min<int64_t>(int64_t(s->gslot[k.resident_slot].free.size()),
                                    int64_t(k.host_free.size()));
     *ready = (res && need <= avail) ? 1 : 0;
+    if (!res) ++s->not_ready_resident;
+    else if (need > avail) ++s->not_ready_growth;
     return DS_OK;
 }
 
@@ -992,7 +996,9 @@ ds_status ds_stage_kernel_stats(ds_stage* s, char* out, size_t cap, int64_t* lau
                  k ? "," : "", kPkName[k], (long long)n[k], ms[k], fl[k], by[k], (long long)rows[k]);
         js += buf;
     }
-    js += ",\"h2d_bytes\":" + std::to_string(s->h2d_bytes) + "}";
+    js += ",\"h2d_bytes\":" + std::to_string(s->h2d_bytes) + ",\"not_ready_resident\":" +
+          std::to_string(s->not_ready_resident) + ",\"not_ready_growth\":" +
+          std::to_string(s->not_ready_growth) + "}";
     if (out && cap) {
         const size_t c = std::min(cap - 1, js.size());
         memcpy(out, js.data(), c);
