@@ -76,6 +76,8 @@ struct GemmParams {
     float* slots;   // [n_clusters][2][CN][tb_pad][128] fp32 pieces of split tiles
     int* counters;  // [tiles][CN] arrivals (self-resetting)
     unsigned long long* trace;  // optional per-CTA phase timestamps (gemm_set_trace)
+    const __nv_bfloat16* w;     // weight base (L2 prefetch addresses)
+    int pf_kb;                  // k-blocks per CTA to prefetch into L2 past the smem pipeline
 };
 
 DS_DEVICE unsigned long long gtime() {
@@ -90,6 +92,11 @@ DS_DEVICE unsigned long long gtime() {
 
 static unsigned long long* g_gemm_trace = nullptr;
 void gemm_set_trace(unsigned long long* buf) { g_gemm_trace = buf; }
+
+DS_DEVICE void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)), "r"(bytes)
+                 : "memory");
+}
 
 DS_DEVICE uint32_t cluster_rank() {
     uint32_t r;
@@ -441,6 +448,25 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
     const int cl_tiles = p.m_tiles / CN;
     const bool leader = !TWO || rank == 0;
 
+    if (warp == 3 && p.pf_kb > 0) {
+        // L2 prefetch of this CTA's weight stream past what the smem pipeline loads up front:
+        // independent of the previous kernel, so it is issued before griddepcontrol.wait and
+        // streams while the previous kernel drains (its epilogue and tail leave HBM idle); the
+        // main loop's TMA loads then hit L2. One contiguous run per weight row and segment.
+        int skip = p.stages, budget = p.pf_kb;
+        for_each_seg(p, cluster, kidx, [&](const Seg& w) {
+            int kb = w.kb0;
+            const int sk = min(skip, w.kb1 - kb);
+            kb += sk;
+            skip -= sk;
+            const int n = min(budget, w.kb1 - kb);
+            if (n <= 0) return;
+            budget -= n;
+            const int mt = tile_mtc(p, w.ut, cl_tiles) * CN + int(rank);
+            for (int r = lane; r < kBM; r += 32)
+                prefetch_l2_bulk(p.w + (size_t(mt) * kBM + r) * p.K + size_t(kb) * kBK, uint32_t(n * kBK * 2));
+        });
+    }
     if (warp == 0) {
         if (elect_one()) {
             const uint64_t pol_w = policy_evict_first();
@@ -962,6 +988,20 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
     p.counters = reinterpret_cast<int*>(workspace);
     p.slots = workspace + n_cnt;
     p.trace = g_gemm_trace;
+    p.w = w.data;
+    {   // L2 prefetch budget: a weight matrix up to 64 MB entirely, else this many MB in total
+        // spread over the CTAs (DS_GEMM_L2PF=MB overrides; 0 disables)
+        static const int pf_env = getenv("DS_GEMM_L2PF") ? atoi(getenv("DS_GEMM_L2PF")) : 48;
+        const size_t wbytes = size_t(N) * K * 2;
+        const int ctas = p.n_clusters * cn * p.ks;
+        const size_t per_kb = size_t(kBM) * kBK * 2;  // one k-block of one CTA's 128 rows
+        if (pf_env <= 0 || ctas <= 0)
+            p.pf_kb = 0;
+        else if (wbytes <= (size_t(64) << 20))
+            p.pf_kb = 1 << 20;
+        else
+            p.pf_kb = int((size_t(pf_env) << 20) / size_t(ctas) / per_kb);
+    }
     alignas(64) CUtensorMap tx;
     if (make_tmap_2d_bf16(&tx, x, T, K, p.brows, kBK) != 0) return -5;
     const size_t smem = size_t(p.stages) * stage_bytes + fixed;

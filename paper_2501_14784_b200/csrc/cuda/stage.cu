@@ -713,11 +713,15 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     if (T > s->max_rows) return ds_fail(DS_ERR_ARG, "circuit has more rows than max_rows");
     if (R > std::max(1, s->max_slots)) return ds_fail(DS_ERR_ARG, "more sampled rows than slots");
     // residency check (compute-requires-resident, reference replay_check sim.cpp:629-639)
+    bool host_backed = false;  // the step reads or appends a page of the global slot
     for (int64_t i = 0; i < n_rows; ++i)
-        for (int32_t hnd : k.pages[rows[i].slot])
-            if (hnd < 0 && k.host_dev[-hnd - 1] < 0)
+        for (int32_t hnd : k.pages[rows[i].slot]) {
+            if (hnd >= 0) continue;
+            host_backed = true;
+            if (k.host_dev[-hnd - 1] < 0)
                 return ds_fail(DS_ERR_RUNTIME, "compute-before-swap-in: microbatch " +
                                                    std::to_string(mb) + " has non-resident pages");
+        }
 
     const int prevR = int(k.prev_logit_slots.size());
     const size_t need_meta = size_t(10) * T + 2 * size_t(R) + P + prevR + 8;
@@ -810,7 +814,9 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     cudaEvent_t sev[3] = {s->step_ev[0], s->step_ev[1], s->step_ev[2]};
     for (auto& e : s->step_ev) e = nullptr;
     if (sev[0]) CK(cudaEventRecord(sev[0], s->stream));
-    if (k.resident_slot >= 0) {
+    // a step touching only local pages does not depend on the copy streams (their zero-byte or
+    // other-microbatch swaps would otherwise serialise it behind the eviction of a slot occupant)
+    if (k.resident_slot >= 0 && host_backed) {
         const size_t w0 = s->prof ? prof_mark(s) : 0;
         CK(cudaStreamWaitEvent(s->stream, s->ev_h2d, 0));
         if (s->prof) s->recs.push_back({PK_SWAPW, T, 0.0, 0.0, w0, prof_mark(s)});

@@ -104,7 +104,9 @@ def run_one(txt, cdir, policy=None, latency_us=-1, gpus=1, circuits=0, profile=T
                  "measured_swap_wait_us": gpu["swap_wait_us"]},
         "per_stage": [{"device": s["device"], "computes": s["computes"], "busy_ms": round(s["busy_ms"], 1),
                        "swap_plan_bytes": s["swap_plan_bytes"], "swap_in_bytes": s["swap_in_bytes"],
-                       "topups": s["topups"]} for s in gpu["stages"]],
+                       "topups": s["topups"],
+                       "not_ready_resident": s["kernels"].get("not_ready_resident"),
+                       "not_ready_growth": s["kernels"].get("not_ready_growth")} for s in gpu["stages"]],
     }
     if prof is not None:
         summary["kernels"] = kernel_kinds(prof["stages"])
