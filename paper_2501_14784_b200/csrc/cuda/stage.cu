@@ -46,6 +46,7 @@ struct MbKv {
     std::vector<int32_t> slot_tokens;  // per slot: KV positions written (steps enqueued so far)
     std::vector<int32_t> host_slot, host_idx;  // host page -> (slot, page index in that slot)
     int resident_slot = -1;
+    bool h2d_pending = false;  // a swap-in copied pages of this microbatch the next step must await
     cudaEvent_t last_compute = nullptr;
     bool computed = false;
     cudaEvent_t evicted = nullptr;  // end of this microbatch's last eviction (its host pages written)
@@ -421,6 +422,7 @@ ds_status ds_kv_reset(ds_stage* s) {
         k.host_slot.assign(s->host_pages, -1);
         k.host_idx.assign(s->host_pages, -1);
         k.resident_slot = -1;
+        k.h2d_pending = false;
         k.computed = false;
         k.prev_logit_slots.clear();
     }
@@ -647,6 +649,7 @@ ds_status ds_swap_in(ds_stage* s, int32_t mb, int32_t slot, int64_t plan_bytes, 
             ++n_copies;
         }
     if (tev[1]) CK(cudaEventRecord(tev[1], s->h2d));  // in1: refill end
+    if (in + migrated > 0) k.h2d_pending = true;
     gs.owner = mb;
     k.resident_slot = slot;
     // ev_h2d (what the compute waits for) also covers the evictions: the slot pages they read
@@ -816,7 +819,8 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     if (sev[0]) CK(cudaEventRecord(sev[0], s->stream));
     // a step touching only local pages does not depend on the copy streams (their zero-byte or
     // other-microbatch swaps would otherwise serialise it behind the eviction of a slot occupant)
-    if (k.resident_slot >= 0 && host_backed) {
+    if (k.resident_slot >= 0 && (host_backed || k.h2d_pending)) {
+        k.h2d_pending = false;
         const size_t w0 = s->prof ? prof_mark(s) : 0;
         CK(cudaStreamWaitEvent(s->stream, s->ev_h2d, 0));
         if (s->prof) s->recs.push_back({PK_SWAPW, T, 0.0, 0.0, w0, prof_mark(s)});
