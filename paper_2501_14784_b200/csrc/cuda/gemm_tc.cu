@@ -989,9 +989,11 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
     p.slots = workspace + n_cnt;
     p.trace = g_gemm_trace;
     p.w = w.data;
-    {   // L2 prefetch budget: a weight matrix up to 64 MB entirely, else this many MB in total
-        // spread over the CTAs (DS_GEMM_L2PF=MB overrides; 0 disables)
-        static const int pf_env = getenv("DS_GEMM_L2PF") ? atoi(getenv("DS_GEMM_L2PF")) : 48;
+    {   // L2 prefetch budget (DS_GEMM_L2PF=MB: a weight matrix up to 64 MB entirely, else this
+        // many MB over the CTAs). Off: measured slower on every 8B shape (qkv 20.7 -> 22.4 us,
+        // down 30.8 -> 33.6 us at T = 180) and 14.13 k -> 13.69 k tok/s on config 2
+        // (profiles/r02_ab_l2pf.txt): the prefetch competes with the previous kernel's stream.
+        static const int pf_env = getenv("DS_GEMM_L2PF") ? atoi(getenv("DS_GEMM_L2PF")) : 0;
         const size_t wbytes = size_t(N) * K * 2;
         const int ctas = p.n_clusters * cn * p.ks;
         const size_t per_kb = size_t(kBM) * kBK * 2;  // one k-block of one CTA's 128 rows
