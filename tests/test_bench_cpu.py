@@ -1,0 +1,66 @@
+"""CPU checks of bench.py's measurement legs (no GPU): the schedule fixture the reference arm
+times is the reference's own schedule, and the reference arm never loads the product library."""
+import gzip
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CONFIGS = os.path.join(ROOT, "configs")
+
+
+def test_schedule_fixture_is_the_reference_schedule(tmp_path):
+    """configs/llama8b_1stage.schedule.json.gz (tools/make_schedule_fixture.py): every circuit's
+    (eff_batch, n_decode) equals the ComputeStart events of the reference's own run() trace of
+    configs/llama8b_1stage.json (oracle/_ref), and its rows add up to them."""
+    import oracle
+    fx = json.load(gzip.open(os.path.join(CONFIGS, "llama8b_1stage.schedule.json.gz"), "rt"))
+    txt = open(os.path.join(CONFIGS, "llama8b_1stage.json")).read()
+    tr = str(tmp_path / "ref.trace")
+    oracle.Ref().sim_config(txt, CONFIGS, trace_path=tr)
+    starts = []
+    for line in open(tr):
+        if "kind=ComputeStart" in line:
+            f = dict(x.split("=", 1) for x in line.split())
+            starts.append((int(f["a"]), int(f["b"])))
+    assert [(c["eff_batch"], c["n_decode"]) for c in fx] == starts
+    for c in fx:
+        assert sum(r[2] for r in c["rows"]) == c["eff_batch"]
+        assert sum(r[4] for r in c["rows"]) == c["n_decode"]
+
+
+def test_reference_arm_does_not_load_the_product(tmp_path):
+    """bench.py's CPU legs import only oracle/: a process running them has no libdeserve_b200.so
+    mapped (the reference arm measures the reference's CPU path, nothing of ours)."""
+    code = (
+        "import sys, os; sys.path.insert(0, %r); import bench\n"
+        "circs = bench.systematic_sample(761, 3)\n"
+        "import oracle\n"
+        "fx = oracle.load_schedule_fixture(bench.SCHEDULE_FIXTURE)\n"
+        "assert len(fx) == 761 and circs == sorted(set(circs))\n"
+        "maps = open('/proc/self/maps').read()\n"
+        "assert 'libdeserve_b200' not in maps, 'product library loaded'\n"
+        "assert 'paper_2501_14784_b200' not in sys.modules\n"
+        "print('ok')\n" % ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr[-500:]
+
+
+def test_pipesim_timing_runs_on_one_core():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "oracle", "time_pipesim.py"),
+                        os.path.join(CONFIGS, "llama8b_1stage.json"), "1"],
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr[-500:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["cores"] == 1 and d["simulated_output_tokens"] == 68699 and d["wall_s"] > 0
+
+
+@pytest.mark.parametrize("var", ["DS_SKIP", "DS_ATTN_SKIP", "DS_GEMM_NOFINISH"])
+def test_bench_refuses_invalidating_switches(var):
+    env = dict(os.environ, **{var: "1"})
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1"],
+                       capture_output=True, text=True, timeout=120, env=env)
+    assert r.returncode != 0 and var in r.stderr
