@@ -347,6 +347,293 @@ attn_prompt_kernel(const __nv_bfloat16* __restrict__ q, int n_h, const int32_t* 
 }
 
 
+DS_DEVICE void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// TMA-staged variant of attn_prompt_kernel (the default when the pool has its 64-row tensor map):
+// each 64-token K / V tile is DH/64 bulk tensor loads of 64 x 64 boxes (128-byte swizzle, so the
+// ldmatrix reads are conflict-free without padding) completing on the pair buffer's mbarrier,
+// issued by one thread; the Q rows still stream with cp.async. Same MMAs, masking, online softmax
+// and merges as attn_prompt_kernel.
+template <int DH>
+struct PromptTmaSmem {
+    static constexpr int kTileElems = kTile * DH;  // DH/64 boxes of 64 rows x 64 elements
+    alignas(1024) __nv_bfloat16 k[2][2][kTileElems];  // [pair buffer][parity]
+    alignas(1024) __nv_bfloat16 v[2][2][kTileElems];
+    __nv_bfloat16 q[64][DH + 8];
+    uint64_t bar[2];
+};
+
+// byte offset of (row, 16-byte chunk c over d_head) in a 64-row tile of 64-element boxes
+DS_DEVICE uint32_t swz64(int row, int c) {
+    return uint32_t((c >> 3) * (kTile * 128) + row * 128 + (((c & 7) ^ (row & 7)) << 4));
+}
+
+template <int DH>
+__global__ void __launch_bounds__(kPromptWarps * 32)
+attn_prompt_tma_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __nv_bfloat16* __restrict__ q,
+                       int n_h, const int32_t* __restrict__ row_pos, const int32_t* __restrict__ row_page_off,
+                       const int32_t* __restrict__ flat_pages, const int32_t* __restrict__ blocks, KvLayout kv,
+                       int layer, int splits, int stride, __nv_bfloat16* __restrict__ o, float* __restrict__ ws,
+                       int* __restrict__ counters) {
+    pdl_launch_dependents();
+    extern __shared__ __align__(1024) uint8_t attn_smem_raw[];
+    PromptTmaSmem<DH>& sm = *reinterpret_cast<PromptTmaSmem<DH>*>(
+        (reinterpret_cast<uintptr_t>(attn_smem_raw) + 1023) & ~uintptr_t(1023));
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&tmap_kv);
+        mbar_init(&sm.bar[0], 1);
+        mbar_init(&sm.bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    pdl_wait();
+    constexpr int NT = DH / 8;
+    constexpr int KS = DH / 16;
+    constexpr int SN = kTile / 8;
+    const int n_kv = kv.n_kv;
+    const int G = n_h / n_kv;
+    const int split = blockIdx.x % splits;
+    const int kvh = (blockIdx.x / splits) % n_kv;
+    const int bi = blockIdx.x / (splits * n_kv);
+    const int t0 = blocks[3 * bi], npos = blocks[3 * bi + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rg = warp & 3, par = warp >> 2;
+    const int g = lane >> 2, tq = lane & 3;
+    const int rows = npos * G;
+    const int pos0 = row_pos[t0];
+    const int last_pos = pos0 + npos - 1;
+    const int n_tiles = (last_pos + kTile) / kTile;
+    const int tile0 = split * n_tiles / splits, tile1 = (split + 1) * n_tiles / splits;
+    const int32_t* pages = flat_pages + row_page_off[t0];
+
+    const int r_base = rg * 16;
+    const bool warp_active = r_base < rows;
+    uint32_t qa[KS][4];
+    const float qs = rsqrtf(float(DH)) * 1.4426950408889634f;
+    for (int i = threadIdx.x; i < rows * (DH / 8); i += blockDim.x) {
+        const int r = i / (DH / 8), c = (i % (DH / 8)) * 8;
+        cp_async16(&sm.q[r][c], q + (size_t(t0 + r / G) * n_h + kvh * G + r % G) * DH + c);
+    }
+    cp_async_commit();
+    int rpos[2];
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+        const int r = r_base + g + 8 * hr;
+        rpos[hr] = r < rows ? pos0 + r / G : -1;
+    }
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+    float acc[NT][4];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+
+    const int row_k = (layer * 2 + 0) * n_kv + kvh;
+    const int row_v = (layer * 2 + 1) * n_kv + kvh;
+    const int rows_per_page = kv.n_layers * 2 * n_kv * 256;
+    const int n_pairs = (tile1 - tile0 + 1) / 2;
+    auto load_pair = [&](int pi, int buf) {  // thread 0 only
+        const int nt_here = min(2, tile1 - (tile0 + 2 * pi));
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&sm.bar[buf], uint32_t(nt_here * 2 * kTile * DH * 2));
+        for (int pp = 0; pp < nt_here; ++pp) {
+            const int tok0 = (tile0 + 2 * pi + pp) * kTile;
+            const int base = pages[tok0 >> 8] * rows_per_page + (tok0 & 255);
+#pragma unroll
+            for (int bx = 0; bx < DH / 64; ++bx) {
+                tma_load_2d(&sm.k[buf][pp][bx * kTile * 64], &tmap_kv, &sm.bar[buf], bx * 64, base + row_k * 256);
+                tma_load_2d(&sm.v[buf][pp][bx * kTile * 64], &tmap_kv, &sm.bar[buf], bx * 64, base + row_v * 256);
+            }
+        }
+    };
+    if (threadIdx.x == 0 && n_pairs > 0) load_pair(0, 0);
+    cp_async_wait<0>();
+    __syncthreads();
+    if (warp_active) {  // Q fragments
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk)
+            ldsm_x4(smem_u32(&sm.q[r_base + (lane & 15)][kk * 16 + (lane >> 4) * 8]), qa[kk][0], qa[kk][1],
+                    qa[kk][2], qa[kk][3]);
+    }
+    for (int pi = 0; pi < n_pairs; ++pi) {
+        const int buf = pi & 1;
+        if (threadIdx.x == 0 && pi + 1 < n_pairs) load_pair(pi + 1, buf ^ 1);
+        mbar_wait(&sm.bar[buf], uint32_t((pi >> 1) & 1));
+        for (int pp = 0; pp < 2; ++pp) {  // zero V rows past the last valid token
+            const int tile = tile0 + 2 * pi + pp;
+            if (tile >= tile1) break;
+            const int valid = min(kTile, last_pos + 1 - tile * kTile);
+            uint8_t* vb = reinterpret_cast<uint8_t*>(&sm.v[buf][pp][0]);
+            for (int i = threadIdx.x; i < (kTile - valid) * (DH / 8); i += blockDim.x) {
+                const int r = valid + i / (DH / 8), c = i % (DH / 8);
+                *reinterpret_cast<uint4*>(vb + swz64(r, c)) = make_uint4(0, 0, 0, 0);
+            }
+        }
+        __syncthreads();
+        const int tile = tile0 + 2 * pi + par;
+        if (warp_active && tile < tile1) {
+            const int tok0 = tile * kTile;
+            float s[SN][4];
+#pragma unroll
+            for (int j = 0; j < SN; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+            const uint32_t kbase = smem_u32(&sm.k[buf][par][0]);
+#pragma unroll
+            for (int j = 0; j < SN; ++j)
+#pragma unroll
+                for (int kk = 0; kk < KS; kk += 2) {
+                    const int mi = lane >> 3, rr = lane & 7;
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4(kbase + swz64(j * 8 + rr, kk * 2 + mi), b0, b1, b2, b3);
+                    mma16816(s[j], qa[kk], b0, b1);
+                    mma16816(s[j], qa[kk + 1], b2, b3);
+                }
+            float mt[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+            for (int j = 0; j < SN; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int hr = e >> 1;
+                    s[j][e] = tok0 + j * 8 + 2 * tq + (e & 1) > rpos[hr] ? -INFINITY : s[j][e] * qs;
+                    mt[hr] = fmaxf(mt[hr], s[j][e]);
+                }
+            float alpha[2];
+#pragma unroll
+            for (int hr = 0; hr < 2; ++hr) {
+                mt[hr] = fmaxf(mt[hr], __shfl_xor_sync(0xffffffffu, mt[hr], 1));
+                mt[hr] = fmaxf(mt[hr], __shfl_xor_sync(0xffffffffu, mt[hr], 2));
+                const float mn = fmaxf(m_run[hr], mt[hr]);
+                alpha[hr] = mn == -INFINITY ? 1.f : exp2f(m_run[hr] - mn);
+                m_run[hr] = mn;
+            }
+            float ls[2] = {0.f, 0.f};
+            uint32_t pa[SN / 2][4];
+#pragma unroll
+            for (int j = 0; j < SN; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int hr = e >> 1;
+                    const float pv = m_run[hr] == -INFINITY ? 0.f : exp2f(s[j][e] - m_run[hr]);
+                    s[j][e] = pv;
+                    ls[hr] += pv;
+                }
+#pragma unroll
+            for (int hr = 0; hr < 2; ++hr) l_run[hr] = l_run[hr] * alpha[hr] + ls[hr];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                acc[j][0] *= alpha[0];
+                acc[j][1] *= alpha[0];
+                acc[j][2] *= alpha[1];
+                acc[j][3] *= alpha[1];
+            }
+#pragma unroll
+            for (int kk = 0; kk < SN / 2; ++kk) {
+                pa[kk][0] = pack2(s[2 * kk][0], s[2 * kk][1]);
+                pa[kk][1] = pack2(s[2 * kk][2], s[2 * kk][3]);
+                pa[kk][2] = pack2(s[2 * kk + 1][0], s[2 * kk + 1][1]);
+                pa[kk][3] = pack2(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+            }
+            const uint32_t vbase = smem_u32(&sm.v[buf][par][0]);
+#pragma unroll
+            for (int kk = 0; kk < SN / 2; ++kk)
+#pragma unroll
+                for (int nt = 0; nt < NT; nt += 2) {
+                    const int mi = lane >> 3, rr = lane & 7;
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4_t(vbase + swz64(kk * 16 + (mi & 1) * 8 + rr, nt + (mi >> 1)), b0, b1, b2, b3);
+                    mma16816(acc[nt], pa[kk], b0, b1);
+                    mma16816(acc[nt + 1], pa[kk], b2, b3);
+                }
+        }
+        __syncthreads();  // pair buffer `buf` is refilled by the load of pair pi + 2
+    }
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+        l_run[hr] += __shfl_xor_sync(0xffffffffu, l_run[hr], 1);
+        l_run[hr] += __shfl_xor_sync(0xffffffffu, l_run[hr], 2);
+    }
+    float* red = reinterpret_cast<float*>(&sm.k[0][0][0]);  // [4 row groups][16 rows][DH + 2]
+    if (par == 1 && warp_active) {
+#pragma unroll
+        for (int hr = 0; hr < 2; ++hr) {
+            float* dst = red + (rg * 16 + g + 8 * hr) * (DH + 2);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                dst[nt * 8 + 2 * tq] = acc[nt][2 * hr];
+                dst[nt * 8 + 2 * tq + 1] = acc[nt][2 * hr + 1];
+            }
+            if (tq == 0) {
+                dst[DH] = m_run[hr];
+                dst[DH + 1] = l_run[hr];
+            }
+        }
+    }
+    __syncthreads();
+    if (par == 0 && warp_active) {
+#pragma unroll
+        for (int hr = 0; hr < 2; ++hr) {
+            const int r = r_base + g + 8 * hr;
+            const float* oth = red + (rg * 16 + g + 8 * hr) * (DH + 2);
+            const float m1 = oth[DH], l1 = oth[DH + 1];
+            const float M = fmaxf(m_run[hr], m1);
+            const float w0 = m_run[hr] == -INFINITY ? 0.f : exp2f(m_run[hr] - M);
+            const float w1 = m1 == -INFINITY ? 0.f : exp2f(m1 - M);
+            const float L = l_run[hr] * w0 + l1 * w1;
+            if (r >= rows) continue;
+            const int p = r / G, h = r % G;
+            const size_t row_head = size_t(t0 + p) * n_h + kvh * G + h;
+            if (splits == 1) {
+                const float inv = 1.0f / L;
+                __nv_bfloat16* dst = o + row_head * DH;
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    const int c = nt * 8 + 2 * tq;
+                    *reinterpret_cast<uint32_t*>(dst + c) =
+                        pack2((acc[nt][2 * hr] * w0 + oth[c] * w1) * inv, (acc[nt][2 * hr + 1] * w0 + oth[c + 1] * w1) * inv);
+                }
+            } else {
+                float* dst = ws + (row_head * stride + split) * (DH + 2);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    const int c = nt * 8 + 2 * tq;
+                    __stcg(dst + c, acc[nt][2 * hr] * w0 + oth[c] * w1);
+                    __stcg(dst + c + 1, acc[nt][2 * hr + 1] * w0 + oth[c + 1] * w1);
+                }
+                if (tq == 0) {
+                    __stcg(dst + DH, M);
+                    __stcg(dst + DH + 1, L);
+                }
+            }
+        }
+    }
+    if (splits == 1) return;
+    __threadfence();
+    __syncthreads();
+    __shared__ int last_cta;
+    if (threadIdx.x == 0) {
+        int* cnt = counters + size_t(bi) * n_kv + kvh;
+        const int old = atomicAdd(cnt, 1);
+        last_cta = old == splits - 1;
+        if (last_cta) *cnt = 0;
+    }
+    __syncthreads();
+    if (!last_cta) return;
+    __threadfence();
+    for (int i = threadIdx.x; i < rows * DH; i += blockDim.x) {
+        const int r = i / DH, dd = i % DH;
+        const size_t row_head = size_t(t0 + r / G) * n_h + kvh * G + r % G;
+        const float* base = ws + row_head * stride * (DH + 2);
+        float M = -INFINITY;
+        for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, __ldcg(base + sp * (DH + 2) + DH));
+        float num = 0.f, den = 0.f;
+        for (int sp = 0; sp < splits; ++sp) {
+            const float ms = __ldcg(base + sp * (DH + 2) + DH);
+            if (ms == -INFINITY) continue;
+            const float w = exp2f(ms - M);
+            num += __ldcg(base + sp * (DH + 2) + dd) * w;
+            den += __ldcg(base + sp * (DH + 2) + DH + 1) * w;
+        }
+        o[row_head * DH + dd] = f2bf(num / den);
+    }
+}
+
 // ------------------------------------------------------------------ decode rows ----
 // One decode row x one KV head x one context split per CTA. The split's context is cut into
 // 16-token chunks dealt round-robin to the 4 warps; every warp streams its chunks through its
@@ -845,7 +1132,6 @@ DS_DEVICE uint32_t swz_off(int row, int c) {
     return uint32_t((c >> 3) * (kDecChunk * 128) + row * 128 + (((c & 7) ^ (row & 7)) << 4));
 }
 
-DS_DEVICE void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 template <int DH, int ST>
 __global__ void __launch_bounds__(kAttnWarps * 32)
@@ -1132,7 +1418,14 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
     if (skip & 1) n_blocks = 0;
     if (skip & 2) n_drows = 0;
     const int stride = std::max(sp, sd);
-    if (n_blocks > 0)
+    // DS_ATTN_PROMPT=1: the cp.async-staged prompt kernel (default: TMA when the pool has its map)
+    static const int prompt_env = getenv("DS_ATTN_PROMPT") ? atoi(getenv("DS_ATTN_PROMPT")) : 2;
+    if (n_blocks > 0 && prompt_env == 2 && kv.tmap64)
+        launch_pdl(attn_prompt_tma_kernel<DH>, dim3(n_blocks * kv.n_kv * sp), dim3(kPromptWarps * 32),
+                   sizeof(PromptTmaSmem<DH>) + 1024, stream, *static_cast<const CUtensorMap*>(kv.tmap64), q,
+                   n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, sp, stride, o, ws,
+                   counters + size_t(T) * kv.n_kv);
+    else if (n_blocks > 0)
         launch_pdl(attn_prompt_kernel<DH>, dim3(n_blocks * kv.n_kv * sp), dim3(kPromptWarps * 32),
                    sizeof(PromptSmem<DH>), stream, q, n_h, row_pos, row_page_off, flat_pages, blocks,
                    kv, layer, sp, stride, o, ws, counters + size_t(T) * kv.n_kv,
@@ -1247,6 +1540,12 @@ static void preload_decode() {
 
 void preload_attention() {
     cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, attn_prompt_tma_kernel<128>);
+    cudaFuncGetAttributes(&a, attn_prompt_tma_kernel<64>);
+    cudaFuncSetAttribute(attn_prompt_tma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(PromptTmaSmem<128>) + 1024));
+    cudaFuncSetAttribute(attn_prompt_tma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(PromptTmaSmem<64>) + 1024));
     cudaFuncGetAttributes(&a, attn_prompt_kernel<128>);
     cudaFuncGetAttributes(&a, attn_prompt_kernel<64>);
     cudaFuncSetAttribute(attn_prompt_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,

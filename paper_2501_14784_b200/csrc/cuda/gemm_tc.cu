@@ -686,8 +686,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         tc_fence_after();
         ksplit_epilogue<CN>(p, smem, tmem_base, cluster, kidx, int(rank), warp, lane);
         tc_fence_before();
+        if (threadIdx.x == 128) GEMM_TRACE(3);
     }
     if (csize > 1) cluster_sync();
+    if (threadIdx.x == 0) GEMM_TRACE(5);
     if (warp == 2) {
         tc_fence_after();
         if constexpr (TWO)

@@ -77,6 +77,7 @@ struct KvLayout {
     // elements, row = ((page * L + layer) * 2 + K|V) * n_kv + kv head) * 256 + token; 16-row x
     // 64-element boxes, 128-byte swizzle. Null: the decode kernel stages with cp.async.
     const void* tmap = nullptr;
+    const void* tmap64 = nullptr;  // the same view with 64-row boxes (prompt K/V tiles)
 };
 // 2-D bf16 tensor map (rows x cols, K-major) with box_rows x box_cols boxes, 128-byte swizzle.
 int make_tmap_2d_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t cols,

@@ -101,7 +101,8 @@ struct ds_stage {
 
     // KV
     KvLayout kv;
-    alignas(128) CUtensorMap kv_tmap;  // TMA view of the pool (KvLayout::tmap)
+    alignas(128) CUtensorMap kv_tmap;    // TMA view of the pool (KvLayout::tmap), 16-row boxes
+    alignas(128) CUtensorMap kv_tmap64;  // 64-row boxes (KvLayout::tmap64)
     int64_t page_bytes = 0;
     int n_mb = 0;
     int local_pages = 0, slot_pages = 0, host_pages = 0;
@@ -387,6 +388,10 @@ ds_status ds_kv_create(ds_stage* s, int64_t page_bytes, int64_t n_mb, int64_t lo
         if (rows > 0 && rows < (uint64_t(1) << 31) &&
             ds::make_tmap_2d_bf16(&s->kv_tmap, s->kv.pool, rows, uint64_t(m.d_head), 16, 64) == 0)
             s->kv.tmap = &s->kv_tmap;
+        s->kv.tmap64 = nullptr;
+        if (s->kv.tmap &&
+            ds::make_tmap_2d_bf16(&s->kv_tmap64, s->kv.pool, rows, uint64_t(m.d_head), 64, 64) == 0)
+            s->kv.tmap64 = &s->kv_tmap64;
     }
     if (s->host_pages > 0) {
         cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&s->host_backing),
