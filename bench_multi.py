@@ -132,6 +132,12 @@ def run_multi(args):
         subs.append(pl.trace_report(merged, world, a, b, wl["rng_seed"])["output_throughput"])
     open(os.path.join(out_dir, "report.kv"), "w").write(
         pl.report_kv(rep, plan_txt, cfg["links"][0]["latency_us"], "config"))
+    import gzip
+    import shutil
+    with open(merged, "rb") as fi, gzip.open(merged + ".gz", "wb") as fo:
+        shutil.copyfileobj(fi, fo)
+    for f in [merged] + [os.path.join(out_dir, f"rank{i}.trace") for i in range(world)]:
+        os.remove(f)
     sim = pl.sim_config(txt, CONFIGS)
     clocks = gathered[0]["clk"]
     clocks["per_rank_sm_mhz"] = [g["clk"]["sm_mhz"] for g in gathered]

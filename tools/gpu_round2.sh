@@ -5,6 +5,7 @@ tag=${1:-r02b}
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/${tag}_gputests.log 2>&1
 echo "gpu tests rc=$?"; tail -3 gpurun_out/${tag}_gputests.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${tag}_smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/${tag}_smoke.log
 python bench.py --steps 3 --warmup 3 > gpurun_out/${tag}_bench_n1.json 2> gpurun_out/${tag}_bench_n1.err
 echo "bench rc=$?"; python -c "import json;d=json.load(open('gpurun_out/${tag}_bench_n1.json'));print(d['value'],d['ms_per_step'],{k:v['ms'] for k,v in d['roofline']['by_kind'].items()})"
 python tools/calibrate_stage.py --model llama3-8b --layers 32 --ctx 512 --decode "" \

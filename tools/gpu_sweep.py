@@ -55,6 +55,7 @@ def main():
             os.makedirs(out, exist_ok=True)
             try:
                 s = run_one(txt, cdir, p, lat, a.gpus, 0, False, out)
+                os.remove(os.path.join(out, "hw.trace.gz"))  # per-cell traces: report.kv + summary kept
                 row_g.append(s["report"]["output_throughput"])
                 row_r.append(s["reference_sim"]["output_throughput"])
                 cells.append(s)

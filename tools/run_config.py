@@ -115,6 +115,12 @@ def run_one(txt, cdir, policy=None, latency_us=-1, gpus=1, circuits=0, profile=T
     if out:
         open(os.path.join(out, "report.kv"), "w").write(kv)
         json.dump(summary, open(os.path.join(out, "summary.json"), "w"), indent=1)
+        # keep gpurun_out small (the call returns <= 64 MiB): the trace travels gzipped
+        import gzip
+        import shutil
+        with open(trace, "rb") as fi, gzip.open(trace + ".gz", "wb") as fo:
+            shutil.copyfileobj(fi, fo)
+        os.remove(trace)
     return summary
 
 
