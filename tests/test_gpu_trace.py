@@ -19,7 +19,7 @@ from paper_2501_14784_b200 import pipeline as pl
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CDIR = os.path.join(ROOT, "configs")
-OUT = os.path.join(ROOT, "gpurun_out")
+OUT = os.path.join("/tmp", "ds_trace_tests")
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(n_devices() < 1, reason="needs a GPU")]
 
 
