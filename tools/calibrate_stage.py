@@ -43,13 +43,13 @@ def main():
     dec = [int(x) for x in a.decode.split(",") if x]
     pre = [int(x) for x in a.prefill.split(",") if x]
     max_rows = max(dec + pre)
-    slots = max(max(dec), max(pre) // a.prompt + 2)
+    slots = max(max(dec, default=1), max(pre, default=0) // a.prompt + 2)
     md = pl.model_desc(dims)
     st = C.c_void_p()
     nat.check(nat.lib.ds_stage_create(0, C.byref(md), lb, le, int(first), int(last), pl.WEIGHT_SEED,
                                       (max_rows + 15) // 16 * 16, slots, C.byref(st)))
     page = 256 * a.layers * 2 * dims["n_kv_heads"] * dims["d_head"] * 2
-    need_pages = max(max(dec) * ((a.ctx + 1 + 255) // 256), max(pre) // 256 + slots)
+    need_pages = max(max(dec, default=0) * ((a.ctx + 1 + 255) // 256), max(pre, default=0) // 256 + slots)
     nat.check(nat.lib.ds_kv_create(st, page, 1, need_pages * page, 0, 0))
     act = C.c_void_p()
     nat.check(nat.lib.ds_dbg_alloc(0, max_rows * dims["d_model"] * 2, C.byref(act)))
