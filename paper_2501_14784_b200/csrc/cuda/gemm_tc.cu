@@ -328,91 +328,57 @@ DS_DEVICE void ksplit_epilogue(const GemmParams& p, uint8_t* smem, uint32_t tmem
     const int ipr = silu ? 16 : 32;  // 4-feature items per token row (SiLU: gate quads only)
     for (int w0 = 0; w0 < t_here; w0 += 256) {
         const int wn = min(256, t_here - w0);
-        // park: two 16-column TMEM loads in flight per wait
-        for (int c = cgrp * 16; c < wn; c += 64) {
-            uint32_t r[2][16];
-            tmem_ld16(tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(w0 + c), r[0]);
-            if (c + 32 < wn) tmem_ld16(tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(w0 + c + 32), r[1]);
+        for (int c = cgrp * 16; c < wn; c += 32) {
+            uint32_t r[16];
+            tmem_ld16(tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(w0 + c), r);
             tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 16; ++j) part[(c + j) * kBM + quarter * 32 + lane] = __uint_as_float(r[0][j]);
-            if (c + 32 < wn) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) part[(c + 32 + j) * kBM + quarter * 32 + lane] = __uint_as_float(r[1][j]);
-            }
+            for (int j = 0; j < 16; ++j) part[(c + j) * kBM + quarter * 32 + lane] = __uint_as_float(r[j]);
         }
         cluster_sync();  // every CTA's window parked and visible cluster-wide
         const int r0 = kidx * wn / p.ks, r1 = (kidx + 1) * wn / p.ks;
-        const int n_it = (r1 - r0) * ipr;
-        for (int it0 = threadIdx.x; it0 < n_it; it0 += 2 * kGemmThreads) {
-            // two items per pass, all their peer loads (and residuals) issued before any sum
-            float4 a[2][4], u[2][4];
-            uint2 rv[2] = {make_uint2(0, 0), make_uint2(0, 0)};
-            int tt[2], ff[2];
-            bool ok[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int it = it0 + h * kGemmThreads;
-                ok[h] = it < n_it;
-                const int row = r0 + (ok[h] ? it : 0) / ipr, q4 = (ok[h] ? it : 0) % ipr;
-                const int f = silu ? (q4 >> 2) * 32 + (q4 & 3) * 4 : q4 * 4;
-                tt[h] = t0 + w0 + row;
-                ff[h] = mt * kBM + f;
-                const uint32_t off = part_u32 + uint32_t((row * kBM + f) * 4);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (k < p.ks && ok[h]) {
-                        const uint32_t peer = mapa_shared(off, uint32_t(k * CN + rank));
-                        a[h][k] = ld_dsmem_f4(peer);
-                        if (silu) u[h][k] = ld_dsmem_f4(peer + 64);
-                    }
-                }
-                if (ok[h] && p.epi == EPI_RESID)
-                    rv[h] = *reinterpret_cast<const uint2*>(p.resid + size_t(tt[h]) * p.N + ff[h]);
+        for (int it = threadIdx.x; it < (r1 - r0) * ipr; it += kGemmThreads) {
+            const int row = r0 + it / ipr, q4 = it % ipr;
+            const int f = silu ? (q4 >> 2) * 32 + (q4 & 3) * 4 : q4 * 4;
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f), u = a;
+            const uint32_t off = part_u32 + uint32_t((row * kBM + f) * 4);
+            for (int k = 0; k < p.ks; ++k) {  // k order: deterministic
+                const uint32_t peer = uint32_t(k * CN + rank);
+                add4(a, ld_dsmem_f4(mapa_shared(off, peer)));
+                if (silu) add4(u, ld_dsmem_f4(mapa_shared(off + 64, peer)));
             }
+            const int t = t0 + w0 + row, fg = mt * kBM + f;
+            const float v[4] = {a.x, a.y, a.z, a.w};
+            if (p.epi == EPI_F32) {
+                *reinterpret_cast<float4*>(p.out_f32 + size_t(t) * p.N + fg) = a;
+            } else if (silu) {
+                const float uu[4] = {u.x, u.y, u.z, u.w};
+                float h[4];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (!ok[h]) continue;
-                float4 s4 = a[h][0], su = silu ? u[h][0] : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                for (int k = 1; k < 4; ++k) {  // k order: deterministic
-                    if (k < p.ks) {
-                        add4(s4, a[h][k]);
-                        if (silu) add4(su, u[h][k]);
-                    }
+                for (int j = 0; j < 4; ++j) {
+                    const float gb = round_bf(v[j]);
+                    h[j] = round_bf(__fdividef(gb, 1.0f + __expf(-gb))) * round_bf(uu[j]);
                 }
-                const int t = tt[h], fg = ff[h];
-                const float v[4] = {s4.x, s4.y, s4.z, s4.w};
-                if (p.epi == EPI_F32) {
-                    *reinterpret_cast<float4*>(p.out_f32 + size_t(t) * p.N + fg) = s4;
-                } else if (silu) {
-                    const float uu[4] = {su.x, su.y, su.z, su.w};
-                    float hh[4];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const float gb = round_bf(v[j]);
-                        hh[j] = round_bf(__fdividef(gb, 1.0f + __expf(-gb))) * round_bf(uu[j]);
-                    }
-                    uint2 hv;
-                    hv.x = pack2(hh[0], hh[1]);
-                    hv.y = pack2(hh[2], hh[3]);
-                    *reinterpret_cast<uint2*>(p.out_bf16 + size_t(t) * (p.N / 2) + (fg / 32) * 16 + fg % 32) = hv;
-                } else {
-                    float o[4] = {v[0], v[1], v[2], v[3]};
-                    const size_t oi = size_t(t) * p.N + fg;
-                    if (p.epi == EPI_RESID) {
-                        const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv[h]);
-                        const float2 x0 = __bfloat1622float2(rh[0]), x1 = __bfloat1622float2(rh[1]);
-                        o[0] = x0.x + round_bf(o[0]);
-                        o[1] = x0.y + round_bf(o[1]);
-                        o[2] = x1.x + round_bf(o[2]);
-                        o[3] = x1.y + round_bf(o[3]);
-                    }
-                    uint2 ov;
-                    ov.x = pack2(o[0], o[1]);
-                    ov.y = pack2(o[2], o[3]);
-                    *reinterpret_cast<uint2*>(p.out_bf16 + oi) = ov;
+                uint2 hv;
+                hv.x = pack2(h[0], h[1]);
+                hv.y = pack2(h[2], h[3]);
+                *reinterpret_cast<uint2*>(p.out_bf16 + size_t(t) * (p.N / 2) + (fg / 32) * 16 + fg % 32) = hv;
+            } else {
+                float o[4] = {v[0], v[1], v[2], v[3]};
+                const size_t oi = size_t(t) * p.N + fg;
+                if (p.epi == EPI_RESID) {
+                    const uint2 rv = *reinterpret_cast<const uint2*>(p.resid + oi);
+                    const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
+                    const float2 x0 = __bfloat1622float2(rh[0]), x1 = __bfloat1622float2(rh[1]);
+                    o[0] = x0.x + round_bf(o[0]);
+                    o[1] = x0.y + round_bf(o[1]);
+                    o[2] = x1.x + round_bf(o[2]);
+                    o[3] = x1.y + round_bf(o[3]);
                 }
+                uint2 ov;
+                ov.x = pack2(o[0], o[1]);
+                ov.y = pack2(o[2], o[3]);
+                *reinterpret_cast<uint2*>(p.out_bf16 + oi) = ov;
             }
         }
         cluster_sync();  // peers done reading before the next window overwrites it
@@ -647,27 +613,16 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                 // arriver sums all pieces in k order (deterministic) and runs the epilogue.
                 if (p.planes) {  // narrow GEMM: fp32 partial into plane (k range) [T][N]
                     float* plane = p.slots + size_t(cluster % p.planes) * p.T * p.N;
-                    auto put = [&](uint32_t* rr, int c0) {
-                        if (transpose16(stage, reinterpret_cast<float*>(rr), lane, c0, t_here, v)) {
+                    for (int c0 = 0; c0 < t_here; c0 += 16) {
+                        tmem_ld16(acc + c0, r);
+                        tmem_ld_wait();
+                        if (transpose16(stage, reinterpret_cast<float*>(r), lane, c0, t_here, v)) {
                             float4* dst = reinterpret_cast<float4*>(plane + size_t(t0 + c0 + row) * p.N +
                                                                     f_slice + half * 16);
 #pragma unroll
                             for (int i = 0; i < 4; ++i)
                                 __stcg(dst + i, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
                         }
-                    };
-                    // the next chunk's TMEM load is in flight while this chunk is transposed and stored
-                    uint32_t rb[16];
-                    tmem_ld16(acc, r);
-                    tmem_ld_wait();
-                    for (int c0 = 0; c0 < t_here; c0 += 32) {
-                        if (c0 + 16 < t_here) tmem_ld16(acc + c0 + 16, rb);
-                        put(r, c0);
-                        tmem_ld_wait();
-                        if (c0 + 16 >= t_here) break;
-                        if (c0 + 32 < t_here) tmem_ld16(acc + c0 + 32, r);
-                        put(rb, c0 + 16);
-                        tmem_ld_wait();
                     }
                     goto seg_done;  // planes summed by splitk_reduce_kernel
                 }
