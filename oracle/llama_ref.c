@@ -52,6 +52,11 @@ float lr_weight(uint64_t seed, uint64_t tensor_id, int64_t index, float scale) {
     return bf((2.0f * u - 1.0f) * scale);
 }
 
+void lr_fill_weights(uint64_t seed, uint64_t tensor_id, int64_t n, float scale, float* out) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) out[i] = lr_weight(seed, tensor_id, i, scale);
+}
+
 int32_t lr_prompt_token(int64_t req_id, int32_t pos) {
     if (pos == 0) return 128000;
     uint64_t z = 0x5EEDULL ^ ((uint64_t)req_id * 0x9E3779B97F4A7C15ULL) ^ (uint64_t)pos;

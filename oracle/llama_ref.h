@@ -23,6 +23,8 @@ typedef struct lr_stage lr_stage;
 
 float lr_weight(uint64_t seed, uint64_t tensor_id, int64_t index, float scale);
 int32_t lr_prompt_token(int64_t req_id, int32_t pos);
+/* out[i] = lr_weight(seed, tensor_id, i, scale) for i < n (bf16 values held in fp32) */
+void lr_fill_weights(uint64_t seed, uint64_t tensor_id, int64_t n, float scale, float* out);
 lr_stage* lr_stage_create(const lr_model* m, int32_t layer_begin, int32_t layer_end,
                           int32_t is_first, int32_t is_last, uint64_t seed, int32_t max_handles);
 void lr_stage_destroy(lr_stage* s);

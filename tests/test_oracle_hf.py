@@ -27,7 +27,16 @@ def _mix64(z):
 
 
 def _weights(seed, tensor_id, rows, cols, scale):
-    """lr_weight (oracle/llama_ref.c:49-53) for a whole [rows, cols] tensor, as float32."""
+    """lr_weight (oracle/llama_ref.c:49-53) for a whole [rows, cols] tensor, as float32 (the
+    oracle's own OpenMP filler for big tensors; the numpy restatement below for small ones, which
+    also cross-checks the filler)."""
+    if rows * cols >= (1 << 22):
+        import oracle
+        lib = oracle.LlamaRef().lib
+        lib.lr_fill_weights.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_float, C.c_void_p]
+        out = np.empty((rows, cols), dtype=np.float32)
+        lib.lr_fill_weights(seed, tensor_id, rows * cols, scale, out.ctypes.data)
+        return out
     idx = np.arange(rows * cols, dtype=np.uint64)
     with np.errstate(over="ignore"):
         h = _mix64(np.uint64(seed) + np.uint64(tensor_id) * PHI + idx * MIX_C)
@@ -98,6 +107,33 @@ def test_oracle_matches_hf_llama(req, n_tok):
     model = _hf_model(dims, seed)
     with torch.no_grad():
         hf = model(torch.from_numpy(tok.astype(np.int64))[None, :]).logits[0, -1].float().numpy()
+    err = np.abs(ours - hf)
+    assert np.all(err <= 0.08 + 0.02 * np.abs(hf)), float(err.max())
+    top = np.sort(hf)[-2:]
+    if top[1] - top[0] > 0.16:
+        assert int(np.argmax(ours)) == int(np.argmax(hf))
+
+
+def test_weight_filler_matches_numpy_restatement():
+    import oracle
+    lib = oracle.LlamaRef().lib
+    lib.lr_fill_weights.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_float, C.c_void_p]
+    out = np.empty((64, 96), dtype=np.float32)
+    lib.lr_fill_weights(pl.WEIGHT_SEED, 37, out.size, 0.05, out.ctypes.data)
+    assert np.array_equal(out, _weights(pl.WEIGHT_SEED, 37, 64, 96, 0.05))
+
+
+def test_oracle_matches_hf_llama_at_8b_dims():
+    """The same pin at the real Llama-3-8B dimensions (d 4096, 32 query / 8 KV heads of 128,
+    ffn 14336, vocab 128256, RoPE theta 5e5), two layers: the GQA 4:1 head mapping, the 128-wide
+    rotary halves and the LM head over the full vocabulary are checked, not just the tiny model's."""
+    dims = dict(pl.MODEL_DIMS["llama3-8b"], n_layers=2)
+    seed = pl.WEIGHT_SEED
+    tok, ours = _oracle_logits(dims, seed, 21, 12)
+    model = _hf_model(dims, seed)
+    with torch.no_grad():
+        hf = model(torch.from_numpy(tok.astype(np.int64))[None, :]).logits[0, -1].float().numpy()
+    del model
     err = np.abs(ours - hf)
     assert np.all(err <= 0.08 + 0.02 * np.abs(hf)), float(err.max())
     top = np.sort(hf)[-2:]
