@@ -335,7 +335,9 @@ DS_DEVICE void ksplit_epilogue(const GemmParams& p, uint8_t* smem, uint32_t tmem
 #pragma unroll
             for (int j = 0; j < 16; ++j) part[(c + j) * kBM + quarter * 32 + lane] = __uint_as_float(r[j]);
         }
+        if (threadIdx.x == 128 && w0 == 0) GEMM_TRACE(6);  // window parked
         cluster_sync();  // every CTA's window parked and visible cluster-wide
+        if (threadIdx.x == 128 && w0 == 0) GEMM_TRACE(7);  // cluster arrived
         const int r0 = kidx * wn / p.ks, r1 = (kidx + 1) * wn / p.ks;
         for (int it = threadIdx.x; it < (r1 - r0) * ipr; it += kGemmThreads) {
             const int row = r0 + it / ipr, q4 = it % ipr;
@@ -684,6 +686,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         pdl_wait();
         mbar_wait(&tfull_bar[0], 0);
         tc_fence_after();
+        if (threadIdx.x == 128) GEMM_TRACE(4);  // accumulator complete
         ksplit_epilogue<CN>(p, smem, tmem_base, cluster, kidx, int(rank), warp, lane);
         tc_fence_before();
         if (threadIdx.x == 128) GEMM_TRACE(3);

@@ -1167,8 +1167,9 @@ ds_status ds_dbg_gemm_bench(int32_t T, int32_t N, int32_t K, int32_t epi, int32_
         unsigned long long t0 = ~0ull;
         for (int c = 0; c < kNumSMsHost; ++c)
             if (h[c * 8]) t0 = std::min(t0, h[c * 8]);
-        const char* names[6] = {"start", "loads_issued", "mma_done", "epi_main_done", "fixup_done", "end"};
-        for (int k = 0; k < 6; ++k) {
+        const char* names[8] = {"start", "loads_issued", "mma_done", "epi_main_done", "fixup_done|ks_acc_ready", "end",
+                                "ks_parked", "ks_cluster_sync"};
+        for (int k = 0; k < 8; ++k) {
             std::vector<double> v;
             for (int c = 0; c < kNumSMsHost; ++c)
                 if (h[c * 8 + k]) v.push_back(double(h[c * 8 + k] - t0) / 1000.0);
