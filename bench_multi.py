@@ -48,7 +48,7 @@ def run_multi(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
-    os.environ.setdefault("NCCL_DEBUG", "WARN")  # rank 0's stdout carries exactly one JSON line
+    os.environ["NCCL_DEBUG"] = "WARN"  # stdout carries exactly one JSON line (no NCCL version banner)
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}: launch with torchrun")
     dist.init_process_group("gloo", init_method="env://", rank=rank, world_size=world)
