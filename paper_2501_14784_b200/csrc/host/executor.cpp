@@ -24,6 +24,7 @@
 #include <memory>
 #include <mutex>
 #include <sstream>
+#include <string>
 #include <thread>
 
 #include "capi_util.hpp"
@@ -128,6 +129,9 @@ struct Worker {
     std::vector<SwapTiming> swap_t;
     std::vector<SwapPair> swap_pairs;
     size_t swaps_done = 0;
+    int phys_owner[2] = {-1, -1};  // microbatch physically holding each global slot
+    // per microbatch: op indices of its computes on this stage (slot choice looks ahead)
+    std::vector<std::vector<int64_t>> comp_pos;
     std::string error;
     // per mb: the last circuit whose step (reading recv[mb]) is enqueued, and an event after it.
     // A producer may overwrite recv[mb] with the mb's next input only after that step: a circuit
@@ -288,6 +292,9 @@ Session* session_create(const Config& cfg, const Plan& plan, Schedule sched, con
         XK(cudaSetDevice(w.device));
         XK(cudaEventCreate(&w.t_begin));
         XK(cudaEventCreate(&w.t_end));
+        w.comp_pos.assign(NB, {});
+        for (size_t oi = 0; oi < S->sched.ops[s].size(); ++oi)
+            if (S->sched.ops[s][oi].kind == OpKind::Compute) w.comp_pos[S->sched.ops[s][oi].mb].push_back(int64_t(oi));
         w.in.resize(NB);
         w.recv.assign(NB, nullptr);
         w.consumed_c.assign(NB, -1);
@@ -457,6 +464,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
         w.send_us.clear();
         w.swap_pairs.clear();
         w.swaps_done = 0;
+        w.phys_owner[0] = w.phys_owner[1] = -1;
         w.error.clear();
     }
     std::fill(S->done.t.begin(), S->done.t.end(), int64_t(-1));
@@ -509,6 +517,33 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
         S->cap_meta.clear();
     }
 
+    // Physical global slot for a swap-in of `target` at op index `pos`: the plan's slot numbers
+    // (served % 2, sim.cpp:417-421) are its integer contract and stay in the trace, but the
+    // plan does not mark a microbatch absent when another prefetch reuses its slot (SURVEY.md
+    // H3), so following them evicts microbatches just before they compute. The executor knows
+    // the whole op sequence: it keeps the target where it already is, else uses an empty slot,
+    // else evicts the occupant whose next compute comes later (DS_SWAP_SLOTS=plan: the plan's).
+    static const bool plan_slots = getenv("DS_SWAP_SLOTS") && std::string(getenv("DS_SWAP_SLOTS")) == "plan";
+    auto pick_slot = [&](Worker& w, int32_t target, int64_t pos, int plan_slot) -> int {
+        if (plan_slots) return plan_slot;
+        for (int k = 0; k < 2; ++k)
+            if (w.phys_owner[k] == target) return k;
+        for (int k : {plan_slot, 1 - plan_slot})
+            if (w.phys_owner[k] < 0) return k;
+        auto next_use = [&](int32_t m) -> int64_t {
+            const auto& v = w.comp_pos[m];
+            auto it = std::upper_bound(v.begin(), v.end(), pos);
+            return it == v.end() ? INT64_MAX : *it;
+        };
+        const int64_t u0 = next_use(w.phys_owner[0]), u1 = next_use(w.phys_owner[1]);
+        if (u0 == u1) return plan_slot;
+        return u0 > u1 ? 0 : 1;
+    };
+    auto note_swap = [](Worker& w, int32_t target, int slot) {
+        if (w.phys_owner[1 - slot] == target) w.phys_owner[1 - slot] = -1;
+        w.phys_owner[slot] = target;
+    };
+
     auto body = [&](Worker& w) {
         try {
             XK(cudaSetDevice(w.device));
@@ -516,7 +551,9 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
             Worker* next = S->nccl ? nullptr : &S->W[(s + 1) % NS];
             const bool last = s == NS - 1;
             std::vector<ds_row> rows;
-            for (const StageOp& op : S->sched.ops[s]) {
+            const auto& ops = S->sched.ops[s];
+            for (size_t oi = 0; oi < ops.size(); ++oi) {
+                const StageOp& op = ops[oi];
                 if (failed) return;
                 if (op.kind == OpKind::Release) {
                     DK(ds_kv_release(w.st, op.mb, op.slot));
@@ -531,7 +568,9 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                     SwapTiming& t = w.swap_t[w.swaps_done++];
                     DK(ds_swap_events(w.st, t.e[0], t.e[1], t.e[2], t.e[3]));
                     int64_t mi = 0, mo = 0;
-                    DK(ds_swap_in(w.st, op.mb, op.slot, op.plan_bytes, &mi, &mo));
+                    const int ps = pick_slot(w, op.mb, int64_t(oi), op.slot);
+                    DK(ds_swap_in(w.st, op.mb, ps, op.plan_bytes, &mi, &mo));
+                    note_swap(w, op.mb, ps);
                     w.moved_in += mi;
                     w.moved_out += mo;
                     w.plan_in += op.plan_bytes;
@@ -610,7 +649,9 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 if (!resident) {
                     int64_t mi = 0, mo = 0;
                     DK(ds_swap_events(w.st, nullptr, nullptr, nullptr, nullptr));
-                    DK(ds_swap_in(w.st, mb, int32_t(w.served % 2), 0, &mi, &mo));
+                    const int ps = pick_slot(w, mb, int64_t(oi), int(w.served % 2));
+                    DK(ds_swap_in(w.st, mb, ps, 0, &mi, &mo));
+                    note_swap(w, mb, ps);
                     w.moved_in += mi;
                     w.moved_out += mo;
                     w.topups++;
