@@ -78,6 +78,7 @@ struct GemmParams {
     unsigned long long* trace;  // optional per-CTA phase timestamps (gemm_set_trace)
     const __nv_bfloat16* w;     // weight base (L2 prefetch addresses)
     int pf_kb;                  // k-blocks per CTA to prefetch into L2 past the smem pipeline
+    int ks_push;                // k-split epilogue: peers push row blocks with bulk DSMEM copies
 };
 
 DS_DEVICE unsigned long long gtime() {
@@ -307,6 +308,130 @@ DS_DEVICE void add4(float4& a, const float4& b) {
     a.y += b.y;
     a.z += b.z;
     a.w += b.w;
+}
+
+DS_DEVICE void bulk_s2cluster(uint32_t dst_cluster, uint32_t src, uint32_t bytes, uint32_t bar_cluster) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            dst_cluster),
+        "r"(src), "r"(bytes), "r"(bar_cluster)
+        : "memory");
+}
+DS_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+DS_DEVICE void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+DS_DEVICE void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+constexpr int kPushWin = 128;  // token rows per window of the push epilogue
+
+// Shared memory the push epilogue needs: the parked window + (ks - 1) received row blocks + a barrier.
+inline size_t ksplit_push_smem(int ks) {
+    const size_t rows = size_t((kPushWin + ks - 1) / ks);
+    return size_t(kPushWin) * kBM * 4 + size_t(ks - 1) * rows * kBM * 4 + 64;
+}
+
+// k-split cluster epilogue, push form: every CTA parks a window of <= 128 token columns, then
+// ONE thread sends each peer its row block with a bulk shared::cta -> shared::cluster copy (the
+// copy engine moves it; completion on the peer's mbarrier), and each CTA sums its own rows from
+// local shared memory in k order (deterministic, as the pull form) and applies the epilogue.
+template <int CN>
+DS_DEVICE void ksplit_epilogue_push(const GemmParams& p, uint8_t* smem, uint32_t tmem_base, int cluster,
+                                    int kidx, int rank, int warp, int lane) {
+    const int cl_tiles = p.m_tiles / CN;
+    const int tbk = tile_tbk(p, cluster, cl_tiles);
+    const int mt = tile_mtc(p, cluster, cl_tiles) * CN + rank;
+    const int t0 = tbk * p.tb;
+    const int t_here = min(p.tb, p.T - t0);
+    const int ks = p.ks;
+    const int max_rows = (kPushWin + ks - 1) / ks;
+    float* part = reinterpret_cast<float*>(smem);              // [128 tokens][128 features]
+    float* recv = part + size_t(kPushWin) * kBM;               // [ks - 1][max_rows][128]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(recv + size_t(ks - 1) * max_rows * kBM);
+    const int quarter = warp & 3, cgrp = warp >> 2;
+    const bool silu = p.epi == EPI_SILU;
+    const int ipr = silu ? 16 : 32;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    int phase = 0;
+    for (int w0 = 0; w0 < t_here; w0 += kPushWin, phase ^= 1) {
+        const int wn = min(kPushWin, t_here - w0);
+        for (int c = cgrp * 16; c < wn; c += 32) {
+            uint32_t r[16];
+            tmem_ld16(tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(w0 + c), r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) part[(c + j) * kBM + quarter * 32 + lane] = __uint_as_float(r[j]);
+        }
+        if (threadIdx.x == 128 && w0 == 0) GEMM_TRACE(6);
+        // every CTA parked (and done reading its receive buffers of the previous window)
+        cluster_sync();
+        if (threadIdx.x == 128 && w0 == 0) GEMM_TRACE(7);
+        const int r0 = kidx * wn / ks, r1 = (kidx + 1) * wn / ks;
+        if (threadIdx.x == 0) {
+            fence_async_smem();  // the parked window (generic writes) is the copies' source
+            mbar_arrive_expect_tx(bar, uint32_t((ks - 1) * (r1 - r0) * kBM * 4));
+            for (int k = 0; k < ks; ++k) {
+                if (k == kidx) continue;
+                const int q0 = k * wn / ks, q1 = (k + 1) * wn / ks;  // peer k's rows
+                if (q1 <= q0) continue;
+                const int slot = kidx < k ? kidx : kidx - 1;         // my block in peer k's recv
+                const uint32_t peer = uint32_t(k * CN + rank);
+                const uint32_t dst = mapa_shared(smem_u32(recv + size_t(slot) * max_rows * kBM), peer);
+                bulk_s2cluster(dst, smem_u32(part + size_t(q0) * kBM), uint32_t((q1 - q0) * kBM * 4),
+                               mapa_shared(smem_u32(bar), peer));
+            }
+            bulk_commit();
+        }
+        mbar_wait(bar, uint32_t(phase));  // the peers' blocks of my rows landed
+        for (int it = threadIdx.x; it < (r1 - r0) * ipr; it += kGemmThreads) {
+            const int row = r0 + it / ipr, q4 = it % ipr;
+            const int f = silu ? (q4 >> 2) * 32 + (q4 & 3) * 4 : q4 * 4;
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f), u = a;
+            for (int k = 0; k < ks; ++k) {  // k order: deterministic
+                const float* src = k == kidx ? part + size_t(row) * kBM
+                                             : recv + (size_t(k < kidx ? k : k - 1) * max_rows + (row - r0)) * kBM;
+                add4(a, *reinterpret_cast<const float4*>(src + f));
+                if (silu) add4(u, *reinterpret_cast<const float4*>(src + f + 16));
+            }
+            const int t = t0 + w0 + row, fg = mt * kBM + f;
+            const float v[4] = {a.x, a.y, a.z, a.w};
+            if (p.epi == EPI_F32) {
+                *reinterpret_cast<float4*>(p.out_f32 + size_t(t) * p.N + fg) = a;
+            } else if (silu) {
+                const float uu[4] = {u.x, u.y, u.z, u.w};
+                float h[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float gb = round_bf(v[j]);
+                    h[j] = round_bf(__fdividef(gb, 1.0f + __expf(-gb))) * round_bf(uu[j]);
+                }
+                uint2 hv;
+                hv.x = pack2(h[0], h[1]);
+                hv.y = pack2(h[2], h[3]);
+                *reinterpret_cast<uint2*>(p.out_bf16 + size_t(t) * (p.N / 2) + (fg / 32) * 16 + fg % 32) = hv;
+            } else {
+                float o[4] = {v[0], v[1], v[2], v[3]};
+                const size_t oi = size_t(t) * p.N + fg;
+                if (p.epi == EPI_RESID) {
+                    const uint2 rv = *reinterpret_cast<const uint2*>(p.resid + oi);
+                    const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv);
+                    const float2 x0 = __bfloat1622float2(rh[0]), x1 = __bfloat1622float2(rh[1]);
+                    o[0] = x0.x + round_bf(o[0]);
+                    o[1] = x0.y + round_bf(o[1]);
+                    o[2] = x1.x + round_bf(o[2]);
+                    o[3] = x1.y + round_bf(o[3]);
+                }
+                uint2 ov;
+                ov.x = pack2(o[0], o[1]);
+                ov.y = pack2(o[2], o[3]);
+                *reinterpret_cast<uint2*>(p.out_bf16 + oi) = ov;
+            }
+        }
+        if (threadIdx.x == 0) bulk_wait_read0();  // my window read out before it is re-parked
+        __syncthreads();
+    }
+    cluster_sync();  // every push into this CTA landed and was consumed before anyone exits
 }
 
 // k-split cluster epilogue (all 256 threads): the ks CTAs holding the same 128 features park
@@ -687,7 +812,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         mbar_wait(&tfull_bar[0], 0);
         tc_fence_after();
         if (threadIdx.x == 128) GEMM_TRACE(4);  // accumulator complete
-        ksplit_epilogue<CN>(p, smem, tmem_base, cluster, kidx, int(rank), warp, lane);
+        if (p.ks_push)
+            ksplit_epilogue_push<CN>(p, smem, tmem_base, cluster, kidx, int(rank), warp, lane);
+        else
+            ksplit_epilogue<CN>(p, smem, tmem_base, cluster, kidx, int(rank), warp, lane);
         tc_fence_before();
         if (threadIdx.x == 128) GEMM_TRACE(3);
     }
@@ -1008,6 +1136,12 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
             p.pf_kb = 1 << 20;
         else
             p.pf_kb = int((size_t(pf_env) << 20) / size_t(ctas) / per_kb);
+    }
+    {   // k-split epilogue: push form when the parked window + receive blocks fit the pipeline
+        // shared memory (DS_GEMM_KSPUSH=0: the pull form, peers read with ld.shared::cluster)
+        static const int push_env = getenv("DS_GEMM_KSPUSH") ? atoi(getenv("DS_GEMM_KSPUSH")) : 1;
+        p.ks_push = (push_env && p.ks > 1 &&
+                     ksplit_push_smem(p.ks) <= size_t(p.stages) * size_t(kBM * kBK * 2 + p.b_bytes)) ? 1 : 0;
     }
     alignas(64) CUtensorMap tx;
     if (make_tmap_2d_bf16(&tx, x, T, K, p.brows, kBK) != 0) return -5;
