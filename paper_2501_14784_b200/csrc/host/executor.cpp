@@ -130,6 +130,7 @@ struct Worker {
     std::vector<SwapPair> swap_pairs;
     size_t swaps_done = 0;
     int phys_owner[2] = {-1, -1};  // microbatch physically holding each global slot
+    int32_t last_mb = -1;          // microbatch of the latest enqueued compute (may still run)
     // per microbatch: op indices of its computes on this stage (slot choice looks ahead)
     std::vector<std::vector<int64_t>> comp_pos;
     std::string error;
@@ -465,6 +466,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
         w.swap_pairs.clear();
         w.swaps_done = 0;
         w.phys_owner[0] = w.phys_owner[1] = -1;
+        w.last_mb = -1;
         w.error.clear();
     }
     std::fill(S->done.t.begin(), S->done.t.end(), int64_t(-1));
@@ -530,6 +532,10 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
             if (w.phys_owner[k] == target) return k;
         for (int k : {plan_slot, 1 - plan_slot})
             if (w.phys_owner[k] < 0) return k;
+        // never the microbatch of the latest compute: its eviction (and the refill behind it)
+        // would wait for that compute, serialising the swap with it
+        for (int k = 0; k < 2; ++k)
+            if (w.phys_owner[k] == w.last_mb) return 1 - k;
         auto next_use = [&](int32_t m) -> int64_t {
             const auto& v = w.comp_pos[m];
             auto it = std::upper_bound(v.begin(), v.end(), pos);
@@ -676,6 +682,7 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                                             : (ring_slot >= 0 ? S->recv_ring[ring_slot] : w.recv[mb]);
                 void* act_out = (last && NS == 1) ? w.recv[mb] : nullptr;  // ids loop back
                 DK(ds_stage_step(w.st, mb, rows.data(), int64_t(rows.size()), act_in, act_out));
+                w.last_mb = mb;
                 XK(cudaEventRecord(w.consumed_ev[mb], w.stream));  // recv[mb] read by this step
                 if (ring_slot >= 0) {  // the ring slot may be refilled once this step has read it
                     XK(cudaEventRecord(S->ev_consumed[ring_slot], w.stream));
