@@ -1138,8 +1138,9 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
             p.pf_kb = int((size_t(pf_env) << 20) / size_t(ctas) / per_kb);
     }
     {   // k-split epilogue: push form when the parked window + receive blocks fit the pipeline
-        // shared memory (DS_GEMM_KSPUSH=0: the pull form, peers read with ld.shared::cluster)
-        static const int push_env = getenv("DS_GEMM_KSPUSH") ? atoi(getenv("DS_GEMM_KSPUSH")) : 1;
+        // shared memory (DS_GEMM_KSPUSH=1). Off by default: measured slower than the pull form
+        // (o at T = 180: 18.9 vs 15.3-15.9 us per launch, profiles/r02_gemm_trace_push.txt)
+        static const int push_env = getenv("DS_GEMM_KSPUSH") ? atoi(getenv("DS_GEMM_KSPUSH")) : 0;
         p.ks_push = (push_env && p.ks > 1 &&
                      ksplit_push_smem(p.ks) <= size_t(p.stages) * size_t(kBM * kBK * 2 + p.b_bytes)) ? 1 : 0;
     }

@@ -526,16 +526,18 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
     // the whole op sequence: it keeps the target where it already is, else uses an empty slot,
     // else evicts the occupant whose next compute comes later (DS_SWAP_SLOTS=plan: the plan's).
     static const bool plan_slots = getenv("DS_SWAP_SLOTS") && std::string(getenv("DS_SWAP_SLOTS")) == "plan";
+    static const bool pin_last = getenv("DS_SWAP_SLOTS") && std::string(getenv("DS_SWAP_SLOTS")) == "pin";
     auto pick_slot = [&](Worker& w, int32_t target, int64_t pos, int plan_slot) -> int {
         if (plan_slots) return plan_slot;
         for (int k = 0; k < 2; ++k)
             if (w.phys_owner[k] == target) return k;
         for (int k : {plan_slot, 1 - plan_slot})
             if (w.phys_owner[k] < 0) return k;
-        // never the microbatch of the latest compute: its eviction (and the refill behind it)
-        // would wait for that compute, serialising the swap with it
-        for (int k = 0; k < 2; ++k)
-            if (w.phys_owner[k] == w.last_mb) return 1 - k;
+        // (pinning the microbatch of the latest compute -- DS_SWAP_SLOTS=pin -- measured worse:
+        // 70B 4-stage swap 411.6 vs 444.6 tok/s, twice the top-ups)
+        if (pin_last)
+            for (int k = 0; k < 2; ++k)
+                if (w.phys_owner[k] == w.last_mb) return 1 - k;
         auto next_use = [&](int32_t m) -> int64_t {
             const auto& v = w.comp_pos[m];
             auto it = std::upper_bound(v.begin(), v.end(), pos);
