@@ -97,9 +97,20 @@ def test_tiny_pipeline_matches_oracle(name):
         assert sum(s["swap_plan_bytes"] for s in st) > 0
 
 
-def test_tiny_pipeline_real_delay_and_trace_timing():
-    txt = _cfg("tiny_2stage.json", bench_duration_s=30, warmup_s=1)
-    r = pl.gpu_run_config(txt, CONFIGS, max_circuits=40, real_delay=True)
+def test_tiny_pipeline_real_delay_and_trace_timing(tmp_path):
+    txt = _cfg("tiny_2stage.json", bench_duration_s=30, warmup_s=0)
+    tr = str(tmp_path / "hw.trace")
+    res = pl.run(txt, CONFIGS, max_circuits=40, real_delay=True, trace_path=tr)
+    r = res["gpu"]
     assert r["error"] == ""
     # 40 circuits over 8 microbatches at 10 ms per hop: >= 5 ring rounds * 2 hops * 10 ms
     assert r["wall_us"] >= 5 * 2 * 10000
+    # every hop arrival in the real-clock trace honours send + latency + serialisation (the
+    # reference's transfer-causality rule, sim.cpp:656-669), measured on the host clock
+    n = 0
+    for line in open(tr):
+        f = dict(x.split("=", 1) for x in line.split())
+        if f["kind"] == "TransferArrive" and int(f["t"]) > 0:
+            n += 1
+            assert int(f["t"]) >= int(f["a"]) + 10000 + (int(f["b"]) * 10**6 + 1250000000 - 1) // 1250000000
+    assert n > 0
