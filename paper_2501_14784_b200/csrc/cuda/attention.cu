@@ -634,6 +634,230 @@ attn_prompt_tma_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __nv_b
     }
 }
 
+// ------------------------------------------------------ prompt blocks, tcgen05 ----
+// Chunked-prefill attention on 5th-generation tensor cores (d_head 128, G <= 8): one CTA per
+// (query block of 128 rows = 128/G prompt positions x G heads, KV head), FlashAttention-style
+// over the request's 64-token KV tiles:
+//   S  = Q . K^T   tcgen05.mma M=128 N=64 K=128 (Q, K K-major SW128 tiles from TMA), S in TMEM
+//   P  = softmax   4 warps, one thread per row (TMEM lane), online max / sum in the log2 domain,
+//                  P rows (bf16) written to shared memory as the next MMA's K-major A operand
+//   O += P . V     tcgen05.mma M=128 N=128 K=64 with V as an MN-major B operand (the page layout
+//                  [token][d_head] loaded by TMA, no transpose), O in TMEM, rescaled in place
+//                  (tcgen05.ld / st) when a row's running max moves
+// Warp roles: w0 TMA producer (Q once, K/V tiles double-buffered), w1 MMA issuer, w2 TMEM
+// allocator, w4-7 softmax / correction / epilogue.
+constexpr int kTcRows = 128;
+struct PromptTcSmem {
+    alignas(1024) __nv_bfloat16 q[2][kTcRows * 64];      // [dim half][row][64]
+    alignas(1024) __nv_bfloat16 k[2][2][kTile * 64];     // [stage][dim half][token][64]
+    alignas(1024) __nv_bfloat16 v[2][2][kTile * 64];     // [stage][dim half][token][64]
+    alignas(1024) __nv_bfloat16 p[kTcRows * kTile];      // [row][64 tokens], SW128
+    uint64_t full[2], empty[2], q_full, s_full, s_free, p_full, o_done;
+    uint32_t tmem;
+};
+
+template <int G>
+__global__ void __launch_bounds__(256)
+attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_constant__ CUtensorMap tmap_q,
+                      int n_h, const int32_t* __restrict__ row_pos, const int32_t* __restrict__ row_page_off,
+                      const int32_t* __restrict__ flat_pages, const int32_t* __restrict__ blocks, KvLayout kv,
+                      int layer, __nv_bfloat16* __restrict__ o) {
+    constexpr int DH = 128;
+    constexpr int P_POS = kTcRows / G;  // prompt positions per block
+    pdl_launch_dependents();
+    extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
+    PromptTcSmem& sm = *reinterpret_cast<PromptTcSmem*>(
+        (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_kv = kv.n_kv;
+    const int kvh = blockIdx.x % n_kv;
+    const int bi = blockIdx.x / n_kv;
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&tmap_kv);
+        tma_prefetch_desc(&tmap_q);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&sm.full[b], 1);
+            mbar_init(&sm.empty[b], 1);
+        }
+        mbar_init(&sm.q_full, 1);
+        mbar_init(&sm.s_full, 1);
+        mbar_init(&sm.s_free, 128);
+        mbar_init(&sm.p_full, 128);
+        mbar_init(&sm.o_done, 1);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(&sm.tmem, 256);  // S [0, 64), O [128, 256)
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem;
+    pdl_wait();
+    const int t0 = blocks[3 * bi], npos = blocks[3 * bi + 1];
+    const int rows = npos * G;
+    const int pos0 = row_pos[t0];
+    const int last_pos = pos0 + npos - 1;
+    const int n_tiles = (last_pos + kTile) / kTile;
+    const int32_t* pages = flat_pages + row_page_off[t0];
+    const int rows_per_page = kv.n_layers * 2 * n_kv * 256;
+    const int row_k = (layer * 2 + 0) * n_kv + kvh, row_v = (layer * 2 + 1) * n_kv + kvh;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // Q: [positions][G heads][64] boxes of the q buffer viewed as (dims, heads, rows)
+            mbar_arrive_expect_tx(&sm.q_full, uint32_t(kTcRows * DH * 2));
+            for (int bx = 0; bx < 2; ++bx)
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(&sm.q[bx][0])),
+                    "l"(reinterpret_cast<uint64_t>(&tmap_q)), "r"(smem_u32(&sm.q_full)), "r"(bx * 64),
+                    "r"(kvh * G), "r"(t0)
+                    : "memory");
+            for (int j = 0; j < n_tiles; ++j) {
+                const int st = j & 1;
+                if (j >= 2) mbar_wait(&sm.empty[st], uint32_t(((j >> 1) - 1) & 1));
+                const int tok0 = j * kTile;
+                const int base = pages[tok0 >> 8] * rows_per_page + (tok0 & 255);
+                mbar_arrive_expect_tx(&sm.full[st], uint32_t(2 * kTile * DH * 2));
+                for (int bx = 0; bx < 2; ++bx) {
+                    tma_load_2d(&sm.k[st][bx][0], &tmap_kv, &sm.full[st], bx * 64, base + row_k * 256);
+                    tma_load_2d(&sm.v[st][bx][0], &tmap_kv, &sm.full[st], bx * 64, base + row_v * 256);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc_s = umma_idesc_bf16(kTcRows, kTile);
+            const uint32_t idesc_o = umma_idesc_bf16_bmn(kTcRows, DH);
+            auto issue_s = [&](int j) {  // S_j = Q . K_j^T into TMEM columns [0, 64)
+                const int st = j & 1;
+                mbar_wait(&sm.full[st], uint32_t((j >> 1) & 1));
+                if (j > 0) mbar_wait(&sm.s_free, uint32_t((j - 1) & 1));  // S_{j-1} read out
+                tc_fence_after();
+#pragma unroll
+                for (int ks = 0; ks < DH / 16; ++ks) {
+                    const uint64_t a = umma_sdesc_sw128(smem_u32(&sm.q[ks >> 2][0]) + (ks & 3) * 32);
+                    const uint64_t b = umma_sdesc_sw128(smem_u32(&sm.k[st][ks >> 2][0]) + (ks & 3) * 32);
+                    umma_bf16(tmem, a, b, idesc_s, ks > 0 ? 1u : 0u);
+                }
+                umma_commit(&sm.s_full);
+            };
+            mbar_wait(&sm.q_full, 0);
+            if (n_tiles > 0) issue_s(0);
+            for (int j = 0; j < n_tiles; ++j) {
+                const int st = j & 1;
+                if (j + 1 < n_tiles) issue_s(j + 1);  // overlaps the softmax of tile j
+                mbar_wait(&sm.p_full, uint32_t(j & 1));  // P_j written, O rescaled
+                tc_fence_after();
+#pragma unroll
+                for (int ks = 0; ks < kTile / 16; ++ks) {
+                    const uint64_t a = umma_sdesc_sw128(smem_u32(&sm.p[0]) + ks * 32);
+                    // V: 16 tokens per step = two 8-token groups of 1024 B; dim halves 8 KB apart
+                    const uint64_t b = umma_sdesc_sw128_mn(smem_u32(&sm.v[st][0][0]) + ks * 2048, 8192, 1024);
+                    umma_bf16(tmem + 128, a, b, idesc_o, (j > 0 || ks > 0) ? 1u : 0u);
+                }
+                umma_commit(&sm.o_done);
+                umma_commit(&sm.empty[st]);
+            }
+        }
+    } else if (warp >= 4) {
+        const int r = (warp - 4) * 32 + lane;  // this thread's row = TMEM lane
+        const uint32_t lane_off = uint32_t((warp - 4) * 32) << 16;
+        const int my_pos = r < rows ? pos0 + r / G : -1;
+        const float qs = rsqrtf(float(DH)) * 1.4426950408889634f;
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int j = 0; j < n_tiles; ++j) {
+            const int st = j & 1;
+            const int tok0 = j * kTile;
+            mbar_wait(&sm.s_full, uint32_t(j & 1));
+            tc_fence_after();
+            float sv[kTile];
+#pragma unroll
+            for (int c = 0; c < kTile; c += 16) tmem_ld16(tmem + lane_off + uint32_t(c), reinterpret_cast<uint32_t*>(sv + c));
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(&sm.s_free);
+            float mt = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < kTile; ++c) {
+                sv[c] = tok0 + c > my_pos ? -INFINITY : sv[c] * qs;
+                mt = fmaxf(mt, sv[c]);
+            }
+            const float mn = fmaxf(m_run, mt);
+            const float alpha = mn == -INFINITY ? 1.f : exp2f(m_run - mn);
+            m_run = mn;
+            float ls = 0.f;
+            uint32_t pk[kTile / 2];
+#pragma unroll
+            for (int c = 0; c < kTile; c += 2) {
+                const float p0 = mn == -INFINITY ? 0.f : exp2f(sv[c] - mn);
+                const float p1 = mn == -INFINITY ? 0.f : exp2f(sv[c + 1] - mn);
+                ls += p0 + p1;
+                pk[c / 2] = pack2(p0, p1);
+            }
+            l_run = l_run * alpha + ls;
+            if (j > 0) {
+                mbar_wait(&sm.o_done, uint32_t((j - 1) & 1));  // PV_{j-1} done: O stable, P free
+                tc_fence_after();
+                if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+                    for (int c = 0; c < DH; c += 16) {
+                        uint32_t ov[16];
+                        tmem_ld16(tmem + 128 + lane_off + uint32_t(c), ov);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+                        tmem_st16(tmem + 128 + lane_off + uint32_t(c), ov);
+                    }
+                    tmem_st_wait();
+                }
+            }
+            // P row r: 8 chunks of 8 tokens, 128-byte swizzle (chunk ^ row % 8)
+            uint8_t* prow = reinterpret_cast<uint8_t*>(&sm.p[0]) + r * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) =
+                    make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+            // V rows past the last valid token must be zero (0 * garbage must not be NaN)
+            const int valid = min(kTile, last_pos + 1 - tok0);
+            if (valid < kTile) {
+                mbar_wait(&sm.full[st], uint32_t((j >> 1) & 1));  // the tile landed (already, for S)
+                for (int i = r; i < (kTile - valid) * 16; i += 128) {
+                    const int tr = valid + i / 16, c = i % 16;  // token row, 16-byte chunk over 128 dims
+                    uint8_t* vb = reinterpret_cast<uint8_t*>(&sm.v[st][c >> 3][0]);
+                    *reinterpret_cast<uint4*>(vb + tr * 128 + (((c & 7) ^ (tr & 7)) << 4)) = make_uint4(0, 0, 0, 0);
+                }
+            }
+            fence_proxy_async_smem();  // P (and zeroed V) are read by the MMA's async proxy
+            tc_fence_before();
+            mbar_arrive(&sm.p_full);
+        }
+        // epilogue: O / l, bf16, scattered rows (position, head)
+        mbar_wait(&sm.o_done, uint32_t((n_tiles - 1) & 1));
+        tc_fence_after();
+        const float inv = l_run > 0.f ? 1.0f / l_run : 0.f;
+        __nv_bfloat16* dst = r < rows ? o + (size_t(t0 + r / G) * n_h + kvh * G + r % G) * DH : nullptr;
+#pragma unroll
+        for (int c = 0; c < DH; c += 16) {
+            uint32_t ov[16];
+            tmem_ld16(tmem + 128 + lane_off + uint32_t(c), ov);
+            tmem_ld_wait();
+            if (dst) {
+                float f[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(ov[e]) * inv;
+                reinterpret_cast<uint4*>(dst + c)[0] = pack8(f);
+                reinterpret_cast<uint4*>(dst + c)[1] = pack8(f + 8);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 256);
+    }
+}
+
 // ------------------------------------------------------------------ decode rows ----
 // One decode row x one KV head x one context split per CTA. The split's context is cut into
 // 16-token chunks dealt round-robin to the 4 warps; every warp streams its chunks through its
@@ -1347,7 +1571,21 @@ attn_decode_tma_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __nv_b
     }
 }
 
-int attention_block_positions(int n_h, int n_kv) { return (kAttnWarps * 16) / (n_h / n_kv); }
+// DS_ATTN_PROMPT: 1 cp.async-staged mma.sync kernel, 2 TMA-staged mma.sync kernel, 3 tcgen05
+// kernel (d_head 128, G <= 8, no prompt context splits; 128-row query blocks)
+static int prompt_kernel_env() {
+    static const int v = getenv("DS_ATTN_PROMPT") ? atoi(getenv("DS_ATTN_PROMPT")) : 2;
+    return v;
+}
+static bool prompt_tc(int n_h, int n_kv, int d_head) {
+    static const int sp_tiles = getenv("DS_ATTN_PROMPT_TILES") ? atoi(getenv("DS_ATTN_PROMPT_TILES")) : 0;
+    const int G = n_h / n_kv;
+    return prompt_kernel_env() == 3 && d_head == 128 && (G == 1 || G == 2 || G == 4 || G == 8) && sp_tiles == 0;
+}
+int attention_block_positions(int n_h, int n_kv, int d_head) {
+    if (prompt_tc(n_h, n_kv, d_head)) return kTcRows / (n_h / n_kv);
+    return (kAttnWarps * 16) / (n_h / n_kv);
+}
 
 // Context splits (flash-decoding): at least kSplitTarget CTAs per SM when the (block, kv head)
 // count alone is short of that, each split keeping >= 2 tiles (128 tokens) of the longest context.
@@ -1418,9 +1656,19 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
     if (skip & 1) n_blocks = 0;
     if (skip & 2) n_drows = 0;
     const int stride = std::max(sp, sd);
-    // DS_ATTN_PROMPT=1: the cp.async-staged prompt kernel (default: TMA when the pool has its map)
-    static const int prompt_env = getenv("DS_ATTN_PROMPT") ? atoi(getenv("DS_ATTN_PROMPT")) : 2;
-    if (n_blocks > 0 && prompt_env == 2 && kv.tmap64)
+    const int prompt_env = prompt_kernel_env();
+    if (n_blocks > 0 && prompt_tc(n_h, kv.n_kv, DH) && kv.tmap64 && kv.tmap_q) {
+        const CUtensorMap& tk = *static_cast<const CUtensorMap*>(kv.tmap64);
+        const CUtensorMap& tq = *static_cast<const CUtensorMap*>(kv.tmap_q);
+        const dim3 g(n_blocks * kv.n_kv), b(256);
+        const size_t sm_bytes = sizeof(PromptTcSmem) + 1024;
+        switch (n_h / kv.n_kv) {
+            case 1: launch_pdl(attn_prompt_tc_kernel<1>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o); break;
+            case 2: launch_pdl(attn_prompt_tc_kernel<2>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o); break;
+            case 4: launch_pdl(attn_prompt_tc_kernel<4>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o); break;
+            default: launch_pdl(attn_prompt_tc_kernel<8>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o); break;
+        }
+    } else if (n_blocks > 0 && prompt_env >= 2 && kv.tmap64)
         launch_pdl(attn_prompt_tma_kernel<DH>, dim3(n_blocks * kv.n_kv * sp), dim3(kPromptWarps * 32),
                    sizeof(PromptTmaSmem<DH>) + 1024, stream, *static_cast<const CUtensorMap*>(kv.tmap64), q,
                    n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, sp, stride, o, ws,
@@ -1538,7 +1786,19 @@ static void preload_decode() {
                          int(sizeof(DecSmem<DH, ST>)));
 }
 
+template <int G>
+static void preload_prompt_tc() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, attn_prompt_tc_kernel<G>);
+    cudaFuncSetAttribute(attn_prompt_tc_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(PromptTcSmem) + 1024));
+}
+
 void preload_attention() {
+    preload_prompt_tc<1>();
+    preload_prompt_tc<2>();
+    preload_prompt_tc<4>();
+    preload_prompt_tc<8>();
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, attn_prompt_tma_kernel<128>);
     cudaFuncGetAttributes(&a, attn_prompt_tma_kernel<64>);

@@ -227,6 +227,25 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
            | ((uint32_t(N) >> 3) << 17) | ((uint32_t(M) >> 4) << 24);
 }
 
+// Instruction descriptor: kind::f16, bf16 inputs, f32 accumulator, A K-major, B MN-major (B stored
+// [K rows][N contiguous], e.g. V [tokens][dims] for O += P.V).
+__host__ __device__ constexpr uint32_t umma_idesc_bf16_bmn(int M, int N) {
+    return umma_idesc_bf16(M, N) | (1u << 16);
+}
+
+// Shared-memory descriptor of an MN-major SWIZZLE_128B tile: 128-byte rows along MN (64 bf16),
+// K rows 128 B apart, 8-row groups `sbo` bytes apart, successive 64-element MN blocks `lbo` bytes
+// apart (CUTLASS canonical Major-MN SW128 layout ((8,n),(8,k)):((1,LBO),(8,SBO)) in 16-byte units).
+DS_DEVICE uint64_t umma_sdesc_sw128_mn(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= uint64_t((smem_addr & 0x3FFFFu) >> 4);
+    d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
+    d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(2) << 61;
+    return d;
+}
+
 // Shared-memory matrix descriptor for a K-major tile written by TMA with
 // SWIZZLE_128B: rows of 128 B, 8-row core groups 1024 B apart.
 DS_DEVICE uint64_t umma_sdesc_sw128(uint32_t smem_addr) {
@@ -250,6 +269,15 @@ DS_DEVICE void tmem_ld16(uint32_t taddr, uint32_t* r) {
         : "r"(taddr));
 }
 DS_DEVICE void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+DS_DEVICE void tmem_st16(uint32_t taddr, const uint32_t* r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+DS_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // Programmatic dependent launch: every stage-forward kernel is launched with
 // programmaticStreamSerialization, lets its successor start its prologue early

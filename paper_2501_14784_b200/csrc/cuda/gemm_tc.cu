@@ -957,6 +957,21 @@ int make_tmap_2d_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t 
     return r == CUDA_SUCCESS ? 0 : -2;
 }
 
+int make_tmap_3d_bf16(void* tmap_out, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                      uint32_t b0, uint32_t b1, uint32_t b2) {
+    auto fn = get_encode_fn();
+    if (!fn) return -1;
+    CUtensorMap* m = reinterpret_cast<CUtensorMap*>(tmap_out);
+    cuuint64_t dims[3] = {d0, d1, d2};
+    cuuint64_t strides[2] = {d0 * 2, d0 * d1 * 2};
+    cuuint32_t box[3] = {b0, b1, b2};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 size_t gemm_workspace_floats() { return kWorkspaceFloats; }
 
 static int pick_cn(int N) {

@@ -78,10 +78,15 @@ struct KvLayout {
     // 64-element boxes, 128-byte swizzle. Null: the decode kernel stages with cp.async.
     const void* tmap = nullptr;
     const void* tmap64 = nullptr;  // the same view with 64-row boxes (prompt K/V tiles)
+    const void* tmap_q = nullptr;  // the step's q buffer [max_rows][n_h][d_head] as (dims, heads,
+                                   // rows) with 64 x G x 128/G boxes (tcgen05 prompt kernel)
 };
 // 2-D bf16 tensor map (rows x cols, K-major) with box_rows x box_cols boxes, 128-byte swizzle.
 int make_tmap_2d_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t cols,
                       uint32_t box_rows, uint32_t box_cols);
+// 3-D bf16 tensor map over [d2][d1][d0] (d0 contiguous), boxes b0 x b1 x b2, 128-byte swizzle.
+int make_tmap_3d_bf16(void* tmap_out, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                      uint32_t b0, uint32_t b1, uint32_t b2);
 
 // Rotary embedding on q and k (rotate-half, table [max_pos][d_head/2] cos / sin) and
 // the paged KV append of k, v for every row at row_pos[t] into page row_page[t].
@@ -99,7 +104,7 @@ void rope_kv_append(const __nv_bfloat16* qkv, int T, int n_h, int n_kv, int d_he
 // Context splits: s_prompt for the prompt blocks, s_decode for the decode rows; each kernel's
 // last CTA of a (row or block, KV head) merges the split partials (`counters`: zeroed ints,
 // >= 2 x rows x n_kv, self-resetting; ws: rows x n_h x max(splits) x (d_head + 2) floats).
-int attention_block_positions(int n_h, int n_kv);
+int attention_block_positions(int n_h, int n_kv, int d_head);
 void attention_splits(int T, int n_h, int d_head, int n_blocks, int n_drows, int n_kv, int max_ctx,
                       int max_prompt_ctx, size_t ws_floats, int* s_prompt, int* s_decode);
 int attention_launches(int n_blocks, int n_drows, int s_prompt, int s_decode);

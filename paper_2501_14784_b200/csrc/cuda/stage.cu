@@ -103,6 +103,7 @@ struct ds_stage {
     KvLayout kv;
     alignas(128) CUtensorMap kv_tmap;    // TMA view of the pool (KvLayout::tmap), 16-row boxes
     alignas(128) CUtensorMap kv_tmap64;  // 64-row boxes (KvLayout::tmap64)
+    alignas(128) CUtensorMap q_tmap;     // the q buffer (KvLayout::tmap_q)
     int64_t page_bytes = 0;
     int n_mb = 0;
     int local_pages = 0, slot_pages = 0, host_pages = 0;
@@ -392,6 +393,12 @@ ds_status ds_kv_create(ds_stage* s, int64_t page_bytes, int64_t n_mb, int64_t lo
         if (s->kv.tmap &&
             ds::make_tmap_2d_bf16(&s->kv_tmap64, s->kv.pool, rows, uint64_t(m.d_head), 64, 64) == 0)
             s->kv.tmap64 = &s->kv_tmap64;
+        const int G = m.n_heads / m.n_kv_heads;
+        s->kv.tmap_q = nullptr;
+        if (m.d_head == 128 && G <= 8 && (G & (G - 1)) == 0 &&
+            ds::make_tmap_3d_bf16(&s->q_tmap, s->q, uint64_t(m.d_head), uint64_t(m.n_heads),
+                                  uint64_t(s->max_rows), 64, uint32_t(G), uint32_t(128 / G)) == 0)
+            s->kv.tmap_q = &s->q_tmap;
     }
     if (s->host_pages > 0) {
         cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&s->host_backing),
@@ -779,7 +786,7 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
         for (int j = 0; j < prevR; ++j) prev_slot[j] = k.prev_logit_slots[j];
         // attention work: QP-position query blocks of each prompt group, then the list of
         // single-position (decode) rows, packed behind the blocks in the same 3*T ints
-        const int qp = ds::attention_block_positions(m.n_heads, m.n_kv_heads);
+        const int qp = ds::attention_block_positions(m.n_heads, m.n_kv_heads, m.d_head);
         int tb = 0;
         for (int64_t i = 0; i < n_rows; ++i) {
             const ds_row& rw = rows[i];

@@ -29,3 +29,17 @@ def test_tma_attention_bit_identical_to_cp_async(tmp_path):
     f = (tma.astype(np.uint32) << 16).view(np.float32)
     assert np.isfinite(f).all()
     assert np.array_equal(tma, ref)
+
+
+def test_tcgen05_prompt_attention_matches(tmp_path):
+    """The tcgen05 chunked-prefill kernel (DS_ATTN_PROMPT=3: S and O accumulated in TMEM, P through
+    shared memory, 128-row query blocks) agrees with the mma.sync kernels within bf16 rounding
+    (different accumulation order, not bit-identical)."""
+    tc = _run(tmp_path, 3, 3)
+    ref = _run(tmp_path, 3, 2)
+    a = (tc.astype(np.uint32) << 16).view(np.float32).reshape(-1, 4096)
+    b = (ref.astype(np.uint32) << 16).view(np.float32).reshape(-1, 4096)
+    assert np.isfinite(a).all()
+    err = np.abs(a - b).max(axis=1)
+    scale = np.abs(b).max(axis=1)
+    assert np.all(err <= 0.02 * scale), float((err / scale).max())
