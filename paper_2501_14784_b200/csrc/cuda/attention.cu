@@ -651,8 +651,8 @@ struct PromptTcSmem {
     alignas(1024) __nv_bfloat16 q[2][kTcRows * 64];      // [dim half][row][64]
     alignas(1024) __nv_bfloat16 k[2][2][kTile * 64];     // [stage][dim half][token][64]
     alignas(1024) __nv_bfloat16 v[2][2][kTile * 64];     // [stage][dim half][token][64]
-    alignas(1024) __nv_bfloat16 p[kTcRows * kTile];      // [row][64 tokens], SW128
-    uint64_t full[2], empty[2], q_full, s_full, s_free, p_full, o_done;
+    alignas(1024) __nv_bfloat16 p[2][kTcRows * kTile];   // [buffer][row][64 tokens], SW128
+    uint64_t full[2], empty[2], q_full, s_full, s_free, p_full, o_done, p_free[2];
     uint32_t tmem;
 };
 
@@ -684,6 +684,8 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
         mbar_init(&sm.s_free, 128);
         mbar_init(&sm.p_full, 128);
         mbar_init(&sm.o_done, 1);
+        mbar_init(&sm.p_free[0], 1);
+        mbar_init(&sm.p_free[1], 1);
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc(&sm.tmem, 256);  // S [0, 64), O [128, 256)
@@ -750,12 +752,13 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
                 tc_fence_after();
 #pragma unroll
                 for (int ks = 0; ks < kTile / 16; ++ks) {
-                    const uint64_t a = umma_sdesc_sw128(smem_u32(&sm.p[0]) + ks * 32);
+                    const uint64_t a = umma_sdesc_sw128(smem_u32(&sm.p[j & 1][0]) + ks * 32);
                     // V: 16 tokens per step = two 8-token groups of 1024 B; dim halves 8 KB apart
                     const uint64_t b = umma_sdesc_sw128_mn(smem_u32(&sm.v[st][0][0]) + ks * 2048, 8192, 1024);
                     umma_bf16(tmem + 128, a, b, idesc_o, (j > 0 || ks > 0) ? 1u : 0u);
                 }
                 umma_commit(&sm.o_done);
+                umma_commit(&sm.p_free[j & 1]);
                 umma_commit(&sm.empty[st]);
             }
         }
@@ -764,7 +767,10 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
         const uint32_t lane_off = uint32_t((warp - 4) * 32) << 16;
         const int my_pos = r < rows ? pos0 + r / G : -1;
         const float qs = rsqrtf(float(DH)) * 1.4426950408889634f;
-        float m_run = -INFINITY, l_run = 0.f;
+        // online softmax with a lazily moved reference max (FlashAttention-4 practice): P is
+        // taken against m_ref and O, l are rescaled only when a row's max passes m_ref + 8
+        // (log2 units), so P <= 256 and most tiles need no TMEM round trip of O
+        float m_ref = -INFINITY, l_run = 0.f;
         for (int j = 0; j < n_tiles; ++j) {
             const int st = j & 1;
             const int tok0 = j * kTile;
@@ -782,37 +788,37 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
                 sv[c] = tok0 + c > my_pos ? -INFINITY : sv[c] * qs;
                 mt = fmaxf(mt, sv[c]);
             }
-            const float mn = fmaxf(m_run, mt);
-            const float alpha = mn == -INFINITY ? 1.f : exp2f(m_run - mn);
-            m_run = mn;
+            const bool move = mt > m_ref + 8.0f;  // includes the first finite max (m_ref = -inf)
+            const float m_new = move ? mt : m_ref;
+            const float alpha = (!move || m_ref == -INFINITY) ? 1.f : exp2f(m_ref - m_new);
+            m_ref = m_new;
             float ls = 0.f;
             uint32_t pk[kTile / 2];
 #pragma unroll
             for (int c = 0; c < kTile; c += 2) {
-                const float p0 = mn == -INFINITY ? 0.f : exp2f(sv[c] - mn);
-                const float p1 = mn == -INFINITY ? 0.f : exp2f(sv[c + 1] - mn);
+                const float p0 = m_new == -INFINITY ? 0.f : exp2f(sv[c] - m_new);
+                const float p1 = m_new == -INFINITY ? 0.f : exp2f(sv[c + 1] - m_new);
                 ls += p0 + p1;
                 pk[c / 2] = pack2(p0, p1);
             }
             l_run = l_run * alpha + ls;
-            if (j > 0) {
-                mbar_wait(&sm.o_done, uint32_t((j - 1) & 1));  // PV_{j-1} done: O stable, P free
+            if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+                mbar_wait(&sm.o_done, uint32_t((j - 1) & 1));  // PV_{j-1} done: O stable
                 tc_fence_after();
-                if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
-                    for (int c = 0; c < DH; c += 16) {
-                        uint32_t ov[16];
-                        tmem_ld16(tmem + 128 + lane_off + uint32_t(c), ov);
-                        tmem_ld_wait();
+                for (int c = 0; c < DH; c += 16) {
+                    uint32_t ov[16];
+                    tmem_ld16(tmem + 128 + lane_off + uint32_t(c), ov);
+                    tmem_ld_wait();
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-                        tmem_st16(tmem + 128 + lane_off + uint32_t(c), ov);
-                    }
-                    tmem_st_wait();
+                    for (int e = 0; e < 16; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+                    tmem_st16(tmem + 128 + lane_off + uint32_t(c), ov);
                 }
+                tmem_st_wait();
             }
+            if (j >= 2) mbar_wait(&sm.p_free[j & 1], uint32_t(((j >> 1) - 1) & 1));  // PV_{j-2} read it
             // P row r: 8 chunks of 8 tokens, 128-byte swizzle (chunk ^ row % 8)
-            uint8_t* prow = reinterpret_cast<uint8_t*>(&sm.p[0]) + r * 128;
+            uint8_t* prow = reinterpret_cast<uint8_t*>(&sm.p[j & 1][0]) + r * 128;
 #pragma unroll
             for (int c = 0; c < 8; ++c)
                 *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) =
