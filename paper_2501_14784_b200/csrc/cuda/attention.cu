@@ -652,7 +652,7 @@ struct PromptTcSmem {
     alignas(1024) __nv_bfloat16 k[2][2][kTile * 64];     // [stage][dim half][token][64]
     alignas(1024) __nv_bfloat16 v[2][2][kTile * 64];     // [stage][dim half][token][64]
     alignas(1024) __nv_bfloat16 p[2][kTcRows * kTile];   // [buffer][row][64 tokens], SW128
-    uint64_t full[2], empty[2], q_full, s_full, s_free, p_full, o_done, p_free[2];
+    uint64_t full[2], empty[2], q_full, s_full, s_free, p_full, p_free[2];
     uint32_t tmem;
 };
 
@@ -683,7 +683,6 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
         mbar_init(&sm.s_full, 1);
         mbar_init(&sm.s_free, 128);
         mbar_init(&sm.p_full, 128);
-        mbar_init(&sm.o_done, 1);
         mbar_init(&sm.p_free[0], 1);
         mbar_init(&sm.p_free[1], 1);
         fence_mbar_init();
@@ -757,7 +756,6 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
                     const uint64_t b = umma_sdesc_sw128_mn(smem_u32(&sm.v[st][0][0]) + ks * 2048, 8192, 1024);
                     umma_bf16(tmem + 128, a, b, idesc_o, (j > 0 || ks > 0) ? 1u : 0u);
                 }
-                umma_commit(&sm.o_done);
                 umma_commit(&sm.p_free[j & 1]);
                 umma_commit(&sm.empty[st]);
             }
@@ -803,7 +801,10 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
             }
             l_run = l_run * alpha + ls;
             if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-                mbar_wait(&sm.o_done, uint32_t((j - 1) & 1));  // PV_{j-1} done: O stable
+                // PV_{j-1} done: O stable. Waited on its P buffer's barrier: S_j having landed
+                // implies PV_{j-2} (and so every older use of that buffer) completed, so the parity
+                // window is exact even though most tiles skip this wait.
+                mbar_wait(&sm.p_free[(j - 1) & 1], uint32_t(((j - 1) >> 1) & 1));
                 tc_fence_after();
 #pragma unroll
                 for (int c = 0; c < DH; c += 16) {
@@ -837,8 +838,8 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
             tc_fence_before();
             mbar_arrive(&sm.p_full);
         }
-        // epilogue: O / l, bf16, scattered rows (position, head)
-        mbar_wait(&sm.o_done, uint32_t((n_tiles - 1) & 1));
+        // epilogue: O / l, bf16, scattered rows (position, head); PV_{n-1} (and so every PV) done
+        mbar_wait(&sm.p_free[(n_tiles - 1) & 1], uint32_t(((n_tiles - 1) >> 1) & 1));
         tc_fence_after();
         const float inv = l_run > 0.f ? 1.0f / l_run : 0.f;
         __nv_bfloat16* dst = r < rows ? o + (size_t(t0 + r / G) * n_h + kvh * G + r % G) * DH : nullptr;
