@@ -643,16 +643,19 @@ attn_prompt_tma_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __nv_b
 //                  P rows (bf16) written to shared memory as the next MMA's K-major A operand
 //   O += P . V     tcgen05.mma M=128 N=128 K=64 with V as an MN-major B operand (the page layout
 //                  [token][d_head] loaded by TMA, no transpose), O in TMEM, rescaled in place
-//                  (tcgen05.ld / st) when a row's running max moves
-// Warp roles: w0 TMA producer (Q once, K/V tiles double-buffered), w1 MMA issuer, w2 TMEM
-// allocator, w4-7 softmax / correction / epilogue.
+//                  (tcgen05.ld / st) only when a row's max passes its reference max by > 8
+//                  (log2 units; a lazily moved reference, so P <= 256)
+// Warp roles: w0 TMA producer (Q once, K/V tiles double-buffered), w1 MMA issuer (S_{j+1} issued
+// before PV_j so the QK^T of the next tile overlaps the softmax), w2 TMEM allocator, w4-7
+// softmax / correction / epilogue. P is double-buffered, each buffer with its own full / free
+// mbarrier pair, so the softmax of tile j+1 never waits for PV_j.
 constexpr int kTcRows = 128;
 struct PromptTcSmem {
     alignas(1024) __nv_bfloat16 q[2][kTcRows * 64];      // [dim half][row][64]
     alignas(1024) __nv_bfloat16 k[2][2][kTile * 64];     // [stage][dim half][token][64]
     alignas(1024) __nv_bfloat16 v[2][2][kTile * 64];     // [stage][dim half][token][64]
     alignas(1024) __nv_bfloat16 p[2][kTcRows * kTile];   // [buffer][row][64 tokens], SW128
-    uint64_t full[2], empty[2], q_full, s_full, s_free, p_full, p_free[2];
+    uint64_t full[2], empty[2], q_full, s_full, s_free, p_full[2], p_free[2];
     uint32_t tmem;
 };
 
@@ -682,7 +685,8 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
         mbar_init(&sm.q_full, 1);
         mbar_init(&sm.s_full, 1);
         mbar_init(&sm.s_free, 128);
-        mbar_init(&sm.p_full, 128);
+        mbar_init(&sm.p_full[0], 128);
+        mbar_init(&sm.p_full[1], 128);
         mbar_init(&sm.p_free[0], 1);
         mbar_init(&sm.p_free[1], 1);
         fence_mbar_init();
@@ -747,7 +751,9 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
             for (int j = 0; j < n_tiles; ++j) {
                 const int st = j & 1;
                 if (j + 1 < n_tiles) issue_s(j + 1);  // overlaps the softmax of tile j
-                mbar_wait(&sm.p_full, uint32_t(j & 1));  // P_j written, O rescaled
+                // P_j written, O rescaled. Per-buffer barrier: with two P buffers the softmax can
+                // finish tile j+1 before this wait, which would alias a single barrier's parity
+                mbar_wait(&sm.p_full[j & 1], uint32_t((j >> 1) & 1));
                 tc_fence_after();
 #pragma unroll
                 for (int ks = 0; ks < kTile / 16; ++ks) {
@@ -836,7 +842,7 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
             }
             fence_proxy_async_smem();  // P (and zeroed V) are read by the MMA's async proxy
             tc_fence_before();
-            mbar_arrive(&sm.p_full);
+            mbar_arrive(&sm.p_full[j & 1]);
         }
         // epilogue: O / l, bf16, scattered rows (position, head); PV_{n-1} (and so every PV) done
         mbar_wait(&sm.p_free[(n_tiles - 1) & 1], uint32_t(((n_tiles - 1) >> 1) & 1));

@@ -10,3 +10,5 @@ DS_ATTN_PROMPT=3 timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-basel
 echo "bench tc rc=$?"; python -c "import json;d=json.load(open('gpurun_out/tc_bench.json'));print(d['value'],d['ms_per_step'],{k:v['ms'] for k,v in d['roofline']['by_kind'].items()})"
 DS_ATTN_PROMPT=3 timeout 300 ncu --set full --clock-control none -k regex:attn_prompt_tc --launch-skip 3000 --launch-count 1 -o gpurun_out/tc_prompt -f python tools/step_driver.py --circuits 320 > gpurun_out/tc_ncu.log 2>&1
 python tools/summarize_ncu.py full gpurun_out/tc_prompt.ncu-rep > gpurun_out/tc_prompt_ncu.csv 2>&1; cat gpurun_out/tc_prompt_ncu.csv
+timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/tc_bench_default.json 2> gpurun_out/tc_bench_default.err
+echo "bench default rc=$?"; python -c "import json;d=json.load(open('gpurun_out/tc_bench_default.json'));print(d['value'],d['ms_per_step'],{k:v['ms'] for k,v in d['roofline']['by_kind'].items()})"
