@@ -639,62 +639,86 @@ attn_prompt_tma_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __nv_b
 // (query block of 128 rows = 128/G prompt positions x G heads, KV head), FlashAttention-style
 // over the request's 64-token KV tiles:
 //   S  = Q . K^T   tcgen05.mma M=128 N=64 K=128 (Q, K K-major SW128 tiles from TMA), S in TMEM
-//   P  = softmax   4 warps, one thread per row (TMEM lane), online max / sum in the log2 domain,
-//                  P rows (bf16) written to shared memory as the next MMA's K-major A operand
+//   P  = softmax   one thread per row (TMEM lane), online max / sum in the log2 domain, P rows
+//                  (bf16) written to shared memory as the next MMA's K-major A operand
 //   O += P . V     tcgen05.mma M=128 N=128 K=64 with V as an MN-major B operand (the page layout
-//                  [token][d_head] loaded by TMA, no transpose), O in TMEM, rescaled in place
-//                  (tcgen05.ld / st) only when a row's max passes its reference max by > 8
-//                  (log2 units; a lazily moved reference, so P <= 256)
-// Warp roles: w0 TMA producer (Q once, K/V tiles double-buffered), w1 MMA issuer (S_{j+1} issued
-// before PV_j so the QK^T of the next tile overlaps the softmax), w2 TMEM allocator, w4-7
-// softmax / correction / epilogue. P is double-buffered, each buffer with its own full / free
-// mbarrier pair, so the softmax of tile j+1 never waits for PV_j.
+//                  [token][d_head] loaded by TMA, no transpose), O in TMEM
+// The softmax is a latency chain per tile (TMEM load -> max -> exp2 -> pack -> shared store ->
+// fence -> arrive), so the tiles are split by parity between two independent softmax groups
+// (warps 4-7: even tiles, warps 8-11: odd tiles), each with its own S buffer, P buffer, O
+// accumulator, running max and sum: two chains in flight keep the tensor pipe fed (the
+// FlashAttention-4 ping-pong, here over KV tiles of one query tile so Q and every K/V tile are
+// staged once). The two partial softmax states merge in the epilogue. Each group moves its
+// reference max lazily (rescales O / l only when a row's max passes it by > 8 in log2 units).
+// Warp roles: w0 TMA producer (Q once, K/V tiles through a kTcStages ring), w1 S issuer (runs
+// ahead, bounded by the S buffers), w2 TMEM allocator, w3 PV issuer, w4-11 softmax.
+// TMEM columns: S even [0, 64), S odd [64, 128), O even [128, 256), O odd [256, 384).
 constexpr int kTcRows = 128;
+// K/V ring depth: a tile's MMAs take ~0.3 us, a TMA round trip from L2 / HBM ~1 us, so the loads
+// run 3 tiles ahead (2 stages left them exposed)
+constexpr int kTcStages = 4;
 struct PromptTcSmem {
-    alignas(1024) __nv_bfloat16 q[2][kTcRows * 64];      // [dim half][row][64]
-    alignas(1024) __nv_bfloat16 k[2][2][kTile * 64];     // [stage][dim half][token][64]
-    alignas(1024) __nv_bfloat16 v[2][2][kTile * 64];     // [stage][dim half][token][64]
-    alignas(1024) __nv_bfloat16 p[2][kTcRows * kTile];   // [buffer][row][64 tokens], SW128
-    uint64_t full[2], empty[2], q_full, s_full, s_free, p_full[2], p_free[2];
+    alignas(1024) __nv_bfloat16 q[2][kTcRows * 64];              // [dim half][row][64]
+    alignas(1024) __nv_bfloat16 k[kTcStages][2][kTile * 64];     // [stage][dim half][token][64]
+    alignas(1024) __nv_bfloat16 v[kTcStages][2][kTile * 64];     // [stage][dim half][token][64]
+    alignas(1024) __nv_bfloat16 p[2][kTcRows * kTile];           // [group][row][64 tokens], SW128
+    float m_x[2][kTcRows], l_x[2][kTcRows];                      // [group][row] epilogue merge
+    // per group g (tile parity): s_full / s_free (S buffer g), p_full / p_free (P buffer g and
+    // the group's PV into O_g)
+    uint64_t full[kTcStages], empty[kTcStages], q_full, s_full[2], s_free[2], p_full[2], p_free[2];
     uint32_t tmem;
 };
 
+// 2^x on the SFU without the denormal fix-up exp2f carries (P underflow to 0 is harmless)
+__device__ __forceinline__ float ex2_sfu(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+
 template <int G>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(384)
 attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_constant__ CUtensorMap tmap_q,
                       int n_h, const int32_t* __restrict__ row_pos, const int32_t* __restrict__ row_page_off,
                       const int32_t* __restrict__ flat_pages, const int32_t* __restrict__ blocks, KvLayout kv,
                       int layer, __nv_bfloat16* __restrict__ o) {
     constexpr int DH = 128;
-    constexpr int P_POS = kTcRows / G;  // prompt positions per block
-    pdl_launch_dependents();
     extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
     PromptTcSmem& sm = *reinterpret_cast<PromptTcSmem*>(
         (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_kv = kv.n_kv;
     const int kvh = blockIdx.x % n_kv;
-    const int bi = blockIdx.x / n_kv;
+    // blocks in reverse: a request's later query blocks walk more KV tiles, so the longest CTAs
+    // start in the first wave and the short ones fill the tail
+    const int bi = int(gridDim.x) / n_kv - 1 - int(blockIdx.x) / n_kv;
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmap_kv);
         tma_prefetch_desc(&tmap_q);
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kTcStages; ++b) {
             mbar_init(&sm.full[b], 1);
             mbar_init(&sm.empty[b], 1);
         }
         mbar_init(&sm.q_full, 1);
-        mbar_init(&sm.s_full, 1);
-        mbar_init(&sm.s_free, 128);
-        mbar_init(&sm.p_full[0], 128);
-        mbar_init(&sm.p_full[1], 128);
-        mbar_init(&sm.p_free[0], 1);
-        mbar_init(&sm.p_free[1], 1);
+        for (int g = 0; g < 2; ++g) {
+            mbar_init(&sm.s_full[g], 1);
+            mbar_init(&sm.s_free[g], 128);
+            mbar_init(&sm.p_full[g], 128);
+            mbar_init(&sm.p_free[g], 1);
+        }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc(&sm.tmem, 256);  // S [0, 64), O [128, 256)
+    if (warp == 2) tmem_alloc(&sm.tmem, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    // dependents launch only once every CTA holds its TMEM: a PDL-launched GEMM CTA that took
+    // columns first on this SM would wait for this grid while this CTA waits for its columns
+    pdl_launch_dependents();
     const uint32_t tmem = sm.tmem;
     pdl_wait();
     const int t0 = blocks[3 * bi], npos = blocks[3 * bi + 1];
@@ -718,8 +742,8 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
                     "r"(kvh * G), "r"(t0)
                     : "memory");
             for (int j = 0; j < n_tiles; ++j) {
-                const int st = j & 1;
-                if (j >= 2) mbar_wait(&sm.empty[st], uint32_t(((j >> 1) - 1) & 1));
+                const int st = j % kTcStages;
+                if (j >= kTcStages) mbar_wait(&sm.empty[st], uint32_t((j / kTcStages - 1) & 1));
                 const int tok0 = j * kTile;
                 const int base = pages[tok0 >> 8] * rows_per_page + (tok0 & 255);
                 mbar_arrive_expect_tx(&sm.full[st], uint32_t(2 * kTile * DH * 2));
@@ -730,134 +754,155 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (lane == 0) {  // S_j = Q . K_j^T into S buffer j % 2
             const uint32_t idesc_s = umma_idesc_bf16(kTcRows, kTile);
-            const uint32_t idesc_o = umma_idesc_bf16_bmn(kTcRows, DH);
-            auto issue_s = [&](int j) {  // S_j = Q . K_j^T into TMEM columns [0, 64)
-                const int st = j & 1;
-                mbar_wait(&sm.full[st], uint32_t((j >> 1) & 1));
-                if (j > 0) mbar_wait(&sm.s_free, uint32_t((j - 1) & 1));  // S_{j-1} read out
+            mbar_wait(&sm.q_full, 0);
+            for (int j = 0; j < n_tiles; ++j) {
+                const int st = j % kTcStages, g = j & 1;
+                mbar_wait(&sm.full[st], uint32_t((j / kTcStages) & 1));
+                if (j >= 2) mbar_wait(&sm.s_free[g], uint32_t(((j >> 1) - 1) & 1));  // S_{j-2} read out
                 tc_fence_after();
 #pragma unroll
                 for (int ks = 0; ks < DH / 16; ++ks) {
                     const uint64_t a = umma_sdesc_sw128(smem_u32(&sm.q[ks >> 2][0]) + (ks & 3) * 32);
                     const uint64_t b = umma_sdesc_sw128(smem_u32(&sm.k[st][ks >> 2][0]) + (ks & 3) * 32);
-                    umma_bf16(tmem, a, b, idesc_s, ks > 0 ? 1u : 0u);
+                    umma_bf16(tmem + uint32_t(g * kTile), a, b, idesc_s, ks > 0 ? 1u : 0u);
                 }
-                umma_commit(&sm.s_full);
-            };
-            mbar_wait(&sm.q_full, 0);
-            if (n_tiles > 0) issue_s(0);
+                umma_commit(&sm.s_full[g]);
+            }
+        }
+    } else if (warp == 3) {
+        if (lane == 0) {  // O_g += P_j . V_j, g = j % 2
+            const uint32_t idesc_o = umma_idesc_bf16_bmn(kTcRows, DH);
             for (int j = 0; j < n_tiles; ++j) {
-                const int st = j & 1;
-                if (j + 1 < n_tiles) issue_s(j + 1);  // overlaps the softmax of tile j
-                // P_j written, O rescaled. Per-buffer barrier: with two P buffers the softmax can
-                // finish tile j+1 before this wait, which would alias a single barrier's parity
-                mbar_wait(&sm.p_full[j & 1], uint32_t((j >> 1) & 1));
+                const int st = j % kTcStages, g = j & 1;
+                mbar_wait(&sm.p_full[g], uint32_t((j >> 1) & 1));  // P_j written, O_g rescaled
                 tc_fence_after();
 #pragma unroll
                 for (int ks = 0; ks < kTile / 16; ++ks) {
-                    const uint64_t a = umma_sdesc_sw128(smem_u32(&sm.p[j & 1][0]) + ks * 32);
+                    const uint64_t a = umma_sdesc_sw128(smem_u32(&sm.p[g][0]) + ks * 32);
                     // V: 16 tokens per step = two 8-token groups of 1024 B; dim halves 8 KB apart
                     const uint64_t b = umma_sdesc_sw128_mn(smem_u32(&sm.v[st][0][0]) + ks * 2048, 8192, 1024);
-                    umma_bf16(tmem + 128, a, b, idesc_o, (j > 0 || ks > 0) ? 1u : 0u);
+                    umma_bf16(tmem + 128 + uint32_t(g * DH), a, b, idesc_o, (j >= 2 || ks > 0) ? 1u : 0u);
                 }
-                umma_commit(&sm.p_free[j & 1]);
-                umma_commit(&sm.empty[st]);
+                umma_commit(&sm.p_free[g]);
+                umma_commit(&sm.empty[st]);  // S_j (K) completed before P_j existed
             }
         }
     } else if (warp >= 4) {
-        const int r = (warp - 4) * 32 + lane;  // this thread's row = TMEM lane
-        const uint32_t lane_off = uint32_t((warp - 4) * 32) << 16;
+        const int grp = (warp - 4) >> 2, quarter = warp & 3;
+        const int r = quarter * 32 + lane;  // this thread's row = TMEM lane
+        const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+        const uint32_t o_col = 128 + uint32_t(grp * DH);
         const int my_pos = r < rows ? pos0 + r / G : -1;
         const float qs = rsqrtf(float(DH)) * 1.4426950408889634f;
-        // online softmax with a lazily moved reference max (FlashAttention-4 practice): P is
-        // taken against m_ref and O, l are rescaled only when a row's max passes m_ref + 8
-        // (log2 units), so P <= 256 and most tiles need no TMEM round trip of O
+        const uint32_t prow = smem_u32(&sm.p[grp][0]) + uint32_t(r * 128);
         float m_ref = -INFINITY, l_run = 0.f;
-        for (int j = 0; j < n_tiles; ++j) {
-            const int st = j & 1;
+        for (int j = grp; j < n_tiles; j += 2) {
+            const int st = j % kTcStages, u = j >> 1;  // u: this group's use count of its buffers
             const int tok0 = j * kTile;
-            mbar_wait(&sm.s_full, uint32_t(j & 1));
+            mbar_wait(&sm.s_full[grp], uint32_t(u & 1));
             tc_fence_after();
             float sv[kTile];
 #pragma unroll
-            for (int c = 0; c < kTile; c += 16) tmem_ld16(tmem + lane_off + uint32_t(c), reinterpret_cast<uint32_t*>(sv + c));
+            for (int c = 0; c < kTile; c += 16)
+                tmem_ld16(tmem + lane_off + uint32_t(grp * kTile + c), reinterpret_cast<uint32_t*>(sv + c));
             tmem_ld_wait();
             tc_fence_before();
-            mbar_arrive(&sm.s_free);
+            mbar_arrive(&sm.s_free[grp]);
+            // max over the raw scores (the scale qs > 0 keeps the order), scaled once; the causal
+            // mask only touches the tiles that reach this row's position
+            if (tok0 + kTile - 1 > my_pos) {
+#pragma unroll
+                for (int c = 0; c < kTile; ++c)
+                    if (tok0 + c > my_pos) sv[c] = -INFINITY;
+            }
             float mt = -INFINITY;
 #pragma unroll
-            for (int c = 0; c < kTile; ++c) {
-                sv[c] = tok0 + c > my_pos ? -INFINITY : sv[c] * qs;
-                mt = fmaxf(mt, sv[c]);
-            }
+            for (int c = 0; c < kTile; ++c) mt = fmaxf(mt, sv[c]);
+            mt *= qs;
             const bool move = mt > m_ref + 8.0f;  // includes the first finite max (m_ref = -inf)
             const float m_new = move ? mt : m_ref;
-            const float alpha = (!move || m_ref == -INFINITY) ? 1.f : exp2f(m_ref - m_new);
+            const float alpha = (!move || m_ref == -INFINITY) ? 1.f : ex2_sfu(m_ref - m_new);
             m_ref = m_new;
+            const float neg_m = m_new == -INFINITY ? 0.f : -m_new;  // all-masked row: exp2(-inf) = 0
             float ls = 0.f;
             uint32_t pk[kTile / 2];
 #pragma unroll
             for (int c = 0; c < kTile; c += 2) {
-                const float p0 = m_new == -INFINITY ? 0.f : exp2f(sv[c] - m_new);
-                const float p1 = m_new == -INFINITY ? 0.f : exp2f(sv[c + 1] - m_new);
+                const float p0 = ex2_sfu(fmaf(sv[c], qs, neg_m));
+                const float p1 = ex2_sfu(fmaf(sv[c + 1], qs, neg_m));
                 ls += p0 + p1;
                 pk[c / 2] = pack2(p0, p1);
             }
             l_run = l_run * alpha + ls;
-            if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-                // PV_{j-1} done: O stable. Waited on its P buffer's barrier: S_j having landed
-                // implies PV_{j-2} (and so every older use of that buffer) completed, so the parity
-                // window is exact even though most tiles skip this wait.
-                mbar_wait(&sm.p_free[(j - 1) & 1], uint32_t(((j - 1) >> 1) & 1));
+            // this group's previous PV (tile j-2) done: O_g stable and P buffer g free. The
+            // window is exact: the group awaited the use before it at tile j-2.
+            if (j >= 2) {
+                mbar_wait(&sm.p_free[grp], uint32_t((u - 1) & 1));
                 tc_fence_after();
+                if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
-                for (int c = 0; c < DH; c += 16) {
-                    uint32_t ov[16];
-                    tmem_ld16(tmem + 128 + lane_off + uint32_t(c), ov);
-                    tmem_ld_wait();
+                    for (int c = 0; c < DH; c += 16) {
+                        uint32_t ov[16];
+                        tmem_ld16(tmem + lane_off + o_col + uint32_t(c), ov);
+                        tmem_ld_wait();
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-                    tmem_st16(tmem + 128 + lane_off + uint32_t(c), ov);
+                        for (int e = 0; e < 16; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+                        tmem_st16(tmem + lane_off + o_col + uint32_t(c), ov);
+                    }
+                    tmem_st_wait();
                 }
-                tmem_st_wait();
             }
-            if (j >= 2) mbar_wait(&sm.p_free[j & 1], uint32_t(((j >> 1) - 1) & 1));  // PV_{j-2} read it
             // P row r: 8 chunks of 8 tokens, 128-byte swizzle (chunk ^ row % 8)
-            uint8_t* prow = reinterpret_cast<uint8_t*>(&sm.p[j & 1][0]) + r * 128;
 #pragma unroll
             for (int c = 0; c < 8; ++c)
-                *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) =
-                    make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+                sts128(prow + uint32_t((c ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
             // V rows past the last valid token must be zero (0 * garbage must not be NaN)
             const int valid = min(kTile, last_pos + 1 - tok0);
             if (valid < kTile) {
-                mbar_wait(&sm.full[st], uint32_t((j >> 1) & 1));  // the tile landed (already, for S)
+                mbar_wait(&sm.full[st], uint32_t((j / kTcStages) & 1));  // the tile landed (already, for S)
                 for (int i = r; i < (kTile - valid) * 16; i += 128) {
                     const int tr = valid + i / 16, c = i % 16;  // token row, 16-byte chunk over 128 dims
-                    uint8_t* vb = reinterpret_cast<uint8_t*>(&sm.v[st][c >> 3][0]);
-                    *reinterpret_cast<uint4*>(vb + tr * 128 + (((c & 7) ^ (tr & 7)) << 4)) = make_uint4(0, 0, 0, 0);
+                    sts128(smem_u32(&sm.v[st][c >> 3][0]) + uint32_t(tr * 128 + (((c & 7) ^ (tr & 7)) << 4)), 0, 0, 0, 0);
                 }
             }
             fence_proxy_async_smem();  // P (and zeroed V) are read by the MMA's async proxy
             tc_fence_before();
-            mbar_arrive(&sm.p_full[j & 1]);
+            mbar_arrive(&sm.p_full[grp]);
         }
-        // epilogue: O / l, bf16, scattered rows (position, head); PV_{n-1} (and so every PV) done
-        mbar_wait(&sm.p_free[(n_tiles - 1) & 1], uint32_t(((n_tiles - 1) >> 1) & 1));
-        tc_fence_after();
-        const float inv = l_run > 0.f ? 1.0f / l_run : 0.f;
-        __nv_bfloat16* dst = r < rows ? o + (size_t(t0 + r / G) * n_h + kvh * G + r % G) * DH : nullptr;
+        // epilogue: merge the two groups' (O, max, sum) per row; group g writes O columns
+        // [64 g, 64 g + 64). The exchange comes first: after it the partner has passed its own
+        // last P-buffer wait, so both groups' final PV waits below have exact parity windows.
+        sm.m_x[grp][r] = m_ref;
+        sm.l_x[grp][r] = l_run;
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");  // warps w and w + 4
+        const float m0 = sm.m_x[0][r], m1 = sm.m_x[1][r];
+        const float mx = fmaxf(m0, m1);
+        const float a0 = m0 == -INFINITY ? 0.f : ex2_sfu(m0 - mx);
+        const float a1 = m1 == -INFINITY ? 0.f : ex2_sfu(m1 - mx);
+        const float l_row = sm.l_x[0][r] * a0 + sm.l_x[1][r] * a1;
+        const int n_g[2] = {(n_tiles + 1) >> 1, n_tiles >> 1};  // tiles per group
 #pragma unroll
-        for (int c = 0; c < DH; c += 16) {
-            uint32_t ov[16];
-            tmem_ld16(tmem + 128 + lane_off + uint32_t(c), ov);
+        for (int g = 0; g < 2; ++g)
+            if (n_g[g] > 0) mbar_wait(&sm.p_free[g], uint32_t((n_g[g] - 1) & 1));
+        tc_fence_after();
+        const float inv = l_row > 0.f ? 1.0f / l_row : 0.f;
+        const float w0 = a0 * inv, w1 = n_g[1] > 0 ? a1 * inv : 0.f;
+        __nv_bfloat16* dst =
+            r < rows ? o + (size_t(t0 + r / G) * n_h + kvh * G + r % G) * DH + grp * (DH / 2) : nullptr;
+#pragma unroll
+        for (int c = 0; c < DH / 2; c += 16) {
+            const uint32_t col = uint32_t(grp * (DH / 2) + c);
+            uint32_t o0[16], o1[16];
+            tmem_ld16(tmem + lane_off + 128 + col, o0);
+            if (n_g[1] > 0) tmem_ld16(tmem + lane_off + 128 + DH + col, o1);
             tmem_ld_wait();
             if (dst) {
                 float f[16];
 #pragma unroll
-                for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(ov[e]) * inv;
+                for (int e = 0; e < 16; ++e)
+                    f[e] = __uint_as_float(o0[e]) * w0 + (n_g[1] > 0 ? __uint_as_float(o1[e]) * w1 : 0.f);
                 reinterpret_cast<uint4*>(dst + c)[0] = pack8(f);
                 reinterpret_cast<uint4*>(dst + c)[1] = pack8(f + 8);
             }
@@ -867,7 +912,7 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem, 256);
+        tmem_dealloc(tmem, 512);
     }
 }
 
@@ -1673,7 +1718,7 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
     if (n_blocks > 0 && prompt_tc(n_h, kv.n_kv, DH) && kv.tmap64 && kv.tmap_q) {
         const CUtensorMap& tk = *static_cast<const CUtensorMap*>(kv.tmap64);
         const CUtensorMap& tq = *static_cast<const CUtensorMap*>(kv.tmap_q);
-        const dim3 g(n_blocks * kv.n_kv), b(256);
+        const dim3 g(n_blocks * kv.n_kv), b(384);
         const size_t sm_bytes = sizeof(PromptTcSmem) + 1024;
         switch (n_h / kv.n_kv) {
             case 1: launch_pdl(attn_prompt_tc_kernel<1>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o); break;
