@@ -650,8 +650,8 @@ attn_prompt_tma_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __nv_b
 // FlashAttention-4 ping-pong, here over KV tiles of one query tile so Q and every K/V tile are
 // staged once). The two partial softmax states merge in the epilogue. Each group moves its
 // reference max lazily (rescales O / l only when a row's max passes it by > 8 in log2 units).
-// Warp roles: w0 TMA producer (Q once, K/V tiles through a kTcStages ring), w1 S issuer (runs
-// ahead, bounded by the S buffers), w2 TMEM allocator, w3 PV issuer, w4-11 softmax.
+// Warp roles: w0 TMA producer of Q and the K ring, w1 S issuer (runs ahead, bounded by the S
+// buffers), w2 TMEM allocator then V-ring producer, w3 PV issuer, w4-11 softmax.
 // TMEM columns: S even [0, 64), S odd [64, 128), O even [128, 256), O odd [256, 384).
 constexpr int kTcRows = 128;
 // K/V ring depth: a tile's MMAs take ~0.3 us, a TMA round trip from L2 / HBM ~1 us, so the loads
@@ -665,7 +665,10 @@ struct PromptTcSmem {
     float m_x[2][kTcRows], l_x[2][kTcRows];                      // [group][row] epilogue merge
     // per group g (tile parity): s_full / s_free (S buffer g), p_full / p_free (P buffer g and
     // the group's PV into O_g)
-    uint64_t full[kTcStages], empty[kTcStages], q_full, s_full[2], s_free[2], p_full[2], p_free[2];
+    // K and V rings are separate: K_j frees when S_j completes (long before PV_j), so the K loads
+    // run further ahead than a joint ring allows
+    uint64_t k_full[kTcStages], k_empty[kTcStages], v_full[kTcStages], v_empty[kTcStages];
+    uint64_t q_full, s_full[2], s_free[2], p_full[2], p_free[2];
     uint32_t tmem;
 };
 
@@ -685,7 +688,7 @@ __global__ void __launch_bounds__(384)
 attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_constant__ CUtensorMap tmap_q,
                       int n_h, const int32_t* __restrict__ row_pos, const int32_t* __restrict__ row_page_off,
                       const int32_t* __restrict__ flat_pages, const int32_t* __restrict__ blocks, KvLayout kv,
-                      int layer, __nv_bfloat16* __restrict__ o) {
+                      int layer, __nv_bfloat16* __restrict__ o, int dbg) {
     constexpr int DH = 128;
     extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
     PromptTcSmem& sm = *reinterpret_cast<PromptTcSmem*>(
@@ -700,8 +703,10 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
         tma_prefetch_desc(&tmap_kv);
         tma_prefetch_desc(&tmap_q);
         for (int b = 0; b < kTcStages; ++b) {
-            mbar_init(&sm.full[b], 1);
-            mbar_init(&sm.empty[b], 1);
+            mbar_init(&sm.k_full[b], 1);
+            mbar_init(&sm.k_empty[b], 1);
+            mbar_init(&sm.v_full[b], 1);
+            mbar_init(&sm.v_empty[b], 1);
         }
         mbar_init(&sm.q_full, 1);
         for (int g = 0; g < 2; ++g) {
@@ -741,16 +746,28 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
                     "l"(reinterpret_cast<uint64_t>(&tmap_q)), "r"(smem_u32(&sm.q_full)), "r"(bx * 64),
                     "r"(kvh * G), "r"(t0)
                     : "memory");
-            for (int j = 0; j < n_tiles; ++j) {
+            for (int j = 0; j < n_tiles; ++j) {  // K tiles
                 const int st = j % kTcStages;
-                if (j >= kTcStages) mbar_wait(&sm.empty[st], uint32_t((j / kTcStages - 1) & 1));
+                if (j >= kTcStages) mbar_wait(&sm.k_empty[st], uint32_t((j / kTcStages - 1) & 1));
                 const int tok0 = j * kTile;
                 const int base = pages[tok0 >> 8] * rows_per_page + (tok0 & 255);
-                mbar_arrive_expect_tx(&sm.full[st], uint32_t(2 * kTile * DH * 2));
-                for (int bx = 0; bx < 2; ++bx) {
-                    tma_load_2d(&sm.k[st][bx][0], &tmap_kv, &sm.full[st], bx * 64, base + row_k * 256);
-                    tma_load_2d(&sm.v[st][bx][0], &tmap_kv, &sm.full[st], bx * 64, base + row_v * 256);
-                }
+                if (dbg & 8) { mbar_arrive(&sm.k_full[st]); continue; }
+                mbar_arrive_expect_tx(&sm.k_full[st], uint32_t(kTile * DH * 2));
+                for (int bx = 0; bx < 2; ++bx)
+                    tma_load_2d(&sm.k[st][bx][0], &tmap_kv, &sm.k_full[st], bx * 64, base + row_k * 256);
+            }
+        }
+    } else if (warp == 2) {
+        if (lane == 0) {
+            for (int j = 0; j < n_tiles; ++j) {  // V tiles
+                const int st = j % kTcStages;
+                if (j >= kTcStages) mbar_wait(&sm.v_empty[st], uint32_t((j / kTcStages - 1) & 1));
+                const int tok0 = j * kTile;
+                const int base = pages[tok0 >> 8] * rows_per_page + (tok0 & 255);
+                if (dbg & 8) { mbar_arrive(&sm.v_full[st]); continue; }
+                mbar_arrive_expect_tx(&sm.v_full[st], uint32_t(kTile * DH * 2));
+                for (int bx = 0; bx < 2; ++bx)
+                    tma_load_2d(&sm.v[st][bx][0], &tmap_kv, &sm.v_full[st], bx * 64, base + row_v * 256);
             }
         }
     } else if (warp == 1) {
@@ -759,16 +776,18 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
             mbar_wait(&sm.q_full, 0);
             for (int j = 0; j < n_tiles; ++j) {
                 const int st = j % kTcStages, g = j & 1;
-                mbar_wait(&sm.full[st], uint32_t((j / kTcStages) & 1));
+                mbar_wait(&sm.k_full[st], uint32_t((j / kTcStages) & 1));
                 if (j >= 2) mbar_wait(&sm.s_free[g], uint32_t(((j >> 1) - 1) & 1));  // S_{j-2} read out
                 tc_fence_after();
 #pragma unroll
                 for (int ks = 0; ks < DH / 16; ++ks) {
+                    if (dbg & 4) break;
                     const uint64_t a = umma_sdesc_sw128(smem_u32(&sm.q[ks >> 2][0]) + (ks & 3) * 32);
                     const uint64_t b = umma_sdesc_sw128(smem_u32(&sm.k[st][ks >> 2][0]) + (ks & 3) * 32);
                     umma_bf16(tmem + uint32_t(g * kTile), a, b, idesc_s, ks > 0 ? 1u : 0u);
                 }
                 umma_commit(&sm.s_full[g]);
+                umma_commit(&sm.k_empty[st]);
             }
         }
     } else if (warp == 3) {
@@ -777,16 +796,18 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
             for (int j = 0; j < n_tiles; ++j) {
                 const int st = j % kTcStages, g = j & 1;
                 mbar_wait(&sm.p_full[g], uint32_t((j >> 1) & 1));  // P_j written, O_g rescaled
+                mbar_wait(&sm.v_full[st], uint32_t((j / kTcStages) & 1));
                 tc_fence_after();
 #pragma unroll
                 for (int ks = 0; ks < kTile / 16; ++ks) {
+                    if (dbg & 2) break;
                     const uint64_t a = umma_sdesc_sw128(smem_u32(&sm.p[g][0]) + ks * 32);
                     // V: 16 tokens per step = two 8-token groups of 1024 B; dim halves 8 KB apart
                     const uint64_t b = umma_sdesc_sw128_mn(smem_u32(&sm.v[st][0][0]) + ks * 2048, 8192, 1024);
                     umma_bf16(tmem + 128 + uint32_t(g * DH), a, b, idesc_o, (j >= 2 || ks > 0) ? 1u : 0u);
                 }
                 umma_commit(&sm.p_free[g]);
-                umma_commit(&sm.empty[st]);  // S_j (K) completed before P_j existed
+                umma_commit(&sm.v_empty[st]);
             }
         }
     } else if (warp >= 4) {
@@ -830,8 +851,8 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
             uint32_t pk[kTile / 2];
 #pragma unroll
             for (int c = 0; c < kTile; c += 2) {
-                const float p0 = ex2_sfu(fmaf(sv[c], qs, neg_m));
-                const float p1 = ex2_sfu(fmaf(sv[c + 1], qs, neg_m));
+                const float p0 = (dbg & 1) ? sv[c] : ex2_sfu(fmaf(sv[c], qs, neg_m));
+                const float p1 = (dbg & 1) ? sv[c + 1] : ex2_sfu(fmaf(sv[c + 1], qs, neg_m));
                 ls += p0 + p1;
                 pk[c / 2] = pack2(p0, p1);
             }
@@ -861,7 +882,7 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
             // V rows past the last valid token must be zero (0 * garbage must not be NaN)
             const int valid = min(kTile, last_pos + 1 - tok0);
             if (valid < kTile) {
-                mbar_wait(&sm.full[st], uint32_t((j / kTcStages) & 1));  // the tile landed (already, for S)
+                mbar_wait(&sm.v_full[st], uint32_t((j / kTcStages) & 1));  // V_j landed
                 for (int i = r; i < (kTile - valid) * 16; i += 128) {
                     const int tr = valid + i / 16, c = i % 16;  // token row, 16-byte chunk over 128 dims
                     sts128(smem_u32(&sm.v[st][c >> 3][0]) + uint32_t(tr * 128 + (((c & 7) ^ (tr & 7)) << 4)), 0, 0, 0, 0);
@@ -1631,6 +1652,12 @@ attn_decode_tma_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __nv_b
 
 // DS_ATTN_PROMPT: 1 cp.async-staged mma.sync kernel, 2 TMA-staged mma.sync kernel, 3 tcgen05
 // kernel (d_head 128, G <= 8, no prompt context splits; 128-row query blocks)
+// timing experiments only (results invalid): DS_TC_DBG bit 0 no exp2, 1 no PV MMAs, 2 no S MMAs,
+// 3 no K/V loads
+static int tc_dbg() {
+    static const int v = getenv("DS_TC_DBG") ? atoi(getenv("DS_TC_DBG")) : 0;
+    return v;
+}
 static int prompt_kernel_env() {
     static const int v = getenv("DS_ATTN_PROMPT") ? atoi(getenv("DS_ATTN_PROMPT")) : 2;
     return v;
@@ -1721,10 +1748,10 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
         const dim3 g(n_blocks * kv.n_kv), b(384);
         const size_t sm_bytes = sizeof(PromptTcSmem) + 1024;
         switch (n_h / kv.n_kv) {
-            case 1: launch_pdl(attn_prompt_tc_kernel<1>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o); break;
-            case 2: launch_pdl(attn_prompt_tc_kernel<2>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o); break;
-            case 4: launch_pdl(attn_prompt_tc_kernel<4>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o); break;
-            default: launch_pdl(attn_prompt_tc_kernel<8>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o); break;
+            case 1: launch_pdl(attn_prompt_tc_kernel<1>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o, tc_dbg()); break;
+            case 2: launch_pdl(attn_prompt_tc_kernel<2>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o, tc_dbg()); break;
+            case 4: launch_pdl(attn_prompt_tc_kernel<4>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o, tc_dbg()); break;
+            default: launch_pdl(attn_prompt_tc_kernel<8>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o, tc_dbg()); break;
         }
     } else if (n_blocks > 0 && prompt_env >= 2 && kv.tmap64)
         launch_pdl(attn_prompt_tma_kernel<DH>, dim3(n_blocks * kv.n_kv * sp), dim3(kPromptWarps * 32),
