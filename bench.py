@@ -333,7 +333,7 @@ def run_reference(args):
 
 
 # timing-experiment switches that skip work (their results are invalid): the bench refuses them
-INVALIDATING_ENV = ("DS_SKIP", "DS_ATTN_SKIP", "DS_GEMM_NOFINISH", "DS_GEMM_TRACE")
+INVALIDATING_ENV = ("DS_SKIP", "DS_ATTN_SKIP", "DS_GEMM_NOFINISH", "DS_GEMM_TRACE", "DS_TC_DBG")
 
 
 def ds_env():

@@ -1650,16 +1650,17 @@ attn_decode_tma_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __nv_b
     }
 }
 
-// DS_ATTN_PROMPT: 1 cp.async-staged mma.sync kernel, 2 TMA-staged mma.sync kernel, 3 tcgen05
-// kernel (d_head 128, G <= 8, no prompt context splits; 128-row query blocks)
 // timing experiments only (results invalid): DS_TC_DBG bit 0 no exp2, 1 no PV MMAs, 2 no S MMAs,
 // 3 no K/V loads
 static int tc_dbg() {
     static const int v = getenv("DS_TC_DBG") ? atoi(getenv("DS_TC_DBG")) : 0;
     return v;
 }
+// DS_ATTN_PROMPT: 1 cp.async-staged mma.sync kernel, 2 TMA-staged mma.sync kernel, 3 (default)
+// tcgen05 kernel where it applies (d_head 128, G <= 8, no prompt context splits; 128-row query
+// blocks), else 2
 static int prompt_kernel_env() {
-    static const int v = getenv("DS_ATTN_PROMPT") ? atoi(getenv("DS_ATTN_PROMPT")) : 2;
+    static const int v = getenv("DS_ATTN_PROMPT") ? atoi(getenv("DS_ATTN_PROMPT")) : 3;
     return v;
 }
 static bool prompt_tc(int n_h, int n_kv, int d_head) {
