@@ -640,9 +640,10 @@ attn_prompt_tma_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __nv_b
 // over the request's 64-token KV tiles:
 //   S  = Q . K^T   tcgen05.mma M=128 N=64 K=128 (Q, K K-major SW128 tiles from TMA), S in TMEM
 //   P  = softmax   one thread per row (TMEM lane), online max / sum in the log2 domain, P rows
-//                  (bf16) written to shared memory as the next MMA's K-major A operand
-//   O += P . V     tcgen05.mma M=128 N=128 K=64 with V as an MN-major B operand (the page layout
-//                  [token][d_head] loaded by TMA, no transpose), O in TMEM
+//                  (bf16 pairs) stored back into TMEM (tcgen05.st) as the next MMA's A operand
+//   O += P . V     tcgen05.mma M=128 N=128 K=64 with P read from TMEM and V as an MN-major B
+//                  operand (the page layout [token][d_head] loaded by TMA, no transpose), O in
+//                  TMEM -- P never touches shared memory, whose bandwidth bounds this kernel
 // The softmax is a latency chain per tile (TMEM load -> max -> exp2 -> pack -> shared store ->
 // fence -> arrive), so the tiles are split by parity between two independent softmax groups
 // (warps 4-7: even tiles, warps 8-11: odd tiles), each with its own S buffer, P buffer, O
@@ -650,9 +651,11 @@ attn_prompt_tma_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __nv_b
 // FlashAttention-4 ping-pong, here over KV tiles of one query tile so Q and every K/V tile are
 // staged once). The two partial softmax states merge in the epilogue. Each group moves its
 // reference max lazily (rescales O / l only when a row's max passes it by > 8 in log2 units).
-// Warp roles: w0 TMA producer of Q and the K ring, w1 S issuer (runs ahead, bounded by the S
-// buffers), w2 TMEM allocator then V-ring producer, w3 PV issuer, w4-11 softmax.
-// TMEM columns: S even [0, 64), S odd [64, 128), O even [128, 256), O odd [256, 384).
+// Warp roles: w0 TMA producer of Q and the K ring, w1 / w3 MMA issuers of the even / odd group
+// (S_{j+2} issued as soon as S_j is read, ahead of PV_j), w2 TMEM allocator then V-ring
+// producer, w4-11 softmax.
+// TMEM columns: S even [0, 64), S odd [64, 128), O even [128, 256), O odd [256, 384), P even
+// [384, 416), P odd [416, 448).
 constexpr int kTcRows = 128;
 // K/V ring depth: a tile's MMAs take ~0.3 us, a TMA round trip from L2 / HBM ~1 us, so the loads
 // run 3 tiles ahead (2 stages left them exposed)
@@ -661,7 +664,6 @@ struct PromptTcSmem {
     alignas(1024) __nv_bfloat16 q[2][kTcRows * 64];              // [dim half][row][64]
     alignas(1024) __nv_bfloat16 k[kTcStages][2][kTile * 64];     // [stage][dim half][token][64]
     alignas(1024) __nv_bfloat16 v[kTcStages][2][kTile * 64];     // [stage][dim half][token][64]
-    alignas(1024) __nv_bfloat16 p[2][kTcRows * kTile];           // [group][row][64 tokens], SW128
     float m_x[2][kTcRows], l_x[2][kTcRows];                      // [group][row] epilogue merge
     // per group g (tile parity): s_full / s_free (S buffer g), p_full / p_free (P buffer g and
     // the group's PV into O_g)
@@ -770,12 +772,16 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
                     tma_load_2d(&sm.v[st][bx][0], &tmap_kv, &sm.v_full[st], bx * 64, base + row_v * 256);
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {  // S_j = Q . K_j^T into S buffer j % 2
+    } else if (warp == 1 || warp == 3) {
+        // one MMA issuer per softmax group (warp 1: even tiles, warp 3: odd tiles): a
+        // tcgen05.mma costs its issuing thread ~100 cycles, about 3x the tensor time of an
+        // M128 N64 K16 step, so a single issuer for both groups paced the whole kernel
+        if (lane == 0) {
+            const int g = warp >> 1;
             const uint32_t idesc_s = umma_idesc_bf16(kTcRows, kTile);
-            mbar_wait(&sm.q_full, 0);
-            for (int j = 0; j < n_tiles; ++j) {
-                const int st = j % kTcStages, g = j & 1;
+            const uint32_t idesc_o = umma_idesc_bf16_bmn(kTcRows, DH);
+            auto issue_s = [&](int j) {  // S_j = Q . K_j^T into S buffer g
+                const int st = j % kTcStages;
                 mbar_wait(&sm.k_full[st], uint32_t((j / kTcStages) & 1));
                 if (j >= 2) mbar_wait(&sm.s_free[g], uint32_t(((j >> 1) - 1) & 1));  // S_{j-2} read out
                 tc_fence_after();
@@ -788,23 +794,24 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
                 }
                 umma_commit(&sm.s_full[g]);
                 umma_commit(&sm.k_empty[st]);
-            }
-        }
-    } else if (warp == 3) {
-        if (lane == 0) {  // O_g += P_j . V_j, g = j % 2
-            const uint32_t idesc_o = umma_idesc_bf16_bmn(kTcRows, DH);
-            for (int j = 0; j < n_tiles; ++j) {
-                const int st = j % kTcStages, g = j & 1;
+            };
+            mbar_wait(&sm.q_full, 0);
+            if (g < n_tiles) issue_s(g);
+            for (int j = g; j < n_tiles; j += 2) {
+                const int st = j % kTcStages;
+                // S_{j+2} as soon as the group has read S_j, ahead of PV_j
+                if (j + 2 < n_tiles) issue_s(j + 2);
                 mbar_wait(&sm.p_full[g], uint32_t((j >> 1) & 1));  // P_j written, O_g rescaled
                 mbar_wait(&sm.v_full[st], uint32_t((j / kTcStages) & 1));
                 tc_fence_after();
 #pragma unroll
-                for (int ks = 0; ks < kTile / 16; ++ks) {
+                for (int ks = 0; ks < kTile / 16; ++ks) {  // O_g += P_j . V_j
                     if (dbg & 2) break;
-                    const uint64_t a = umma_sdesc_sw128(smem_u32(&sm.p[g][0]) + ks * 32);
+                    // P: 16 tokens per step = 8 TMEM columns of bf16 pairs
+                    const uint32_t a = tmem + 384 + uint32_t(g * (kTile / 2) + ks * 8);
                     // V: 16 tokens per step = two 8-token groups of 1024 B; dim halves 8 KB apart
                     const uint64_t b = umma_sdesc_sw128_mn(smem_u32(&sm.v[st][0][0]) + ks * 2048, 8192, 1024);
-                    umma_bf16(tmem + 128 + uint32_t(g * DH), a, b, idesc_o, (j >= 2 || ks > 0) ? 1u : 0u);
+                    umma_bf16_ts(tmem + 128 + uint32_t(g * DH), a, b, idesc_o, (j >= 2 || ks > 0) ? 1u : 0u);
                 }
                 umma_commit(&sm.p_free[g]);
                 umma_commit(&sm.v_empty[st]);
@@ -817,7 +824,7 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
         const uint32_t o_col = 128 + uint32_t(grp * DH);
         const int my_pos = r < rows ? pos0 + r / G : -1;
         const float qs = rsqrtf(float(DH)) * 1.4426950408889634f;
-        const uint32_t prow = smem_u32(&sm.p[grp][0]) + uint32_t(r * 128);
+        const uint32_t p_col = 384 + uint32_t(grp * (kTile / 2));
         float m_ref = -INFINITY, l_run = 0.f;
         for (int j = grp; j < n_tiles; j += 2) {
             const int st = j % kTcStages, u = j >> 1;  // u: this group's use count of its buffers
@@ -875,10 +882,9 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
                     tmem_st_wait();
                 }
             }
-            // P row r: 8 chunks of 8 tokens, 128-byte swizzle (chunk ^ row % 8)
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-                sts128(prow + uint32_t((c ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+            // P row r: 32 columns of bf16 pairs in this lane
+            tmem_st16(tmem + lane_off + p_col, pk);
+            tmem_st16(tmem + lane_off + p_col + 16, pk + 16);
             // V rows past the last valid token must be zero (0 * garbage must not be NaN)
             const int valid = min(kTile, last_pos + 1 - tok0);
             if (valid < kTile) {
@@ -887,8 +893,9 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
                     const int tr = valid + i / 16, c = i % 16;  // token row, 16-byte chunk over 128 dims
                     sts128(smem_u32(&sm.v[st][c >> 3][0]) + uint32_t(tr * 128 + (((c & 7) ^ (tr & 7)) << 4)), 0, 0, 0, 0);
                 }
+                fence_proxy_async_smem();  // the zeroed V rows are read by the MMA's async proxy
             }
-            fence_proxy_async_smem();  // P (and zeroed V) are read by the MMA's async proxy
+            tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&sm.p_full[grp]);
         }
