@@ -638,7 +638,8 @@ attn_prompt_tma_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __nv_b
 // Chunked-prefill attention on 5th-generation tensor cores (d_head 128, G <= 8): one CTA per
 // (query block of 128 rows = 128/G prompt positions x G heads, KV head), FlashAttention-style
 // over the request's 64-token KV tiles:
-//   S  = Q . K^T   tcgen05.mma M=128 N=64 K=128 (Q, K K-major SW128 tiles from TMA), S in TMEM
+//   S  = Q . K^T   tcgen05.mma M=128 N=64 K=128, Q read from TMEM (stored there once by the
+//                  softmax threads), K a K-major SW128 tile from TMA; S in TMEM
 //   P  = softmax   one thread per row (TMEM lane), online max / sum in the log2 domain, P rows
 //                  (bf16 pairs) stored back into TMEM (tcgen05.st) as the next MMA's A operand
 //   O += P . V     tcgen05.mma M=128 N=128 K=64 with P read from TMEM and V as an MN-major B
@@ -655,13 +656,14 @@ attn_prompt_tma_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __nv_b
 // (S_{j+2} issued as soon as S_j is read, ahead of PV_j), w2 TMEM allocator then V-ring
 // producer, w4-11 softmax.
 // TMEM columns: S even [0, 64), S odd [64, 128), O even [128, 256), O odd [256, 384), P even
-// [384, 416), P odd [416, 448).
+// [384, 416), P odd [416, 448), Q [448, 512). Shared memory carries only the K and V rings: with
+// Q in shared memory an M128 N64 S step read 6 KB per 32-cycle dispatch and the operand reads
+// plus the TMA writes bounded the tensor pipe at about half its floor.
 constexpr int kTcRows = 128;
 // K/V ring depth: a tile's MMAs take ~0.3 us, a TMA round trip from L2 / HBM ~1 us, so the loads
 // run 3 tiles ahead (2 stages left them exposed)
 constexpr int kTcStages = 4;
 struct PromptTcSmem {
-    alignas(1024) __nv_bfloat16 q[2][kTcRows * 64];              // [dim half][row][64]
     alignas(1024) __nv_bfloat16 k[kTcStages][2][kTile * 64];     // [stage][dim half][token][64]
     alignas(1024) __nv_bfloat16 v[kTcStages][2][kTile * 64];     // [stage][dim half][token][64]
     float m_x[2][kTcRows], l_x[2][kTcRows];                      // [group][row] epilogue merge
@@ -687,7 +689,7 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
 
 template <int G>
 __global__ void __launch_bounds__(384)
-attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_constant__ CUtensorMap tmap_q,
+attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __nv_bfloat16* __restrict__ q,
                       int n_h, const int32_t* __restrict__ row_pos, const int32_t* __restrict__ row_page_off,
                       const int32_t* __restrict__ flat_pages, const int32_t* __restrict__ blocks, KvLayout kv,
                       int layer, __nv_bfloat16* __restrict__ o, int dbg) {
@@ -703,14 +705,13 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
     const int bi = int(gridDim.x) / n_kv - 1 - int(blockIdx.x) / n_kv;
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmap_kv);
-        tma_prefetch_desc(&tmap_q);
         for (int b = 0; b < kTcStages; ++b) {
             mbar_init(&sm.k_full[b], 1);
             mbar_init(&sm.k_empty[b], 1);
             mbar_init(&sm.v_full[b], 1);
             mbar_init(&sm.v_empty[b], 1);
         }
-        mbar_init(&sm.q_full, 1);
+        mbar_init(&sm.q_full, 256);
         for (int g = 0; g < 2; ++g) {
             mbar_init(&sm.s_full[g], 1);
             mbar_init(&sm.s_free[g], 128);
@@ -739,15 +740,6 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
 
     if (warp == 0) {
         if (lane == 0) {
-            // Q: [positions][G heads][64] boxes of the q buffer viewed as (dims, heads, rows)
-            mbar_arrive_expect_tx(&sm.q_full, uint32_t(kTcRows * DH * 2));
-            for (int bx = 0; bx < 2; ++bx)
-                asm volatile(
-                    "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-                    " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(&sm.q[bx][0])),
-                    "l"(reinterpret_cast<uint64_t>(&tmap_q)), "r"(smem_u32(&sm.q_full)), "r"(bx * 64),
-                    "r"(kvh * G), "r"(t0)
-                    : "memory");
             for (int j = 0; j < n_tiles; ++j) {  // K tiles
                 const int st = j % kTcStages;
                 if (j >= kTcStages) mbar_wait(&sm.k_empty[st], uint32_t((j / kTcStages - 1) & 1));
@@ -788,14 +780,14 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
 #pragma unroll
                 for (int ks = 0; ks < DH / 16; ++ks) {
                     if (dbg & 4) break;
-                    const uint64_t a = umma_sdesc_sw128(smem_u32(&sm.q[ks >> 2][0]) + (ks & 3) * 32);
+                    const uint32_t a = tmem + 448 + uint32_t(ks * 8);  // Q: 16 dims = 8 columns
                     const uint64_t b = umma_sdesc_sw128(smem_u32(&sm.k[st][ks >> 2][0]) + (ks & 3) * 32);
-                    umma_bf16(tmem + uint32_t(g * kTile), a, b, idesc_s, ks > 0 ? 1u : 0u);
+                    umma_bf16_ts(tmem + uint32_t(g * kTile), a, b, idesc_s, ks > 0 ? 1u : 0u);
                 }
                 umma_commit(&sm.s_full[g]);
                 umma_commit(&sm.k_empty[st]);
             };
-            mbar_wait(&sm.q_full, 0);
+            mbar_wait(&sm.q_full, 0);  // Q in TMEM
             if (g < n_tiles) issue_s(g);
             for (int j = g; j < n_tiles; j += 2) {
                 const int st = j % kTcStages;
@@ -825,6 +817,26 @@ attn_prompt_tc_kernel(const __grid_constant__ CUtensorMap tmap_kv, const __grid_
         const int my_pos = r < rows ? pos0 + r / G : -1;
         const float qs = rsqrtf(float(DH)) * 1.4426950408889634f;
         const uint32_t p_col = 384 + uint32_t(grp * (kTile / 2));
+        {  // Q row r, dims [64 grp, 64 grp + 64), into TMEM columns 448 + 32 grp (bf16 pairs)
+            uint32_t qv[32];
+            if (r < rows) {
+                const uint4* src = reinterpret_cast<const uint4*>(
+                    q + (size_t(t0 + r / G) * n_h + kvh * G + r % G) * DH + grp * 64);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const uint4 v4 = __ldg(src + c);
+                    qv[4 * c] = v4.x, qv[4 * c + 1] = v4.y, qv[4 * c + 2] = v4.z, qv[4 * c + 3] = v4.w;
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < 32; ++c) qv[c] = 0u;
+            }
+            tmem_st16(tmem + lane_off + 448 + uint32_t(grp * 32), qv);
+            tmem_st16(tmem + lane_off + 448 + uint32_t(grp * 32 + 16), qv + 16);
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&sm.q_full);
+        }
         float m_ref = -INFINITY, l_run = 0.f;
         for (int j = grp; j < n_tiles; j += 2) {
             const int st = j % kTcStages, u = j >> 1;  // u: this group's use count of its buffers
@@ -1750,16 +1762,15 @@ static void launch(const __nv_bfloat16* q, int T, int n_h, const int32_t* row_po
     if (skip & 2) n_drows = 0;
     const int stride = std::max(sp, sd);
     const int prompt_env = prompt_kernel_env();
-    if (n_blocks > 0 && prompt_tc(n_h, kv.n_kv, DH) && kv.tmap64 && kv.tmap_q) {
+    if (n_blocks > 0 && prompt_tc(n_h, kv.n_kv, DH) && kv.tmap64) {
         const CUtensorMap& tk = *static_cast<const CUtensorMap*>(kv.tmap64);
-        const CUtensorMap& tq = *static_cast<const CUtensorMap*>(kv.tmap_q);
         const dim3 g(n_blocks * kv.n_kv), b(384);
         const size_t sm_bytes = sizeof(PromptTcSmem) + 1024;
         switch (n_h / kv.n_kv) {
-            case 1: launch_pdl(attn_prompt_tc_kernel<1>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o, tc_dbg()); break;
-            case 2: launch_pdl(attn_prompt_tc_kernel<2>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o, tc_dbg()); break;
-            case 4: launch_pdl(attn_prompt_tc_kernel<4>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o, tc_dbg()); break;
-            default: launch_pdl(attn_prompt_tc_kernel<8>, g, b, sm_bytes, stream, tk, tq, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o, tc_dbg()); break;
+            case 1: launch_pdl(attn_prompt_tc_kernel<1>, g, b, sm_bytes, stream, tk, q, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o, tc_dbg()); break;
+            case 2: launch_pdl(attn_prompt_tc_kernel<2>, g, b, sm_bytes, stream, tk, q, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o, tc_dbg()); break;
+            case 4: launch_pdl(attn_prompt_tc_kernel<4>, g, b, sm_bytes, stream, tk, q, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o, tc_dbg()); break;
+            default: launch_pdl(attn_prompt_tc_kernel<8>, g, b, sm_bytes, stream, tk, q, n_h, row_pos, row_page_off, flat_pages, blocks, kv, layer, o, tc_dbg()); break;
         }
     } else if (n_blocks > 0 && prompt_env >= 2 && kv.tmap64)
         launch_pdl(attn_prompt_tma_kernel<DH>, dim3(n_blocks * kv.n_kv * sp), dim3(kPromptWarps * 32),
