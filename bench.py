@@ -341,6 +341,23 @@ def ds_env():
     return {k: v for k, v in sorted(os.environ.items()) if k.startswith("DS_")}
 
 
+class StdoutToStderr:
+    """fd-level redirect of stdout to stderr while the run executes, so that anything native code
+    prints (NCCL's version banner, CUDA library notices) cannot join the one JSON line on stdout."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+        return False
+
+
 def main():
     bad = [k for k in INVALIDATING_ENV if os.environ.get(k) not in (None, "", "0")]
     if bad:
@@ -355,16 +372,18 @@ def main():
     ap.add_argument("--dump", default=None, help="write per-run reports (steps, kernels) here")
     args = ap.parse_args()
     if args.impl == "reference":
-        out = run_reference(args)
+        with StdoutToStderr():
+            out = run_reference(args)
         if out is not None:
             print(json.dumps(out))
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
-        from bench_multi import run_multi
-        out = run_multi(args)
-    else:
-        out = run_single(args)
+    with StdoutToStderr():
+        if world > 1 or args.gpus > 1:
+            from bench_multi import run_multi
+            out = run_multi(args)
+        else:
+            out = run_single(args)
     if out is not None:
         out["ds_env"] = ds_env()
         print(json.dumps(out))
