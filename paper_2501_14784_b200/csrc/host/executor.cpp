@@ -592,6 +592,27 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 const Circuit& circ = circs[c];
                 const int32_t mb = circ.mb;
                 w.served++;
+                // ---- residency top-up (SURVEY.md H3): the plan's prefetch may be stale, or the
+                // step's growth may exceed the whole local pages before the plan's byte figure
+                // shows a global portion. Checked before the input wait, so the refill copy
+                // overlaps the hop (and the previous step) instead of delaying this step; the
+                // copies still wait for the evicted occupant's last compute and the step waits
+                // for the refill.
+                rows.clear();
+                for (const auto& r : circ.rows)
+                    rows.push_back({r.slot, r.pos, r.n_tok, r.need_logits, r.is_decode, 0, r.req});
+                int32_t resident = 1;
+                DK(ds_kv_ready(w.st, mb, rows.data(), int64_t(rows.size()), &resident));
+                if (!resident) {
+                    int64_t mi = 0, mo = 0;
+                    DK(ds_swap_events(w.st, nullptr, nullptr, nullptr, nullptr));
+                    const int ps = pick_slot(w, mb, int64_t(oi), int(w.served % 2));
+                    DK(ds_swap_in(w.st, mb, ps, 0, &mi, &mo));
+                    note_swap(w, mb, ps);
+                    w.moved_in += mi;
+                    w.moved_out += mo;
+                    w.topups++;
+                }
                 // ---- input dependency: previous stage, or (stage 0) this mb's previous circuit
                 const int64_t need = s == 0 ? S->prev[c] : c;
                 bool has_input = need >= 0;
@@ -646,24 +667,6 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
                 }
                 w.arr_us.push_back(arr);
                 w.send_us.push_back(sent);
-                // ---- residency top-up (SURVEY.md H3): the plan's prefetch may be stale, or the
-                // step's growth may exceed the whole local pages before the plan's byte figure
-                // shows a global portion
-                rows.clear();
-                for (const auto& r : circ.rows)
-                    rows.push_back({r.slot, r.pos, r.n_tok, r.need_logits, r.is_decode, 0, r.req});
-                int32_t resident = 1;
-                DK(ds_kv_ready(w.st, mb, rows.data(), int64_t(rows.size()), &resident));
-                if (!resident) {
-                    int64_t mi = 0, mo = 0;
-                    DK(ds_swap_events(w.st, nullptr, nullptr, nullptr, nullptr));
-                    const int ps = pick_slot(w, mb, int64_t(oi), int(w.served % 2));
-                    DK(ds_swap_in(w.st, mb, ps, 0, &mi, &mo));
-                    note_swap(w, mb, ps);
-                    w.moved_in += mi;
-                    w.moved_out += mo;
-                    w.topups++;
-                }
                 // ---- the stage step
                 StepTiming* tm = nullptr;
                 if (opt.step_timing) {
