@@ -524,17 +524,21 @@ GpuRunResult session_run(Session* S, bool profile, bool collect_tokens) {
     // plan does not mark a microbatch absent when another prefetch reuses its slot (SURVEY.md
     // H3), so following them evicts microbatches just before they compute. The executor knows
     // the whole op sequence: it keeps the target where it already is, else uses an empty slot,
-    // else evicts the occupant whose next compute comes later (DS_SWAP_SLOTS=plan: the plan's).
-    static const bool plan_slots = getenv("DS_SWAP_SLOTS") && std::string(getenv("DS_SWAP_SLOTS")) == "plan";
-    static const bool pin_last = getenv("DS_SWAP_SLOTS") && std::string(getenv("DS_SWAP_SLOTS")) == "pin";
+    // else never evicts the microbatch of the latest launched compute (its refill would wait for
+    // that step to finish and then stall the next one), else evicts the occupant whose next
+    // compute comes later. DS_SWAP_SLOTS=plan: the plan's numbers; =lookahead: no pinning.
+    // Measured with the early top-up (profiles/r02_swap_slot_policies.md): 70B 4-stage swap
+    // 582.8 tok/s pinned vs 521.2 lookahead, 8B 4-stage swap 3,042 vs 3,013; pinning doubles the
+    // top-ups, which the early top-up overlaps with the hop.
+    static const std::string slot_env = getenv("DS_SWAP_SLOTS") ? getenv("DS_SWAP_SLOTS") : "";
+    static const bool plan_slots = slot_env == "plan";
+    static const bool pin_last = slot_env != "lookahead";
     auto pick_slot = [&](Worker& w, int32_t target, int64_t pos, int plan_slot) -> int {
         if (plan_slots) return plan_slot;
         for (int k = 0; k < 2; ++k)
             if (w.phys_owner[k] == target) return k;
         for (int k : {plan_slot, 1 - plan_slot})
             if (w.phys_owner[k] < 0) return k;
-        // (pinning the microbatch of the latest compute -- DS_SWAP_SLOTS=pin -- measured worse:
-        // 70B 4-stage swap 411.6 vs 444.6 tok/s, twice the top-ups)
         if (pin_last)
             for (int k = 0; k < 2; ++k)
                 if (w.phys_owner[k] == w.last_mb) return 1 - k;
