@@ -288,6 +288,13 @@ ds_status ds_session_create_rank(const char* config_json, const char* config_dir
  * ------------------------------------------------------------------------------------------ */
 ds_status ds_dbg_gemm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t N, int32_t K,
                       int32_t epi, const uint16_t* resid, int32_t k_splits, void* out);
+/* RowNorm pair: out_x = bf16(resid + bf16(x.W1^T)) [T, N] (producer, slice sums of squares in
+ * its epilogue), then out_y = bf16(r[t] * out_x[t].W2^T) [T, N2], r = 1/sqrt(mean(out_x^2) + eps)
+ * (consumer row scale; *fused = 1) — or, where a partition does not allow it (*fused = 0), the
+ * RMSNorm kernel and the plain GEMM of bf16(out_x * r). */
+ds_status ds_dbg_gemm_norm(const uint16_t* x, const uint16_t* w1, int32_t T, int32_t N, int32_t K,
+                           const uint16_t* resid, const uint16_t* w2, int32_t N2, float eps,
+                           uint16_t* out_x, uint16_t* out_y, int32_t* fused);
 ds_status ds_dbg_gemm_bench(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters,
                             int32_t k_splits, float* ms_out);
 ds_status ds_dbg_has_device(int32_t* n_devices);

@@ -118,6 +118,7 @@ def _load() -> C.CDLL:
         "ds_sweep_csv": (I32, [P, I32, S, P, P, C.c_size_t, P]),
         "ds_session_captured": (I32, [P, P, P, I64, P]),
         "ds_dbg_gemm": (I32, [P, P, I32, I32, I32, I32, P, I32, P]),
+        "ds_dbg_gemm_norm": (I32, [P, P, I32, I32, I32, P, P, I32, C.c_float, P, P, P]),
         "ds_dbg_has_device": (I32, [P]),
         "ds_dbg_gemm_bench": (I32, [I32, I32, I32, I32, I32, I32, P]),
         "ds_dbg_alloc": (I32, [I32, I64, P]),

@@ -177,6 +177,18 @@ __global__ void __launch_bounds__(512) rope_kv_kernel(const __nv_bfloat16* __res
     const int t = blockIdx.x;
     const int pos = row_pos[t];
     const int half = dh / 2;
+    float sc = 1.f;  // RowNorm scale of the row (q/k/v GEMM of the un-normalised x, planes deferred)
+    if (pl.n > 0 && pl.rs_ssq) {
+        __shared__ float rs_row;
+        if (threadIdx.x < 32) {
+            float ss = 0.f;
+            for (int i = threadIdx.x; i < pl.rs_parts; i += 32) ss += __ldcg(pl.rs_ssq + size_t(i) * gridDim.x + t);
+            ss = warp_sum(ss);
+            if (threadIdx.x == 0) rs_row = 1.0f / sqrtf(ss / float(pl.rs_d) + pl.rs_eps);
+        }
+        __syncthreads();
+        sc = rs_row;
+    }
     const int width = (n_h + 2 * n_kv) * dh;
     const __nv_bfloat16* src = qkv + size_t(t) * width;
     const float* c = rc + size_t(pos) * half;
@@ -194,6 +206,8 @@ __global__ void __launch_bounds__(512) rope_kv_kernel(const __nv_bfloat16* __res
             if (pl.n > 0) {
                 float a[8];
                 sum_planes8(pl, size_t(t) * width + (n_h + n_kv) * dh + kh * dh + i, a);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) a[j] *= sc;
                 val = pack8(a);
             } else {
                 val = *reinterpret_cast<const uint4*>(src + (n_h + n_kv) * dh + kh * dh + i);
@@ -210,8 +224,8 @@ __global__ void __launch_bounds__(512) rope_kv_kernel(const __nv_bfloat16* __res
             sum_planes8(pl, size_t(t) * width + head * dh + i + half, x2);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                x1[j] = round_bf(x1[j]);
-                x2[j] = round_bf(x2[j]);
+                x1[j] = round_bf(x1[j] * sc);
+                x2[j] = round_bf(x2[j] * sc);
             }
         } else {
             unpack8(*reinterpret_cast<const uint4*>(src + head * dh + i), x1);

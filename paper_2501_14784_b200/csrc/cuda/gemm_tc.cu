@@ -45,7 +45,10 @@ constexpr int kSmemBudget = 222 * 1024;
 constexpr int kStageStride = 36;  // floats per row of the epilogue transpose buffer
 constexpr size_t kWorkspaceFloats = size_t(24) << 20;  // arrival counters + stream-K pieces
 constexpr size_t kCounterInts = size_t(64) << 10;
-constexpr int kFixedSmem = 4 * 16 * kStageStride * 4 + 256 + 1024;  // transpose buffers, barriers, align
+constexpr int kRsMax = 1024;  // token rows a consumer GEMM can scale (RowNorm)
+constexpr int kRsFloats = 4 * kMaxTB;  // RowNorm smem: consumer scales [kRsMax] / producer slices [4][kMaxTB]
+constexpr int kFixedSmem = 4 * 16 * kStageStride * 4 + 256 + kRsFloats * 4 + 1024;  // transpose buffers,
+                                                                                  // barriers, RowNorm, align
 
 struct GemmParams {
     int T, N, K;
@@ -79,6 +82,13 @@ struct GemmParams {
     const __nv_bfloat16* w;     // weight base (L2 prefetch addresses)
     int pf_kb;                  // k-blocks per CTA to prefetch into L2 past the smem pipeline
     int ks_push;                // k-split epilogue: peers push row blocks with bulk DSMEM copies
+    // RMSNorm split across the residual GEMM and its consumer (RowNorm):
+    float* ssq_out;       // producer (EPI_RESID): sums of squares of its output row slices
+                          // [m_tiles][T] (one per 128-feature tile)
+    const float* rs_ssq;  // consumer: those parts; out row t is scaled by
+    int rs_parts;         //   r[t] = 1 / sqrt(sum of its rs_parts parts / rs_d + rs_eps)
+    int rs_d;
+    float rs_eps;
 };
 
 DS_DEVICE unsigned long long gtime() {
@@ -233,8 +243,13 @@ DS_DEVICE void store_silu(const GemmParams& p, const float* v, bool ok, int lane
     *reinterpret_cast<uint4*>(p.out_bf16 + size_t(t) * ld + (f_slice / 32) * 16 + half * 8) = pack8(o);
 }
 
-// Final epilogue of a transposed chunk (all lanes call; `ok` = this lane's token row is real).
-DS_DEVICE void epi_store(const GemmParams& p, float* v, bool ok, int lane, int t, int f_slice) {
+// Final epilogue of a transposed chunk (all lanes call; `ok` = this lane's token row is real);
+// sc = the row's RMSNorm scale (RowNorm consumer) or 1.
+DS_DEVICE void epi_store(const GemmParams& p, float* v, bool ok, int lane, int t, int f_slice, float sc = 1.f) {
+    if (p.rs_ssq) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] *= sc;
+    }
     if (p.epi == EPI_SILU) {
         store_silu(p, v, ok, lane, t, f_slice);
         return;
@@ -440,7 +455,7 @@ DS_DEVICE void ksplit_epilogue_push(const GemmParams& p, uint8_t* smem, uint32_t
 // (ld.shared::cluster), then applies the fused epilogue 4 features per thread.
 template <int CN>
 DS_DEVICE void ksplit_epilogue(const GemmParams& p, uint8_t* smem, uint32_t tmem_base, int cluster,
-                               int kidx, int rank, int warp, int lane) {
+                               int kidx, int rank, int warp, int lane, const float* rs) {
     const int cl_tiles = p.m_tiles / CN;
     const int tbk = tile_tbk(p, cluster, cl_tiles);
     const int mt = tile_mtc(p, cluster, cl_tiles) * CN + rank;
@@ -475,6 +490,11 @@ DS_DEVICE void ksplit_epilogue(const GemmParams& p, uint8_t* smem, uint32_t tmem
                 if (silu) add4(u, ld_dsmem_f4(mapa_shared(off + 64, peer)));
             }
             const int t = t0 + w0 + row, fg = mt * kBM + f;
+            if (p.rs_ssq) {
+                const float sc = rs[t];
+                a.x *= sc, a.y *= sc, a.z *= sc, a.w *= sc;
+                u.x *= sc, u.y *= sc, u.z *= sc, u.w *= sc;
+            }
             const float v[4] = {a.x, a.y, a.z, a.w};
             if (p.epi == EPI_F32) {
                 *reinterpret_cast<float4*>(p.out_f32 + size_t(t) * p.N + fg) = a;
@@ -506,6 +526,16 @@ DS_DEVICE void ksplit_epilogue(const GemmParams& p, uint8_t* smem, uint32_t tmem
                 ov.x = pack2(o[0], o[1]);
                 ov.y = pack2(o[2], o[3]);
                 *reinterpret_cast<uint2*>(p.out_bf16 + oi) = ov;
+                if (p.ssq_out) {  // one warp = one token row's 128 features of this tile
+                    float ss = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float xb = round_bf(o[j]);  // the stored bf16 of x
+                        ss += xb * xb;
+                    }
+                    ss = warp_sum(ss);
+                    if (lane == 0) p.ssq_out[size_t(mt) * p.T + t] = ss;
+                }
             }
         }
         cluster_sync();  // peers done reading before the next window overwrites it
@@ -536,6 +566,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
     uint64_t* tfull_bar = empty_bar + p.stages;  // [2]
     uint64_t* tempty_bar = tfull_bar + 2;        // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    float* rs = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full_bar) + 256);  // [kRsFloats]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -593,6 +624,25 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
             for (int r = lane; r < kBM; r += 32)
                 prefetch_l2_bulk(p.w + (size_t(mt) * kBM + r) * p.K + size_t(kb) * kBK, uint32_t(n * kBK * 2));
         });
+    }
+    if (p.rs_ssq && warp >= 3) {
+        // RowNorm consumer: the RMSNorm scale of every token row from the producer's slice sums
+        // of squares (parts summed in order: deterministic), by warps 3..7 while the producer
+        // and MMA warps stream the first tiles; 32 loads per thread in flight
+        pdl_wait();
+        for (int t = int(threadIdx.x) - 96; t < p.T; t += kGemmThreads - 96) {
+            float s = 0.f;
+            for (int i0 = 0; i0 < p.rs_parts; i0 += 32) {
+                float v[32];
+#pragma unroll
+                for (int k = 0; k < 32; ++k)
+                    v[k] = i0 + k < p.rs_parts ? __ldcg(p.rs_ssq + size_t(i0 + k) * p.T + t) : 0.f;
+#pragma unroll
+                for (int k = 0; k < 32; ++k) s += v[k];
+            }
+            rs[t] = 1.0f / sqrtf(s / float(p.rs_d) + p.rs_eps);
+        }
+        asm volatile("bar.sync 2, 160;" ::: "memory");  // warps 3..7: the scales are in smem
     }
     if (warp == 0) {
         if (elect_one()) {
@@ -732,7 +782,24 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                     tmem_ld16(acc + c0, r);
                     tmem_ld_wait();
                     const bool ok = transpose16(stage, reinterpret_cast<float*>(r), lane, c0, t_here, v);
-                    epi_store(p, v, ok, lane, t0 + c0 + row, f_slice);
+                    epi_store(p, v, ok, lane, t0 + c0 + row, f_slice, ok && p.rs_ssq ? rs[t0 + c0 + row] : 1.f);
+                    if (p.ssq_out) {  // slice (tile, warp q) of token row t: lanes 2r, 2r+1
+                        float ss = 0.f;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const float xb = round_bf(v[j]);  // the stored bf16 of x
+                            ss += xb * xb;
+                        }
+                        ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+                        if (ok && half == 0) rs[q * kMaxTB + c0 + row] = ss;  // smem [warp][row]
+                    }
+                }
+                if (p.ssq_out) {  // the 4 warps' slices of each row, summed in warp order
+                    epi_bar();
+                    for (int i = int(threadIdx.x) - 128; i < t_here; i += 128)
+                        p.ssq_out[size_t(mt) * p.T + t0 + i] =
+                            ((rs[i] + rs[kMaxTB + i]) + rs[2 * kMaxTB + i]) + rs[3 * kMaxTB + i];
+                    epi_bar();
                 }
             } else {
                 // split tile: park this piece (TMEM-native layout [chunk][feature][16 tokens]: each
@@ -789,7 +856,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                         sum_pieces(p, CN, rank, tile_g0, c_lo, c_hi, size_t(ch) * kBM * 16 + fo, cluster,
                                    own, sum);
                         const bool ok = transpose16(stage, sum, lane, ch * 16, t_here, v);
-                        epi_store(p, v, ok, lane, t0 + ch * 16 + row, f_slice);
+                        epi_store(p, v, ok, lane, t0 + ch * 16 + row, f_slice,
+                                  ok && p.rs_ssq ? rs[t0 + ch * 16 + row] : 1.f);
                     }
                 }
             }
@@ -815,7 +883,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
         if (p.ks_push)
             ksplit_epilogue_push<CN>(p, smem, tmem_base, cluster, kidx, int(rank), warp, lane);
         else
-            ksplit_epilogue<CN>(p, smem, tmem_base, cluster, kidx, int(rank), warp, lane);
+            ksplit_epilogue<CN>(p, smem, tmem_base, cluster, kidx, int(rank), warp, lane, rs);
         tc_fence_before();
         if (threadIdx.x == 128) GEMM_TRACE(3);
     }
@@ -1110,11 +1178,30 @@ static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) 
     return p;
 }
 
+// A consumer row scale is applied wherever the output is finished: the kernel's epilogues (whole
+// tiles, the stream-K last arriver, k-split pull) or the consumer of deferred planes — not the
+// separate reduction / finish kernels, and for at most kRsMax rows (shared-memory scales).
+static bool rowscale_ok(const GemmParams& p, int T, bool deferred) {
+    if (p.T < 0 || T > kRsMax || p.ks_push) return false;
+    if (p.planes) return deferred;
+    return !p.defer;
+}
+
+bool gemm_rowscale_ok(int T, int N, int K, bool deferred) {
+    int cn = 0;
+    GemmParams p = plan_gemm(T, N, K, 0, &cn);
+    static const int push_env = getenv("DS_GEMM_KSPUSH") ? atoi(getenv("DS_GEMM_KSPUSH")) : 0;
+    p.ks_push = (push_env && p.ks > 1 &&
+                 ksplit_push_smem(p.ks) <= size_t(p.stages) * size_t(kBM * kBK * 2 + p.b_bytes)) ? 1 : 0;
+    return rowscale_ok(p, T, deferred);
+}
+
 int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_bfloat16* out_bf16,
               const __nv_bfloat16* resid, float* out_f32, float* workspace, size_t workspace_floats,
-              int max_clusters, cudaStream_t stream, Planes* defer) {
+              int max_clusters, cudaStream_t stream, Planes* defer, const RowNorm* rn, int* ssq_parts) {
     const int N = w.N, K = w.K;
     if (defer) *defer = Planes{};
+    if (ssq_parts) *ssq_parts = 0;
     if (T <= 0) return 0;
     int cn = 1;
     GemmParams p = plan_gemm(T, N, K, max_clusters, &cn);
@@ -1159,6 +1246,23 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
         p.ks_push = (push_env && p.ks > 1 &&
                      ksplit_push_smem(p.ks) <= size_t(p.stages) * size_t(kBM * kBK * 2 + p.b_bytes)) ? 1 : 0;
     }
+    if (rn && rn->ssq_out && epi == EPI_RESID && T <= rn->max_rows) {
+        // RowNorm producer: only where every output row slice is final inside this kernel
+        // (k-split clusters with the pull epilogue, or whole tiles: no stream-K pieces, no planes)
+        const bool whole = p.ks == 1 && !p.planes && !p.defer && (p.sk_tiles == 0 || p.n_sk == p.sk_tiles);
+        const bool ksplit = p.ks > 1 && !p.ks_push;
+        if (whole || ksplit) {
+            p.ssq_out = rn->ssq_out;
+            if (ssq_parts) *ssq_parts = p.m_tiles;  // one slice per 128-feature tile
+        }
+    }
+    if (rn && rn->ssq_in) {  // RowNorm consumer (the caller checked gemm_rowscale_ok)
+        if (!rowscale_ok(p, T, defer != nullptr) || p.ssq_out) return -8;
+        p.rs_ssq = rn->ssq_in;
+        p.rs_parts = rn->parts;
+        p.rs_d = rn->d;
+        p.rs_eps = rn->eps;
+    }
     alignas(64) CUtensorMap tx;
     if (make_tmap_2d_bf16(&tx, x, T, K, p.brows, kBK) != 0) return -5;
     const size_t smem = size_t(p.stages) * stage_bytes + fixed;
@@ -1186,6 +1290,12 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
         defer->p = p.slots;
         defer->n = p.planes;
         defer->stride = size_t(T) * N;
+        if (p.rs_ssq) {  // the consumer of the planes applies the row scale
+            defer->rs_ssq = p.rs_ssq;
+            defer->rs_parts = p.rs_parts;
+            defer->rs_d = p.rs_d;
+            defer->rs_eps = p.rs_eps;
+        }
     } else if (p.planes && !no_finish) {
         const size_t total4 = size_t(T) * N / 4;
         const int blocks = int(std::min<size_t>((total4 + 255) / 256, size_t(kNumSMs) * 8));

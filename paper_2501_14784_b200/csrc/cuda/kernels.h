@@ -32,6 +32,24 @@ struct Planes {
     const float* p = nullptr;
     int n = 0;
     size_t stride = 0;
+    // RowNorm consumer deferred with the planes: row t of the sum is scaled by
+    // 1 / sqrt(sum of rs_parts parts rs_ssq[i * T + t] / rs_d + rs_eps) before rounding
+    const float* rs_ssq = nullptr;
+    int rs_parts = 0, rs_d = 0;
+    float rs_eps = 0.f;
+};
+
+// RMSNorm split across a residual GEMM and the GEMM that consumes the normalised rows (unit
+// gains): the producer (EPI_RESID, out = x) writes the sums of squares of its output row slices
+// (ssq_out[part][t], parts returned through ssq_parts: no atomics, no extra pass); the consumer
+// reads x itself and scales its output row t by r[t] = 1 / sqrt(sum of the parts / d + eps):
+// out = bf16(r[t] * sum_k x[t, k] W[n, k]) instead of the GEMM of bf16(x[t] * r[t]).
+struct RowNorm {
+    float* ssq_out = nullptr;  // producer side (>= (N / 128) * T floats)
+    int max_rows = 0;
+    const float* ssq_in = nullptr;  // consumer side
+    int parts = 0, d = 0;
+    float eps = 0.f;
 };
 
 int gemm_weight_init(GemmWeight* w, const __nv_bfloat16* data, int N, int K);
@@ -47,9 +65,15 @@ int gemm_launch_count(int T, int N, int K, bool deferred = false);
 // With `defer` != nullptr, a GEMM that would end in the split-K reduction kernel instead leaves
 // its planes in the workspace and describes them in *defer (the consumer kernel finishes it);
 // otherwise *defer = {} and the output is final.
+// RowNorm: as producer (rn->ssq_out, EPI_RESID) the GEMM writes the slice sums of squares when
+// its partition finishes whole rows in-kernel (k-split clusters or whole tiles) and returns the
+// part count in *ssq_parts (0: not written, the caller normalises with rmsnorm_rows); as consumer
+// (rn->ssq_in) it scales its output rows — only where gemm_rowscale_ok (returns -8 otherwise).
 int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_bfloat16* out_bf16,
               const __nv_bfloat16* resid, float* out_f32, float* workspace, size_t workspace_floats,
-              int max_clusters, cudaStream_t stream, Planes* defer = nullptr);
+              int max_clusters, cudaStream_t stream, Planes* defer = nullptr,
+              const RowNorm* rn = nullptr, int* ssq_parts = nullptr);
+bool gemm_rowscale_ok(int T, int N, int K, bool deferred);
 
 // Counter-based weight init (bf16(uniform(-1,1) * scale)); see oracle/llama_ref.c ds_ref_weight.
 // interleave_part >= 0 writes the [rows, cols] tensor into the gate/up interleaved layout:

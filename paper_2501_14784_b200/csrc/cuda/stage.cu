@@ -91,6 +91,8 @@ struct ds_stage {
     float* attn_ws = nullptr;
     size_t attn_ws_floats = 0;
     int* attn_cnt = nullptr;  // decode context-split arrival counters [max_rows][n_kv]
+    float* norm_ssq = nullptr;  // RowNorm: slice sums of squares of x [d / 128][max_rows]
+    bool unit_gains = true;     // RMSNorm gains are 1 (init): the consumer GEMMs may scale rows
 
     // step metadata: pinned host staging (double-buffered) + device copy
     int32_t* h_meta[2] = {nullptr, nullptr};
@@ -318,6 +320,7 @@ ds_status ds_stage_create(int32_t device, const ds_model_desc* md, int64_t layer
         // [decode rows x n_kv | prompt blocks x n_kv] (the prompt half starts at T * n_kv)
         if ((st = A((void**)&s->attn_cnt, 2 * R * m.n_kv_heads * 4))) { delete s; return st; }
         CK(cudaMemset(s->attn_cnt, 0, 2 * R * m.n_kv_heads * 4));
+        if ((st = A((void**)&s->norm_ssq, size_t(std::max(1, d / 128)) * R * 4))) { delete s; return st; }
     }
     s->meta_cap = 16 * R + size_t(max_slots) * 64 + R * size_t((m.max_seq_len + 255) / 256) + 64;
     for (int i = 0; i < 2; ++i) {
@@ -337,6 +340,7 @@ ds_status ds_stage_destroy(ds_stage* s) {
     for (void* p : {(void*)s->wbuf, (void*)s->rope_cos, (void*)s->rope_sin, (void*)s->x, (void*)s->xn,
                     (void*)s->qkv, (void*)s->q, (void*)s->attn, (void*)s->h,
                     (void*)s->logits, (void*)s->ids, (void*)s->ws, (void*)s->attn_ws, (void*)s->attn_cnt,
+                    (void*)s->norm_ssq,
                     (void*)s->d_meta, (void*)s->kv.pool, (void*)s->last_token,
                     (void*)s->pending_ids})
         if (p) cudaFree(p);
@@ -897,16 +901,39 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     // +87 ms attention / -11 ms o GEMM per step on config 2 (the prefetch competes with the KV
     // stream more than it shortens the GEMM's pipeline fill).
     static const int pf_env = getenv("DS_L2_PREFETCH") ? atoi(getenv("DS_L2_PREFETCH")) : 0;
+    // RMSNorm split across the residual GEMMs (o, down: slice sums of squares of x in their
+    // epilogue) and the GEMMs that consume the normalised rows (q/k/v, gate/up: read x, scale each
+    // output row by its RMSNorm factor) wherever both partitions allow it (ds::RowNorm; the gains
+    // are unit at init); otherwise the RMSNorm kernel writes xn as before.
+    ds::RowNorm rn_out;
+    rn_out.ssq_out = s->norm_ssq;
+    rn_out.max_rows = s->max_rows;
+    auto rn_in = [&](int parts) {
+        ds::RowNorm r;
+        r.ssq_in = s->norm_ssq;
+        r.parts = parts;
+        r.d = d;
+        r.eps = m.norm_eps;
+        return r;
+    };
+    static const bool rownorm_env = !getenv("DS_ROWNORM") || atoi(getenv("DS_ROWNORM")) != 0;
+    const bool rownorm = rownorm_env && s->unit_gains && !(skip & 1);
+    int x_parts = 0;  // > 0: norm_ssq holds the slice sums of squares of the current x
     for (int li = 0; li < s->L; ++li) {
         LayerW& lw = s->layers[li];
         ds::Planes pq, po;
+        const bool fuse_qkv = rownorm && x_parts > 0 && ds::gemm_rowscale_ok(T, qkv_rows, d, true);
+        if (!fuse_qkv) {
+            begin();
+            if (!(skip & 1))
+                ds::rmsnorm_rows(s->x, nullptr, T, d, lw.attn_norm, m.norm_eps, s->xn, st, pend);
+            end_other(PK_ELEM, 0, (4.0 + 4.0 * pend.n) * T * d, 1);
+        }
         begin();
-        if (!(skip & 1))
-            ds::rmsnorm_rows(s->x, nullptr, T, d, lw.attn_norm, m.norm_eps, s->xn, st, pend);
-        end_other(PK_ELEM, 0, (4.0 + 4.0 * pend.n) * T * d, 1);
-        begin();
-        int rc = (skip & 16) ? 0 : ds::gemm_bf16(lw.wqkv, s->xn, T, ds::EPI_BF16, s->qkv, nullptr,
-                                                  nullptr, s->ws, s->ws_floats, 0, st, &pq);
+        const ds::RowNorm rq = rn_in(x_parts);
+        int rc = (skip & 16) ? 0 : ds::gemm_bf16(lw.wqkv, fuse_qkv ? s->x : s->xn, T, ds::EPI_BF16, s->qkv,
+                                                  nullptr, nullptr, s->ws, s->ws_floats, 0, st, &pq,
+                                                  fuse_qkv ? &rq : nullptr);
         end_gemm(PK_QKV, T, qkv_rows, d, 2, true);
         begin();
         if (!(skip & 2))
@@ -924,23 +951,30 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
         end_other(PK_ATTN, attn_flops, attn_bytes,
                   ds::attention_launches(n_blk, n_drow, s_prompt, s_decode));
         begin();
+        int o_parts = 0;
         if (!(skip & 16))
             rc |= ds::gemm_bf16(lw.wo, s->attn, T, ds::EPI_RESID, s->x, s->x, nullptr, s->ws,
-                                s->ws_floats, 0, st, &po);
+                                s->ws_floats, 0, st, &po, rownorm ? &rn_out : nullptr, &o_parts);
         end_gemm(PK_O, T, d, qdim, 4, true);
-        begin();
-        if (!(skip & 1))
-            ds::rmsnorm_rows(s->x, nullptr, T, d, lw.mlp_norm, m.norm_eps, s->xn, st, po);
-        end_other(PK_ELEM, 0, (4.0 + 4.0 * po.n) * T * d, 1);
+        const bool fuse_gu = rownorm && o_parts > 0 && ds::gemm_rowscale_ok(T, 2 * m.ffn, d, false);
+        if (!fuse_gu) {
+            begin();
+            if (!(skip & 1))
+                ds::rmsnorm_rows(s->x, nullptr, T, d, lw.mlp_norm, m.norm_eps, s->xn, st, po);
+            end_other(PK_ELEM, 0, (4.0 + 4.0 * po.n) * T * d, 1);
+        }
+        const ds::RowNorm rg = rn_in(o_parts);
         begin();
         if (!(skip & 16))
-            rc |= ds::gemm_bf16(lw.wgu, s->xn, T, ds::EPI_SILU, s->h, nullptr, nullptr, s->ws,
-                            s->ws_floats, 0, st);
+            rc |= ds::gemm_bf16(lw.wgu, fuse_gu ? s->x : s->xn, T, ds::EPI_SILU, s->h, nullptr, nullptr,
+                                s->ws, s->ws_floats, 0, st, nullptr, fuse_gu ? &rg : nullptr);
         end_gemm(PK_GU, T, 2 * m.ffn, d, 1);  // SiLU fused: writes h[T, ffn]
         begin();
+        x_parts = 0;
         if (!(skip & 16))
             rc |= ds::gemm_bf16(lw.wd, s->h, T, ds::EPI_RESID, s->x, s->x, nullptr, s->ws,
-                                s->ws_floats, 0, st, &pend);
+                                s->ws_floats, 0, st, &pend, (rownorm && li + 1 < s->L) ? &rn_out : nullptr,
+                                &x_parts);
         end_gemm(PK_DOWN, T, d, m.ffn, 4, true);
         if (rc)
             return ds_fail(DS_ERR_RUNTIME, "kernel launch failed in layer " + std::to_string(li) +
@@ -1237,6 +1271,66 @@ ds_status ds_dbg_gemm(const uint16_t* x, const uint16_t* w, int32_t T, int32_t N
     cudaFree(dres);
     cudaFree(df);
     cudaFree(dws);
+    return DS_OK;
+}
+
+ds_status ds_dbg_gemm_norm(const uint16_t* x, const uint16_t* w1, int32_t T, int32_t N, int32_t K,
+                           const uint16_t* resid, const uint16_t* w2, int32_t N2, float eps,
+                           uint16_t* out_x, uint16_t* out_y, int32_t* fused) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return ds_fail(DS_ERR_NO_DEVICE, "no CUDA device");
+    ds::preload_all();
+    bf16 *dx = nullptr, *dw1 = nullptr, *dw2 = nullptr, *dout = nullptr, *dres = nullptr, *dg = nullptr,
+         *dxn = nullptr, *dy = nullptr;
+    float *dws = nullptr, *dssq = nullptr;
+    const size_t out_elems = size_t(T) * N;
+    CK(cudaMalloc(&dx, size_t(T) * K * 2));
+    CK(cudaMalloc(&dw1, size_t(N) * K * 2));
+    CK(cudaMalloc(&dw2, size_t(N2) * N * 2));
+    CK(cudaMalloc(&dout, out_elems * 2));
+    CK(cudaMalloc(&dres, out_elems * 2));
+    CK(cudaMalloc(&dxn, out_elems * 2));
+    CK(cudaMalloc(&dy, size_t(T) * N2 * 2));
+    CK(cudaMalloc(&dg, size_t(N) * 2));
+    CK(cudaMalloc(&dssq, size_t(N / 128) * T * 4));
+    const size_t wsf = ds::gemm_workspace_floats();
+    CK(cudaMalloc(&dws, wsf * 4));
+    CK(cudaMemset(dws, 0, wsf * 4));
+    CK(cudaMemcpy(dx, x, size_t(T) * K * 2, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dw1, w1, size_t(N) * K * 2, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dw2, w2, size_t(N2) * N * 2, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dres, resid, out_elems * 2, cudaMemcpyHostToDevice));
+    ds::fill_bf16(dg, N, 1.0f, 0);
+    GemmWeight g1, g2;
+    if (ds::gemm_weight_init(&g1, dw1, N, K) || ds::gemm_weight_init(&g2, dw2, N2, N))
+        return ds_fail(DS_ERR_RUNTIME, "tensor map");
+    ds::RowNorm out_rn;
+    out_rn.ssq_out = dssq;
+    out_rn.max_rows = T;
+    int parts = 0;
+    // three back-to-back producer -> consumer pairs on one workspace
+    for (int rep = 0; rep < 3; ++rep) {
+        int rc = ds::gemm_bf16(g1, dx, T, ds::EPI_RESID, dout, dres, nullptr, dws, wsf, 0, 0, nullptr,
+                               &out_rn, &parts);
+        const bool fuse = parts > 0 && ds::gemm_rowscale_ok(T, N2, N, false);
+        ds::RowNorm in_rn;
+        in_rn.ssq_in = dssq;
+        in_rn.parts = parts;
+        in_rn.d = N;
+        in_rn.eps = eps;
+        if (!fuse) ds::rmsnorm_rows(dout, nullptr, T, N, dg, eps, dxn, 0);
+        rc |= ds::gemm_bf16(g2, fuse ? dout : dxn, T, ds::EPI_BF16, dy, nullptr, nullptr, dws, wsf, 0, 0,
+                            nullptr, fuse ? &in_rn : nullptr);
+        if (rc) return ds_fail(DS_ERR_RUNTIME, "gemm launch rc=" + std::to_string(rc));
+        *fused = fuse ? 1 : 0;
+    }
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out_x, dout, out_elems * 2, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out_y, dy, size_t(T) * N2 * 2, cudaMemcpyDeviceToHost));
+    for (void* p : {(void*)dx, (void*)dw1, (void*)dw2, (void*)dout, (void*)dres, (void*)dxn, (void*)dy,
+                    (void*)dg, (void*)dssq, (void*)dws})
+        cudaFree(p);
     return DS_OK;
 }
 

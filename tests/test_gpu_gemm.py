@@ -112,3 +112,43 @@ def test_gemm_wide_silu_multi_token_blocks(T):
     nat.check(nat.lib.ds_dbg_gemm(x.ctypes.data, w.ctypes.data, T, N, K, 3, None, 0, out.ctypes.data))
     got = from_bf16(out).astype(np.float64)
     assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max() + 1e-3
+
+
+def _run_norm(T, N, K, N2, seed=0):
+    from paper_2501_14784_b200 import _native as nat
+    from paper_2501_14784_b200.bf16 import from_bf16, to_bf16
+    rng = np.random.default_rng(seed)
+    x = to_bf16(rng.standard_normal((T, K)).astype(np.float32))
+    w1 = to_bf16((rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32))
+    w2 = to_bf16((rng.standard_normal((N2, N)) / np.sqrt(N)).astype(np.float32))
+    resid = to_bf16(rng.standard_normal((T, N)).astype(np.float32))
+    ox = np.zeros((T, N), dtype=np.uint16)
+    oy = np.zeros((T, N2), dtype=np.uint16)
+    fused = C.c_int32(0)
+    eps = 1e-5
+    nat.check(nat.lib.ds_dbg_gemm_norm(x.ctypes.data, w1.ctypes.data, T, N, K, resid.ctypes.data,
+                                       w2.ctypes.data, N2, eps, ox.ctypes.data, oy.ctypes.data,
+                                       C.byref(fused)))
+    ref = from_bf16(x).astype(np.float64) @ from_bf16(w1).astype(np.float64).T
+    ref_x = from_bf16(resid) + from_bf16(to_bf16(ref.astype(np.float32)))
+    gx = from_bf16(ox).astype(np.float64)
+    # RMSNorm (unit gains) of the x the producer wrote, then the consumer GEMM, in float64
+    r = 1.0 / np.sqrt((gx ** 2).sum(1) / N + eps)
+    y_ref = (gx * r[:, None]) @ from_bf16(w2).astype(np.float64).T
+    return gx, ref_x, from_bf16(oy).astype(np.float64), y_ref, fused.value
+
+
+# RMSNorm split across a residual GEMM and its consumer (RowNorm): k-split producers (o / down at
+# 8B, T <= 256) and whole-tile producers (token-split o, prefill shapes) feeding whole-tile,
+# stream-K and k-split consumers (q/k/v, gate/up shapes); a 70B-sized producer at T = 180 leaves
+# k-range planes, so that pair falls back to the RMSNorm kernel
+@pytest.mark.parametrize("T,N,K,N2,want_fused", [
+    (1, 4096, 4096, 4096, 1), (37, 4096, 4096, 28672, 1), (180, 4096, 4096, 28672, 1),
+    (256, 4096, 14336, 6144, 0), (300, 4096, 4096, 6144, 1), (1000, 4096, 4096, 28672, 1),
+    (600, 8192, 8192, 10240, 1), (180, 8192, 8192, 28672, 0),
+])
+def test_gemm_rownorm_pair(T, N, K, N2, want_fused):
+    gx, ref_x, gy, y_ref, fused = _run_norm(T, N, K, N2, seed=T + N)
+    assert fused == want_fused
+    assert np.abs(gx - ref_x).max() <= 2e-2 * np.abs(ref_x).max() + 1e-3
+    assert np.abs(gy - y_ref).max() <= 2e-2 * np.abs(y_ref).max() + 1e-3
