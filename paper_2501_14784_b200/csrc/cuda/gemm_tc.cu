@@ -1114,7 +1114,12 @@ static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) 
     static const int ts_min = getenv("DS_GEMM_TS_MIN") ? atoi(getenv("DS_GEMM_TS_MIN")) : 257;
     const int tiles1 = p.t_blocks * p.m_tiles;
     static const int ks2_env = getenv("DS_GEMM_KS2") ? atoi(getenv("DS_GEMM_KS2")) : 0;
-    const int ks_pick = kNumSMs / tiles1 >= 4 ? 4 : (ks2_env && kNumSMs / tiles1 >= 2 ? 2 : 1);
+    // DS_GEMM_KS3=1: 3-way k-split clusters where 3 * tiles fill the SMs (q/k/v at 8B: 144 CTAs)
+    static const int ks3_env = getenv("DS_GEMM_KS3") ? atoi(getenv("DS_GEMM_KS3")) : 0;
+    const int ks_pick = kNumSMs / tiles1 >= 4   ? 4
+                        : (ks3_env && kNumSMs / tiles1 >= 3) ? 3
+                        : (ks2_env && kNumSMs / tiles1 >= 2) ? 2
+                                                              : 1;
     if (ksplit_env && max_clusters <= 0 && p.tb_pad <= 256 && p.KB >= 8 && ks_pick > 1 &&
         T < ts_min) {
         GemmParams q = p;
