@@ -95,7 +95,8 @@ def load_peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
-NCU_FULL = {"gemm_gate_up": "r02_ncu_full_gemm_gate_up.csv", "attention": "r02_ncu_full_attn_decode.csv",
+NCU_FULL = {"gemm_gate_up": "r02_ncu_full_gemm_gate_up.csv", "attention_decode": "r02_ncu_full_attn_decode.csv",
+            "attention_prompt": "r02_ncu_full_attn_prompt_tc.csv",
             "gemm_down": "r02_ncu_full_gemm_down.csv", "gemm_o": "r02_ncu_full_gemm_o.csv",
             "gemm_qkv": "r02_ncu_full_gemm_qkv.csv"}
 

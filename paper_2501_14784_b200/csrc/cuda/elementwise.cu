@@ -177,18 +177,9 @@ __global__ void __launch_bounds__(512) rope_kv_kernel(const __nv_bfloat16* __res
     const int t = blockIdx.x;
     const int pos = row_pos[t];
     const int half = dh / 2;
-    float sc = 1.f;  // RowNorm scale of the row (q/k/v GEMM of the un-normalised x, planes deferred)
-    if (pl.n > 0 && pl.rs_ssq) {
-        __shared__ float rs_row;
-        if (threadIdx.x < 32) {
-            float ss = 0.f;
-            for (int i = threadIdx.x; i < pl.rs_parts; i += 32) ss += __ldcg(pl.rs_ssq + size_t(i) * gridDim.x + t);
-            ss = warp_sum(ss);
-            if (threadIdx.x == 0) rs_row = 1.0f / sqrtf(ss / float(pl.rs_d) + pl.rs_eps);
-        }
-        __syncthreads();
-        sc = rs_row;
-    }
+    // RowNorm scale of the row (q/k/v GEMM of the un-normalised x, planes deferred), published by
+    // the GEMM; independent of the plane loads, so both are in flight together
+    const float sc = (pl.n > 0 && pl.rs) ? __ldcg(pl.rs + t) : 1.f;
     const int width = (n_h + 2 * n_kv) * dh;
     const __nv_bfloat16* src = qkv + size_t(t) * width;
     const float* c = rc + size_t(pos) * half;

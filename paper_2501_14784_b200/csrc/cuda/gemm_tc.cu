@@ -89,6 +89,7 @@ struct GemmParams {
     int rs_parts;         //   r[t] = 1 / sqrt(sum of its rs_parts parts / rs_d + rs_eps)
     int rs_d;
     float rs_eps;
+    float* rs_out;        // consumer with deferred planes: CTA 0 publishes the row scales [T]
 };
 
 DS_DEVICE unsigned long long gtime() {
@@ -641,6 +642,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
                 for (int k = 0; k < 32; ++k) s += v[k];
             }
             rs[t] = 1.0f / sqrtf(s / float(p.rs_d) + p.rs_eps);
+            if (p.rs_out && blockIdx.x == 0) p.rs_out[t] = rs[t];
         }
         asm volatile("bar.sync 2, 160;" ::: "memory");  // warps 3..7: the scales are in smem
     }
@@ -1166,7 +1168,7 @@ static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) 
         p.n_sk = p.sk_tiles * std::min(p.n_sk / p.sk_tiles, p.KB);
         p.n_clusters = p.n_sk;
         // one plane per k range while they fit the workspace (else TMEM-layout pieces)
-        if (size_t(p.n_sk / p.sk_tiles) * T * N <= kWorkspaceFloats - kCounterInts)
+        if (size_t(p.n_sk / p.sk_tiles) * T * N + T <= kWorkspaceFloats - kCounterInts)
             p.planes = p.n_sk / p.sk_tiles;
     }
     // Remainder tiles run whole (n_sk = sk_tiles: one whole tile per remainder cluster) above
@@ -1217,7 +1219,7 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
     // workspace: [counters: kCounterInts, shared by every shape: a launch leaves them all 0]
     //            [slots: n_clusters * 2 * cn * tb_pad * 128 floats]
     const size_t n_cnt = kCounterInts;
-    const size_t need = n_cnt + (p.planes ? size_t(p.planes) * T * N
+    const size_t need = n_cnt + (p.planes ? size_t(p.planes) * T * N + T
                                           : size_t(p.n_clusters) * 2 * cn * p.tb_pad * kBM);
     if (p.sk_tiles > 0 && (!workspace || workspace_floats < need || size_t(tiles) * cn > n_cnt))
         return -7;
@@ -1267,6 +1269,7 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
         p.rs_parts = rn->parts;
         p.rs_d = rn->d;
         p.rs_eps = rn->eps;
+        if (p.planes) p.rs_out = p.slots + size_t(p.planes) * T * N;  // behind the planes
     }
     alignas(64) CUtensorMap tx;
     if (make_tmap_2d_bf16(&tx, x, T, K, p.brows, kBK) != 0) return -5;
@@ -1295,12 +1298,7 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
         defer->p = p.slots;
         defer->n = p.planes;
         defer->stride = size_t(T) * N;
-        if (p.rs_ssq) {  // the consumer of the planes applies the row scale
-            defer->rs_ssq = p.rs_ssq;
-            defer->rs_parts = p.rs_parts;
-            defer->rs_d = p.rs_d;
-            defer->rs_eps = p.rs_eps;
-        }
+        if (p.rs_ssq) defer->rs = p.rs_out;  // the consumer of the planes applies the row scales
     } else if (p.planes && !no_finish) {
         const size_t total4 = size_t(T) * N / 4;
         const int blocks = int(std::min<size_t>((total4 + 255) / 256, size_t(kNumSMs) * 8));

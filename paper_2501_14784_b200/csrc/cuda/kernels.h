@@ -32,11 +32,9 @@ struct Planes {
     const float* p = nullptr;
     int n = 0;
     size_t stride = 0;
-    // RowNorm consumer deferred with the planes: row t of the sum is scaled by
-    // 1 / sqrt(sum of rs_parts parts rs_ssq[i * T + t] / rs_d + rs_eps) before rounding
-    const float* rs_ssq = nullptr;
-    int rs_parts = 0, rs_d = 0;
-    float rs_eps = 0.f;
+    // RowNorm consumer deferred with the planes: row t of the sum is scaled by rs[t] (the
+    // GEMM's row scales) before rounding; nullptr: no scale
+    const float* rs = nullptr;
 };
 
 // RMSNorm split across a residual GEMM and the GEMM that consumes the normalised rows (unit

@@ -159,9 +159,10 @@ uint8_t* host_page_ptr(ds_stage* s, int mb, int h) {
 bf16* dev_page_ptr(ds_stage* s, int p) { return s->kv.pool + size_t(p) * s->kv.page_elems; }
 
 // PK_SWAPW: time the compute stream waits for the KV swap-in of its microbatch (not a kernel)
-enum ProfKind { PK_QKV, PK_ATTN, PK_O, PK_GU, PK_DOWN, PK_LMHEAD, PK_ELEM, PK_SWAPW, PK_COUNT };
-const char* kPkName[PK_COUNT] = {"gemm_qkv", "attention", "gemm_o", "gemm_gate_up", "gemm_down",
-                                 "gemm_lm_head", "elementwise", "swap_wait"};
+// PK_ATTN: prompt (chunked-prefill) attention; PK_ATTN_DEC: decode-row attention
+enum ProfKind { PK_QKV, PK_ATTN, PK_O, PK_GU, PK_DOWN, PK_LMHEAD, PK_ELEM, PK_SWAPW, PK_ATTN_DEC, PK_COUNT };
+const char* kPkName[PK_COUNT] = {"gemm_qkv", "attention_prompt", "gemm_o", "gemm_gate_up", "gemm_down",
+                                 "gemm_lm_head", "elementwise", "swap_wait", "attention_decode"};
 
 size_t prof_mark(ds_stage* s) {
     if (s->ev_used == s->ev_pool.size()) {
@@ -863,14 +864,17 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
     // algorithmic work per launch group (roofline accounting)
     const int qkv_rows = m.n_heads * m.d_head + 2 * m.n_kv_heads * m.d_head;
     const int qdim = m.n_heads * m.d_head;
-    double attn_bytes = 0, attn_flops = 0;
+    // algorithmic attention work, prompt rows and decode rows (n_tok == 1) apart: K and V of the
+    // request once, q in and o out
+    double attn_bytes = 0, attn_flops = 0, dec_bytes = 0, dec_flops = 0;
     for (int64_t i = 0; i < n_rows; ++i) {
         const double end = double(rows[i].pos + rows[i].n_tok);
-        attn_bytes += end * m.n_kv_heads * m.d_head * 4.0;
+        double& by = rows[i].n_tok == 1 ? dec_bytes : attn_bytes;
+        double& fl = rows[i].n_tok == 1 ? dec_flops : attn_flops;
+        by += end * m.n_kv_heads * m.d_head * 4.0 + double(rows[i].n_tok) * qdim * 4.0;
         for (int j = 0; j < rows[i].n_tok; ++j)
-            attn_flops += 4.0 * m.n_heads * m.d_head * double(rows[i].pos + j + 1);
+            fl += 4.0 * m.n_heads * m.d_head * double(rows[i].pos + j + 1);
     }
-    attn_bytes += double(T) * qdim * 4.0;
     size_t mark = 0;
     auto begin = [&]() { if (s->prof) mark = prof_mark(s); };
     static const bool check_each = getenv("DS_CHECK_LAUNCH") != nullptr;  // debug: name the failing group
@@ -943,13 +947,26 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
         begin();
         ds::L2Prefetch pf_o;
         if (pf_env) pf_o = {lw.wo.data, size_t(d) * qdim * 2};
-        if (!(skip & 4))
-            rc |= ds::attention_paged(s->q, T, m.n_heads, d_pos, d_poff, d_flat, d_blk, n_blk,
-                                      d_blk + 3 * n_blk, n_drow, s->kv, li, s_prompt,
-                                      s_decode, s->attn, s->attn_ws, s->attn_ws_floats, s->attn_cnt,
-                                      pf_o, st);
-        end_other(PK_ATTN, attn_flops, attn_bytes,
-                  ds::attention_launches(n_blk, n_drow, s_prompt, s_decode));
+        if (s->prof) {  // profiled run: the prompt and decode launches timed apart (same launches)
+            if (!(skip & 4) && n_blk > 0)
+                rc |= ds::attention_paged(s->q, T, m.n_heads, d_pos, d_poff, d_flat, d_blk, n_blk,
+                                          d_blk + 3 * n_blk, 0, s->kv, li, s_prompt, s_decode, s->attn,
+                                          s->attn_ws, s->attn_ws_floats, s->attn_cnt, pf_o, st);
+            if (n_blk > 0) end_other(PK_ATTN, attn_flops, attn_bytes, ds::attention_launches(n_blk, 0, s_prompt, s_decode));
+            begin();
+            if (!(skip & 4) && n_drow > 0)
+                rc |= ds::attention_paged(s->q, T, m.n_heads, d_pos, d_poff, d_flat, d_blk, 0,
+                                          d_blk + 3 * n_blk, n_drow, s->kv, li, s_prompt, s_decode, s->attn,
+                                          s->attn_ws, s->attn_ws_floats, s->attn_cnt, pf_o, st);
+            if (n_drow > 0) end_other(PK_ATTN_DEC, dec_flops, dec_bytes, ds::attention_launches(0, n_drow, s_prompt, s_decode));
+        } else {
+            if (!(skip & 4))
+                rc |= ds::attention_paged(s->q, T, m.n_heads, d_pos, d_poff, d_flat, d_blk, n_blk,
+                                          d_blk + 3 * n_blk, n_drow, s->kv, li, s_prompt,
+                                          s_decode, s->attn, s->attn_ws, s->attn_ws_floats, s->attn_cnt,
+                                          pf_o, st);
+            s->launches += ds::attention_launches(n_blk, n_drow, s_prompt, s_decode);
+        }
         begin();
         int o_parts = 0;
         if (!(skip & 16))
