@@ -1235,11 +1235,15 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
         // many MB over the CTAs). Off: measured slower on every 8B shape (qkv 20.7 -> 22.4 us,
         // down 30.8 -> 33.6 us at T = 180) and 14.13 k -> 13.69 k tok/s on config 2
         // (profiles/r02_ab_l2pf.txt): the prefetch competes with the previous kernel's stream.
+        // DS_GEMM_L2PF_KMIN restricts it to GEMMs with K >= the value (the down projection, whose
+        // CTAs start on the SMs gate/up's last round leaves idle): slower too
+        // (profiles/r02_ab_l2pf_down.txt).
         static const int pf_env = getenv("DS_GEMM_L2PF") ? atoi(getenv("DS_GEMM_L2PF")) : 0;
+        static const int pf_kmin = getenv("DS_GEMM_L2PF_KMIN") ? atoi(getenv("DS_GEMM_L2PF_KMIN")) : 0;
         const size_t wbytes = size_t(N) * K * 2;
         const int ctas = p.n_clusters * cn * p.ks;
         const size_t per_kb = size_t(kBM) * kBK * 2;  // one k-block of one CTA's 128 rows
-        if (pf_env <= 0 || ctas <= 0)
+        if (pf_env <= 0 || ctas <= 0 || K < pf_kmin)
             p.pf_kb = 0;
         else if (wbytes <= (size_t(64) << 20))
             p.pf_kb = 1 << 20;

@@ -4,6 +4,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -808,6 +809,25 @@ ds_status ds_stage_step(ds_stage* s, int32_t mb, const ds_row* rows, int64_t n_r
         for (int64_t i = 0; i < n_rows; ++i) {
             if (rows[i].n_tok == 1) blk[3 * n_blk + n_drow++] = tb;
             tb += rows[i].n_tok;
+        }
+        // Longest work first (DS_ATTN_LPT=1): the block scheduler hands out CTAs in blockIdx
+        // order, so query blocks by descending last position and decode rows by descending
+        // context keep the longest CTAs out of the last wave. A pure reordering of CTA -> work
+        // (every output row is written by the same arithmetic: bit-identical). Off: measured
+        // neutral on config 2 (14.26 k vs 14.27 k tok/s, decode attention 979 vs 983 ms per
+        // profiled step, profiles/r02_ab_lpt.txt) -- the decode grids run 3-5 waves of
+        // similar-length CTAs, so the tail was already short.
+        static const bool lpt = getenv("DS_ATTN_LPT") && atoi(getenv("DS_ATTN_LPT")) != 0;
+        if (lpt) {
+            std::vector<std::array<int32_t, 3>> bl(static_cast<size_t>(n_blk));
+            for (int b = 0; b < n_blk; ++b) bl[b] = {blk[3 * b], blk[3 * b + 1], blk[3 * b + 2]};
+            std::stable_sort(bl.begin(), bl.end(), [&](const auto& a, const auto& b) {
+                return row_pos[a[0]] + a[1] > row_pos[b[0]] + b[1];
+            });
+            for (int b = 0; b < n_blk; ++b)
+                for (int j = 0; j < 3; ++j) blk[3 * b + j] = bl[b][j];
+            std::stable_sort(blk + 3 * n_blk, blk + 3 * n_blk + n_drow,
+                             [&](int32_t a, int32_t b) { return row_pos[a] > row_pos[b]; });
         }
         int max_prompt_ctx = 1;
         for (int64_t i = 0; i < n_rows; ++i)
