@@ -40,6 +40,7 @@ namespace ds {
 constexpr int kBM = 128;      // weight rows per CTA tile (UMMA M)
 constexpr int kBK = 64;       // K elements per stage = one 128-byte swizzle row
 constexpr int kMaxTB = 512;   // tokens per block (TMEM columns)
+constexpr int kSkPieces = 8;  // stream-K pieces per remainder tile (0: uncapped); DS_GEMM_SKP
 constexpr int kGemmThreads = 256;
 constexpr int kSmemBudget = 222 * 1024;
 constexpr int kStageStride = 36;  // floats per row of the epilogue transpose buffer
@@ -1178,6 +1179,17 @@ static GemmParams plan_gemm(int T, int N, int K, int max_clusters, int* cn_out) 
     static const int whole_env = getenv("DS_GEMM_WHOLE") ? atoi(getenv("DS_GEMM_WHOLE")) : -1;
     const bool whole = whole_env >= 0 ? whole_env != 0 : p.tb_pad > 128;
     if (p.dp_rounds > 0 && whole) p.n_sk = p.sk_tiles;
+    // Pieces per stream-K remainder tile (DS_GEMM_SKP; 0 = as many as clusters): a tile split
+    // over many clusters makes its last arriver read every other piece's partial sums before
+    // its data-parallel tiles. 70B gate/up (224 pair tiles: 3 rounds + 2 remainder tiles over 74
+    // clusters, 37 pieces each) at T = 49: 188 us uncapped, 153 / 148 / 146 us with 2 / 4 / 8
+    // pieces, 155 us with 16; T = 128: 225 -> 151 us; 8B gate/up and the LM head unchanged
+    // (their remainders already split in <= 2). Measured twice: profiles/r02_gemm_skp.txt.
+    // (Capped stream-K remainders above 128 tokens instead of whole tiles: faster for 70B gate/up
+    // at T = 160-256, slower on the 8B and prefill shapes -- not adopted.)
+    static const int skp = getenv("DS_GEMM_SKP") ? atoi(getenv("DS_GEMM_SKP")) : kSkPieces;
+    if (p.dp_rounds > 0 && !whole && skp > 0 && p.sk_tiles > 0)
+        p.n_sk = std::min(p.n_sk, p.sk_tiles * skp);
     // the in-kernel last arriver pays off when its reads overlap the next tile's MMAs (data-
     // parallel tiles follow, accumulator double-buffered); otherwise a finish kernel spreads them
     p.defer = (p.sk_tiles > 0 && p.dp_rounds == 0) ? 1 : 0;

@@ -12,7 +12,8 @@ from paper_2501_14784_b200._native import check, lib  # noqa: E402
 peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
 HBM, TF = peaks["hbm_gbs"], peaks["bf16_tflops"]
 shapes = {"qkv8b": (6144, 4096), "o8b": (4096, 4096), "gu8b": (28672, 4096), "down8b": (4096, 14336),
-          "lm": (128256, 4096), "gu70b": (57344, 8192)}
+          "lm": (128256, 4096), "gu70b": (57344, 8192), "qkv70b": (10240, 8192), "o70b": (8192, 8192),
+          "down70b": (8192, 28672)}
 Ts = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [1, 16, 64, 128, 256, 384, 512]
 MC = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0]
 only = sys.argv[3].split(",") if len(sys.argv) > 3 else None
