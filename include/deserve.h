@@ -297,6 +297,11 @@ ds_status ds_dbg_gemm_norm(const uint16_t* x, const uint16_t* w1, int32_t T, int
                            uint16_t* out_x, uint16_t* out_y, int32_t* fused);
 ds_status ds_dbg_gemm_bench(int32_t T, int32_t N, int32_t K, int32_t epi, int32_t iters,
                             int32_t k_splits, float* ms_out);
+/* The GEMM work partition for a [T x K] . [N x K]^T product, host arithmetic only (no device):
+ * out[12] = {0, CTAs per cluster, clusters, data-parallel rounds, stream-K remainder tiles,
+ * stream-K clusters, k-split ways, planes, deferred finish, tokens per block, token blocks,
+ * k-blocks per tile}. */
+ds_status ds_dbg_gemm_plan(int32_t T, int32_t N, int32_t K, int32_t* out);
 ds_status ds_dbg_has_device(int32_t* n_devices);
 ds_status ds_dbg_alloc(int32_t device, int64_t bytes, void** out);
 ds_status ds_dbg_free(void* ptr);

@@ -121,6 +121,7 @@ def _load() -> C.CDLL:
         "ds_dbg_gemm_norm": (I32, [P, P, I32, I32, I32, P, P, I32, C.c_float, P, P, P]),
         "ds_dbg_has_device": (I32, [P]),
         "ds_dbg_gemm_bench": (I32, [I32, I32, I32, I32, I32, I32, P]),
+        "ds_dbg_gemm_plan": (I32, [I32, I32, I32, P]),
         "ds_dbg_alloc": (I32, [I32, I64, P]),
         "ds_dbg_free": (I32, [P]),
         "ds_dbg_copy": (I32, [P, P, I64]),

@@ -1206,6 +1206,15 @@ static bool rowscale_ok(const GemmParams& p, int T, bool deferred) {
     return !p.defer;
 }
 
+int gemm_describe(int T, int N, int K, int32_t* out) {
+    int cn = 0;
+    const GemmParams p = plan_gemm(T, N, K, 0, &cn);
+    const int32_t v[12] = {p.T < 0 ? p.T : 0, cn, p.n_clusters, p.dp_rounds, p.sk_tiles, p.n_sk, p.ks,
+                           p.planes, p.defer, p.tb, p.t_blocks, p.KB};
+    for (int i = 0; i < 12; ++i) out[i] = v[i];
+    return p.T < 0 ? p.T : 0;
+}
+
 bool gemm_rowscale_ok(int T, int N, int K, bool deferred) {
     int cn = 0;
     GemmParams p = plan_gemm(T, N, K, 0, &cn);

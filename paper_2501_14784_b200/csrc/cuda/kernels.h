@@ -72,6 +72,10 @@ int gemm_bf16(const GemmWeight& w, const __nv_bfloat16* x, int T, int epi, __nv_
               int max_clusters, cudaStream_t stream, Planes* defer = nullptr,
               const RowNorm* rn = nullptr, int* ssq_parts = nullptr);
 bool gemm_rowscale_ok(int T, int N, int K, bool deferred);
+// The work partition plan_gemm picks (host arithmetic only, no device): out[12] = {status, CTAs
+// per cluster, clusters, data-parallel rounds, stream-K tiles, stream-K clusters, k-split ways,
+// planes, deferred finish, tokens per block, token blocks, k-blocks per tile}.
+int gemm_describe(int T, int N, int K, int32_t* out);
 
 // Counter-based weight init (bf16(uniform(-1,1) * scale)); see oracle/llama_ref.c ds_ref_weight.
 // interleave_part >= 0 writes the [rows, cols] tensor into the gate/up interleaved layout:

@@ -179,6 +179,12 @@ size_t prof_mark(ds_stage* s) {
 
 extern "C" {
 
+ds_status ds_dbg_gemm_plan(int32_t T, int32_t N, int32_t K, int32_t* out) {
+    if (!out || T < 1 || N < 1 || K < 1) return ds_fail(DS_ERR_ARG, "bad GEMM shape");
+    if (ds::gemm_describe(T, N, K, out) < 0) return ds_fail(DS_ERR_ARG, "unsupported GEMM shape");
+    return DS_OK;
+}
+
 ds_status ds_dbg_has_device(int32_t* n) {
     int c = 0;
     cudaError_t e = cudaGetDeviceCount(&c);
