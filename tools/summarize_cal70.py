@@ -1,5 +1,5 @@
 #!/usr/bin/env python3
-"""Summarise tools/gpu_70b_attn.sh's ncu launch list (cold-cache, serialised launches) into
+"""Summarise tools/gpu_calls/gpu_70b_attn.sh's ncu launch list (cold-cache, serialised launches) into
 per-kind time, DRAM bytes, and fractions of the measured peaks at Llama-3-70B stage shapes.
 Algorithmic bytes: weights + bf16 activations in/out (GEMMs); K and V of every row's context
 once + q/o (decode attention). Usage: summarize_cal70.py launches.csv [peaks.json]"""
