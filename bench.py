@@ -308,6 +308,12 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    n = max(world, args.gpus)
+    config = dict(ARM_CONFIG)
+    if n > 1:  # our arm's N>1 config (same dict); the CPU has no stage split: whole-model rows
+        from bench_multi import arm_config
+        config = arm_config(n)
     idx = systematic_sample(761, args.steps)
     res, n_circ, toks = oracle_circuits(idx, warmup=args.warmup)
     t = sum(x[1] for x in res)
@@ -319,13 +325,16 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init weights, counter-RNG prompts; lengths from the reference "
                     "generator seed 42)",
-            "config": dict(ARM_CONFIG),
+            "config": config,
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
                              "sample": f"oracle/llama_ref.c (OpenMP, {os.cpu_count()} threads), all 32 "
                                        f"layers + embedding + LM head, one circuit per step: "
                                        f"circuits {idx} of {n_circ} (exact rows; warm-up "
                                        f"{args.warmup} x the smallest circuit); {dec} decode rows "
-                                       f"in {t:.2f} s",
+                                       f"in {t:.2f} s" + (
+                                           "; at N > 1 the same full-depth circuits of the 8B "
+                                           "offline schedule: one host's cores run the whole "
+                                           "model whatever the stage split" if n > 1 else ""),
                              "per_circuit": [{"circuit": i, "s": round(x, 3), "decode_rows": d,
                                               "rows": e} for i, x, d, e in res],
                              "est_whole_batch_s": round(t * n_circ / len(res), 1)},

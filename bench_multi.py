@@ -38,6 +38,18 @@ def pipeline_config(n_stages, name=BASE_CONFIG, latency_us=None):
     return cfg
 
 
+def arm_config(world):
+    """The N>1 arm's `config` (deterministic for a given N; the run-dependent window and counts go
+    to `workload_detail`). Read from the config document alone, so bench.py's reference arm emits
+    the identical dict without loading the product."""
+    nb = json.load(open(os.path.join(CONFIGS, BASE_CONFIG)))["scheduler"]["nb_override"]
+    return {"workload": f"Llama-3-8B {world}-stage pipeline on {world}xB200, 100 ms injected "
+                        f"latency per hop, {nb} microbatches, KV swap on (configs/{BASE_CONFIG} "
+                        f"with {world} nodes, as written)",
+            "parallelism": f"pp{world}",
+            "hops": "NCCL send/recv over NVLink, one 2-rank communicator per ring link"}
+
+
 def run_multi(args):
     import torch.distributed as dist
 
@@ -153,12 +165,9 @@ def run_multi(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights, counter-RNG prompts; lengths from the reference "
                 "generator seed 42)",
-        "config": {"workload": f"Llama-3-8B {world}-stage pipeline on {world}xB200, 100 ms injected "
-                               f"latency per hop, {nb} microbatches, KV swap on (configs/{BASE_CONFIG} "
-                               f"with {world} nodes, as written)",
-                   "parallelism": f"pp{world}",
-                   "window_us": [w0, w1], "circuits": last["circuits"], "rows": last["rows"],
-                   "hops": "NCCL send/recv over NVLink, one 2-rank communicator per ring link"},
+        "config": arm_config(world),
+        "workload_detail": {"microbatches": nb, "window_us": [w0, w1], "circuits": last["circuits"],
+                            "rows": last["rows"]},
         "window": "reference windowed_stats over [warmup_s, min(bench_duration_s, run end)) of the "
                   "real-clock EventTrace (merged over ranks); steps = equal sub-windows",
         "sub_window_tokens_per_s": [round(x, 1) for x in subs],
