@@ -64,3 +64,20 @@ def test_bench_refuses_invalidating_switches(var):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1"],
                        capture_output=True, text=True, timeout=120, env=env)
     assert r.returncode != 0 and var in r.stderr
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_multi_gpu_config_is_shared_and_product_free(n):
+    """The N>1 arm's `config` comes from the config document alone (bench_multi.arm_config), so
+    the reference arm under torchrun prints the identical dict without loading the product."""
+    code = (
+        "import sys, json; sys.path.insert(0, %r); import bench_multi\n"
+        "c = bench_multi.arm_config(%d)\n"
+        "assert 'paper_2501_14784_b200' not in sys.modules\n"
+        "print(json.dumps(c))\n" % (ROOT, n))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr[-500:]
+    c = json.loads(r.stdout.strip().splitlines()[-1])
+    assert c["parallelism"] == f"pp{n}" and f"{n}-stage pipeline on {n}xB200" in c["workload"]
+    assert "32 microbatches" in c["workload"] and "KV swap on" in c["workload"]
+    assert set(c) == {"workload", "parallelism", "hops"}  # no run-dependent fields
