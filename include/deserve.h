@@ -254,6 +254,13 @@ ds_status ds_trace_report(const char* trace_path, int64_t n_stages, int64_t w0_u
  * JSON (ds_run / ds_session_trace / ds_sim_config "report") on its plan document. */
 ds_status ds_report_kv(const char* report_json, const char* plan_json, int64_t latency_us,
                        const char* policy, char* out, size_t cap, size_t* needed);
+/* report_kv with the pricing block (report_to_kv with a ProfitAnalysis, src/sweep.cpp:187-194):
+ * pricing_json is a config document's "pricing" object ({"preset": name} or the money fields,
+ * src/config.cpp:169-199); the analysis is the reference's analyze (src/economics.cpp:21-59).
+ * DS_ERR_ARG on a bad pricing object or a zero unified price, DS_ERR_RUNTIME on an empty window. */
+ds_status ds_report_kv_priced(const char* report_json, const char* plan_json, int64_t latency_us,
+                              const char* policy, const char* pricing_json, char* out, size_t cap,
+                              size_t* needed);
 /* The reference's sweep.csv (SweepResult::to_csv, src/sweep.cpp:68-82): policies x latencies
  * output throughputs (row-major; NaN = failed cell). policies: comma-separated names. */
 ds_status ds_sweep_csv(const int64_t* latencies_us, int32_t n_latencies, const char* policies,

@@ -58,6 +58,7 @@ class Ref:
             "ref_windowed_stats": [S, L, L, C.c_int, P],
             "ref_request": [C.c_ulonglong, L, L, L, L, L, P],
             "ref_report_kv": [S, S, S, L, L, P, C.c_size_t],
+            "ref_report_kv_priced": [S, S, S, L, L, P, C.c_size_t],
             "ref_sweep_csv": [S, S, P, C.c_size_t],
         }.items():
             getattr(lib, name).argtypes = args
@@ -92,6 +93,12 @@ class Ref:
         buf = C.create_string_buffer(1 << 16)
         self._ok(self.lib.ref_report_kv(_b(text), _b(cdir), _b(policy or ""), latency_us, nb, buf,
                                         len(buf)))
+        return buf.value.decode()
+
+    def report_kv_priced(self, text, cdir="", policy=None, latency_us=-1, nb=-1) -> str:
+        buf = C.create_string_buffer(1 << 16)
+        self._ok(self.lib.ref_report_kv_priced(_b(text), _b(cdir), _b(policy or ""), latency_us, nb,
+                                               buf, len(buf)))
         return buf.value.decode()
 
     def sweep_csv(self, text, cdir="") -> str:

@@ -14,6 +14,7 @@
 #include <string>
 
 #include "pipesim/config.hpp"
+#include "pipesim/economics.hpp"
 #include "pipesim/perf_model.hpp"
 #include "pipesim/planner.hpp"
 #include "pipesim/sim.hpp"
@@ -117,6 +118,21 @@ int ref_report_kv(const char* text, const char* dir, const char* policy, long lo
         SimResult r = run(p.plan, p.topo, p.cfg.workload, p.cfg.model);
         const Micros lat = p.topo.links.empty() ? 0 : p.topo.links.front().latency_us;
         put(report_to_kv(r.report, p.plan, lat, policy && *policy ? policy : "config", nullptr), out, cap);
+        return 0;
+    });
+}
+
+// report_to_kv with the config's pricing (analyze, src/economics.cpp:21-59): the reference's
+// priced report.kv of run() on the config; pricing_json (optional) replaces the config's section
+int ref_report_kv_priced(const char* text, const char* dir, const char* policy, long long latency,
+                         long long nb, char* out, size_t cap) {
+    return guard([&] {
+        Planned p = make(text, dir, policy, latency, nb);
+        if (!p.cfg.has_pricing) throw ConfigError("config has no pricing section");
+        SimResult r = run(p.plan, p.topo, p.cfg.workload, p.cfg.model);
+        const Micros lat = p.topo.links.empty() ? 0 : p.topo.links.front().latency_us;
+        const ProfitAnalysis pa = analyze(r.report, p.cfg.pricing);
+        put(report_to_kv(r.report, p.plan, lat, policy && *policy ? policy : "config", &pa), out, cap);
         return 0;
     });
 }

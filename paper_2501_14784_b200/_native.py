@@ -115,6 +115,7 @@ def _load() -> C.CDLL:
         "ds_session_capture": (I32, [P, P, I64]),
         "ds_session_limit": (I32, [P, I64, P]),
         "ds_report_kv": (I32, [S, S, I64, S, P, C.c_size_t, P]),
+        "ds_report_kv_priced": (I32, [S, S, I64, S, S, P, C.c_size_t, P]),
         "ds_sweep_csv": (I32, [P, I32, S, P, P, C.c_size_t, P]),
         "ds_session_captured": (I32, [P, P, P, I64, P]),
         "ds_dbg_gemm": (I32, [P, P, I32, I32, I32, I32, P, I32, P]),

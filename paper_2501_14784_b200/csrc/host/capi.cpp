@@ -402,6 +402,22 @@ ds_status ds_report_kv(const char* report_json, const char* plan_json, int64_t l
     });
 }
 
+ds_status ds_report_kv_priced(const char* report_json, const char* plan_json, int64_t latency_us,
+                              const char* policy, const char* pricing_json, char* out, size_t cap,
+                              size_t* needed) {
+    return guarded([&] {
+        if (!report_json || !plan_json || !pricing_json)
+            return ds_fail(DS_ERR_ARG, "null report/plan/pricing");
+        const dsb::Report r = dsb::report_from_json(report_json);
+        const dsb::Plan p = dsb::Plan::from_json(plan_json);
+        const dsb::Pricing pr = dsb::parse_pricing(pricing_json);
+        copy_out(dsb::report_kv(r, p, latency_us, policy ? policy : "") +
+                     dsb::profit_kv(dsb::analyze(r, pr)),
+                 out, cap, needed);
+        return DS_OK;
+    });
+}
+
 ds_status ds_sweep_csv(const int64_t* lat, int32_t n_lat, const char* policies, const double* tput,
                        char* out, size_t cap, size_t* needed) {
     return guarded([&] {

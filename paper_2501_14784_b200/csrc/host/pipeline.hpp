@@ -189,6 +189,26 @@ std::string report_kv(const Report& r, const Plan& p, Micros latency, const std:
 std::string sweep_csv(const std::vector<Micros>& lat, const std::vector<std::string>& pol,
                       const std::vector<double>& tput);
 
+// ---- profit model on reports (economics.cpp; reference economics.cpp:9-81, config.cpp:169-199)
+struct Pricing {
+    std::string name;
+    int64_t cost_per_hour_micro = 0;  // C
+    int64_t price_nano = 0;           // P (unified price per token)
+    int64_t price_in_nano = 0;        // P_I
+    int64_t price_out_nano = 0;       // P_O
+    bool unified() const { return price_in_nano == price_nano && price_out_nano == price_nano; }
+};
+struct Profit {
+    int64_t revenue_micro = 0, cost_micro = 0, profit_micro = 0;
+    double min_throughput = 0, achieved_throughput = 0;
+    bool profitable = false;
+};
+// the config's "pricing" object ({"preset": name} or money fields); throws ConfigError
+Pricing parse_pricing(const std::string& json_text);
+Profit analyze(const Report& r, const Pricing& p);
+// the pricing block report_to_kv appends (src/sweep.cpp:187-194)
+std::string profit_kv(const Profit& p);
+
 struct StageStats {
     Micros busy = 0, stall = 0, bubble = 0;
     double busy_frac = 0, stall_frac = 0, bubble_frac = 0;

@@ -172,13 +172,23 @@ def trace_report(trace_path: str, n_stages: int, w0_us: int, w1_us: int, seed: i
     return json.loads(buf.value.decode())
 
 
-def report_kv(report: dict, plan_json: str, latency_us: int, policy: str) -> str:
-    """report.kv text of a report (reference report_to_kv, sweep.cpp:146-195)."""
+def report_kv(report: dict, plan_json: str, latency_us: int, policy: str, pricing=None) -> str:
+    """report.kv text of a report (reference report_to_kv, sweep.cpp:146-195). `pricing` (a config
+    document's "pricing" object, e.g. {"preset": "whattomine-8x4090"}) appends the profit block of
+    the reference's analyze (economics.cpp:21-59), as report_to_kv does with a ProfitAnalysis."""
     need = C.c_size_t(0)
     rj = _b(json.dumps(report))
-    check(lib.ds_report_kv(rj, _b(plan_json), latency_us, _b(policy), None, 0, C.byref(need)))
+    if pricing is None:
+        check(lib.ds_report_kv(rj, _b(plan_json), latency_us, _b(policy), None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        check(lib.ds_report_kv(rj, _b(plan_json), latency_us, _b(policy), buf, need.value, None))
+        return buf.value.decode()
+    pj = _b(pricing if isinstance(pricing, str) else json.dumps(pricing))
+    check(lib.ds_report_kv_priced(rj, _b(plan_json), latency_us, _b(policy), pj, None, 0,
+                                  C.byref(need)))
     buf = C.create_string_buffer(need.value)
-    check(lib.ds_report_kv(rj, _b(plan_json), latency_us, _b(policy), buf, need.value, None))
+    check(lib.ds_report_kv_priced(rj, _b(plan_json), latency_us, _b(policy), pj, buf, need.value,
+                                  None))
     return buf.value.decode()
 
 

@@ -4,6 +4,7 @@ CPU only."""
 import hashlib
 import json
 import os
+import sys
 
 import pytest
 
@@ -383,3 +384,64 @@ def test_reference_binding_links_and_maps_errors(tmp_path):
     with pytest.raises(oracle.RefError, match="CUDA device"):
         oracle.binding_run_and_check(txt, CONFIGS, pl.plan_config(txt, CONFIGS),
                                      pl.model_desc("tiny-llama"), opts, str(tmp_path / "t.trace"))
+
+
+PRICINGS = [
+    {"preset": "whattomine-8x4090"}, {"preset": "gcp-8xL4"}, {"preset": "runpod-8x4090"},
+    {"preset": "ionet-8x4090"},
+    {"compute_cost_per_hour": 2.5, "price_per_token": 0.0000009},
+    {"compute_cost_per_hour": 13.878, "price_per_token": 0.0000002,
+     "price_in_per_token": 0.0000001, "price_out_per_token": 0.0000004},
+    {"compute_cost_per_hour": 40.0, "price_per_token": 0.00000001},  # unprofitable
+]
+
+
+@pytest.mark.parametrize("pricing", PRICINGS)
+@pytest.mark.parametrize("policy,latency", [("opt", 64000), ("baseline", 16000)])
+def test_priced_report_kv_identical(ref, pricing, policy, latency):
+    """report.kv with the profit block (ds_report_kv_priced: economics.cpp restated) is
+    byte-identical to the reference's report_to_kv(report, plan, latency, policy, &analyze(...))
+    for presets, unified and split prices, profitable or not."""
+    cfg = json.load(open(os.path.join(REF_CONFIGS, "reference_8stage.json")))
+    cfg["pricing"] = pricing
+    txt = json.dumps(cfg)
+    rep = pl.sim_config(txt, REF_CONFIGS, policy=policy, latency_us=latency)
+    plan = pl.plan_config(txt, REF_CONFIGS, policy=policy, latency_us=latency)
+    ours = pl.report_kv(rep, plan, latency, policy, pricing)
+    assert ours == ref.report_kv_priced(txt, REF_CONFIGS, policy, latency)
+    assert ours.startswith(pl.report_kv(rep, plan, latency, policy)) and "profitable=" in ours
+
+
+@pytest.mark.parametrize("pricing,msg", [
+    ({"preset": "nope"}, "unknown pricing preset"),
+    ({"preset": "gcp-8xL4", "price_per_token": 1}, "unknown field"),
+    ({"compute_cost_per_hour": 1.0}, "no price fields"),
+    ({"compute_cost_per_hour": 1.0000001, "price_per_token": 0.000001}, "finer than"),
+    ({"compute_cost_per_hour": 1.0, "price_in_per_token": 0.000001}, "positive price per token"),
+])
+def test_priced_report_kv_errors(ref, pricing, msg):
+    """Pricing errors as the reference raises them: config parsing (config.cpp:169-199) and
+    analyze's zero unified price (economics.cpp:16-20: split prices without price_per_token)."""
+    cfg = json.load(open(os.path.join(REF_CONFIGS, "reference_8stage.json")))
+    cfg["pricing"] = pricing
+    txt = json.dumps(cfg)
+    rep = pl.sim_config(json.dumps(dict(cfg, pricing={"preset": "gcp-8xL4"})), REF_CONFIGS)
+    plan = pl.plan_config(json.dumps(dict(cfg, pricing={"preset": "gcp-8xL4"})), REF_CONFIGS)
+    with pytest.raises(Exception, match=msg):
+        pl.report_kv(rep, plan, 0, "config", pricing)
+    with pytest.raises(Exception, match=msg):
+        ref.report_kv_priced(txt, REF_CONFIGS)
+
+
+@pytest.mark.parametrize("run", ["r02_70b_8stage_4gpu", "r02_8b_4stage_swap_pin",
+                                 "r02_70b_4stage_swap_pin"])
+def test_hardware_runs_repriced(tmp_path, run):
+    """Economics on GPU runs: the committed real-clock hardware trace of a B200 run rebuilds its
+    committed report.kv byte for byte (ds_trace_report), and the priced report appends the
+    reference's profit block (tools/price_runs.py; profiles/<run>/report_priced.kv)."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import price_runs
+    d = os.path.join(ROOT, "profiles", run)
+    out = price_runs.price_run(d, {"preset": "whattomine-8x4090"}, out_dir=str(tmp_path))
+    assert out["profitable"] == "1" and int(out["revenue_micro_usd"]) > int(out["cost_micro_usd"])
+    assert open(tmp_path / "report_priced.kv").read() == open(os.path.join(d, "report_priced.kv")).read()

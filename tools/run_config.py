@@ -69,7 +69,8 @@ def run_one(txt, cdir, policy=None, latency_us=-1, gpus=1, circuits=0, profile=T
     if lat < 0:
         links = json.loads(txt).get("links", [])
         lat = links[0]["latency_us"] if links else 0
-    kv = pl.report_kv(rep, plan, lat, policy or "config")
+    # the config's pricing section, when it has one, adds the reference's profit block
+    kv = pl.report_kv(rep, plan, lat, policy or "config", json.loads(txt).get("pricing"))
     viol = oracle.Ref().replay_check(trace, plan)
     kinds = {}
     for v in viol:
