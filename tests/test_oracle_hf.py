@@ -139,3 +139,21 @@ def test_oracle_matches_hf_llama_at_8b_dims():
     top = np.sort(hf)[-2:]
     if top[1] - top[0] > 0.16:
         assert int(np.argmax(ours)) == int(np.argmax(hf))
+
+
+def test_oracle_matches_hf_llama_at_70b_dims():
+    """The pin at the Llama-3-70B dimensions (d 8192, 64 query / 8 KV heads of 128 = GQA 8:1, ffn
+    28672, vocab 128256), one layer: the 8:1 head mapping the 70B stages use, checked against
+    transformers on the same counter-hash weights."""
+    dims = dict(pl.MODEL_DIMS["llama3-70b-bf16"], n_layers=1)
+    seed = pl.WEIGHT_SEED
+    tok, ours = _oracle_logits(dims, seed, 5, 10)
+    model = _hf_model(dims, seed)
+    with torch.no_grad():
+        hf = model(torch.from_numpy(tok.astype(np.int64))[None, :]).logits[0, -1].float().numpy()
+    del model
+    err = np.abs(ours - hf)
+    assert np.all(err <= 0.08 + 0.02 * np.abs(hf)), float(err.max())
+    top = np.sort(hf)[-2:]
+    if top[1] - top[0] > 0.16:
+        assert int(np.argmax(ours)) == int(np.argmax(hf))
