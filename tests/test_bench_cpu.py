@@ -81,3 +81,18 @@ def test_multi_gpu_config_is_shared_and_product_free(n):
     assert c["parallelism"] == f"pp{n}" and f"{n}-stage pipeline on {n}xB200" in c["workload"]
     assert "32 microbatches" in c["workload"] and "KV swap on" in c["workload"]
     assert set(c) == {"workload", "parallelism", "hops"}  # no run-dependent fields
+
+
+@pytest.mark.parametrize("run,lo", [("r02_70b_8stage_4gpu", 0.9), ("r02_8b_4stage_swap_pin", 0.95),
+                                    ("r02_70b_4stage_swap_pin", 0.5)])
+def test_pipeline_roofline_of_committed_runs(run, lo):
+    """SURVEY.md 8(d) pipeline fraction of the committed multi-stage B200 runs
+    (tools/pipeline_roofline.py): every last-stage compute in the window maps onto its schedule
+    circuit (checked), and the windowed output throughput sits below the roofline bound."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import pipeline_roofline
+    r = pipeline_roofline.pipeline_roofline(os.path.join(ROOT, "profiles", run))
+    assert r["circuits_in_window"] > 1000
+    assert lo <= r["pipeline_fraction"] <= 1.0
+    committed = json.load(open(os.path.join(ROOT, "profiles", run, "pipeline_roofline.json")))
+    assert committed["pipeline_fraction"] == r["pipeline_fraction"]
