@@ -35,10 +35,11 @@ def peaks():
         return 6548.5, 1381.7, "round-2 measured values (MEASURED_PEAKS.json absent)"
 
 
-def pipeline_roofline(run_dir):
-    summary = json.load(open(os.path.join(run_dir, "summary.json")))
+def pipeline_roofline(run_dir, cfg_txt=None):
+    """run_dir: report.kv + hw.trace.gz, and summary.json naming the config unless cfg_txt is
+    given (bench.py --gpus N directories: bench_multi.pipeline_config(N))."""
     kv = dict(line.split("=", 1) for line in open(os.path.join(run_dir, "report.kv")).read().splitlines())
-    txt = open(os.path.join(ROOT, summary["config"])).read()
+    txt = cfg_txt or open(os.path.join(ROOT, json.load(open(os.path.join(run_dir, "summary.json")))["config"])).read()
     plan = json.loads(pl.plan_config(txt, CONFIGS))
     dm = pl.MODEL_DIMS[json.loads(txt)["model"]["name"]]
     d, nh, nkv, dh, ffn, V = (dm["d_model"], dm["n_heads"], dm["n_kv_heads"], dm["d_head"], dm["ffn"],
@@ -47,7 +48,9 @@ def pipeline_roofline(run_dir):
     bw, tf, src = peaks()
     stages = [(st["layer_end"] - st["layer_begin"], i == 0, i == len(plan["stages"]) - 1)
               for i, st in enumerate(plan["stages"])]
-    sched = pl.schedule_config(txt, CONFIGS, max_circuits=int(summary["circuits"]))
+    with gzip.open(os.path.join(run_dir, "hw.trace.gz"), "rt") as f:
+        n_started = sum(1 for line in f if "kind=ComputeStart" in line and " stage=0 " in line)
+    sched = pl.schedule_config(txt, CONFIGS, max_circuits=n_started)
     w0, w1 = int(kv["window_start_us"]), int(kv["window_end_us"])
     last_s = str(len(stages) - 1)
     # the k-th last-stage compute of microbatch m is the k-th schedule circuit of m (stages see a
@@ -67,6 +70,9 @@ def pipeline_roofline(run_dir):
             if e["kind"] == "ComputeStart":
                 k = seen.get(m, 0)
                 seen[m] = k + 1
+                if k >= len(by_mb.get(m, [])):
+                    raise SystemExit(f"{run_dir}: the trace does not follow the current plan's "
+                                     "schedule (calibration or config changed since the run)")
                 i = by_mb[m][k]
                 c = sched["circuits"][i]
                 if (c["eff_batch"], c["n_decode"]) != (int(e["a"]), int(e["b"])):
@@ -109,7 +115,12 @@ def pipeline_roofline(run_dir):
 
 if __name__ == "__main__":
     for d in sys.argv[1:]:
-        r = pipeline_roofline(d)
+        cfg = None
+        if not os.path.exists(os.path.join(d, "summary.json")):  # a bench.py --gpus N directory
+            import bench_multi
+            n = int(dict(line.split("=", 1) for line in open(os.path.join(d, "report.kv")))["n_stages"])
+            cfg = json.dumps(bench_multi.pipeline_config(n))
+        r = pipeline_roofline(d, cfg)
         with open(os.path.join(d, "pipeline_roofline.json"), "w") as f:
             json.dump(r, f, indent=1)
         print(json.dumps(r))
