@@ -96,3 +96,15 @@ def test_pipeline_roofline_of_committed_runs(run, lo):
     assert lo <= r["pipeline_fraction"] <= 1.0
     committed = json.load(open(os.path.join(ROOT, "profiles", run, "pipeline_roofline.json")))
     assert committed["pipeline_fraction"] == r["pipeline_fraction"]
+
+
+def test_pipeline_roofline_of_the_n4_bench_run():
+    """The same for the committed N=4 bench run (one process per GPU over NCCL; its config is
+    bench_multi.pipeline_config(4), BASELINE configs[2] as written)."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import bench_multi
+    import pipeline_roofline
+    d = os.path.join(ROOT, "profiles", "r02_bench_n4")
+    r = pipeline_roofline.pipeline_roofline(d, json.dumps(bench_multi.pipeline_config(4)))
+    assert 0.9 <= r["pipeline_fraction"] <= 1.0 and r["stages"] == 4
+    assert json.load(open(os.path.join(d, "pipeline_roofline.json")))["pipeline_fraction"] == r["pipeline_fraction"]
