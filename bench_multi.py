@@ -20,6 +20,7 @@ included, sampled ids copied to host every circuit).
 import ctypes as C
 import json
 import os
+import sys
 
 CONFIGS = os.path.join(os.path.dirname(os.path.abspath(__file__)), "configs")
 METRIC = "generated tokens/sec (whole pipeline) at injected inter-stage latency; roofline fraction"
@@ -150,6 +151,15 @@ def run_multi(args):
         shutil.copyfileobj(fi, fo)
     for f in [merged] + [os.path.join(out_dir, f"rank{i}.trace") for i in range(world)]:
         os.remove(f)
+    try:  # SURVEY.md 8(d) pipeline roofline of this run (tools/pipeline_roofline.py)
+        sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools"))
+        from pipeline_roofline import pipeline_roofline
+        pr = pipeline_roofline(out_dir, txt)
+        pipe_rf = {k: pr[k] for k in ("pipeline_roofline_tokens_per_s", "pipeline_fraction",
+                                      "t_roof_stage_us_mean", "decode_rows_per_circuit_mean",
+                                      "circuits_in_window")}
+    except (Exception, SystemExit) as e:  # reported, never fatal to the bench line
+        pipe_rf = {"error": str(e)[:200]}
     sim = pl.sim_config(txt, CONFIGS)
     clocks = gathered[0]["clk"]
     clocks["per_rank_sm_mhz"] = [g["clk"]["sm_mhz"] for g in gathered]
@@ -175,6 +185,7 @@ def run_multi(args):
                                         "swap_stall_us", "completed_requests")},
         "reference_sim_tokens_per_s": sim["output_throughput"],
         "analytic_bound_tokens_per_s": pl.steady_state_throughput(plan_txt),
+        "pipeline_roofline": pipe_rf,
         "e2e": {"value": round(last["tokens"] / (wall_max / 1e6), 2), "unit": "tokens/s",
                 "h2d_bytes_per_step": sum(g["h2d"] for g in gathered),
                 "d2h_bytes_per_step": last["d2h"],
