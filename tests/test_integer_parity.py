@@ -445,3 +445,38 @@ def test_hardware_runs_repriced(tmp_path, run):
     out = price_runs.price_run(d, {"preset": "whattomine-8x4090"}, out_dir=str(tmp_path))
     assert out["profitable"] == "1" and int(out["revenue_micro_usd"]) > int(out["cost_micro_usd"])
     assert open(tmp_path / "report_priced.kv").read() == open(os.path.join(d, "report_priced.kv")).read()
+
+
+def _write_trace(lines, path):
+    """Trace lines with seq renumbered to the line index (write_trace's invariant)."""
+    with open(path, "w") as f:
+        for i, ln in enumerate(lines):
+            fs = ln.split()
+            fs[1] = f"seq={i}"
+            f.write(" ".join(fs) + "\n")
+
+
+def test_committed_hardware_trace_passes_and_tampering_is_caught(ref, tmp_path):
+    """The reference's replay_check (sim.cpp:606-697) on a committed B200 hardware trace (70B,
+    8 stages on 4 GPUs): 0 violations; the same trace with one compute duplicated, or with a hop
+    arriving before the compute that sends it, is rejected -- the gate is live, not vacuous."""
+    import gzip
+    d = os.path.join(ROOT, "profiles", "r02_70b_8stage_4gpu")
+    s = json.load(open(os.path.join(d, "summary.json")))
+    plan = pl.plan_config(open(os.path.join(ROOT, s["config"])).read(), os.path.join(ROOT, "configs"))
+    lines = gzip.open(os.path.join(d, "hw.trace.gz"), "rt").read().splitlines()
+    clean = str(tmp_path / "clean.trace")
+    _write_trace(lines, clean)
+    assert ref.replay_check(clean, plan) == []
+    # double compute: a second ComputeStart of stage 1's first compute
+    i = next(k for k, ln in enumerate(lines) if "kind=ComputeStart stage=1 " in ln)
+    dup = str(tmp_path / "dup.trace")
+    _write_trace(lines[:i + 1] + [lines[i]] + lines[i + 1:], dup)
+    assert ref.replay_check(dup, plan) != []
+    # causality: stage 1's first arrival moved to t=1 (t=0 marks initial placements), before its
+    # send time + hop latency
+    j = next(k for k, ln in enumerate(lines) if "kind=TransferArrive stage=1 " in ln)
+    early = lines[:j] + [" ".join(["t=1"] + lines[j].split()[1:])] + lines[j + 1:]
+    bad = str(tmp_path / "early.trace")
+    _write_trace(early, bad)
+    assert ref.replay_check(bad, plan) != []
