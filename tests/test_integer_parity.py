@@ -509,3 +509,8 @@ def test_every_committed_hardware_trace_replays_clean(ref, tmp_path, run):
     trace.write_text(gzip.open(os.path.join(d, "hw.trace.gz"), "rt").read())
     kinds = {v.split()[0] for v in ref.replay_check(str(trace), plan)}
     assert kinds <= {"swap-bandwidth-exceeded"}
+    # and the reference's windowed_stats (workload.cpp:82-116) over the report's window counts
+    # exactly the committed report's tokens: the headline numbers are the reference metric
+    kv = dict(ln.split("=", 1) for ln in open(os.path.join(d, "report.kv")).read().splitlines())
+    n_in, n_out, _ = ref.windowed_stats(str(trace), int(kv["window_start_us"]), int(kv["window_end_us"]))
+    assert (n_in, n_out) == (int(kv["input_tokens"]), int(kv["output_tokens"]))
