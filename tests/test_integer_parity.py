@@ -514,3 +514,22 @@ def test_every_committed_hardware_trace_replays_clean(ref, tmp_path, run):
     kv = dict(ln.split("=", 1) for ln in open(os.path.join(d, "report.kv")).read().splitlines())
     n_in, n_out, _ = ref.windowed_stats(str(trace), int(kv["window_start_us"]), int(kv["window_end_us"]))
     assert (n_in, n_out) == (int(kv["input_tokens"]), int(kv["output_tokens"]))
+
+
+def test_committed_gpu_sweep_is_against_the_reference_sweep(ref):
+    """profiles/r02_sweep_70b (config 5 on 4 B200s, tools/gpu_sweep.py --duration 60 --warmup 20):
+    its sweep_reference.csv is the reference's own run_sweep(...).to_csv() of the same document,
+    and sweep_gpu.csv (ds_sweep_csv) holds the per-cell hardware throughputs of cells.jsonl."""
+    d = os.path.join(ROOT, "profiles", "r02_sweep_70b")
+    cfg = json.load(open(os.path.join(ROOT, "configs", "llama70b_sweep_4gpu.json")))
+    cfg["workload"].update(bench_duration_s=60, warmup_s=20)
+    assert open(os.path.join(d, "sweep_reference.csv")).read() == \
+        ref.sweep_csv(json.dumps(cfg), os.path.join(ROOT, "configs"))
+    cells = [json.loads(ln) for ln in open(os.path.join(d, "cells.jsonl"))]
+    rows = {ln.split(",")[0]: ln.strip().split(",")[1:]
+            for ln in open(os.path.join(d, "sweep_gpu.csv")).read().splitlines()[1:]}
+    lats = open(os.path.join(d, "sweep_gpu.csv")).readline().strip().split(",")[1:]
+    for c in cells:
+        assert c["replay_check"]["violations"] == 0
+        got = float(rows[c["policy"]][lats.index(str(c["latency_us"]))])
+        assert abs(got - c["gpu_tps"]) <= 0.06
