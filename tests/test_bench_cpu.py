@@ -108,3 +108,24 @@ def test_pipeline_roofline_of_the_n4_bench_run():
     r = pipeline_roofline.pipeline_roofline(d, json.dumps(bench_multi.pipeline_config(4)))
     assert 0.9 <= r["pipeline_fraction"] <= 1.0 and r["stages"] == 4
     assert json.load(open(os.path.join(d, "pipeline_roofline.json")))["pipeline_fraction"] == r["pipeline_fraction"]
+
+
+def test_committed_n1_bench_line_is_self_consistent():
+    """profiles/r02_bench_n1_latest.json (the default `python bench.py` on a B200): value =
+    decode tokens of the offline batch / ms_per_step; roofline.frac = achieved / peak with achieved
+    = algorithmic bytes per launch / average launch time; stage_roofline recomputed here from the
+    schedule equals the line's, and its frac = t_roof / ms_per_step."""
+    sys.path.insert(0, ROOT)
+    import bench
+    d = json.load(open(os.path.join(ROOT, "profiles", "r02_bench_n1_latest.json")))
+    assert d["report"]["output_tokens"] == d["workload_detail"]["tokens_per_step"] == 68699
+    assert abs(d["value"] - 68699 / (d["ms_per_step"] / 1e3)) < 0.01 * d["value"] / 100
+    rf = d["roofline"]
+    ach = rf["algorithmic_bytes_per_launch"] / (rf["avg_launch_ms"] / 1e3) / 1e9
+    assert abs(ach - rf["achieved"]) < 0.01 and abs(rf["achieved"] / rf["peak"] - rf["frac"]) < 1e-4
+    if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")):
+        sr = bench.stage_roofline(open(os.path.join(CONFIGS, "llama8b_1stage.json")).read())
+        assert sr["t_roof_s_per_step"] == d["stage_roofline"]["t_roof_s_per_step"]
+    assert abs(d["stage_roofline"]["t_roof_s_per_step"] / (d["ms_per_step"] / 1e3)
+               - d["stage_roofline"]["frac"]) < 1e-4
+    assert d["e2e"]["value"] > 0.99 * d["value"] and d["gpu_launches"] > 0
