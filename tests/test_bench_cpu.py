@@ -129,3 +129,26 @@ def test_committed_n1_bench_line_is_self_consistent():
     assert abs(d["stage_roofline"]["t_roof_s_per_step"] / (d["ms_per_step"] / 1e3)
                - d["stage_roofline"]["frac"]) < 1e-4
     assert d["e2e"]["value"] > 0.99 * d["value"] and d["gpu_launches"] > 0
+
+
+def test_roofline_traffic_and_70b_summary_come_from_the_committed_captures():
+    """The bench line's roofline.traffic is the DRAM read + write of the committed ncu --set full
+    capture it names; profiles/r02_70b_shapes/summary.json is tools/summarize_cal70.py applied
+    to the committed launch list."""
+    import csv
+    d = json.load(open(os.path.join(ROOT, "profiles", "r02_bench_n1_latest.json")))
+    rows = list(csv.reader(open(os.path.join(ROOT, "profiles", "r02_ncu_full_gemm_gate_up.csv"))))
+    h, units, v = rows[0], rows[1], rows[2]
+    mb = {"Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Gbyte": 1e9}
+    rd = float(v[h.index("dram__bytes_read.sum")]) * mb[units[h.index("dram__bytes_read.sum")]]
+    wr = float(v[h.index("dram__bytes_write.sum")]) * mb[units[h.index("dram__bytes_write.sum")]]
+    assert abs(rd + wr - d["roofline"]["traffic"]) < 1.0
+    s70 = os.path.join(ROOT, "profiles", "r02_70b_shapes")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "summarize_cal70.py"),
+                        os.path.join(s70, "cal70_launches.csv"), os.path.join(ROOT, "MEASURED_PEAKS.json")],
+                       capture_output=True, text=True, timeout=120, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-300:]
+    got, want = json.loads(r.stdout), json.load(open(os.path.join(s70, "summary.json")))
+    assert got["configs"] == want["configs"]
+    dec = {c["T"]: c["kinds"]["attention_decode"]["alg_frac_of_hbm"] for c in got["configs"] if c["T"] < 1000}
+    assert dec[49] >= 0.7 and dec[256] >= 0.7  # the north-star decode-attention target at 70B
